@@ -1,0 +1,155 @@
+/*
+ * aderstp — B200-native (sm_100a) linear ADER-DG Space-Time Predictor, C ABI.
+ *
+ * This is the drop-in boundary for the reference's hot path.  Each entry point names the
+ * reference interface it replaces (paths relative to /root/reference/proj):
+ *
+ *   aderstp_predict_batch       <- ader::predict(Variant, const ElementTensor& q, const LinearPde&,
+ *                                  double dt, const BasisOperators&, ScratchArena&,
+ *                                  PredictorOutput&, double t_start)
+ *                                  include/ader/predictor.hpp:118-120 (+ stp_* :94-116)
+ *                                  followed by ader::extrapolate_faces(PredictorOutput&, ...)
+ *                                  include/ader/predictor.hpp:125
+ *                                  One call = one batch of independent elements on the GPU.
+ *   aderstp_predict_batch_host  <- same, with host buffers (the call a CPU caller such as
+ *                                  run_simulation, src/solver.cpp:334-345, makes); copies in and
+ *                                  out are pipelined against the kernel.
+ *   aderstp_plan_create         <- SolverConfig (include/ader/config.hpp:21-28) + make_basis
+ *                                  (include/ader/basis.hpp:37, src/basis.cpp:110-122) + the
+ *                                  LinearPde factories (include/ader/pde.hpp:62-84).  Kernels never
+ *                                  allocate (include/ader/predictor.hpp:31-34): all state lives
+ *                                  in the plan.
+ *   aderstp_basis               <- ader::make_basis (src/basis.cpp:110-122), host side.
+ *   aderstp_flop_count          <- ader::flop_count (include/ader/predictor.hpp:86), reporting the
+ *                                  algorithmic count of this implementation.
+ *   aderstp_last_error          <- the std::invalid_argument messages of validate_stp
+ *                                  (src/predictor_common.cpp:129-146); nothing is thrown across
+ *                                  the ABI.
+ *
+ * All device pointers are plain CUDA device addresses; `stream` is a cudaStream_t (NULL = the
+ * legacy default stream).  Calls are asynchronous on `stream` unless stated otherwise.
+ * Thread-safe for distinct (plan, stream) pairs.
+ *
+ * Batch layouts (e = element index, n = order = nodes per dim, m = quantities):
+ *   q            ADERSTP_LAYOUT_AOSOA : [e][k3][k2][s < q_stride][k1]     (native, x fastest)
+ *                ADERSTP_LAYOUT_AOS   : [e][k3][k2][k1][s < q_stride]     (reference ElementTensor,
+ *                                                                           q_stride = m_pad = 16)
+ *   qavg         same layout kind as q, quantity slots = out_stride (padding written as 0.0)
+ *   favg         [e][d = 0..2][ one qavg-shaped tensor ]
+ *   face_q/f     [e][f][a][b][s < m], f = -x,+x,-y,+y,-z,+z; (a,b) = the two in-face dims in
+ *                (z,y,x) order; exactly the reference's PredictorOutput::face_q/face_f arrays
+ *                (include/ader/predictor.hpp:16-29).
+ *   par          [e][3]: (lambda, mu, rho) or (rho, cp, cs) per element (elastic kinds only).
+ */
+#ifndef ADERSTP_H
+#define ADERSTP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADERSTP_ABI_VERSION 1
+
+/* status codes */
+#define ADERSTP_OK 0
+#define ADERSTP_ERR_INVALID_ARG 1   /* shape / pointer / dt checks of validate_stp            */
+#define ADERSTP_ERR_UNSUPPORTED 2   /* order or quantity count without a compiled kernel        */
+#define ADERSTP_ERR_NONFINITE 3     /* "stp: non-finite input DOFs" (predictor_common.cpp:143)   */
+#define ADERSTP_ERR_MATERIAL 4      /* "elastic_pde: need rho > 0, mu >= 0, lambda + 2mu > 0"   */
+#define ADERSTP_ERR_CUDA 5          /* CUDA runtime error (message in aderstp_last_error)        */
+
+/* PDE kinds: the reference's factories (include/ader/pde.hpp:62-84) */
+#define ADERSTP_PDE_ELASTIC 0        /* elastic_pde(lambda, mu, rho) per element, m = 9           */
+#define ADERSTP_PDE_ADVECTION 1      /* advection_pde(v, m): pde_args[0..2] = v                   */
+#define ADERSTP_PDE_NCP_ADVECTION 2  /* ncp_advection_pde(v, m): pde_args[0..2] = v               */
+#define ADERSTP_PDE_DEMO 3           /* paper_demo_pde(), m = 6                                   */
+#define ADERSTP_PDE_ELASTIC_SOURCE 4 /* elastic_pde(lambda, mu, rho, PointSourceSpec) per element */
+#define ADERSTP_PDE_SOURCE_ONLY 5    /* source_only_pde(m, PointSourceSpec)                       */
+#define ADERSTP_PDE_LINEAR 6         /* any constant-coefficient LinearPde, given by its probed
+                                        flux Jacobians A_d and ncp matrices B_d (aderstp_config) */
+
+/* point source spec in pde_args (include/ader/pde.hpp:47-56):
+ *   [0..2] position, [3] component, [4] amplitude, [5] center, [6] width */
+
+#define ADERSTP_PAR_LAMBDA_MU_RHO 0
+#define ADERSTP_PAR_RHO_CP_CS 1
+
+#define ADERSTP_LAYOUT_AOSOA 0
+#define ADERSTP_LAYOUT_AOS 1
+
+#define ADERSTP_MAX_QUANTITIES 16
+
+typedef struct aderstp_config {
+  int order;       /* n = nodes per dimension (reference cfg.order); 2..10 compiled      */
+  int quantities;  /* m; 9 for the elastic kinds                                          */
+  int pde_kind;    /* ADERSTP_PDE_*                                                       */
+  int layout;      /* ADERSTP_LAYOUT_* for q, qavg, favg                                  */
+  int q_stride;    /* quantity slots per node in q (>= m); 0 = m                          */
+  int out_stride;  /* quantity slots per node in qavg/favg (>= m); 0 = m                  */
+  int par_kind;    /* ADERSTP_PAR_* (elastic kinds)                                       */
+  int check_inputs;/* 1 = flag non-finite q / invalid material (validate_stp semantics)  */
+  double pde_args[8];
+  /* ADERSTP_PDE_LINEAR only: row-major m x m, linear[d] = A_d (flux Jacobian, F_d(q) = A_d q)
+   * and linear[3 + d] = B_d (ncp: out = B_d * grad_d q); NULL entries mean zero. */
+  const double* linear[6];
+} aderstp_config;
+
+typedef struct aderstp_plan aderstp_plan;
+
+/* ---- plan ---------------------------------------------------------------------------- */
+int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** plan);
+void aderstp_plan_destroy(aderstp_plan* plan);
+/* Elements per second of this plan are independent; the plan is immutable after creation. */
+
+/* ---- the hot path ---------------------------------------------------------------------- */
+/* Device buffers.  favg, face_q and face_f may be NULL (not computed / not written).
+ * Asynchronous; with check_inputs the input checks are reported by aderstp_plan_status. */
+int aderstp_predict_batch(const aderstp_plan* plan, int64_t n_elem, const double* q,
+                          const double* par, double dt, double t_start, double* qavg,
+                          double* favg, double* face_q, double* face_f, void* stream);
+
+/* Host buffers (pinned or pageable).  Synchronous: splits the batch into chunks and overlaps
+ * host->device copies, the kernel and device->host copies on two streams, using device
+ * scratch owned by the plan (allocated on first use, aderstp_plan_reserve_host_path to size
+ * it up front).  Returns the input-check status directly. */
+int aderstp_predict_batch_host(aderstp_plan* plan, int64_t n_elem, const double* q,
+                               const double* par, double dt, double t_start, double* qavg,
+                               double* favg, double* face_q, double* face_f);
+int aderstp_plan_reserve_host_path(aderstp_plan* plan, int64_t chunk_elems);
+
+/* Synchronises `stream` and returns (and clears) the input-check status of the plan's
+ * previous launches: ADERSTP_OK, ADERSTP_ERR_NONFINITE or ADERSTP_ERR_MATERIAL. */
+int aderstp_plan_status(aderstp_plan* plan, void* stream);
+
+/* ---- layouts (reference AoS <-> native AoSoA, include/ader/layout.hpp:44-50,
+ *      src/layout.cpp:168-194), device buffers, asynchronous ------------------------------ */
+int aderstp_convert_layout(int order, int quantities, int64_t n_elem, int src_layout,
+                           int src_stride, const double* src, int dst_layout, int dst_stride,
+                           double* dst, void* stream);
+
+/* ---- seeded synthetic inputs on the device (BASELINE.json configs) --------------------
+ * dist 0: Q ~ U[-1,1]; 1: Q ~ N(0,1) (Box-Muller); 2: three random-phase sinusoids per
+ * quantity on a periodic grid of `grid` elements per side.  Elements [e0, e0+n_elem) of the
+ * stream defined in DESIGN.md (SplitMix64, element-major draw order); par receives
+ * (rho, cp, cs) per element.  q uses the plan-independent layout given here, m = 9. */
+int aderstp_generate(int dist, uint64_t seed, int order, int64_t e0, int64_t n_elem, int grid,
+                     int layout, int q_stride, double* q, double* par, void* stream);
+
+/* ---- host helpers -------------------------------------------------------------------- */
+int aderstp_basis(int order, double* nodes, double* weights, double* d, double* face_left,
+                  double* face_right);
+/* algorithmic fp64 FLOPs and HBM bytes per element of the elastic STP */
+double aderstp_flop_count(int order, int quantities);
+double aderstp_byte_count(int order, int quantities, int with_favg);
+int aderstp_supported_order(int order);
+const char* aderstp_last_error(void);
+int aderstp_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ADERSTP_H */

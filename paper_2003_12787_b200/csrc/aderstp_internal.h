@@ -1,0 +1,65 @@
+// Internal interface between the host C ABI (capi.cpp) and the sm_100a kernels (stp_kernels.cu).
+#pragma once
+
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace aderstp {
+
+constexpr int kMinOrder = 2;
+constexpr int kMaxOrder = 10;
+constexpr int kMaxM = 16;      // ADERSTP_MAX_QUANTITIES
+constexpr int kMaxTerms = 4;   // nonzeros per (row s, dim d) of a table PDE
+
+// Host-side basis, derived from scratch (basis.cpp).  d[k*n + l] = phi_l'(x_k).
+struct HostBasis {
+  int n = 0;
+  double nodes[kMaxOrder], weights[kMaxOrder], d[kMaxOrder * kMaxOrder];
+  double face_left[kMaxOrder], face_right[kMaxOrder];
+};
+int make_host_basis(int n, HostBasis* out);
+void lagrange_values(int n, const double* nodes, double x, double* vals);
+
+// Everything a kernel launch needs besides the batch pointers; lives in the plan.
+struct LaunchPlan {
+  int n = 0, m = 0, kind = 0;        // order, quantities, ADERSTP_PDE_*
+  int layout = 0, q_stride = 0, out_stride = 0, par_kind = 0, check = 0;
+  HostBasis basis;
+  // table PDE terms (non-elastic kinds), t_s += sum_k tc * D_d (p_{tr}) and favg via fr/fc
+  int n_terms = 1;
+  signed char tr[kMaxM][3][kMaxTerms];
+  double tc[kMaxM][3][kMaxTerms];
+  signed char fr[kMaxM][3][kMaxTerms];
+  double fc[kMaxM][3][kMaxTerms];
+  // point source: component < 0 means none; proj factors phi_d(x_src)/w per dim;
+  int src_comp = -1;
+  double src_pos[3] = {0, 0, 0};
+  double src_amp = 0, src_center = 0, src_width = 1;
+  double src_proj[3][kMaxOrder];
+  unsigned int* d_status = nullptr;  // device word: bit0 non-finite q, bit1 bad material
+};
+
+struct BatchArgs {
+  const double* q;
+  const double* par;
+  double* qavg;
+  double* favg;
+  double* face_q;
+  double* face_f;
+  long long n_elem;
+  double dt;
+  double t_start;
+};
+
+// stp_kernels.cu
+cudaError_t launch_stp(const LaunchPlan& plan, const BatchArgs& args, cudaStream_t stream);
+cudaError_t launch_convert(int n, int m, long long n_elem, int src_layout, int src_stride,
+                           const double* src, int dst_layout, int dst_stride, double* dst,
+                           cudaStream_t stream);
+cudaError_t launch_generate(int dist, uint64_t seed, int n, long long e0, long long n_elem,
+                            int grid, int layout, int q_stride, const HostBasis& basis,
+                            double* q, double* par, cudaStream_t stream);
+bool kernel_available(int n);
+
+}  // namespace aderstp

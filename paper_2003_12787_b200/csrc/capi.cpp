@@ -1,0 +1,428 @@
+// Host side of the C ABI (include/aderstp.h): plans, argument validation with the reference's
+// validate_stp semantics (proj/src/predictor_common.cpp:129-146), PDE term tables from the
+// reference's LinearPde factories (proj/src/pde.cpp), and the pipelined host-buffer path.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "../../include/aderstp.h"
+#include "aderstp_internal.h"
+
+using aderstp::HostBasis;
+using aderstp::LaunchPlan;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  return fail(ADERSTP_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kHostStreams = 3;
+
+}  // namespace
+
+struct aderstp_plan {
+  LaunchPlan lp;
+  int device = 0;
+  // host-buffer path scratch (allocated on first use or by aderstp_plan_reserve_host_path)
+  int64_t chunk = 0;
+  double* buf[kHostStreams] = {nullptr, nullptr, nullptr};
+  cudaStream_t streams[kHostStreams] = {nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+// Build the per-(s,d) term tables from flux Jacobians A_d and ncp matrices B_d (row-major
+// m x m): t-terms from A_d + B_d (the CK step applies D_d F_d(p) + B_d D_d p, equal to
+// D_d (A_d + B_d) p for constant coefficients), favg terms from A_d alone.
+int build_terms(LaunchPlan& lp, const double* A[3], const double* B[3]) {
+  const int m = lp.m;
+  std::memset(lp.tr, 0, sizeof lp.tr);
+  std::memset(lp.fr, 0, sizeof lp.fr);
+  for (int s = 0; s < aderstp::kMaxM; ++s)
+    for (int d = 0; d < 3; ++d)
+      for (int k = 0; k < aderstp::kMaxTerms; ++k) lp.tc[s][d][k] = lp.fc[s][d][k] = 0.0;
+  int max_terms = 1;
+  for (int s = 0; s < m; ++s)
+    for (int d = 0; d < 3; ++d) {
+      int nt = 0, nf = 0;
+      for (int r = 0; r < m; ++r) {
+        const double a = A[d] ? A[d][s * m + r] : 0.0;
+        const double b = B[d] ? B[d][s * m + r] : 0.0;
+        if (!std::isfinite(a) || !std::isfinite(b))
+          return fail(ADERSTP_ERR_INVALID_ARG, "linear pde: non-finite coefficient");
+        const double c = a + b;
+        if (c != 0.0) {
+          if (nt == aderstp::kMaxTerms)
+            return fail(ADERSTP_ERR_UNSUPPORTED, "linear pde: more than 4 nonzeros in a row of A_d+B_d");
+          lp.tr[s][d][nt] = (signed char)r;
+          lp.tc[s][d][nt] = c;
+          ++nt;
+        }
+        if (a != 0.0) {
+          if (nf == aderstp::kMaxTerms)
+            return fail(ADERSTP_ERR_UNSUPPORTED, "linear pde: more than 4 nonzeros in a row of A_d");
+          lp.fr[s][d][nf] = (signed char)r;
+          lp.fc[s][d][nf] = a;
+          ++nf;
+        }
+      }
+      if (nt > max_terms) max_terms = nt;
+      if (nf > max_terms) max_terms = nf;
+    }
+  lp.n_terms = max_terms;
+  return ADERSTP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* aderstp_last_error(void) { return g_last_error.c_str(); }
+int aderstp_abi_version(void) { return ADERSTP_ABI_VERSION; }
+int aderstp_supported_order(int order) { return aderstp::kernel_available(order) ? 1 : 0; }
+
+int aderstp_basis(int order, double* nodes, double* weights, double* d, double* face_left,
+                  double* face_right) {
+  HostBasis b;
+  if (aderstp::make_host_basis(order, &b) != 0)
+    return fail(ADERSTP_ERR_INVALID_ARG, "basis: order out of range");
+  const int n = order;
+  if (nodes) std::memcpy(nodes, b.nodes, sizeof(double) * n);
+  if (weights) std::memcpy(weights, b.weights, sizeof(double) * n);
+  if (d) std::memcpy(d, b.d, sizeof(double) * n * n);
+  if (face_left) std::memcpy(face_left, b.face_left, sizeof(double) * n);
+  if (face_right) std::memcpy(face_right, b.face_right, sizeof(double) * n);
+  return ADERSTP_OK;
+}
+
+double aderstp_flop_count(int order, int quantities) {
+  const double n = order, m = quantities;
+  return m * n * n * n * ((n - 1.0) * (6.0 * n + 8.0) + 28.0);
+}
+
+double aderstp_byte_count(int order, int quantities, int with_favg) {
+  const double n = order, m = quantities;
+  return 8.0 * m * ((with_favg ? 5.0 : 2.0) * n * n * n + 12.0 * n * n) + 24.0;
+}
+
+int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
+  if (!cfg || !out) return fail(ADERSTP_ERR_INVALID_ARG, "plan_create: null argument");
+  *out = nullptr;
+  const int n = cfg->order, m = cfg->quantities;
+  if (!aderstp::kernel_available(n))
+    return fail(ADERSTP_ERR_UNSUPPORTED, "plan_create: order " + std::to_string(n) +
+                                             " has no compiled kernel (2..10)");
+  if (m < 1 || m > ADERSTP_MAX_QUANTITIES)
+    return fail(ADERSTP_ERR_UNSUPPORTED, "plan_create: quantity count out of range (1..16)");
+  if (cfg->layout != ADERSTP_LAYOUT_AOSOA && cfg->layout != ADERSTP_LAYOUT_AOS)
+    return fail(ADERSTP_ERR_INVALID_ARG, "plan_create: unknown layout");
+  const int qs = cfg->q_stride ? cfg->q_stride : m;
+  const int os = cfg->out_stride ? cfg->out_stride : m;
+  if (qs < m || os < m || qs > 64 || os > 64)
+    return fail(ADERSTP_ERR_INVALID_ARG, "plan_create: quantity strides must be in [m, 64]");
+  const int kind = cfg->pde_kind;
+  const bool elastic = kind == ADERSTP_PDE_ELASTIC || kind == ADERSTP_PDE_ELASTIC_SOURCE;
+  if (elastic && m != 9)
+    return fail(ADERSTP_ERR_INVALID_ARG, "stp: pde/tensor quantity mismatch (elastic has m = 9)");
+  if (kind == ADERSTP_PDE_DEMO && m != 6)
+    return fail(ADERSTP_ERR_INVALID_ARG, "stp: pde/tensor quantity mismatch (demo has m = 6)");
+  if (kind < ADERSTP_PDE_ELASTIC || kind > ADERSTP_PDE_LINEAR)
+    return fail(ADERSTP_ERR_INVALID_ARG, "plan_create: unknown pde kind");
+  if (elastic && cfg->par_kind != ADERSTP_PAR_LAMBDA_MU_RHO && cfg->par_kind != ADERSTP_PAR_RHO_CP_CS)
+    return fail(ADERSTP_ERR_INVALID_ARG, "plan_create: unknown parameter kind");
+
+  aderstp_plan* p = new (std::nothrow) aderstp_plan();
+  if (!p) return fail(ADERSTP_ERR_INVALID_ARG, "plan_create: out of host memory");
+  LaunchPlan& lp = p->lp;
+  lp.n = n;
+  lp.m = m;
+  lp.kind = elastic ? ADERSTP_PDE_ELASTIC : ADERSTP_PDE_LINEAR;
+  lp.layout = cfg->layout;
+  lp.q_stride = qs;
+  lp.out_stride = os;
+  lp.par_kind = cfg->par_kind;
+  lp.check = cfg->check_inputs ? 1 : 0;
+  aderstp::make_host_basis(n, &lp.basis);
+
+  // PDE terms (proj/src/pde.cpp): advection :61-85, ncp-advection :87-117, demo :119-146
+  int rc = ADERSTP_OK;
+  if (!elastic) {
+    double A[3][aderstp::kMaxM * aderstp::kMaxM], B[3][aderstp::kMaxM * aderstp::kMaxM];
+    std::memset(A, 0, sizeof A);
+    std::memset(B, 0, sizeof B);
+    const double* pa[3] = {A[0], A[1], A[2]};
+    const double* pb[3] = {B[0], B[1], B[2]};
+    const double* v = cfg->pde_args;
+    if (kind == ADERSTP_PDE_ADVECTION) {
+      for (int d = 0; d < 3; ++d)
+        for (int s = 0; s < m; ++s) A[d][s * m + s] = -v[d];
+    } else if (kind == ADERSTP_PDE_NCP_ADVECTION) {
+      for (int d = 0; d < 3; ++d)
+        for (int s = 0; s < m; ++s) B[d][s * m + s] = -v[d];
+    } else if (kind == ADERSTP_PDE_DEMO) {
+      // x-flux rows F0 = -(Q0+Q3+Q4), F1 = -(Q1+Q3+Q5), F2 = -(Q2+Q4+Q5); y/z rotate the
+      // quantity indices by (0 1 2)(3 4 5) (pde.hpp:66-70)
+      const int rot[6] = {1, 2, 0, 4, 5, 3};
+      int rows[3][3] = {{0, 3, 4}, {1, 3, 5}, {2, 4, 5}};
+      int outs[3] = {0, 1, 2};
+      for (int d = 0; d < 3; ++d) {
+        for (int r = 0; r < 3; ++r)
+          for (int j = 0; j < 3; ++j) A[d][outs[r] * m + rows[r][j]] = -1.0;
+        for (int r = 0; r < 3; ++r) {
+          outs[r] = rot[outs[r]];
+          for (int j = 0; j < 3; ++j) rows[r][j] = rot[rows[r][j]];
+        }
+      }
+    } else if (kind == ADERSTP_PDE_LINEAR) {
+      for (int d = 0; d < 3; ++d) {
+        pa[d] = cfg->linear[d];
+        pb[d] = cfg->linear[3 + d];
+      }
+    }
+    rc = build_terms(lp, pa, pb);
+    if (rc != ADERSTP_OK) {
+      delete p;
+      return rc;
+    }
+  } else {
+    lp.n_terms = 1;
+  }
+  // point source (pde.hpp:47-56; weak Dirac projection predictor_common.cpp:261-283)
+  if (kind == ADERSTP_PDE_ELASTIC_SOURCE || kind == ADERSTP_PDE_SOURCE_ONLY) {
+    const double* a = cfg->pde_args;
+    const int comp = (int)a[3];
+    if (comp < 0 || comp >= m || (kind == ADERSTP_PDE_ELASTIC_SOURCE && (comp < 6 || comp > 8))) {
+      delete p;
+      return fail(ADERSTP_ERR_INVALID_ARG, "point source: component out of range");
+    }
+    if (!(a[6] > 0.0)) {
+      delete p;
+      return fail(ADERSTP_ERR_INVALID_ARG, "point source: width must be positive");
+    }
+    lp.src_comp = comp;
+    lp.src_amp = a[4];
+    lp.src_center = a[5];
+    lp.src_width = a[6];
+    for (int d = 0; d < 3; ++d) {
+      lp.src_pos[d] = a[d];
+      double phi[aderstp::kMaxOrder];
+      aderstp::lagrange_values(n, lp.basis.nodes, a[d], phi);
+      for (int j = 0; j < n; ++j) lp.src_proj[d][j] = phi[j] / lp.basis.weights[j];
+    }
+  } else {
+    lp.src_comp = -1;
+    for (int d = 0; d < 3; ++d)
+      for (int j = 0; j < aderstp::kMaxOrder; ++j) lp.src_proj[d][j] = 0.0;
+  }
+
+  cudaError_t e = cudaGetDevice(&p->device);
+  if (e == cudaSuccess) e = cudaMalloc(&lp.d_status, sizeof(unsigned int));
+  if (e == cudaSuccess) e = cudaMemset(lp.d_status, 0, sizeof(unsigned int));
+  if (e != cudaSuccess) {
+    delete p;
+    return cuda_fail(e, "plan_create");
+  }
+  *out = p;
+  return ADERSTP_OK;
+}
+
+void aderstp_plan_destroy(aderstp_plan* p) {
+  if (!p) return;
+  for (int i = 0; i < kHostStreams; ++i) {
+    if (p->buf[i]) cudaFree(p->buf[i]);
+    if (p->streams[i]) cudaStreamDestroy(p->streams[i]);
+  }
+  if (p->lp.d_status) cudaFree(p->lp.d_status);
+  delete p;
+}
+
+namespace {
+
+int validate_batch(const aderstp_plan* p, int64_t n_elem, const double* q, const double* par,
+                   double dt, const double* qavg, const double* favg, const double* face_f) {
+  if (!p) return fail(ADERSTP_ERR_INVALID_ARG, "stp: null plan");
+  if (n_elem < 0) return fail(ADERSTP_ERR_INVALID_ARG, "stp: negative element count");
+  if (!(dt > 0.0)) return fail(ADERSTP_ERR_INVALID_ARG, "stp: dt must be positive");
+  if (n_elem > 0 && !q) return fail(ADERSTP_ERR_INVALID_ARG, "stp: null input tensor");
+  if (n_elem > 0 && !qavg) return fail(ADERSTP_ERR_INVALID_ARG, "stp: null qavg output");
+  if (n_elem > 0 && p->lp.kind == ADERSTP_PDE_ELASTIC && !par)
+    return fail(ADERSTP_ERR_INVALID_ARG, "stp: elastic kinds need per-element parameters");
+  (void)favg;
+  (void)face_f;
+  return ADERSTP_OK;
+}
+
+}  // namespace
+
+int aderstp_predict_batch(const aderstp_plan* p, int64_t n_elem, const double* q,
+                          const double* par, double dt, double t_start, double* qavg,
+                          double* favg, double* face_q, double* face_f, void* stream) {
+  int rc = validate_batch(p, n_elem, q, par, dt, qavg, favg, face_f);
+  if (rc != ADERSTP_OK) return rc;
+  if (n_elem == 0) return ADERSTP_OK;
+  aderstp::BatchArgs a{q, par, qavg, favg, face_q, face_f, (long long)n_elem, dt, t_start};
+  cudaError_t e = aderstp::launch_stp(p->lp, a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "predict_batch launch");
+  return ADERSTP_OK;
+}
+
+int aderstp_plan_status(aderstp_plan* p, void* stream) {
+  if (!p) return fail(ADERSTP_ERR_INVALID_ARG, "plan_status: null plan");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  unsigned int flags = 0;
+  cudaError_t e = cudaMemcpyAsync(&flags, p->lp.d_status, sizeof flags, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(p->lp.d_status, 0, sizeof flags, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return cuda_fail(e, "plan_status");
+  if (flags & 1u) return fail(ADERSTP_ERR_NONFINITE, "stp: non-finite input DOFs");
+  if (flags & 2u)
+    return fail(ADERSTP_ERR_MATERIAL, "elastic_pde: need rho > 0, mu >= 0, lambda + 2mu > 0");
+  return ADERSTP_OK;
+}
+
+namespace {
+
+struct ChunkLayout {
+  size_t q, par, qavg, favg, face;  // doubles per element
+};
+
+ChunkLayout chunk_layout(const LaunchPlan& lp) {
+  const size_t n3 = (size_t)lp.n * lp.n * lp.n;
+  ChunkLayout c;
+  c.q = n3 * lp.q_stride;
+  c.par = 3;
+  c.qavg = n3 * lp.out_stride;
+  c.favg = 3 * c.qavg;
+  c.face = 6 * (size_t)lp.n * lp.n * lp.m;
+  return c;
+}
+
+}  // namespace
+
+int aderstp_plan_reserve_host_path(aderstp_plan* p, int64_t chunk_elems) {
+  if (!p || chunk_elems <= 0) return fail(ADERSTP_ERR_INVALID_ARG, "reserve_host_path: bad argument");
+  if (p->chunk >= chunk_elems) return ADERSTP_OK;
+  for (int i = 0; i < kHostStreams; ++i) {
+    if (p->buf[i]) cudaFree(p->buf[i]);
+    p->buf[i] = nullptr;
+  }
+  const ChunkLayout c = chunk_layout(p->lp);
+  const size_t per = c.q + c.par + c.qavg + c.favg + 2 * c.face;
+  for (int i = 0; i < kHostStreams; ++i) {
+    cudaError_t e = cudaSuccess;
+    if (!p->streams[i]) e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaMalloc(&p->buf[i], sizeof(double) * per * chunk_elems);
+    if (e != cudaSuccess) {
+      p->chunk = 0;
+      return cuda_fail(e, "reserve_host_path");
+    }
+  }
+  p->chunk = chunk_elems;
+  return ADERSTP_OK;
+}
+
+int aderstp_predict_batch_host(aderstp_plan* p, int64_t n_elem, const double* q,
+                               const double* par, double dt, double t_start, double* qavg,
+                               double* favg, double* face_q, double* face_f) {
+  int rc = validate_batch(p, n_elem, q, par, dt, qavg, favg, face_f);
+  if (rc != ADERSTP_OK) return rc;
+  if (n_elem == 0) return ADERSTP_OK;
+  const ChunkLayout c = chunk_layout(p->lp);
+  if (p->chunk == 0) {
+    // ~256 MiB of device traffic per chunk
+    const size_t per = c.q + c.par + c.qavg + c.favg + 2 * c.face;
+    int64_t ch = (int64_t)((256u << 20) / (per * sizeof(double)));
+    if (ch < 1) ch = 1;
+    rc = aderstp_plan_reserve_host_path(p, ch);
+    if (rc != ADERSTP_OK) return rc;
+  }
+  const int64_t chunk = p->chunk;
+  const bool elastic = p->lp.kind == ADERSTP_PDE_ELASTIC;
+  int64_t done = 0;
+  int slot = 0;
+  cudaError_t e = cudaSuccess;
+  while (done < n_elem && e == cudaSuccess) {
+    const int64_t cnt = (n_elem - done < chunk) ? n_elem - done : chunk;
+    cudaStream_t st = p->streams[slot];
+    double* b = p->buf[slot];
+    double* dq = b;
+    double* dpar = dq + c.q * chunk;
+    double* dqa = dpar + c.par * chunk;
+    double* dfa = dqa + c.qavg * chunk;
+    double* dfq = dfa + c.favg * chunk;
+    double* dff = dfq + c.face * chunk;
+    e = cudaMemcpyAsync(dq, q + done * c.q, sizeof(double) * c.q * cnt, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && elastic)
+      e = cudaMemcpyAsync(dpar, par + done * 3, sizeof(double) * 3 * cnt, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) {
+      aderstp::BatchArgs a{dq, elastic ? dpar : nullptr, dqa, favg ? dfa : nullptr,
+                           face_q ? dfq : nullptr, face_f ? dff : nullptr, (long long)cnt, dt, t_start};
+      e = aderstp::launch_stp(p->lp, a, st);
+    }
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(qavg + done * c.qavg, dqa, sizeof(double) * c.qavg * cnt, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && favg)
+      e = cudaMemcpyAsync(favg + done * c.favg, dfa, sizeof(double) * c.favg * cnt, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && face_q)
+      e = cudaMemcpyAsync(face_q + done * c.face, dfq, sizeof(double) * c.face * cnt, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess && face_f)
+      e = cudaMemcpyAsync(face_f + done * c.face, dff, sizeof(double) * c.face * cnt, cudaMemcpyDeviceToHost, st);
+    done += cnt;
+    slot = (slot + 1) % kHostStreams;
+  }
+  for (int i = 0; i < kHostStreams; ++i) {
+    cudaError_t e2 = cudaStreamSynchronize(p->streams[i]);
+    if (e == cudaSuccess) e = e2;
+  }
+  if (e != cudaSuccess) return cuda_fail(e, "predict_batch_host");
+  return p->lp.check ? aderstp_plan_status(p, p->streams[0]) : ADERSTP_OK;
+}
+
+int aderstp_convert_layout(int order, int quantities, int64_t n_elem, int src_layout,
+                           int src_stride, const double* src, int dst_layout, int dst_stride,
+                           double* dst, void* stream) {
+  if (order < 1 || order > 64 || quantities < 1 || src_stride < quantities || dst_stride < quantities)
+    return fail(ADERSTP_ERR_INVALID_ARG, "convert_layout: bad shape");
+  if ((src_layout != ADERSTP_LAYOUT_AOS && src_layout != ADERSTP_LAYOUT_AOSOA) ||
+      (dst_layout != ADERSTP_LAYOUT_AOS && dst_layout != ADERSTP_LAYOUT_AOSOA))
+    return fail(ADERSTP_ERR_INVALID_ARG, "convert_layout: unknown layout");
+  if (n_elem < 0 || (n_elem > 0 && (!src || !dst)))
+    return fail(ADERSTP_ERR_INVALID_ARG, "convert_layout: bad buffers");
+  if (src == dst && n_elem > 0) return fail(ADERSTP_ERR_INVALID_ARG, "convert_layout: in-place not supported");
+  cudaError_t e = aderstp::launch_convert(order, quantities, n_elem, src_layout, src_stride, src,
+                                          dst_layout, dst_stride, dst, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "convert_layout");
+  return ADERSTP_OK;
+}
+
+int aderstp_generate(int dist, uint64_t seed, int order, int64_t e0, int64_t n_elem, int grid,
+                     int layout, int q_stride, double* q, double* par, void* stream) {
+  if (dist < 0 || dist > 2) return fail(ADERSTP_ERR_INVALID_ARG, "generate: unknown distribution");
+  if (order < 1 || order > aderstp::kMaxOrder || q_stride < 9 || e0 < 0 || n_elem < 0)
+    return fail(ADERSTP_ERR_INVALID_ARG, "generate: bad shape");
+  if (dist == 2 && grid < 1) return fail(ADERSTP_ERR_INVALID_ARG, "generate: grid must be >= 1");
+  HostBasis b;
+  aderstp::make_host_basis(order, &b);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (q && q_stride > 9 && n_elem > 0) {
+    cudaError_t e = cudaMemsetAsync(q, 0, sizeof(double) * (size_t)n_elem * order * order * order * q_stride, st);
+    if (e != cudaSuccess) return cuda_fail(e, "generate");
+  }
+  cudaError_t e = aderstp::launch_generate(dist, seed, order, e0, n_elem, grid, layout, q_stride,
+                                           b, q, par, st);
+  if (e != cudaSuccess) return cuda_fail(e, "generate");
+  return ADERSTP_OK;
+}
+
+}  // extern "C"
