@@ -1,0 +1,393 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 linear ADER-DG Space-Time Predictor (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1..c4]
+
+A "step" is one pass of the STP (CK recursion + favg + 12 face arrays) over one batch of
+synthetic elastic elements.  Default workload (N=1): BASELINE config C3 -- order N=7 (nDof 8),
+131,072 elements per GPU, padded AoSoA input with nVar padded to 12, per-element random
+material.  Under torchrun (N>1) every rank owns a contiguous element range (weak scaling, no
+collective on the hot path; NCCL only reduces the max step time and a checksum).
+
+`value` is device-resident throughput (inputs in HBM, CUDA events, max over ranks);
+`e2e` is the same metric through the public host-buffer API (aderstp_predict_batch_host) with
+pinned host inputs and outputs, copies inside the timed region.  `--impl reference` times the
+reference's own CPU implementation (oracle/_ref, the unmodified reference sources) on the host
+cores over a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "linear STP elements/s & fp64 GFLOP/s (% of roofline) vs order N, 1–8 B200"
+UNIT = "elements/s"
+
+# BASELINE.json configs (order N = polynomial degree, nDof = N+1)
+CONFIGS = {
+    "c1": dict(n=4, elems=64, dist=0, q_stride=9, desc="C1: elastic STP order N=3 (nDof 4), 64 elements, Q~U[-1,1]"),
+    "c2": dict(n=6, elems=32768, dist=2, q_stride=9, desc="C2: elastic STP order N=5 (nDof 6), 32,768 elements "
+               "(32^3 periodic grid), Q = 3 random-phase sinusoids per quantity"),
+    "c3": dict(n=8, elems=131072, dist=0, q_stride=12, desc="C3: elastic STP order N=7 (nDof 8), 131,072 elements/GPU, "
+               "padded AoSoA (nVar padded to 12), Q~U[-1,1], per-element random material"),
+    "c4": dict(n=10, elems=65536, dist=1, q_stride=9, desc="C4: elastic STP order N=9 (nDof 10), 65,536 elements, Q~N(0,1)"),
+}
+SEED = 20031278
+
+
+def fp64_peak():
+    """Measured fp64 peak on this pool's B200 (tools/fp64_peaks.cu, profiles/fp64_peaks_r01.txt):
+    DMMA 37.1 TFLOP/s, DFMA 34.1 TFLOP/s at 1965 MHz.  MEASURED_PEAKS.json has no fp64 entry."""
+    return 37.1e12
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]) * 1e9, "MEASURED_PEAKS.json hbm_gbs"
+    except Exception:
+        return 6.65e12, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, device_index):
+        self.samples, self.reasons, self.ok = [], 0, False
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(device_index).uuid)
+            try:
+                self.h = pynvml.nvmlDeviceGetHandleByUUID("GPU-" + uuid)
+            except Exception:
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.nv = pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.max_mhz = None
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return world, rank, local
+
+
+def allreduce_max(x):
+    import torch
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return x
+
+
+def allreduce_sum(x):
+    import torch
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+    return x
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+def load_traffic(cfg_name):
+    """dram bytes per launch of the STP kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(cfg_name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
+    """Device-resident timing of one config; returns a dict of per-rank-max numbers."""
+    import torch
+    n, E = cfg["n"], cfg["elems"]
+    grid = round(E ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
+    e0 = rank * E
+    q, par = S.generate(cfg["dist"], SEED, n, e0, E, grid=grid, layout=S.LAYOUT_AOSOA, q_stride=cfg["q_stride"])
+    cp_max = allreduce_max(float(par[:, 1].max().item()))
+    dt = S.stable_dt(n, cp_max, cfl=0.5)
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=cfg["q_stride"], out_stride=9,
+                  par_kind=S.PAR_RHO_CP_CS, check_inputs=True)
+    out = plan.alloc_output(E)
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        plan.predict(q, dt, par=par, out=out)
+    plan.status()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(torch.cuda.current_device()) if want_clocks else None
+    barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__enter__()
+    ev0.record(stream)
+    for _ in range(steps):
+        plan.predict(q, dt, par=par, out=out)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    barrier()
+    ms = ev0.elapsed_time(ev1) / steps
+    plan.status()
+    checksum = float(out.qavg.sum().item()) + float(out.face_q.sum().item())
+    ms_max = allreduce_max(ms)
+    checksum = allreduce_sum(checksum)
+    return dict(ms=ms_max, dt=dt, checksum=checksum, clocks=sampler.summary() if sampler else None,
+                plan=plan, q=q, par=par, out=out)
+
+
+def measure_e2e(S, plan, cfg, world, rank, dt, steps):
+    """Same metric through the host-buffer public API, pinned host memory, copies timed."""
+    import torch
+    n, E = cfg["n"], cfg["elems"]
+    grid = round(E ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
+    q_d, par_d = S.generate(cfg["dist"], SEED, n, rank * E, E, grid=grid, layout=S.LAYOUT_AOSOA,
+                            q_stride=cfg["q_stride"])
+    pin = lambda *shape: torch.empty(*shape, dtype=torch.float64, pin_memory=True)  # noqa: E731
+    q_h = pin(E, plan.q_size)
+    par_h = pin(E, 3)
+    q_h.copy_(q_d)
+    par_h.copy_(par_d)
+    del q_d, par_d
+    out_h = S.PredictorOutput(pin(E, plan.out_size).numpy(), pin(E, 3, plan.out_size).numpy(),
+                              pin(E, 6, plan.face_size).numpy(), pin(E, 6, plan.face_size).numpy())
+    qn, pn = q_h.numpy(), par_h.numpy()
+    plan.predict_host(qn, dt, par=pn, out=out_h)  # warm-up (allocates the plan's chunk buffers)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        plan.predict_host(qn, dt, par=pn, out=out_h)
+    sec = (time.perf_counter() - t0) / steps
+    barrier()
+    sec = allreduce_max(sec)
+    h2d = E * (plan.q_size + 3) * 8
+    d2h = E * (plan.out_size * 4 + plan.face_size * 12) * 8
+    return dict(value=world * E / sec, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h,
+                ms_per_step=sec * 1e3, steps=steps, api="aderstp_predict_batch_host (pinned host buffers)")
+
+
+def cpu_reference_run(cfg, sample, reps=3, threads=None):
+    """The reference's own CPU path (oracle/_ref) on `sample` elements; best of reps, faster of
+    splitck / splitck_aosoa.  Falls back to our C port when _ref is absent."""
+    import numpy as np
+    import oracle as O
+    n = cfg["n"]
+    orc = O.Oracle()
+    grid = round(cfg["elems"] ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
+    q, par = orc.generate(cfg["dist"], SEED, n, 0, sample, grid=grid)
+    lmr = orc.material_lmr(par)
+    dt = O.cfl_dt(n, 6.0)
+    threads = threads or (os.cpu_count() or 1)
+    best = math.inf
+    variant_used = None
+    if O.reference_available():
+        ref = O.Reference()
+        kind = "reference"
+        for variant in ("splitck", "aosoa"):
+            for _ in range(reps):
+                r = ref.stp(n, 9, q, dt, par=lmr, variant=variant, threads=threads)
+                if r.seconds < best:
+                    best, variant_used = r.seconds, variant
+        lib = os.path.basename(ref.path)
+    else:
+        kind = "port"
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            orc.stp(n, 9, q, dt, par=lmr, threads=threads)
+            best = min(best, time.perf_counter() - t0)
+        variant_used, lib = "oracle/stp_oracle.c", "libstp_oracle.so"
+    del np
+    return dict(value=sample / best, unit=UNIT, cores=threads, kind=kind,
+                sample=f"{sample} elements of {cfg['desc'].split(':')[0]}, best of {reps} reps, "
+                       f"variant {variant_used} ({lib}), {threads} threads")
+
+
+def run_reference_arm(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    sample = {"c1": 64, "c2": 8192, "c3": 4096, "c4": 1024}[args.config]
+    values = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        info = cpu_reference_run(cfg, sample, reps=1)
+        if i >= args.warmup:
+            values.append(info["value"])
+    value = statistics.median(values)
+    info["value"] = value
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sample / value * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded SplitMix64, same generator as our arm)",
+            "config": {"workload": cfg["desc"], "n_dof": cfg["n"], "order": cfg["n"] - 1,
+                       "elements_per_step": sample},
+            "cpu_baseline": info,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference_arm(args)
+
+    import torch
+    import paper_2003_12787_b200 as S
+
+    world, rank, local = dist_setup(args)
+    cfg = CONFIGS[args.config]
+    n, E = cfg["n"], cfg["elems"]
+    res = measure_device(S, cfg, world, rank, args.steps, args.warmup)
+    ms = res["ms"]
+    value = world * E / (ms * 1e-3)
+    flop_e = S.flop_count(n, 9)
+    byte_e = S.byte_count(n, 9, True)
+    per_gpu = E / (ms * 1e-3)
+    fp64 = fp64_peak()
+    hbm, hbm_src = hbm_peak()
+    achieved_tf = per_gpu * flop_e / 1e12
+    achieved_gbs = per_gpu * byte_e / 1e9
+    roof_elem = min(fp64 / flop_e, hbm / byte_e)
+    bound = "fp64" if fp64 / flop_e < hbm / byte_e else "hbm"
+    traffic = load_traffic(args.config)
+    if bound == "fp64":
+        roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": fp64 / 1e12, "unit": "TFLOP/s",
+                    "frac": achieved_tf / (fp64 / 1e12), "traffic": traffic,
+                    "peak_source": "measured DMMA fp64 peak, profiles/fp64_peaks_r01.txt (not in MEASURED_PEAKS.json)",
+                    "flop_per_element": flop_e, "byte_per_element": byte_e,
+                    "hbm_achieved_gbs": achieved_gbs, "hbm_frac": achieved_gbs / (hbm / 1e9),
+                    "roofline_elements_per_s": roof_elem, "elements_per_launch": E}
+    else:
+        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm / 1e9, "unit": "GB/s",
+                    "frac": achieved_gbs / (hbm / 1e9), "traffic": traffic, "peak_source": hbm_src,
+                    "flop_per_element": flop_e, "byte_per_element": byte_e,
+                    "fp64_achieved_tflops": achieved_tf, "fp64_frac": achieved_tf / (fp64 / 1e12),
+                    "roofline_elements_per_s": roof_elem, "elements_per_launch": E}
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = measure_e2e(S, res["plan"], cfg, world, rank, res["dt"], args.e2e_steps)
+
+    others = {}
+    if not args.no_other_configs and world == 1:
+        for name in ("c1", "c2", "c4"):
+            if name == args.config:
+                continue
+            c = CONFIGS[name]
+            r = measure_device(S, c, world, rank, max(5, args.steps // 4), 3, want_clocks=False)
+            pg = c["elems"] / (r["ms"] * 1e-3)
+            fe, be = S.flop_count(c["n"], 9), S.byte_count(c["n"], 9, True)
+            roof = min(fp64 / fe, hbm / be)
+            others[name] = {"workload": c["desc"], "elements_per_s": pg, "ms_per_step": r["ms"],
+                            "fp64_gflops": pg * fe / 1e9, "achieved_gbs": pg * be / 1e9,
+                            "roofline_elements_per_s": roof, "frac_of_roofline": pg / roof,
+                            "bound": "fp64" if fp64 / fe < hbm / be else "hbm"}
+            del r
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_reference_run(cfg, 16384 if n <= 8 else 4096)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded SplitMix64 stream, generated on device; per-element rho~U[2,3], "
+                        "cp~U[4,6], cs~U[2,3.5])",
+                "config": {"workload": cfg["desc"], "order": n - 1, "n_dof": n, "elements_per_gpu": E,
+                           "global_elements": world * E, "parallelism": f"element shards x{world} (no hot-path collective)",
+                           "layout": f"AoSoA [e][k3][k2][s<{cfg['q_stride']}][k1] in, [e][k3][k2][9][k1] out",
+                           "dt": res["dt"], "cfl": 0.5,
+                           "l2": "no flush needed: inputs %.1f GB and outputs %.1f GB per step >> 126 MB L2" % (
+                               E * n ** 3 * cfg["q_stride"] * 8 / 1e9, E * (4 * n ** 3 * 9 + 12 * n * n * 9) * 8 / 1e9)},
+                "fp64_gflops_per_gpu": achieved_tf * 1e3,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+                "clocks": res["clocks"], "checksum": res["checksum"], "other_configs": others}
+        print(json.dumps(line), flush=True)
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -38,6 +38,7 @@ struct LaunchPlan {
   double src_amp = 0, src_center = 0, src_width = 1;
   double src_proj[3][kMaxOrder];
   unsigned int* d_status = nullptr;  // device word: bit0 non-finite q, bit1 bad material
+  int force_generic = 0;             // env ADERSTP_FORCE_GENERIC=1: skip specialised kernels
 };
 
 struct BatchArgs {
@@ -61,5 +62,9 @@ cudaError_t launch_generate(int dist, uint64_t seed, int n, long long e0, long l
                             int grid, int layout, int q_stride, const HostBasis& basis,
                             double* q, double* par, cudaStream_t stream);
 bool kernel_available(int n);
+// stp_dmma8.cu: nDof = 8 elastic kernel on the fp64 tensor cores
+bool dmma8_applicable(const LaunchPlan& p);
+cudaError_t init_dmma8(const LaunchPlan& p);  // once per device, at plan creation
+cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 
 }  // namespace aderstp

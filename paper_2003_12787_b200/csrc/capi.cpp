@@ -3,6 +3,7 @@
 // reference's LinearPde factories (proj/src/pde.cpp), and the pipelined host-buffer path.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -152,6 +153,10 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   lp.out_stride = os;
   lp.par_kind = cfg->par_kind;
   lp.check = cfg->check_inputs ? 1 : 0;
+  {
+    const char* env = std::getenv("ADERSTP_FORCE_GENERIC");
+    lp.force_generic = (env && env[0] == '1') ? 1 : 0;
+  }
   aderstp::make_host_basis(n, &lp.basis);
 
   // PDE terms (proj/src/pde.cpp): advection :61-85, ncp-advection :87-117, demo :119-146
@@ -228,6 +233,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   cudaError_t e = cudaGetDevice(&p->device);
   if (e == cudaSuccess) e = cudaMalloc(&lp.d_status, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(lp.d_status, 0, sizeof(unsigned int));
+  if (e == cudaSuccess && aderstp::dmma8_applicable(lp)) e = aderstp::init_dmma8(lp);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "plan_create");

@@ -55,3 +55,22 @@ def test_elastic_parity(stp, oracle, n):
     ref = oracle.stp(n, 9, qc, dt, par=oracle.material_lmr(par_h))
     worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, 9)
     assert max(worst.values()) <= TOL, worst
+
+
+@pytest.mark.parametrize("force_generic", [False, True])
+@pytest.mark.parametrize("q_stride", [9, 12])
+def test_order8_kernels_parity(stp, oracle, monkeypatch, force_generic, q_stride):
+    """nDof 8 runs on the DMMA kernel by default; ADERSTP_FORCE_GENERIC=1 selects the generic one."""
+    S = stp
+    monkeypatch.setenv("ADERSTP_FORCE_GENERIC", "1" if force_generic else "0")
+    n, E = 8, 301
+    q, par = S.generate(0, 77, n, 1000, E, layout=S.LAYOUT_AOSOA, q_stride=q_stride)
+    par_h = par.cpu().numpy()
+    dt = O.cfl_dt(n, par_h[:, 1].max())
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=q_stride, par_kind=S.PAR_RHO_CP_CS)
+    out = plan.predict(q, dt, par=par)
+    plan.status()
+    qc = oracle.from_aosoa(n, 9, q_stride, q.cpu().numpy())
+    ref = oracle.stp(n, 9, qc, dt, par=oracle.material_lmr(par_h))
+    worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, 9)
+    assert max(worst.values()) <= TOL, worst
