@@ -32,7 +32,7 @@ constexpr int NV = 9;
 constexpr int THREADS8 = NV * 32;
 constexpr int PV = N8 * N8 * N8;           // doubles per quantity plane
 constexpr int FACE = N8 * N8 * NV;         // doubles per face array (576)
-constexpr int SMEM8 = (NV * PV + 2 * 6 * FACE) * 8;  // p + face_q + face_f staging = 92,160 B
+constexpr int SMEM8 = 2 * NV * PV * 8;  // p + qavg accumulator = 73,728 B (face staging reuses p)
 
 struct Params8 {
   double d[64];      // d[k*8+l] = phi_l'(x_k)
@@ -107,18 +107,19 @@ __device__ __forceinline__ double2 ld_nc2(const double* p) {
   return v;
 }
 
-__global__ void __maxnreg__(112)
+__global__ void __maxnreg__(80)
 stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   extern __shared__ __align__(16) double sm8[];
-  double* P = sm8;                 // [9][8][8][8] swizzled
-  double* FQ = sm8 + NV * PV;      // [6][8][8][9] face_q staging (reference order)
-  double* FF = FQ + 6 * FACE;      // [6][8][8][9] face_f staging
+  double* P = sm8;             // [9][8][8][8] swizzled: current iterate p
+  double* QA = sm8 + NV * PV;  // [9][8][8][8] swizzled: qavg accumulator
+  double* FQ = P;              // epilogue: face_q staging [6][8][8][9] reuses p
   const long long e = blockIdx.x;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int s = kWarpVar[warp];
   unsigned int flags = 0;
+  const double dt = a.dt;
 
   // ---- material (proj/src/pde.cpp:171-178) -------------------------------------------
   double c4[4];
@@ -141,20 +142,22 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     c4[3] = 1.0 / rho;
   }
 
-  // ---- stage q: AoSoA [k3][k2][s < QS][k1] -> P[s][k3][swizzled k2,k1] ----------------
+  // ---- stage q: AoSoA [k3][k2][s < QS][k1] -> P and QA = dt q -------------------------
   {
     const int qs = kp.q_stride;
     const double* qe = a.q + e * (long long)(PV * qs);
     const int pairs = 64 * qs * 4;
+#pragma unroll 1
     for (int i = tid; i < pairs; i += THREADS8) {
-      const int kp2 = i & 3;
       const int row = i >> 2;  // (k3*8 + k2)*qs + s
       const int si = row % qs;
       if (si >= NV) continue;
       const int k32 = row / qs;
       const double2 v = ld_nc2(qe + 2 * i);
       if (kp.check && !(isfinite(v.x) && isfinite(v.y))) flags |= 1u;
-      *reinterpret_cast<double2*>(P + si * PV + (k32 >> 3) * 64 + phys(k32 & 7, 2 * kp2)) = v;
+      const int j = si * PV + (k32 >> 3) * 64 + phys(k32 & 7, 2 * (i & 3));
+      *reinterpret_cast<double2*>(P + j) = v;
+      *reinterpret_cast<double2*>(QA + j) = make_double2(dt * v.x, dt * v.y);
     }
   }
   __syncthreads();
@@ -166,15 +169,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];  // D[g][kh*4 + t]
   const double bx0 = cx * d0, bx1 = cx * d1;                     // B-fragments of c_x D^T
   const double ay0 = cy * d0, ay1 = cy * d1;                     // A-fragments of c_y D
-  const double dt = a.dt;
-
-  double qa[8][2];
-#pragma unroll
-  for (int k3 = 0; k3 < 8; ++k3) {
-    const double2 v = *reinterpret_cast<const double2*>(P + s * PV + k3 * 64 + phys(g, 2 * t));
-    qa[k3][0] = dt * v.x;
-    qa[k3][1] = dt * v.y;
-  }
+  const int own = s * PV + phys(g, 2 * t);                       // + k3*64: this lane's node pair
 
   // ---- Cauchy-Kowalewsky recursion (proj/src/stp_splitck.cpp:46-70) -------------------
   double coeff = dt;
@@ -184,7 +179,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
 #pragma unroll
     for (int k3 = 0; k3 < 8; ++k3) tt[k3][0] = tt[k3][1] = 0.0;
     if (has_x) {
-      const double* px = P + in_x * PV + phys(g, t);  // + k3*64 ; k1 = t (+4 via swizzle below)
+      const double* px = P + in_x * PV + phys(g, t);
       const double* px1 = P + in_x * PV + phys(g, 4 + t);
 #pragma unroll
       for (int k3 = 0; k3 < 8; ++k3) {
@@ -204,67 +199,79 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     if (has_z) {
       const double* pz = P + in_z * PV + phys(g, 2 * t);
 #pragma unroll
-      for (int lh = 0; lh < 2; ++lh) {
-        double c0[4], c1[4];
+      for (int lq = 0; lq < 4; ++lq) {
+        double c0[2], c1[2];
 #pragma unroll
-        for (int l = 0; l < 4; ++l) {
-          const double2 v = *reinterpret_cast<const double2*>(pz + (lh * 4 + l) * 64);
+        for (int l = 0; l < 2; ++l) {
+          const double2 v = *reinterpret_cast<const double2*>(pz + (lq * 2 + l) * 64);
           c0[l] = cz * v.x;
           c1[l] = cz * v.y;
         }
 #pragma unroll
         for (int k3 = 0; k3 < 8; ++k3) {
-          const double2 da = ldc2(&aderstp_kD8[k3 * 8 + lh * 4]);
-          const double2 db = ldc2(&aderstp_kD8[k3 * 8 + lh * 4 + 2]);
-          const double dk[4] = {da.x, da.y, db.x, db.y};
-#pragma unroll
-          for (int l = 0; l < 4; ++l) {
-            tt[k3][0] = fma(dk[l], c0[l], tt[k3][0]);
-            tt[k3][1] = fma(dk[l], c1[l], tt[k3][1]);
-          }
+          const double2 dk = ldc2(&aderstp_kD8[k3 * 8 + lq * 2]);
+          tt[k3][0] = fma(dk.x, c0[0], tt[k3][0]);
+          tt[k3][1] = fma(dk.x, c1[0], tt[k3][1]);
+          tt[k3][0] = fma(dk.y, c0[1], tt[k3][0]);
+          tt[k3][1] = fma(dk.y, c1[1], tt[k3][1]);
         }
       }
     }
     coeff *= dt / (o + 1);  // dt^(o+1)/(o+1)!
 #pragma unroll
-    for (int k3 = 0; k3 < 8; ++k3) {
-      qa[k3][0] = fma(coeff, tt[k3][0], qa[k3][0]);
-      qa[k3][1] = fma(coeff, tt[k3][1], qa[k3][1]);
+    for (int k3 = 0; k3 < 8; ++k3) {  // qavg += c_o t on this lane's own nodes (no race)
+      double2* q = reinterpret_cast<double2*>(QA + own + k3 * 64);
+      const double2 v = *q;
+      *q = make_double2(fma(coeff, tt[k3][0], v.x), fma(coeff, tt[k3][1], v.y));
     }
-    __syncthreads();  // every warp has finished reading p
     if (o + 1 < N8) {
+      __syncthreads();  // every warp has finished reading p
 #pragma unroll
       for (int k3 = 0; k3 < 8; ++k3)
-        *reinterpret_cast<double2*>(P + s * PV + k3 * 64 + phys(g, 2 * t)) = make_double2(tt[k3][0], tt[k3][1]);
-      __syncthreads();
+        *reinterpret_cast<double2*>(P + own + k3 * 64) = make_double2(tt[k3][0], tt[k3][1]);
     }
+    __syncthreads();
   }
 
   // ---- epilogue ------------------------------------------------------------------------
-  // qavg -> shared (for the face contractions) and -> global straight from registers
-  double* qout = a.qavg + e * (long long)(PV * NV);
+  double qa[8][2];
 #pragma unroll
   for (int k3 = 0; k3 < 8; ++k3) {
-    *reinterpret_cast<double2*>(P + s * PV + k3 * 64 + phys(g, 2 * t)) = make_double2(qa[k3][0], qa[k3][1]);
-    st_cs2(qout + ((k3 * 8 + g) * NV + s) * 8 + 2 * t, qa[k3][0], qa[k3][1]);
+    const double2 v = *reinterpret_cast<const double2*>(QA + own + k3 * 64);
+    qa[k3][0] = v.x;
+    qa[k3][1] = v.y;
+  }
+  // qavg straight from registers, AoSoA [k3][k2][s][k1]
+  {
+    double* qout = a.qavg + e * (long long)(PV * NV) + s * 8 + 2 * t;
+#pragma unroll
+    for (int k3 = 0; k3 < 8; ++k3) st_cs2(qout + (k3 * 8 + g) * NV * 8, qa[k3][0], qa[k3][1]);
   }
   // favg_d[s'] = coef * qavg[s] for every flux entry fed by this warp's quantity
   if (a.favg) {
-    double* fout = a.favg + e * (long long)(3 * PV * NV);
+    double* fout = a.favg + e * (long long)(3 * PV * NV) + 2 * t;
     const int nout = kOutN[s];
+#pragma unroll 1
     for (int k = 0; k < nout; ++k) {
       const int so = kOut[s][k][0], d = kOut[s][k][1];
       const double c = sel4(c4, kOut[s][k][2]);
-      double* base = fout + d * (PV * NV) + so * 8 + 2 * t;
+      double* base = fout + d * (PV * NV) + so * 8;
 #pragma unroll
       for (int k3 = 0; k3 < 8; ++k3) st_cs2(base + (k3 * 8 + g) * NV * 8, c * qa[k3][0], c * qa[k3][1]);
     }
   }
-  __syncthreads();  // P now holds qavg
-
   if (a.face_q || a.face_f) {
     // z normal (faces 4, 5): register-local columns, (a, b) = (k2, k1)
-    double zf[2][2];
+    // x normal (faces 0, 1): C[k2][side] = sum_l Q[k3][k2][l] phi[side][l]  (B = padded phi^T)
+    // y normal (faces 2, 3): C[side][k1] = sum_l phi[side][l] Q[k3][l][k1]  (A = padded phi)
+    const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0;
+    const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
+    const double* qx = QA + s * PV + phys(g, t);
+    const double* qx1 = QA + s * PV + phys(g, 4 + t);
+    const double* qy = QA + s * PV + phys(t, g);
+    const double* qy1 = QA + s * PV + phys(4 + t, g);
+    // the last CK step's write-back was skipped, but p is still being read by no one after the
+    // final barrier: reuse it as the face staging area [f][a][b][s]
 #pragma unroll
     for (int sd = 0; sd < 2; ++sd)
 #pragma unroll
@@ -272,56 +279,29 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
         double acc = 0.0;
 #pragma unroll
         for (int k3 = 0; k3 < 8; ++k3) acc = fma(kp.phi[sd][k3], qa[k3][j], acc);
-        zf[sd][j] = acc;
+        FQ[(4 + sd) * FACE + (g * 8 + 2 * t + j) * NV + s] = acc;
       }
-    // x normal (faces 0, 1): C[k2][side] = sum_l P[k3][k2][l] * phi[side][l]; B = padded phi^T
-    // y normal (faces 2, 3): C[side][k1] = sum_l phi[side][l] * P[k3][l][k1]; A = padded phi
-    const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0;
-    const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
-    const double* px = P + s * PV + phys(g, t);
-    const double* px1 = P + s * PV + phys(g, 4 + t);
-    const double* py = P + s * PV + phys(t, g);
-    const double* py1 = P + s * PV + phys(4 + t, g);
-    double xf[8][2], yf[8][2];
-#pragma unroll
+#pragma unroll 2
     for (int k3 = 0; k3 < 8; ++k3) {
-      xf[k3][0] = xf[k3][1] = yf[k3][0] = yf[k3][1] = 0.0;
-      dmma(xf[k3][0], xf[k3][1], px[k3 * 64], bphi0);
-      dmma(xf[k3][0], xf[k3][1], px1[k3 * 64], bphi1);
-      dmma(yf[k3][0], yf[k3][1], bphi0, py[k3 * 64]);
-      dmma(yf[k3][0], yf[k3][1], bphi1, py1[k3 * 64]);
-    }
-    // stage face_q and this quantity's face_f contributions in the reference face layout
-    // [f][a][b][s] (a, b = the in-face dims in (z,y,x) order)
-    const int nout = kOutN[s];
-    auto put = [&](int f, int ab, double v) {
-      FQ[f * FACE + ab * NV + s] = v;
-      const int d = f >> 1;
-      for (int k = 0; k < nout; ++k)
-        if (kOut[s][k][1] == d) FF[f * FACE + ab * NV + kOut[s][k][0]] = sel4(c4, kOut[s][k][2]) * v;
-    };
-#pragma unroll
-    for (int sd = 0; sd < 2; ++sd)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) put(4 + sd, g * 8 + 2 * t + j, zf[sd][j]);
-    if (t == 0) {  // x faces: lane (g, 0) holds C[k2 = g][side 0, 1] for every k3
-#pragma unroll
-      for (int k3 = 0; k3 < 8; ++k3) {
-        put(0, k3 * 8 + g, xf[k3][0]);
-        put(1, k3 * 8 + g, xf[k3][1]);
+      double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+      dmma(x0, x1, qx[k3 * 64], bphi0);
+      dmma(x0, x1, qx1[k3 * 64], bphi1);
+      dmma(y0, y1, bphi0, qy[k3 * 64]);
+      dmma(y0, y1, bphi1, qy1[k3 * 64]);
+      if (t == 0) {  // lane (g, 0) holds C[k2 = g][side 0, 1]
+        FQ[0 * FACE + (k3 * 8 + g) * NV + s] = x0;
+        FQ[1 * FACE + (k3 * 8 + g) * NV + s] = x1;
       }
-    }
-    if (g < 2) {  // y faces: lane (side = g, t) holds C[side][k1 = 2t, 2t+1] for every k3
-#pragma unroll
-      for (int k3 = 0; k3 < 8; ++k3) {
-        put(2 + g, k3 * 8 + 2 * t, yf[k3][0]);
-        put(2 + g, k3 * 8 + 2 * t + 1, yf[k3][1]);
+      if (g < 2) {  // lane (side = g, t) holds C[side][k1 = 2t, 2t+1]
+        FQ[(2 + g) * FACE + (k3 * 8 + 2 * t) * NV + s] = y0;
+        FQ[(2 + g) * FACE + (k3 * 8 + 2 * t + 1) * NV + s] = y1;
       }
     }
     __syncthreads();
-    // coalesced copy-out of the staged faces (6 * 576 doubles each, contiguous per element)
+    // coalesced copy-out; face_f[f][ab][s] = coef(s, d) * face_q[f][ab][in(s, d)] (linearity)
     if (a.face_q) {
       double* o = a.face_q + e * (long long)(6 * FACE);
+#pragma unroll 1
       for (int i = tid; i < 3 * FACE; i += THREADS8) {
         const double2 v = *reinterpret_cast<const double2*>(FQ + 2 * i);
         st_cs2(o + 2 * i, v.x, v.y);
@@ -329,9 +309,19 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     }
     if (a.face_f) {
       double* o = a.face_f + e * (long long)(6 * FACE);
+#pragma unroll 1
       for (int i = tid; i < 3 * FACE; i += THREADS8) {
-        const double2 v = *reinterpret_cast<const double2*>(FF + 2 * i);
-        st_cs2(o + 2 * i, v.x, v.y);
+        double v[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int idx = 2 * i + h;
+          const int f = idx / FACE;
+          const int rem = idx - f * FACE;
+          const int so = rem % NV;
+          const int d = f >> 1;
+          v[h] = sel4(c4, kCoef[so][d]) * FQ[idx - so + kIn[so][d]];
+        }
+        st_cs2(o + 2 * i, v[0], v[1]);
       }
     }
   }
@@ -360,6 +350,9 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
   cudaError_t err = cudaFuncSetAttribute(stp_dmma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM8);
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(stp_dmma8_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
   if (err != cudaSuccess) return err;
   if (a.n_elem == 0) return cudaSuccess;
   if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
