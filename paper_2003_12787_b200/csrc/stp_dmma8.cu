@@ -32,7 +32,7 @@ constexpr int NV = 9;
 constexpr int THREADS8 = NV * 32;
 constexpr int PV = N8 * N8 * N8;           // doubles per quantity plane
 constexpr int FACE = N8 * N8 * NV;         // doubles per face array (576)
-constexpr int SMEM8 = 2 * NV * PV * 8;  // p + qavg accumulator = 73,728 B (face staging reuses p)
+constexpr int SMEM8 = 3 * NV * PV * 8;  // p, p_next, qavg accumulator = 110,592 B (face staging reuses p)
 
 struct Params8 {
   double d[64];      // d[k*8+l] = phi_l'(x_k)
@@ -110,9 +110,10 @@ __device__ __forceinline__ double2 ld_nc2(const double* p) {
 __global__ void __maxnreg__(80)
 stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   extern __shared__ __align__(16) double sm8[];
-  double* P = sm8;             // [9][8][8][8] swizzled: current iterate p
-  double* QA = sm8 + NV * PV;  // [9][8][8][8] swizzled: qavg accumulator
-  double* FQ = P;              // epilogue: face_q staging [6][8][8][9] reuses p
+  double* P = sm8;                  // [9][8][8][8] swizzled: current iterate p
+  double* PN = sm8 + NV * PV;       // next iterate (double buffer: one barrier per CK step)
+  double* QA = sm8 + 2 * NV * PV;   // [9][8][8][8] swizzled: qavg accumulator
+  double* FQ = sm8;                 // epilogue: face_q staging [6][8][8][9] reuses the p buffers
   const long long e = blockIdx.x;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -143,21 +144,25 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   }
 
   // ---- stage q: AoSoA [k3][k2][s < QS][k1] -> P and QA = dt q -------------------------
+  // 64 rows (k3,k2) x 9 quantities x 4 k1-pairs = 2304 pairs = 8 per thread; all loads are
+  // issued before the first shared store so their latencies overlap.
   {
-    const int qs = kp.q_stride;
-    const double* qe = a.q + e * (long long)(PV * qs);
-    const int pairs = 64 * qs * 4;
-#pragma unroll 1
-    for (int i = tid; i < pairs; i += THREADS8) {
-      const int row = i >> 2;  // (k3*8 + k2)*qs + s
-      const int si = row % qs;
-      if (si >= NV) continue;
-      const int k32 = row / qs;
-      const double2 v = ld_nc2(qe + 2 * i);
-      if (kp.check && !(isfinite(v.x) && isfinite(v.y))) flags |= 1u;
+    const double* qe = a.q + e * (long long)(PV * kp.q_stride);
+    double2 v[8];
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int i = tid + it * THREADS8;
+      const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
+      v[it] = ld_nc2(qe + (k32 * kp.q_stride + si) * 8 + 2 * (i & 3));
+    }
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int i = tid + it * THREADS8;
+      const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
+      if (kp.check && !(isfinite(v[it].x) && isfinite(v[it].y))) flags |= 1u;
       const int j = si * PV + (k32 >> 3) * 64 + phys(k32 & 7, 2 * (i & 3));
-      *reinterpret_cast<double2*>(P + j) = v;
-      *reinterpret_cast<double2*>(QA + j) = make_double2(dt * v.x, dt * v.y);
+      *reinterpret_cast<double2*>(P + j) = v[it];
+      *reinterpret_cast<double2*>(QA + j) = make_double2(dt * v[it].x, dt * v[it].y);
     }
   }
   __syncthreads();
@@ -225,12 +230,14 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
       *q = make_double2(fma(coeff, tt[k3][0], v.x), fma(coeff, tt[k3][1], v.y));
     }
     if (o + 1 < N8) {
-      __syncthreads();  // every warp has finished reading p
 #pragma unroll
       for (int k3 = 0; k3 < 8; ++k3)
-        *reinterpret_cast<double2*>(P + own + k3 * 64) = make_double2(tt[k3][0], tt[k3][1]);
+        *reinterpret_cast<double2*>(PN + own + k3 * 64) = make_double2(tt[k3][0], tt[k3][1]);
     }
-    __syncthreads();
+    __syncthreads();  // p_next complete; every warp has finished reading p
+    double* sw = P;
+    P = PN;
+    PN = sw;
   }
 
   // ---- epilogue ------------------------------------------------------------------------
@@ -298,31 +305,24 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
       }
     }
     __syncthreads();
-    // coalesced copy-out; face_f[f][ab][s] = coef(s, d) * face_q[f][ab][in(s, d)] (linearity)
-    if (a.face_q) {
-      double* o = a.face_q + e * (long long)(6 * FACE);
-#pragma unroll 1
-      for (int i = tid; i < 3 * FACE; i += THREADS8) {
-        const double2 v = *reinterpret_cast<const double2*>(FQ + 2 * i);
-        st_cs2(o + 2 * i, v.x, v.y);
-      }
-    }
-    if (a.face_f) {
-      double* o = a.face_f + e * (long long)(6 * FACE);
-#pragma unroll 1
-      for (int i = tid; i < 3 * FACE; i += THREADS8) {
-        double v[2];
+    // coalesced copy-out.  288 threads = 32 in-face nodes x 9 quantities, so thread tid always
+    // handles quantity so = tid % 9: face_f[f][ab][so] = coef(so, d) * face_q[f][ab][in(so, d)]
+    // (flux linearity), with the coefficients hoisted out of the loop.
+    const int so = tid % NV, ab0 = tid / NV;
+    double* oq = a.face_q ? a.face_q + e * (long long)(6 * FACE) : nullptr;
+    double* of = a.face_f ? a.face_f + e * (long long)(6 * FACE) : nullptr;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const double c = sel4(c4, kCoef[so][d]);
+      const int src = kIn[so][d];
+#pragma unroll
+      for (int sd = 0; sd < 2; ++sd)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int idx = 2 * i + h;
-          const int f = idx / FACE;
-          const int rem = idx - f * FACE;
-          const int so = rem % NV;
-          const int d = f >> 1;
-          v[h] = sel4(c4, kCoef[so][d]) * FQ[idx - so + kIn[so][d]];
+          const int base = (2 * d + sd) * FACE + (ab0 + 32 * h) * NV;
+          if (oq) __stcs(oq + base + so, FQ[base + so]);
+          if (of) __stcs(of + base + so, c * FQ[base + src]);
         }
-        st_cs2(o + 2 * i, v[0], v[1]);
-      }
     }
   }
   if (kp.check && flags) atomicOr(status, flags);
