@@ -39,6 +39,7 @@ struct LaunchPlan {
   double src_proj[3][kMaxOrder];
   unsigned int* d_status = nullptr;  // device word: bit0 non-finite q, bit1 bad material
   int force_generic = 0;             // env ADERSTP_FORCE_GENERIC=1: skip specialised kernels
+  int dmma8_double_buffer = 0;       // env ADERSTP_DMMA8_DB=1: 2 CTAs/SM double-buffered variant
 };
 
 struct BatchArgs {

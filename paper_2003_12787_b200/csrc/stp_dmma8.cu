@@ -1,71 +1,31 @@
 // nDof = 8 elastic STP kernel on the fp64 tensor cores (sm_100a DMMA, mma.sync m8n8k4 f64).
 //
-// One CTA = one element, 9 warps, warp w owns output quantity kWarpVar[w] for ALL nodes.
-// Lane (g = lane/4, t = lane%4) owns the two z-columns (k2 = g, k1 = 2t, 2t+1): 16 nodes.
-// That is exactly the C-fragment of an 8x8 MMA tile C[k2][k1] at fixed k3, so
-//   x-contraction  C[k2][k1] += sum_l P[k3][k2][l] * (c D)[k1][l]   A = p slice, B = c*D^T
-//   y-contraction  C[k2][k1] += sum_l (c D)[k2][l] * P[k3][l][k1]   A = c*D,     B = p slice
-// run as DMMA (16 per field: 8 k3-tiles x 2 k-halves) accumulating straight into the thread's
-// t registers, and the z-contraction is register-local DFMA on the thread's own columns with D
-// as constant-bank operands:  t[k3] += sum_l D[k3][l] * (c p[l]).
-// Flux-first exactly as the reference: t_s = sum_d D_d * F_d(p)_s with the elastic flux
-// F_d(p)_s = c(s,d) p_in(s,d) (proj/src/pde.cpp:180-218, proj/src/stp_splitck.cpp:53-55).
+// One CTA = one element, 8 warps.  Lane (g = lane/4, t = lane%4) of a warp owns node pairs
+// (k2 = g, k1 = 2t, 2t+1) -- exactly the C-fragment of an 8x8 MMA tile C[k2][k1] at fixed k3 --
+// so the three 1-D contractions of a CK step are
+//   x:  C[k2][k1] += sum_l P[k3][k2][l] (cD)[k1][l]    DMMA, A = p slice (smem), B = c D^T
+//   y:  C[k2][k1] += sum_l (cD)[k2][l] P[k3][l][k1]    DMMA, A = c D,            B = p slice
+//   z:  C[k3]     += sum_l D[k3][l] (c p)[l]            DFMA on the lane's own columns, D from
+//                                                        the constant cache
+// all accumulating into the same registers.  The elastic system (proj/src/pde.cpp:180-218)
+// needs 18 derivative fields per step; the warps split them with no redundancy:
+//   warps 4, 5  normal stresses (sxx, syy, szz) on k3 half h: a = Dx u, b = Dy v, c = Dz w,
+//               t_ii = lambda (a + b + c) + 2 mu {a, b, c}_i
+//   warps 3,6,7 shear sxz, sxy, syz:  mu (Dx w + Dz u), mu (Dx v + Dy u), mu (Dy w + Dz v)
+//   warps 0-2   velocities u, v, w:   (1/rho) (Dx s_x. + Dy s_y. + Dz s_z.)
+// paired on the SM sub-partitions (warp % 4) so that every SMSP carries about the same fp64 work.
+// Flux-first exactly like the reference's D_d * F_d(p) (proj/src/stp_splitck.cpp:53-55).
 //
-// Shared memory: the current iterate p, 9 x 8 x 8 x 8 fp64 with an XOR swizzle on the k1 index
-// (bit 2 flipped on rows with k2 & 2) so that every fragment load, column load and write-back
-// is bank-conflict free; plus face_q / face_f staging.  Warps are ordered so that the three
-// light shear warps share SMSP 0 (warp % 4 == 0) and the SMSP loads balance.
-// qavg and favg leave straight from registers; the 12 face arrays are computed by DMMA
-// (x, y normals) and register DFMA (z normal), staged in shared memory and written coalesced.
+// Shared memory (110,592 B, 2 CTAs per SM): p and p_next (double buffer, one barrier per CK step)
+// and the qavg accumulator, each 9 x 8 x 8 x 8 fp64 with an XOR swizzle on k1 (bit 2 flipped on
+// rows with k2 & 2) that makes every fragment load, column load and store bank-conflict free.
+// Epilogue: qavg and favg go out from registers (st.global.cs, 64-byte segments); the 12 face
+// arrays are contracted by DMMA (x, y normals) and DFMA (z normal) from the qavg accumulator,
+// staged in the reference's [f][a][b][s] order and written coalesced, face_f = F_d(face_q).
 #include <cstdint>
-#include <utility>
 
 #include "../../include/aderstp.h"
 #include "aderstp_internal.h"
-
-namespace aderstp {
-
-namespace {
-
-constexpr int N8 = 8;
-constexpr int NV = 9;
-constexpr int THREADS8 = NV * 32;
-constexpr int PV = N8 * N8 * N8;           // doubles per quantity plane
-constexpr int FACE = N8 * N8 * NV;         // doubles per face array (576)
-constexpr int SMEM8 = 3 * NV * PV * 8;  // p, p_next, qavg accumulator = 110,592 B (face staging reuses p)
-
-struct Params8 {
-  double d[64];      // d[k*8+l] = phi_l'(x_k)
-  double phi[2][8];  // phi(0), phi(1)
-  int check;
-  int par_kind;
-  int q_stride;
-};
-
-// warp -> output quantity (shear warps on SMSP 0)
-__constant__ int kWarpVar[NV] = {3, 0, 1, 2, 4, 6, 7, 8, 5};
-// flux table: F_d(q)_s = coef(s,d) * q[in(s,d)]; coef 0: lambda+2mu, 1: lambda, 2: mu, 3: 1/rho, 4: 0
-__constant__ int kIn[NV][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
-                               {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
-__constant__ int kCoef[NV][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
-                                 {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
-// outgoing flux entries of each source quantity r: (s, d, coef) with in(s,d) = r, plus the three
-// identically-zero entries (coef 4) assigned to the shear warps.  Used for favg and face_f.
-__constant__ int kOutN[NV] = {1, 1, 1, 3, 3, 3, 5, 5, 5};
-__constant__ int kOut[NV][5][3] = {
-    {{6, 0, 3}}, {{7, 1, 3}}, {{8, 2, 3}},
-    {{6, 1, 3}, {7, 0, 3}, {3, 2, 4}},
-    {{6, 2, 3}, {8, 0, 3}, {4, 1, 4}},
-    {{7, 2, 3}, {8, 1, 3}, {5, 0, 4}},
-    {{0, 0, 0}, {1, 0, 1}, {2, 0, 1}, {3, 1, 2}, {4, 2, 2}},
-    {{0, 1, 1}, {1, 1, 0}, {2, 1, 1}, {3, 0, 2}, {5, 2, 2}},
-    {{0, 2, 1}, {1, 2, 1}, {2, 2, 0}, {4, 0, 2}, {5, 1, 2}}};
-
-// D of the nDof = 8 Gauss-Legendre basis (identical for every plan), uploaded once per device;
-// read with volatile ld.const so the z-contraction streams it through the constant cache
-// instead of pinning 64 doubles in registers.
-}  // namespace
-}  // namespace aderstp
 
 // D of the nDof = 8 Gauss-Legendre basis (the same for every plan), uploaded once per device.
 // The z-contraction reads it at the point of use through volatile ld.const (constant cache,
@@ -75,7 +35,47 @@ __constant__ double aderstp_kD8[64];
 }
 
 namespace aderstp {
+
 namespace {
+
+constexpr int N8 = 8;
+constexpr int NV = 9;
+constexpr int NWARP = 8;
+constexpr int THREADS8 = NWARP * 32;
+constexpr int PV = N8 * N8 * N8;    // doubles per quantity plane
+constexpr int FACE = N8 * N8 * NV;  // doubles per face array (576)
+// DB = true: p / p_next double buffer (110,592 B, 2 CTAs/SM, one barrier per CK step);
+// DB = false: single p buffer (73,728 B, 3 CTAs/SM, two barriers per CK step).
+constexpr int smem8(bool db) { return (db ? 3 : 2) * NV * PV * 8; }
+
+struct Params8 {
+  double d[64];      // d[k*8+l] = phi_l'(x_k)
+  double phi[2][8];  // phi(0), phi(1)
+  int check;
+  int par_kind;
+  int q_stride;
+};
+
+// role of each warp: a single output quantity (0..8), or -1 / -2 for the normal-stress warps on
+// k3 half 0 / 1.  SMSP pairs (w, w+4): {u, N0}, {v, N1}, {w, sxy}, {sxz, syz}.
+__constant__ int kRole[NWARP] = {6, 7, 8, 4, -1, -2, 3, 5};
+// elastic flux table F_d(q)_s = coef(s,d) q[in(s,d)]; coef 0: lambda+2mu, 1: lambda, 2: mu,
+// 3: 1/rho, 4: 0
+__constant__ int kIn[NV][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
+                               {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+__constant__ int kCoef[NV][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
+                                 {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
+// outgoing flux entries of each source quantity r: (s, d, coef) with in(s,d) = r, plus the three
+// identically-zero entries (coef 4) assigned to the shear quantities.  Used for favg.
+__constant__ int kOutN[NV] = {1, 1, 1, 3, 3, 3, 5, 5, 5};
+__constant__ int kOut[NV][5][3] = {
+    {{6, 0, 3}}, {{7, 1, 3}}, {{8, 2, 3}},
+    {{6, 1, 3}, {7, 0, 3}, {3, 2, 4}},
+    {{6, 2, 3}, {8, 0, 3}, {4, 1, 4}},
+    {{7, 2, 3}, {8, 1, 3}, {5, 0, 4}},
+    {{0, 0, 0}, {1, 0, 1}, {2, 0, 1}, {3, 1, 2}, {4, 2, 2}},
+    {{0, 1, 1}, {1, 1, 0}, {2, 1, 1}, {3, 0, 2}, {5, 2, 2}},
+    {{0, 2, 1}, {1, 2, 1}, {2, 2, 0}, {4, 0, 2}, {5, 1, 2}}};
 
 __device__ __forceinline__ double2 ldc2(const double* p) {
   double2 v;
@@ -107,18 +107,69 @@ __device__ __forceinline__ double2 ld_nc2(const double* p) {
   return v;
 }
 
+__device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void sts2(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+
+// acc[K][j] += x-contraction of field f over tiles k3 = K0 .. K0+NT-1 (B = scaled D^T frags)
+template <int NT>
+__device__ __forceinline__ void mma_x(double (&acc)[NT][2], const double* f, int K0, int g, int t,
+                                      double b0, double b1) {
+  const double* p0 = f + K0 * 64 + phys(g, t);
+  const double* p1 = f + K0 * 64 + phys(g, 4 + t);
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    dmma(acc[k][0], acc[k][1], p0[k * 64], b0);
+    dmma(acc[k][0], acc[k][1], p1[k * 64], b1);
+  }
+}
+
+// acc[K][j] += y-contraction (A = scaled D frags)
+template <int NT>
+__device__ __forceinline__ void mma_y(double (&acc)[NT][2], const double* f, int K0, int g, int t,
+                                      double a0, double a1) {
+  const double* p0 = f + K0 * 64 + phys(t, g);
+  const double* p1 = f + K0 * 64 + phys(4 + t, g);
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    dmma(acc[k][0], acc[k][1], a0, p0[k * 64]);
+    dmma(acc[k][0], acc[k][1], a1, p1[k * 64]);
+  }
+}
+
+// acc[K][j] += sum_l D[K0+K][l] * (c f[l]) on this lane's two columns (full column l = 0..7)
+template <int NT>
+__device__ __forceinline__ void dfma_z(double (&acc)[NT][2], const double* f, int K0, int col, double c) {
+  const double* pz = f + col;
+#pragma unroll
+  for (int lq = 0; lq < 4; ++lq) {
+    const double2 v0 = lds2(pz + (2 * lq) * 64);
+    const double2 v1 = lds2(pz + (2 * lq + 1) * 64);
+    const double c00 = c * v0.x, c01 = c * v1.x, c10 = c * v0.y, c11 = c * v1.y;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double2 dk = ldc2(&aderstp_kD8[(K0 + k) * 8 + 2 * lq]);
+      acc[k][0] = fma(dk.x, c00, acc[k][0]);
+      acc[k][1] = fma(dk.x, c10, acc[k][1]);
+      acc[k][0] = fma(dk.y, c01, acc[k][0]);
+      acc[k][1] = fma(dk.y, c11, acc[k][1]);
+    }
+  }
+}
+
+template <bool DB>
 __global__ void __maxnreg__(80)
 stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   extern __shared__ __align__(16) double sm8[];
-  double* P = sm8;                  // [9][8][8][8] swizzled: current iterate p
-  double* PN = sm8 + NV * PV;       // next iterate (double buffer: one barrier per CK step)
-  double* QA = sm8 + 2 * NV * PV;   // [9][8][8][8] swizzled: qavg accumulator
-  double* FQ = sm8;                 // epilogue: face_q staging [6][8][8][9] reuses the p buffers
+  double* P = sm8;                            // current iterate p   [9][8][8][8] swizzled
+  double* PN = DB ? sm8 + NV * PV : sm8;      // next iterate
+  double* QA = sm8 + (DB ? 2 : 1) * NV * PV;  // qavg accumulator
   const long long e = blockIdx.x;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int s = kWarpVar[warp];
+  const int col = phys(g, 2 * t);  // + k3*64: this lane's node pair within a quantity plane
   unsigned int flags = 0;
   const double dt = a.dt;
 
@@ -144,185 +195,212 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   }
 
   // ---- stage q: AoSoA [k3][k2][s < QS][k1] -> P and QA = dt q -------------------------
-  // 64 rows (k3,k2) x 9 quantities x 4 k1-pairs = 2304 pairs = 8 per thread; all loads are
+  // 64 rows (k3,k2) x 9 quantities x 4 k1-pairs = 2304 pairs = 9 per thread; every load is
   // issued before the first shared store so their latencies overlap.
   {
     const double* qe = a.q + e * (long long)(PV * kp.q_stride);
-    double2 v[8];
+    double2 v[9];
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
+    for (int it = 0; it < 9; ++it) {
       const int i = tid + it * THREADS8;
       const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
       v[it] = ld_nc2(qe + (k32 * kp.q_stride + si) * 8 + 2 * (i & 3));
     }
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
+    for (int it = 0; it < 9; ++it) {
       const int i = tid + it * THREADS8;
       const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
       if (kp.check && !(isfinite(v[it].x) && isfinite(v[it].y))) flags |= 1u;
       const int j = si * PV + (k32 >> 3) * 64 + phys(k32 & 7, 2 * (i & 3));
-      *reinterpret_cast<double2*>(P + j) = v[it];
-      *reinterpret_cast<double2*>(QA + j) = make_double2(dt * v[it].x, dt * v[it].y);
+      sts2(P + j, v[it].x, v[it].y);
+      sts2(QA + j, dt * v[it].x, dt * v[it].y);
     }
   }
   __syncthreads();
 
   // ---- per-warp constants ---------------------------------------------------------------
-  const int in_x = kIn[s][0], in_y = kIn[s][1], in_z = kIn[s][2];
-  const double cx = sel4(c4, kCoef[s][0]), cy = sel4(c4, kCoef[s][1]), cz = sel4(c4, kCoef[s][2]);
-  const bool has_x = kCoef[s][0] != 4, has_y = kCoef[s][1] != 4, has_z = kCoef[s][2] != 4;
+  const int role = kRole[warp];
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];  // D[g][kh*4 + t]
-  const double bx0 = cx * d0, bx1 = cx * d1;                     // B-fragments of c_x D^T
-  const double ay0 = cy * d0, ay1 = cy * d1;                     // A-fragments of c_y D
-  const int own = s * PV + phys(g, 2 * t);                       // + k3*64: this lane's node pair
 
   // ---- Cauchy-Kowalewsky recursion (proj/src/stp_splitck.cpp:46-70) -------------------
   double coeff = dt;
+  if (role >= 0) {
+    const int s = role;
+    const int in_x = kIn[s][0], in_y = kIn[s][1], in_z = kIn[s][2];
+    const double cx = sel4(c4, kCoef[s][0]), cy = sel4(c4, kCoef[s][1]), cz = sel4(c4, kCoef[s][2]);
+    const bool has_x = kCoef[s][0] != 4, has_y = kCoef[s][1] != 4, has_z = kCoef[s][2] != 4;
+    const double bx0 = cx * d0, bx1 = cx * d1;  // B-fragments of c_x D^T
+    const double ay0 = cy * d0, ay1 = cy * d1;  // A-fragments of c_y D
+    const int own = s * PV + col;
 #pragma unroll 1
-  for (int o = 1; o < N8; ++o) {
-    double tt[8][2];
+    for (int o = 1; o < N8; ++o) {
+      double tt[8][2];
 #pragma unroll
-    for (int k3 = 0; k3 < 8; ++k3) tt[k3][0] = tt[k3][1] = 0.0;
-    if (has_x) {
-      const double* px = P + in_x * PV + phys(g, t);
-      const double* px1 = P + in_x * PV + phys(g, 4 + t);
+      for (int k3 = 0; k3 < 8; ++k3) tt[k3][0] = tt[k3][1] = 0.0;
+      if (has_x) mma_x<8>(tt, P + in_x * PV, 0, g, t, bx0, bx1);
+      if (has_y) mma_y<8>(tt, P + in_y * PV, 0, g, t, ay0, ay1);
+      if (has_z) dfma_z<8>(tt, P + in_z * PV, 0, col, cz);
+      coeff *= dt / (o + 1);  // dt^(o+1)/(o+1)!
 #pragma unroll
-      for (int k3 = 0; k3 < 8; ++k3) {
-        dmma(tt[k3][0], tt[k3][1], px[k3 * 64], bx0);
-        dmma(tt[k3][0], tt[k3][1], px1[k3 * 64], bx1);
+      for (int k3 = 0; k3 < 8; ++k3) {  // qavg += c_o t on this lane's own nodes (no race)
+        const double2 v = lds2(QA + own + k3 * 64);
+        sts2(QA + own + k3 * 64, fma(coeff, tt[k3][0], v.x), fma(coeff, tt[k3][1], v.y));
       }
-    }
-    if (has_y) {
-      const double* py = P + in_y * PV + phys(t, g);
-      const double* py1 = P + in_y * PV + phys(4 + t, g);
+      if (o + 1 < N8) {
+        if (!DB) __syncthreads();  // single buffer: every warp has finished reading p
 #pragma unroll
-      for (int k3 = 0; k3 < 8; ++k3) {
-        dmma(tt[k3][0], tt[k3][1], ay0, py[k3 * 64]);
-        dmma(tt[k3][0], tt[k3][1], ay1, py1[k3 * 64]);
+        for (int k3 = 0; k3 < 8; ++k3) sts2(PN + own + k3 * 64, tt[k3][0], tt[k3][1]);
       }
+      __syncthreads();  // p_next complete; every warp has finished reading p
+      double* sw = P;
+      P = PN;
+      PN = sw;
     }
-    if (has_z) {
-      const double* pz = P + in_z * PV + phys(g, 2 * t);
+  } else {
+    // normal stresses on k3 half h: a = Dx u, b = Dy v, c = Dz w (unscaled), then
+    // t_sxx = lambda (a+b+c) + 2 mu a, etc.
+    const int h = -role - 1, K0 = 4 * h;
+    const double lam = c4[1], two_mu = 2.0 * c4[2];
+#pragma unroll 1
+    for (int o = 1; o < N8; ++o) {
+      double ta[4][2], tb[4][2], tc[4][2];
 #pragma unroll
-      for (int lq = 0; lq < 4; ++lq) {
-        double c0[2], c1[2];
+      for (int k = 0; k < 4; ++k) ta[k][0] = ta[k][1] = tb[k][0] = tb[k][1] = tc[k][0] = tc[k][1] = 0.0;
+      mma_x<4>(ta, P + 6 * PV, K0, g, t, d0, d1);
+      mma_y<4>(tb, P + 7 * PV, K0, g, t, d0, d1);
+      dfma_z<4>(tc, P + 8 * PV, K0, col, 1.0);
+      coeff *= dt / (o + 1);
 #pragma unroll
-        for (int l = 0; l < 2; ++l) {
-          const double2 v = *reinterpret_cast<const double2*>(pz + (lq * 2 + l) * 64);
-          c0[l] = cz * v.x;
-          c1[l] = cz * v.y;
+      for (int k = 0; k < 4; ++k)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const double sum = lam * (ta[k][j] + tb[k][j] + tc[k][j]);
+          ta[k][j] = fma(two_mu, ta[k][j], sum);
+          tb[k][j] = fma(two_mu, tb[k][j], sum);
+          tc[k][j] = fma(two_mu, tc[k][j], sum);
         }
 #pragma unroll
-        for (int k3 = 0; k3 < 8; ++k3) {
-          const double2 dk = ldc2(&aderstp_kD8[k3 * 8 + lq * 2]);
-          tt[k3][0] = fma(dk.x, c0[0], tt[k3][0]);
-          tt[k3][1] = fma(dk.x, c1[0], tt[k3][1]);
-          tt[k3][0] = fma(dk.y, c0[1], tt[k3][0]);
-          tt[k3][1] = fma(dk.y, c1[1], tt[k3][1]);
+      for (int k = 0; k < 4; ++k) {
+        const int off = (K0 + k) * 64 + col;
+        const double2 va = lds2(QA + off), vb = lds2(QA + PV + off), vc = lds2(QA + 2 * PV + off);
+        sts2(QA + off, fma(coeff, ta[k][0], va.x), fma(coeff, ta[k][1], va.y));
+        sts2(QA + PV + off, fma(coeff, tb[k][0], vb.x), fma(coeff, tb[k][1], vb.y));
+        sts2(QA + 2 * PV + off, fma(coeff, tc[k][0], vc.x), fma(coeff, tc[k][1], vc.y));
+      }
+      if (o + 1 < N8) {
+        if (!DB) __syncthreads();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int off = (K0 + k) * 64 + col;
+          sts2(PN + off, ta[k][0], ta[k][1]);
+          sts2(PN + PV + off, tb[k][0], tb[k][1]);
+          sts2(PN + 2 * PV + off, tc[k][0], tc[k][1]);
         }
       }
+      __syncthreads();
+      double* sw = P;
+      P = PN;
+      PN = sw;
     }
-    coeff *= dt / (o + 1);  // dt^(o+1)/(o+1)!
-#pragma unroll
-    for (int k3 = 0; k3 < 8; ++k3) {  // qavg += c_o t on this lane's own nodes (no race)
-      double2* q = reinterpret_cast<double2*>(QA + own + k3 * 64);
-      const double2 v = *q;
-      *q = make_double2(fma(coeff, tt[k3][0], v.x), fma(coeff, tt[k3][1], v.y));
-    }
-    if (o + 1 < N8) {
-#pragma unroll
-      for (int k3 = 0; k3 < 8; ++k3)
-        *reinterpret_cast<double2*>(PN + own + k3 * 64) = make_double2(tt[k3][0], tt[k3][1]);
-    }
-    __syncthreads();  // p_next complete; every warp has finished reading p
-    double* sw = P;
-    P = PN;
-    PN = sw;
   }
 
   // ---- epilogue ------------------------------------------------------------------------
-  double qa[8][2];
+  // 18 units (quantity s, k3 half h) over the 8 warps: qavg and favg from registers, x/y faces
+  // by DMMA from the accumulator (staged into the dead p buffers); the unit with h = 0 also does
+  // the z faces, which need the whole column.
+  double* FQ = sm8;  // face_q staging [6][8][8][9] (the p buffer is dead after the last barrier)
+  const bool faces = a.face_q || a.face_f;
+  const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0;  // padded phi (rows / cols = side)
+  const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
+#pragma unroll 1
+  for (int unit = warp; unit < 2 * NV; unit += NWARP) {
+    const int s = unit >> 1, h = unit & 1, K0 = 4 * h;
+    const double* qs = QA + s * PV;
+    double qa[4][2];
 #pragma unroll
-  for (int k3 = 0; k3 < 8; ++k3) {
-    const double2 v = *reinterpret_cast<const double2*>(QA + own + k3 * 64);
-    qa[k3][0] = v.x;
-    qa[k3][1] = v.y;
-  }
-  // qavg straight from registers, AoSoA [k3][k2][s][k1]
-  {
+    for (int k = 0; k < 4; ++k) {
+      const double2 v = lds2(qs + (K0 + k) * 64 + col);
+      qa[k][0] = v.x;
+      qa[k][1] = v.y;
+    }
     double* qout = a.qavg + e * (long long)(PV * NV) + s * 8 + 2 * t;
 #pragma unroll
-    for (int k3 = 0; k3 < 8; ++k3) st_cs2(qout + (k3 * 8 + g) * NV * 8, qa[k3][0], qa[k3][1]);
-  }
-  // favg_d[s'] = coef * qavg[s] for every flux entry fed by this warp's quantity
-  if (a.favg) {
-    double* fout = a.favg + e * (long long)(3 * PV * NV) + 2 * t;
-    const int nout = kOutN[s];
+    for (int k = 0; k < 4; ++k) st_cs2(qout + ((K0 + k) * 8 + g) * NV * 8, qa[k][0], qa[k][1]);
+    if (a.favg) {
+      double* fout = a.favg + e * (long long)(3 * PV * NV) + 2 * t;
+      const int nout = kOutN[s];
 #pragma unroll 1
-    for (int k = 0; k < nout; ++k) {
-      const int so = kOut[s][k][0], d = kOut[s][k][1];
-      const double c = sel4(c4, kOut[s][k][2]);
-      double* base = fout + d * (PV * NV) + so * 8;
+      for (int k = 0; k < nout; ++k) {
+        const int so = kOut[s][k][0], d = kOut[s][k][1];
+        const double c = sel4(c4, kOut[s][k][2]);
+        double* base = fout + d * (PV * NV) + so * 8;
 #pragma unroll
-      for (int k3 = 0; k3 < 8; ++k3) st_cs2(base + (k3 * 8 + g) * NV * 8, c * qa[k3][0], c * qa[k3][1]);
+        for (int kk = 0; kk < 4; ++kk)
+          st_cs2(base + ((K0 + kk) * 8 + g) * NV * 8, c * qa[kk][0], c * qa[kk][1]);
+      }
+    }
+    if (faces) {
+      // x normal (faces 0, 1): C[k2][side] = sum_l Q[k3][k2][l] phi[side][l]   (B = phi^T)
+      // y normal (faces 2, 3): C[side][k1] = sum_l phi[side][l] Q[k3][l][k1]   (A = phi)
+      double xf[4][2], yf[4][2];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) xf[k][0] = xf[k][1] = yf[k][0] = yf[k][1] = 0.0;
+      mma_x<4>(xf, qs, K0, g, t, bphi0, bphi1);
+      mma_y<4>(yf, qs, K0, g, t, bphi0, bphi1);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int k3 = K0 + k;
+        if (t == 0) {  // lane (g, 0) holds C[k2 = g][side 0, 1]
+          FQ[0 * FACE + (k3 * 8 + g) * NV + s] = xf[k][0];
+          FQ[1 * FACE + (k3 * 8 + g) * NV + s] = xf[k][1];
+        }
+        if (g < 2) {  // lane (side = g, t) holds C[side][k1 = 2t, 2t+1]
+          FQ[(2 + g) * FACE + (k3 * 8 + 2 * t) * NV + s] = yf[k][0];
+          FQ[(2 + g) * FACE + (k3 * 8 + 2 * t + 1) * NV + s] = yf[k][1];
+        }
+      }
+      if (h == 0) {  // z normal (faces 4, 5): (a, b) = (k2, k1), full column
+        double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0};
+#pragma unroll
+        for (int k3 = 0; k3 < 8; ++k3) {
+          const double2 v = lds2(qs + k3 * 64 + col);
+          z0[0] = fma(kp.phi[0][k3], v.x, z0[0]);
+          z0[1] = fma(kp.phi[0][k3], v.y, z0[1]);
+          z1[0] = fma(kp.phi[1][k3], v.x, z1[0]);
+          z1[1] = fma(kp.phi[1][k3], v.y, z1[1]);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          FQ[4 * FACE + (g * 8 + 2 * t + j) * NV + s] = z0[j];
+          FQ[5 * FACE + (g * 8 + 2 * t + j) * NV + s] = z1[j];
+        }
+      }
     }
   }
-  if (a.face_q || a.face_f) {
-    // z normal (faces 4, 5): register-local columns, (a, b) = (k2, k1)
-    // x normal (faces 0, 1): C[k2][side] = sum_l Q[k3][k2][l] phi[side][l]  (B = padded phi^T)
-    // y normal (faces 2, 3): C[side][k1] = sum_l phi[side][l] Q[k3][l][k1]  (A = padded phi)
-    const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0;
-    const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
-    const double* qx = QA + s * PV + phys(g, t);
-    const double* qx1 = QA + s * PV + phys(g, 4 + t);
-    const double* qy = QA + s * PV + phys(t, g);
-    const double* qy1 = QA + s * PV + phys(4 + t, g);
-    // the last CK step's write-back was skipped, but p is still being read by no one after the
-    // final barrier: reuse it as the face staging area [f][a][b][s]
-#pragma unroll
-    for (int sd = 0; sd < 2; ++sd)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        double acc = 0.0;
-#pragma unroll
-        for (int k3 = 0; k3 < 8; ++k3) acc = fma(kp.phi[sd][k3], qa[k3][j], acc);
-        FQ[(4 + sd) * FACE + (g * 8 + 2 * t + j) * NV + s] = acc;
-      }
-#pragma unroll 2
-    for (int k3 = 0; k3 < 8; ++k3) {
-      double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
-      dmma(x0, x1, qx[k3 * 64], bphi0);
-      dmma(x0, x1, qx1[k3 * 64], bphi1);
-      dmma(y0, y1, bphi0, qy[k3 * 64]);
-      dmma(y0, y1, bphi1, qy1[k3 * 64]);
-      if (t == 0) {  // lane (g, 0) holds C[k2 = g][side 0, 1]
-        FQ[0 * FACE + (k3 * 8 + g) * NV + s] = x0;
-        FQ[1 * FACE + (k3 * 8 + g) * NV + s] = x1;
-      }
-      if (g < 2) {  // lane (side = g, t) holds C[side][k1 = 2t, 2t+1]
-        FQ[(2 + g) * FACE + (k3 * 8 + 2 * t) * NV + s] = y0;
-        FQ[(2 + g) * FACE + (k3 * 8 + 2 * t + 1) * NV + s] = y1;
-      }
-    }
+  if (faces) {
     __syncthreads();
-    // coalesced copy-out.  288 threads = 32 in-face nodes x 9 quantities, so thread tid always
-    // handles quantity so = tid % 9: face_f[f][ab][so] = coef(so, d) * face_q[f][ab][in(so, d)]
-    // (flux linearity), with the coefficients hoisted out of the loop.
-    const int so = tid % NV, ab0 = tid / NV;
-    double* oq = a.face_q ? a.face_q + e * (long long)(6 * FACE) : nullptr;
-    double* of = a.face_f ? a.face_f + e * (long long)(6 * FACE) : nullptr;
+    // coalesced copy-out; thread tid handles in-face nodes ab = tid / 9 + 28 i, quantity
+    // so = tid % 9 (252 active threads); face_f[f][ab][so] = coef(so, d) face_q[f][ab][in(so, d)]
+    if (tid < 252) {
+      const int so = tid % NV, ab0 = tid / NV;  // ab0 in 0..27
+      double* oq = a.face_q ? a.face_q + e * (long long)(6 * FACE) : nullptr;
+      double* of = a.face_f ? a.face_f + e * (long long)(6 * FACE) : nullptr;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const double c = sel4(c4, kCoef[so][d]);
-      const int src = kIn[so][d];
+      for (int d = 0; d < 3; ++d) {
+        const double c = sel4(c4, kCoef[so][d]);
+        const int src = kIn[so][d];
 #pragma unroll
-      for (int sd = 0; sd < 2; ++sd)
+        for (int sd = 0; sd < 2; ++sd)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int base = (2 * d + sd) * FACE + (ab0 + 32 * h) * NV;
-          if (oq) __stcs(oq + base + so, FQ[base + so]);
-          if (of) __stcs(of + base + so, c * FQ[base + src]);
-        }
+          for (int i = 0; i < 3; ++i) {
+            const int ab = ab0 + 28 * i;
+            if (ab < 64) {
+              const int base = (2 * d + sd) * FACE + ab * NV;
+              if (oq) __stcs(oq + base + so, FQ[base + so]);
+              if (of) __stcs(of + base + so, c * FQ[base + src]);
+            }
+          }
+      }
     }
   }
   if (kp.check && flags) atomicOr(status, flags);
@@ -349,14 +427,16 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   kp.check = p.check;
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
-  cudaError_t err = cudaFuncSetAttribute(stp_dmma8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM8);
+  const bool db = p.dmma8_double_buffer;
+  auto kern = db ? stp_dmma8_kernel<true> : stp_dmma8_kernel<false>;
+  const int smem = smem8(db);
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err == cudaSuccess)
-    err = cudaFuncSetAttribute(stp_dmma8_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (err != cudaSuccess) return err;
   if (a.n_elem == 0) return cudaSuccess;
   if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
-  stp_dmma8_kernel<<<(unsigned)a.n_elem, THREADS8, SMEM8, stream>>>(kp, a, p.d_status);
+  kern<<<(unsigned)a.n_elem, THREADS8, smem, stream>>>(kp, a, p.d_status);
   return cudaGetLastError();
 }
 
