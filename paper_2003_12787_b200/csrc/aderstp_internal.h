@@ -40,6 +40,7 @@ struct LaunchPlan {
   unsigned int* d_status = nullptr;  // device word: bit0 non-finite q, bit1 bad material
   int force_generic = 0;             // env ADERSTP_FORCE_GENERIC=1: skip specialised kernels
   int dmma8_double_buffer = 0;       // env ADERSTP_DMMA8_DB=1: 2 CTAs/SM double-buffered variant
+  int no_dmma8 = 0;                  // env ADERSTP_NO_DMMA8=1: nDof 8 on the line-pass kernel
 };
 
 struct BatchArgs {
@@ -66,6 +67,10 @@ bool kernel_available(int n);
 // stp_dmma8.cu: nDof = 8 elastic kernel on the fp64 tensor cores
 bool dmma8_applicable(const LaunchPlan& p);
 cudaError_t init_dmma8(const LaunchPlan& p);  // once per device, at plan creation
+// stp_pass.cu: line-pass elastic kernel for every order (even/odd split D, uniform operands)
+bool pass_applicable(const LaunchPlan& p);
+cudaError_t init_pass(const LaunchPlan& p);
+cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 
 }  // namespace aderstp

@@ -158,6 +158,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     lp.force_generic = (env && env[0] == '1') ? 1 : 0;
     const char* db = std::getenv("ADERSTP_DMMA8_DB");
     lp.dmma8_double_buffer = (db && db[0] == '1') ? 1 : 0;
+    const char* nd = std::getenv("ADERSTP_NO_DMMA8");
+    lp.no_dmma8 = (nd && nd[0] == '1') ? 1 : 0;
   }
   aderstp::make_host_basis(n, &lp.basis);
 
@@ -236,6 +238,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   if (e == cudaSuccess) e = cudaMalloc(&lp.d_status, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(lp.d_status, 0, sizeof(unsigned int));
   if (e == cudaSuccess && aderstp::dmma8_applicable(lp)) e = aderstp::init_dmma8(lp);
+  if (e == cudaSuccess && aderstp::pass_applicable(lp)) e = aderstp::init_pass(lp);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "plan_create");

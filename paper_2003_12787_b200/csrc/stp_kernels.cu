@@ -465,7 +465,8 @@ cudaError_t dispatch(const LaunchPlan& p, const BatchArgs& a, cudaStream_t st) {
 bool kernel_available(int n) { return n >= kMinOrder && n <= kMaxOrder; }
 
 cudaError_t launch_stp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
-  if (!p.force_generic && dmma8_applicable(p)) return launch_dmma8(p, a, stream);
+  if (!p.force_generic && !p.no_dmma8 && dmma8_applicable(p)) return launch_dmma8(p, a, stream);
+  if (!p.force_generic && pass_applicable(p)) return launch_pass(p, a, stream);
   if (p.kind == ADERSTP_PDE_ELASTIC) return dispatch<true>(p, a, stream);
   return dispatch<false>(p, a, stream);
 }

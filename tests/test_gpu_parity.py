@@ -74,3 +74,22 @@ def test_order8_kernels_parity(stp, oracle, monkeypatch, force_generic, q_stride
     ref = oracle.stp(n, 9, qc, dt, par=oracle.material_lmr(par_h))
     worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, 9)
     assert max(worst.values()) <= TOL, worst
+
+
+@pytest.mark.parametrize("n", [2, 3, 5, 8, 9])
+def test_kernel_variants_agree(stp, oracle, monkeypatch, n):
+    """Every kernel family (DMMA nDof 8, line-pass, generic table) against the oracle."""
+    S = stp
+    E = 19
+    q, par = S.generate(0, 5 + n, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
+    par_h = par.cpu().numpy()
+    dt = O.cfl_dt(n, par_h[:, 1].max())
+    ref = oracle.stp(n, 9, oracle.from_aosoa(n, 9, 9, q.cpu().numpy()), dt, par=oracle.material_lmr(par_h))
+    for env in ({"ADERSTP_NO_DMMA8": "1"}, {"ADERSTP_FORCE_GENERIC": "1"}, {"ADERSTP_DMMA8_DB": "1"}):
+        for k in ("ADERSTP_NO_DMMA8", "ADERSTP_FORCE_GENERIC", "ADERSTP_DMMA8_DB"):
+            monkeypatch.setenv(k, env.get(k, "0"))
+        plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
+        out = plan.predict(q, dt, par=par)
+        plan.status()
+        worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, 9)
+        assert max(worst.values()) <= TOL, (env, worst)
