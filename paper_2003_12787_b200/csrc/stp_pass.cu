@@ -64,7 +64,7 @@ struct Geo {
   static constexpr int EPB = N <= 2 ? 16 : N == 3 ? 8 : N <= 4 ? 4 : N <= 6 ? 2 : 1;
   static constexpr int THREADS = ((TASKS * EPB + 31) / 32) * 32;
   static constexpr int OUTV = NVE * N * N * N;         // qavg values per element
-  static constexpr int QPT = (OUTV * EPB + THREADS - 1) / THREADS;  // qavg values per thread
+  static constexpr int QPT = (ES * EPB + THREADS - 1) / THREADS;  // qavg values per thread
   static constexpr int FQV = 6 * N * N * NVE;                        // face staging
   static constexpr int EB = ES + (ES > FQV ? ES : FQV);             // per-element doubles
   static constexpr int SMEM = EB * EPB * 8;
@@ -113,11 +113,56 @@ __device__ __forceinline__ void eo_apply(double (&p)[N], double (&out)[N]) {
   }
 }
 
+// One task of pass D: contract the line (la, lb) of the slot's source field along direction D
+// and write (pass x; pass y's first touch of syz) or accumulate coef * D_D f into each target.
+template <int N, int D>
+__device__ __forceinline__ void line_pass(const double* P, double* T, int slot, int la, int lb,
+                                          const double (&c4)[4]) {
+  using G = Geo<N>;
+  constexpr int ST = D == 0 ? 1 : D == 1 ? G::RS : G::PL;
+  const int start = D == 0 ? la * G::PL + lb * G::RS : D == 1 ? la * G::PL + lb : la * G::RS + lb;
+  const PassSlot& ps = kPass[D][slot];
+  double p[N], out[N];
+  const double* src = P + ps.src * G::VS + start;
+#pragma unroll
+  for (int l = 0; l < N; ++l) p[l] = src[l * ST];
+  eo_apply<N>(p, out);
+  const bool write = D == 0 || (D == 1 && slot == 2);
+  const int nt = slot == 0 ? 3 : 1;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k < nt) {
+      const double c = pick4(c4, ps.coef[k]);
+      double* dst = T + ps.tgt[k] * G::VS + start;
+      if (write) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) dst[l * ST] = c * out[l];
+      } else {
+#pragma unroll
+        for (int l = 0; l < N; ++l) dst[l * ST] = fma(c, out[l], dst[l * ST]);
+      }
+    }
+  }
+}
+
 template <int N>
 struct PassParams {
   double phi[2][N];
   int check, par_kind, q_stride;
 };
+
+// Node-wise epilogue helpers: the elastic flux F_d(q)_s = coef(s,d) q[in(s,d)] with
+// compile-time (s, d), so every index below folds to a constant.
+__host__ __device__ constexpr int e_in(int s, int d) {
+  constexpr int t[9][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
+                           {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+  return t[s][d];
+}
+__host__ __device__ constexpr int e_coef(int s, int d) {
+  constexpr int t[9][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
+                           {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
+  return t[s][d];
+}
 
 template <int N>
 __global__ void __launch_bounds__(Geo<N>::THREADS, Geo<N>::MINB)
@@ -128,16 +173,17 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   unsigned int flags = 0;
   const double dt = a.dt;
   const long long e0 = (long long)blockIdx.x * G::EPB;
+  auto buf = [&](int ee, int which) { return smp + ee * G::EB + which * G::ES; };
+  constexpr int N3 = N * N * N;
 
-  // task of this thread in every pass: element el, source slot, line index
-  const int task = tid;
-  const int el = task / G::TASKS;
-  const int slot = (task - el * G::TASKS) / G::LINES;
-  const int line = task - el * G::TASKS - slot * G::LINES;
+  // line task of this thread in every pass: element el, source slot, line index
+  const int el = tid / G::TASKS;
+  const int slot = (tid - el * G::TASKS) / G::LINES;
+  const int line = tid - el * G::TASKS - slot * G::LINES;
   const bool active = el < G::EPB && e0 + el < a.n_elem;
-  const int la = line / N, lb = line - la * N;  // line = la * N + lb
+  const int la = line / N, lb = line - la * N;
 
-  // material of the task's element (proj/src/pde.cpp:171-178)
+  // material (proj/src/pde.cpp:171-178) of the task's element
   double c4[4] = {0.0, 0.0, 0.0, 0.0};
   if (active) {
     const double* pr = a.par + 3 * (e0 + el);
@@ -158,215 +204,178 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     c4[3] = 1.0 / rho;
   }
 
-  // ---- stage q (AoSoA [k3][k2][s < QS][k1]) -> P, qavg registers = dt q ----------------
-  // flat qavg ownership in output order [e][k3][k2][s][k1]: entry i = tid + j * THREADS
-  double qa[G::QPT];
+  // ---- stage q: one node (k3,k2,k1) per task, 9 coalesced loads (AoSoA [k3][k2][s][k1]) --
   {
     const int qs = kp.q_stride;
-    for (int i = tid; i < G::EPB * N * N * qs * N; i += G::THREADS) {
-      const int ee = i / (N * N * qs * N);
-      int r = i - ee * (N * N * qs * N);
-      const int k1 = r % N;
-      r /= N;
-      const int s = r % qs;
-      r /= qs;
-      if (s >= NVE || e0 + ee >= a.n_elem) continue;
-      const double v = __ldcs(a.q + (e0 + ee) * (long long)(N * N * qs * N) + (i - ee * (N * N * qs * N)));
-      if (kp.check && !isfinite(v)) flags |= 1u;
-      smp[ee * G::EB + s * G::VS + (r / N) * G::PL + (r % N) * G::RS + k1] = v;
+    for (int i = tid; i < G::EPB * N3; i += G::THREADS) {
+      const int ee = i / N3, node = i - ee * N3;
+      if (e0 + ee >= a.n_elem) continue;
+      const int k1 = node % N, k32 = node / N;  // k32 = k3*N + k2
+      const double* src = a.q + (e0 + ee) * (long long)(N3 * qs) + k32 * qs * N + k1;
+      double* dst = buf(ee, 0) + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+      double v[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) v[s] = __ldcs(src + s * N);
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) {
+        if (kp.check && !isfinite(v[s])) flags |= 1u;
+        dst[s * G::VS] = v[s];
+      }
     }
   }
   __syncthreads();
+  // qavg accumulator in registers, owned in the shared-memory linear order of the padded
+  // tensor (entry j of this thread = offset tid + j*THREADS over all elements of the block)
+  double qa[G::QPT];
 #pragma unroll
   for (int j = 0; j < G::QPT; ++j) {
     const int i = tid + j * G::THREADS;
-    double v = 0.0;
-    if (i < G::EPB * G::OUTV) {
-      const int ee = i / G::OUTV;
-      int r = i - ee * G::OUTV;
-      const int k1 = r % N;
-      r /= N;
-      const int s = r % NVE;
-      r /= NVE;
-      v = dt * smp[ee * G::EB + s * G::VS + (r / N) * G::PL + (r % N) * G::RS + k1];
-    }
-    qa[j] = v;
+    const int ee = i / G::ES;
+    qa[j] = (ee < G::EPB) ? dt * buf(ee, 0)[i - ee * G::ES] : 0.0;
   }
 
-  // buffers of element ee: B(ee, 0) holds p, B(ee, 1) the next iterate; they alternate
-  auto buf = [&](int ee, int which) { return smp + ee * G::EB + which * G::ES; };
   double coeff = dt;
   int cur = 0;  // buffer holding the current iterate p
 #pragma unroll 1
   for (int o = 1; o < N; ++o) {
     const double* P = buf(el < G::EPB ? el : 0, cur);
     double* T = buf(el < G::EPB ? el : 0, cur ^ 1);
-#pragma unroll 1
-    for (int d = 0; d < 3; ++d) {
-      if (active) {
-        const PassSlot ps = kPass[d][slot];
-        int start, stride;  // line start and stride along direction d
-        if (d == 0) {
-          start = la * G::PL + lb * G::RS;  // x-line (k3, k2)
-          stride = 1;
-        } else if (d == 1) {
-          start = la * G::PL + lb;  // y-line (k3, k1)
-          stride = G::RS;
-        } else {
-          start = la * G::RS + lb;  // z-line (k2, k1)
-          stride = G::PL;
-        }
-        double p[N], out[N];
-        const double* src = P + ps.src * G::VS + start;
-#pragma unroll
-        for (int l = 0; l < N; ++l) p[l] = src[l * stride];
-        eo_apply<N>(p, out);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          if (k < ps.nt) {
-            const double c = pick4(c4, ps.coef[k]);
-            double* dst = T + ps.tgt[k] * G::VS + start;
-            // pass x writes every target but syz; pass y writes syz (its first touch)
-            if (d == 0 || (d == 1 && ps.tgt[k] == 5)) {
-#pragma unroll
-              for (int l = 0; l < N; ++l) dst[l * stride] = c * out[l];
-            } else {
-#pragma unroll
-              for (int l = 0; l < N; ++l) dst[l * stride] = fma(c, out[l], dst[l * stride]);
-            }
-          }
-        }
-      }
-      __syncthreads();
-    }
+    if (active) line_pass<N, 0>(P, T, slot, la, lb, c4);
+    __syncthreads();
+    if (active) line_pass<N, 1>(P, T, slot, la, lb, c4);
+    __syncthreads();
+    if (active) line_pass<N, 2>(P, T, slot, la, lb, c4);
+    __syncthreads();
     // T = sum_d D_d F_d(p) is the next iterate: qavg += c_o T  (stp_splitck.cpp:64-69)
     coeff *= dt / (o + 1);
     cur ^= 1;
 #pragma unroll
     for (int j = 0; j < G::QPT; ++j) {
       const int i = tid + j * G::THREADS;
-      if (i < G::EPB * G::OUTV) {
-        const int ee = i / G::OUTV;
-        int r = i - ee * G::OUTV;
-        const int k1 = r % N;
-        r /= N;
-        const int s = r % NVE;
-        r /= NVE;
-        qa[j] = fma(coeff, buf(ee, cur)[s * G::VS + (r / N) * G::PL + (r % N) * G::RS + k1], qa[j]);
-      }
+      const int ee = i / G::ES;
+      if (ee < G::EPB) qa[j] = fma(coeff, buf(ee, cur)[i - ee * G::ES], qa[j]);
     }
-    // no barrier needed: the next pass x reads buf(cur) (read-only) and writes buf(cur ^ 1),
-    // whose last readers were this step's passes, all behind the pass-z barrier
+    // no barrier: the next pass x only reads buf(cur) and writes buf(cur ^ 1), whose readers
+    // (this step's passes) are all behind the pass-z barrier
   }
-  __syncthreads();  // every qavg read of the last iterate is done
-
-  // ---- epilogue --------------------------------------------------------------------------
-  // qavg: registers -> global (flat, coalesced) and -> buffer 0 for favg / faces
+  __syncthreads();  // the qavg reads of the last iterate are done
 #pragma unroll
   for (int j = 0; j < G::QPT; ++j) {
     const int i = tid + j * G::THREADS;
-    if (i < G::EPB * G::OUTV) {
-      const int ee = i / G::OUTV;
-      int r = i - ee * G::OUTV;
-      if (e0 + ee < a.n_elem) __stcs(a.qavg + (e0 + ee) * (long long)G::OUTV + r, qa[j]);
-      const int k1 = r % N;
-      r /= N;
-      const int s = r % NVE;
-      r /= NVE;
-      buf(ee, 0)[s * G::VS + (r / N) * G::PL + (r % N) * G::RS + k1] = qa[j];
-    }
+    const int ee = i / G::ES;
+    if (ee < G::EPB) buf(ee, 0)[i - ee * G::ES] = qa[j];
   }
   __syncthreads();
-  // favg_d[s] = coef(s,d) qavg[in(s,d)]  (proj/src/stp_splitck.cpp:72-78), flat over
-  // [e][d][k3][k2][s][k1]; the element's material is recomputed per entry's element
-  if (a.favg) {
-    for (int i = tid; i < G::EPB * 3 * G::OUTV; i += G::THREADS) {
-      const int ee = i / (3 * G::OUTV);
-      if (e0 + ee >= a.n_elem) continue;
-      int r = i - ee * 3 * G::OUTV;
-      const int d = r / G::OUTV;
-      r -= d * G::OUTV;
-      const int k1 = r % N;
-      int rr = r / N;
-      const int s = rr % NVE;
-      rr /= NVE;
-      const int ci = kCoefE[s][d];
-      double v = 0.0;
-      if (ci != 4) {
+
+  // ---- epilogue --------------------------------------------------------------------------
+  // per node: qavg (9 values) and favg (27 values, F_d(qavg) with compile-time (s, d)) to
+  // AoSoA [k3][k2][s][k1]; consecutive threads = consecutive k1, so every store is coalesced
+  for (int i = tid; i < G::EPB * N3; i += G::THREADS) {
+    const int ee = i / N3, node = i - ee * N3;
+    if (e0 + ee >= a.n_elem) continue;
+    const int k1 = node % N, k32 = node / N;
+    const double* qs = buf(ee, 0) + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+    double v[NVE];
+#pragma unroll
+    for (int s = 0; s < NVE; ++s) v[s] = qs[s * G::VS];
+    const long long ob = (e0 + ee) * (long long)(NVE * N3) + k32 * NVE * N + k1;
+#pragma unroll
+    for (int s = 0; s < NVE; ++s) __stcs(a.qavg + ob + s * N, v[s]);
+    if (a.favg) {
+      double cc[4];
+      {
         const double* pr = a.par + 3 * (e0 + ee);
-        double cc;
         if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
           const double mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
           const double lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
-          cc = ci == 0 ? lam + 2.0 * mu : ci == 1 ? lam : ci == 2 ? mu : 1.0 / pr[0];
+          cc[0] = lam + 2.0 * mu;
+          cc[1] = lam;
+          cc[2] = mu;
+          cc[3] = 1.0 / pr[0];
         } else {
-          cc = ci == 0 ? pr[0] + 2.0 * pr[1] : ci == 1 ? pr[0] : ci == 2 ? pr[1] : 1.0 / pr[2];
+          cc[0] = pr[0] + 2.0 * pr[1];
+          cc[1] = pr[0];
+          cc[2] = pr[1];
+          cc[3] = 1.0 / pr[2];
         }
-        v = cc * buf(ee, 0)[kInE[s][d] * G::VS + (rr / N) * G::PL + (rr % N) * G::RS + k1];
       }
-      __stcs(a.favg + (e0 + ee) * 3LL * G::OUTV + d * G::OUTV + r, v);
+      double* fo = a.favg + (e0 + ee) * (long long)(3 * NVE * N3) + k32 * NVE * N + k1;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int s = 0; s < NVE; ++s)
+          __stcs(fo + d * (NVE * N3) + s * N, e_coef(s, d) == 4 ? 0.0 : cc[e_coef(s, d)] * v[e_in(s, d)]);
     }
   }
   if (a.face_q || a.face_f) {
-    // face_q: task (normal d, a, b, s) contracts one line with phi(0) and phi(1) into the
-    // staging buffer 1 laid out as the reference's [f][a][b][s]
-    constexpr int FV = N * N * NVE;  // one face array
-    for (int i = tid; i < G::EPB * 3 * FV; i += G::THREADS) {
-      const int ee = i / (3 * FV);
-      int r = i - ee * 3 * FV;
-      const int d = r / FV;
-      r -= d * FV;
-      const int s = r % NVE;
-      const int ab = r / NVE;
-      const int aa = ab / N, bb = ab - aa * N;
-      int start, stride;
-      if (d == 0) {
-        start = aa * G::PL + bb * G::RS;
-        stride = 1;
-      } else if (d == 1) {
-        start = aa * G::PL + bb;
-        stride = G::RS;
-      } else {
-        start = aa * G::RS + bb;
-        stride = G::PL;
-      }
-      const double* ln = buf(ee, 0) + s * G::VS + start;
-      double v0 = 0.0, v1 = 0.0;
-#pragma unroll
-      for (int j = 0; j < N; ++j) {
-        const double x = ln[j * stride];
-        v0 = fma(kp.phi[0][j], x, v0);
-        v1 = fma(kp.phi[1][j], x, v1);
-      }
-      double* fq = buf(ee, 1);
-      fq[(2 * d) * FV + ab * NVE + s] = v0;
-      fq[(2 * d + 1) * FV + ab * NVE + s] = v1;
-    }
-    __syncthreads();
-    for (int i = tid; i < G::EPB * 6 * FV; i += G::THREADS) {
-      const int ee = i / (6 * FV);
+    // one task per (normal d, in-face node a, b): all 9 quantities of the normal line, both
+    // sides; face_f = F_d(face_q) on the spot.  Output [f][a][b][s]: 9 contiguous doubles per
+    // (f, ab) and consecutive tasks = consecutive ab.
+    constexpr int FV = N * N * NVE;
+    for (int i = tid; i < G::EPB * 3 * N * N; i += G::THREADS) {
+      const int ee = i / (3 * N * N);
       if (e0 + ee >= a.n_elem) continue;
-      const int r = i - ee * 6 * FV;
-      const double* fq = buf(ee, 1);
-      if (a.face_q) __stcs(a.face_q + (e0 + ee) * 6LL * FV + r, fq[r]);
-      if (a.face_f) {
-        const int f = r / FV, d = f >> 1;
-        const int s = r % NVE;
-        const int ci = kCoefE[s][d];
-        double v = 0.0;
-        if (ci != 4) {
-          const double* pr = a.par + 3 * (e0 + ee);
-          double cc;
-          if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
-            const double mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
-            const double lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
-            cc = ci == 0 ? lam + 2.0 * mu : ci == 1 ? lam : ci == 2 ? mu : 1.0 / pr[0];
-          } else {
-            cc = ci == 0 ? pr[0] + 2.0 * pr[1] : ci == 1 ? pr[0] : ci == 2 ? pr[1] : 1.0 / pr[2];
-          }
-          v = cc * fq[r - s + kInE[s][d]];
+      int r = i - ee * 3 * N * N;
+      const int d = r / (N * N);
+      const int ab = r - d * N * N;
+      const int aa = ab / N, bb = ab - aa * N;
+      const int start = d == 0 ? aa * G::PL + bb * G::RS : d == 1 ? aa * G::PL + bb : aa * G::RS + bb;
+      const int stride = d == 0 ? 1 : d == 1 ? G::RS : G::PL;
+      const double* q0 = buf(ee, 0) + start;
+      double f0[NVE], f1[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) {
+        double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double x = q0[s * G::VS + j * stride];
+          x0 = fma(kp.phi[0][j], x, x0);
+          x1 = fma(kp.phi[1][j], x, x1);
         }
-        __stcs(a.face_f + (e0 + ee) * 6LL * FV + r, v);
+        f0[s] = x0;
+        f1[s] = x1;
+      }
+      const long long fb = (e0 + ee) * 6LL * FV + (2 * d) * FV + ab * NVE;
+      if (a.face_q) {
+#pragma unroll
+        for (int s = 0; s < NVE; ++s) {
+          __stcs(a.face_q + fb + s, f0[s]);
+          __stcs(a.face_q + fb + FV + s, f1[s]);
+        }
+      }
+      if (a.face_f) {
+        double cc[4];
+        const double* pr = a.par + 3 * (e0 + ee);
+        if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
+          const double mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
+          const double lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
+          cc[0] = lam + 2.0 * mu;
+          cc[1] = lam;
+          cc[2] = mu;
+          cc[3] = 1.0 / pr[0];
+        } else {
+          cc[0] = pr[0] + 2.0 * pr[1];
+          cc[1] = pr[0];
+          cc[2] = pr[1];
+          cc[3] = 1.0 / pr[2];
+        }
+        // d is a runtime value here: select the flux row per direction
+#pragma unroll
+        for (int s = 0; s < NVE; ++s) {
+          double g0, g1;
+          if (d == 0) {
+            g0 = e_coef(s, 0) == 4 ? 0.0 : cc[e_coef(s, 0)] * f0[e_in(s, 0)];
+            g1 = e_coef(s, 0) == 4 ? 0.0 : cc[e_coef(s, 0)] * f1[e_in(s, 0)];
+          } else if (d == 1) {
+            g0 = e_coef(s, 1) == 4 ? 0.0 : cc[e_coef(s, 1)] * f0[e_in(s, 1)];
+            g1 = e_coef(s, 1) == 4 ? 0.0 : cc[e_coef(s, 1)] * f1[e_in(s, 1)];
+          } else {
+            g0 = e_coef(s, 2) == 4 ? 0.0 : cc[e_coef(s, 2)] * f0[e_in(s, 2)];
+            g1 = e_coef(s, 2) == 4 ? 0.0 : cc[e_coef(s, 2)] * f1[e_in(s, 2)];
+          }
+          __stcs(a.face_f + fb + s, g0);
+          __stcs(a.face_f + fb + FV + s, g1);
+        }
       }
     }
   }
