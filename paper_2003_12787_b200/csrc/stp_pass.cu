@@ -25,10 +25,11 @@
 #include "../../include/aderstp.h"
 #include "aderstp_internal.h"
 
-// Even/odd derivative operator per order (uploaded once per device at plan creation):
-// [A: h x (h+1)][B: h x h][M: h+1] with h = n/2, stored at offset order*64.
+// Even/odd derivative operator per order (uploaded once per device at plan creation), rows
+// padded to 6 doubles so they load as 16-byte pairs: [A: h x 6][B: h x 6][M: 6], h = n/2,
+// stored at offset order*80.
 extern "C" {
-__constant__ double aderstp_kEO[11 * 64];
+__constant__ double aderstp_kEO[11 * 80];
 }
 
 namespace aderstp {
@@ -71,23 +72,35 @@ struct Geo {
   static constexpr int MINB = N >= 10 ? 1 : 2;
 };
 
-__device__ __forceinline__ double ceo(int i) {
-  double v;
-  asm volatile("{\n .reg .u64 ca;\n cvta.to.const.u64 ca, %1;\n ld.const.f64 %0, [ca];\n}\n"
-               : "=d"(v)
+__device__ __forceinline__ double2 ceo2(int i) {
+  double2 v;
+  asm volatile("{\n .reg .u64 ca;\n cvta.to.const.u64 ca, %2;\n ld.const.v2.f64 {%0, %1}, [ca];\n}\n"
+               : "=d"(v.x), "=d"(v.y)
                : "l"(&aderstp_kEO[i]));
   return v;
+}
+
+// row r of length L (<= 6) at constant offset i, loaded as 16-byte pairs
+template <int L>
+__device__ __forceinline__ void ceo_row(int i, double (&r)[6]) {
+#pragma unroll
+  for (int l = 0; l < L; l += 2) {
+    const double2 v = ceo2(i + l);
+    r[l] = v.x;
+    r[l + 1] = v.y;
+  }
 }
 
 __device__ __forceinline__ double pick4(const double c[4], int i) {
   return i == 0 ? c[0] : i == 1 ? c[1] : i == 2 ? c[2] : c[3];
 }
 
-// out[k] = sum_l D[k][l] p[l] via the even/odd split; p is overwritten.
+// out[k] = sum_l D[k][l] p[l] via the even/odd split.
 template <int N>
-__device__ __forceinline__ void eo_apply(double (&p)[N], double (&out)[N]) {
+__device__ __forceinline__ void eo_apply(const double (&p)[N], double (&out)[N]) {
   constexpr int H = N / 2;
-  const int base = N * 64;
+  constexpr int LA = H + (N % 2);  // A acts on e[0..H) and, for odd N, the middle node
+  const int base = N * 80;
   double e[H + 1], o[H];
 #pragma unroll
   for (int l = 0; l < H; ++l) {
@@ -97,19 +110,24 @@ __device__ __forceinline__ void eo_apply(double (&p)[N], double (&out)[N]) {
   if (N % 2) e[H] = p[H];
 #pragma unroll
   for (int k = 0; k < H; ++k) {
+    double ra[6], rb[6];
+    ceo_row<LA>(base + k * 6, ra);
+    ceo_row<H>(base + 30 + k * 6, rb);
     double al = 0.0, be = 0.0;
 #pragma unroll
-    for (int l = 0; l < H + (N % 2); ++l) al = fma(ceo(base + k * (H + 1) + l), e[l], al);
+    for (int l = 0; l < LA; ++l) al = fma(ra[l], e[l], al);
 #pragma unroll
-    for (int l = 0; l < H; ++l) be = fma(ceo(base + H * (H + 1) + k * H + l), o[l], be);
+    for (int l = 0; l < H; ++l) be = fma(rb[l], o[l], be);
     out[k] = al + be;
     out[N - 1 - k] = be - al;
   }
   if (N % 2) {
+    double rm[6];
+    ceo_row<H + 1>(base + 60, rm);
     double mid = 0.0;
 #pragma unroll
-    for (int l = 0; l < H; ++l) mid = fma(ceo(base + H * (H + 1) + H * H + l), o[l], mid);
-    out[H] = fma(ceo(base + H * (H + 1) + H * H + H), e[H], mid);
+    for (int l = 0; l < H; ++l) mid = fma(rm[l], o[l], mid);
+    out[H] = fma(rm[H], e[H], mid);
   }
 }
 
@@ -415,20 +433,20 @@ bool pass_applicable(const LaunchPlan& p) {
 // Even/odd split of D (see the file comment), per order, into aderstp_kEO[n*64 ...].
 cudaError_t init_pass(const LaunchPlan& p) {
   const int n = p.n, h = n / 2;
-  double buf[64] = {0};
+  double buf[80] = {0};
   const double* D = p.basis.d;
   for (int k = 0; k < h; ++k) {
     for (int l = 0; l < h; ++l) {
-      buf[k * (h + 1) + l] = 0.5 * (D[k * n + l] + D[k * n + (n - 1 - l)]);          // A
-      buf[h * (h + 1) + k * h + l] = 0.5 * (D[k * n + l] - D[k * n + (n - 1 - l)]);  // B
+      buf[k * 6 + l] = 0.5 * (D[k * n + l] + D[k * n + (n - 1 - l)]);       // A
+      buf[30 + k * 6 + l] = 0.5 * (D[k * n + l] - D[k * n + (n - 1 - l)]);  // B
     }
-    if (n % 2) buf[k * (h + 1) + h] = D[k * n + h];  // middle column acts on e[h] = p[h]
+    if (n % 2) buf[k * 6 + h] = D[k * n + h];  // middle column acts on e[h] = p[h]
   }
   if (n % 2) {
-    for (int l = 0; l < h; ++l) buf[h * (h + 1) + h * h + l] = 0.5 * (D[h * n + l] - D[h * n + (n - 1 - l)]);
-    buf[h * (h + 1) + h * h + h] = D[h * n + h];
+    for (int l = 0; l < h; ++l) buf[60 + l] = 0.5 * (D[h * n + l] - D[h * n + (n - 1 - l)]);
+    buf[60 + h] = D[h * n + h];
   }
-  return cudaMemcpyToSymbol(aderstp_kEO, buf, sizeof(buf), sizeof(double) * 64 * n);
+  return cudaMemcpyToSymbol(aderstp_kEO, buf, sizeof(buf), sizeof(double) * 80 * n);
 }
 
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
