@@ -319,6 +319,13 @@ ChunkLayout chunk_layout(const LaunchPlan& lp) {
   return c;
 }
 
+// device sub-buffers of one chunk slot, each starting on a 256-byte boundary
+size_t round256(size_t doubles) { return (doubles + 31) / 32 * 32; }
+size_t chunk_doubles(const ChunkLayout& c, int64_t chunk) {
+  return round256(c.q * chunk) + round256(c.par * chunk) + round256(c.qavg * chunk) +
+         round256(c.favg * chunk) + 2 * round256(c.face * chunk);
+}
+
 }  // namespace
 
 int aderstp_plan_reserve_host_path(aderstp_plan* p, int64_t chunk_elems) {
@@ -329,11 +336,10 @@ int aderstp_plan_reserve_host_path(aderstp_plan* p, int64_t chunk_elems) {
     p->buf[i] = nullptr;
   }
   const ChunkLayout c = chunk_layout(p->lp);
-  const size_t per = c.q + c.par + c.qavg + c.favg + 2 * c.face;
   for (int i = 0; i < kHostStreams; ++i) {
     cudaError_t e = cudaSuccess;
     if (!p->streams[i]) e = cudaStreamCreateWithFlags(&p->streams[i], cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaMalloc(&p->buf[i], sizeof(double) * per * chunk_elems);
+    if (e == cudaSuccess) e = cudaMalloc(&p->buf[i], sizeof(double) * chunk_doubles(c, chunk_elems));
     if (e != cudaSuccess) {
       p->chunk = 0;
       return cuda_fail(e, "reserve_host_path");
@@ -368,11 +374,11 @@ int aderstp_predict_batch_host(aderstp_plan* p, int64_t n_elem, const double* q,
     cudaStream_t st = p->streams[slot];
     double* b = p->buf[slot];
     double* dq = b;
-    double* dpar = dq + c.q * chunk;
-    double* dqa = dpar + c.par * chunk;
-    double* dfa = dqa + c.qavg * chunk;
-    double* dfq = dfa + c.favg * chunk;
-    double* dff = dfq + c.face * chunk;
+    double* dpar = dq + round256(c.q * chunk);
+    double* dqa = dpar + round256(c.par * chunk);
+    double* dfa = dqa + round256(c.qavg * chunk);
+    double* dfq = dfa + round256(c.favg * chunk);
+    double* dff = dfq + round256(c.face * chunk);
     e = cudaMemcpyAsync(dq, q + done * c.q, sizeof(double) * c.q * cnt, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess && elastic)
       e = cudaMemcpyAsync(dpar, par + done * 3, sizeof(double) * 3 * cnt, cudaMemcpyHostToDevice, st);

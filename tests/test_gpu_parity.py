@@ -93,3 +93,209 @@ def test_kernel_variants_agree(stp, oracle, monkeypatch, n):
         plan.status()
         worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, 9)
         assert max(worst.values()) <= TOL, (env, worst)
+
+
+# ---------------------------------------------------------------------------------------------
+# Against the reference's own outputs (tests/golden, produced by the unmodified reference)
+# ---------------------------------------------------------------------------------------------
+import json as _json  # noqa: E402
+import os as _os  # noqa: E402
+
+GOLDEN = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "golden")
+
+
+def _golden_cases():
+    with open(_os.path.join(GOLDEN, "index.json")) as f:
+        return _json.load(f)["cases"]
+
+
+def _pde_for(S, case, g):
+    kind = case.get("pde_kind", 0)
+    args = g["args"] if "args" in g else None
+    if kind == 0:
+        return S.elastic_pde()
+    if kind == 1:
+        return S.advection_pde(args[:3], case["m"])
+    if kind == 2:
+        return S.ncp_advection_pde(args[:3], case["m"])
+    if kind == 3:
+        return S.paper_demo_pde()
+    src = S.PointSourceSpec(tuple(args[:3]), int(args[3]), args[4], args[5], args[6])
+    if kind == 4:
+        return S.elastic_pde(source=src)
+    return S.source_only_pde(case["m"], src)
+
+
+@pytest.mark.parametrize("case", _golden_cases(), ids=lambda c: c["name"])
+@pytest.mark.parametrize("layout", ["aosoa", "aos16"])
+def test_matches_reference_golden(stp, oracle, case, layout):
+    """GPU output vs the reference's own predict(splitck) + extrapolate_faces outputs."""
+    S = stp
+    g = np.load(_os.path.join(GOLDEN, case["name"] + ".npz"))
+    n, m = case["n"], case["m"]
+    E = g["q"].shape[0]
+    pde = _pde_for(S, case, g)
+    if layout == "aosoa":
+        qs, lay = m, S.LAYOUT_AOSOA
+        qdev = oracle.to_aosoa(n, m, qs, g["q"])
+    else:  # the reference ElementTensor layout: AoS, quantity padded to 16 (layout.cpp:9-21)
+        qs, lay = 16, S.LAYOUT_AOS
+        qdev = np.zeros((E, n ** 3, 16))
+        qdev[:, :, :m] = g["q"].reshape(E, n ** 3, m)
+    q = torch.from_numpy(np.ascontiguousarray(qdev).reshape(E, -1)).cuda()
+    par = torch.from_numpy(g["par_lmr"]).cuda() if "par_lmr" in g else None
+    plan = S.Plan(n, pde, layout=lay, q_stride=qs, out_stride=qs, par_kind=S.PAR_LAMBDA_MU_RHO)
+    out = plan.predict(q, float(g["dt"]), par=par, t_start=float(g["t_start"]))
+    plan.status()
+    qa = out.qavg.cpu().numpy()
+    fa = out.favg.cpu().numpy()
+    if layout == "aosoa":
+        qa_c = oracle.from_aosoa(n, m, qs, qa)
+        fa_c = np.stack([oracle.from_aosoa(n, m, qs, fa[:, d]) for d in range(3)], 1)
+    else:
+        qa_c = qa.reshape(E, n ** 3, 16)[:, :, :m].reshape(E, -1)
+        fa_c = fa.reshape(E, 3, n ** 3, 16)[..., :m].reshape(E, 3, -1)
+        # padding lanes of every output stay exactly zero (test_predictor.cpp:157-170)
+        assert not np.any(qa.reshape(E, n ** 3, 16)[:, :, m:])
+        assert not np.any(fa.reshape(E, 3, n ** 3, 16)[..., m:])
+    assert O.per_element_rel_diff(g["qavg"], qa_c) <= TOL
+    assert O.per_element_rel_diff(g["favg"].reshape(E, -1), fa_c.reshape(E, -1)) <= TOL
+    assert O.per_element_rel_diff(g["face_q"].reshape(E, -1), out.face_q.cpu().numpy().reshape(E, -1)) <= TOL
+    assert O.per_element_rel_diff(g["face_f"].reshape(E, -1), out.face_f.cpu().numpy().reshape(E, -1)) <= TOL
+
+
+# ---------------------------------------------------------------------------------------------
+# Properties and edge cases
+# ---------------------------------------------------------------------------------------------
+def test_zero_dynamics_exact(stp):
+    """advection with v = 0: qavg == dt*q bit-exactly, favg == 0 (test_predictor.cpp:36-53)."""
+    S = stp
+    for n in (2, 4, 8):
+        rng = np.random.default_rng(42 + n)
+        qn = rng.uniform(-1, 1, (5, n ** 3 * 3))
+        q = torch.from_numpy(qn).cuda()
+        dt = 0.013
+        plan = S.Plan(n, S.advection_pde([0.0, 0.0, 0.0], 3))
+        out = plan.predict(q, dt)
+        assert torch.equal(out.qavg, dt * q)
+        assert not torch.any(out.favg)
+        assert not torch.any(out.face_f)
+
+
+def test_generator_matches_host_stream(stp, oracle):
+    """The device generator reproduces the documented SplitMix64 stream bit-exactly."""
+    S = stp
+    for n in (3, 8):
+        qd, pd = S.generate(0, 99, n, 7, 5, layout=S.LAYOUT_AOSOA, q_stride=9)
+        qh, ph = oracle.generate(0, 99, n, 7, 5)
+        assert np.array_equal(oracle.from_aosoa(n, 9, 9, qd.cpu().numpy()), qh)
+        assert np.array_equal(pd.cpu().numpy(), ph)
+
+
+def test_layout_conversion_roundtrip(stp, oracle):
+    S = stp
+    n, m, E = 6, 9, 7
+    q, _ = S.generate(0, 3, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=12)
+    aos = torch.empty(E, n ** 3 * 16, dtype=torch.float64, device="cuda")
+    back = torch.empty_like(q)
+    S.convert_layout(n, m, E, S.LAYOUT_AOSOA, 12, q, S.LAYOUT_AOS, 16, aos)
+    S.convert_layout(n, m, E, S.LAYOUT_AOS, 16, aos, S.LAYOUT_AOSOA, 12, back)
+    assert torch.equal(back, q)
+    a = aos.cpu().numpy().reshape(E, n ** 3, 16)
+    assert not np.any(a[:, :, m:])
+    assert np.array_equal(a[:, :, :m].reshape(E, -1), oracle.from_aosoa(n, m, 12, q.cpu().numpy()))
+
+
+@pytest.mark.parametrize("n", [4, 8, 10])
+def test_edge_batches(stp, n):
+    """0, 1 and odd element counts; deterministic (bit-identical reruns)."""
+    S = stp
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=12, par_kind=S.PAR_RHO_CP_CS)
+    q, par = S.generate(0, 1, n, 0, 3, layout=S.LAYOUT_AOSOA, q_stride=12)
+    out0 = plan.predict(q[:0], 1e-3, par=par[:0])
+    assert out0.qavg.shape[0] == 0
+    a = plan.predict(q[:1], 1e-3, par=par[:1])
+    b = plan.predict(q, 1e-3, par=par)
+    c = plan.predict(q, 1e-3, par=par)
+    plan.status()
+    assert torch.equal(a.qavg[0], b.qavg[0]) and torch.equal(b.qavg, c.qavg) and torch.equal(b.face_f, c.face_f)
+
+
+def test_input_checks(stp):
+    """validate_stp semantics: non-finite DOFs and invalid material are reported."""
+    S = stp
+    for n in (4, 8, 10):
+        plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=9, par_kind=S.PAR_LAMBDA_MU_RHO)
+        q = torch.zeros(2, n ** 3 * 9, dtype=torch.float64, device="cuda")
+        par = torch.tensor([[2.0, 1.0, 1.0], [2.0, 1.0, 1.0]], dtype=torch.float64, device="cuda")
+        plan.predict(q, 0.01, par=par)
+        plan.status()
+        q[1, 5] = float("nan")
+        plan.predict(q, 0.01, par=par)
+        with pytest.raises(S.StpError) as e:
+            plan.status()
+        assert e.value.code == S.ADERSTP_ERR_NONFINITE
+        q[1, 5] = 0.0
+        par[0, 0] = -3.0  # lambda + 2 mu <= 0
+        plan.predict(q, 0.01, par=par)
+        with pytest.raises(S.StpError) as e:
+            plan.status()
+        assert e.value.code == S.ADERSTP_ERR_MATERIAL
+        with pytest.raises(S.StpError):
+            plan.predict(q, 0.0, par=par)  # dt <= 0
+
+
+@pytest.mark.parametrize("n", [6, 8])
+def test_host_path_matches_device_path(stp, n):
+    S = stp
+    E = 1000
+    q, par = S.generate(0, 11, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=12)
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=12, par_kind=S.PAR_RHO_CP_CS)
+    plan.reserve_host_path(97)  # several chunks, ragged last chunk
+    dev = plan.predict(q, 2e-3, par=par)
+    host = plan.predict_host(q.cpu().numpy(), 2e-3, par=par.cpu().numpy())
+    for name in ("qavg", "favg", "face_q", "face_f"):
+        assert np.array_equal(getattr(dev, name).cpu().numpy(), getattr(host, name)), name
+
+
+def test_full_size_linearity_and_sampled_parity(stp, oracle):
+    """C3 at full size (131,072 elements): the STP is linear in q, so
+    STP(a q1 + b q2) = a STP(q1) + b STP(q2) per element; plus oracle parity on a sample."""
+    S = stp
+    n, E = 8, 131072
+    q1, par = S.generate(0, 21, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=12)
+    q2, _ = S.generate(0, 22, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=12)
+    dt = 0.5 / (3 * 6.0 * 15)
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=12, par_kind=S.PAR_RHO_CP_CS)
+    o1 = plan.predict(q1, dt, par=par)
+    o2 = plan.predict(q2, dt, par=par)
+    oc = plan.predict(0.75 * q1 - 1.25 * q2, dt, par=par)
+    plan.status()
+    for name in ("qavg", "face_q", "face_f"):
+        want = 0.75 * getattr(o1, name) - 1.25 * getattr(o2, name)
+        got = getattr(oc, name)
+        err = (got - want).abs().reshape(E, -1).amax(1) / want.abs().reshape(E, -1).amax(1)
+        assert float(err.max()) < 1e-12, name
+    idx = torch.tensor([0, 1, 4097, 65536, E - 1], device="cuda")
+    qs = q1[idx].cpu().numpy()
+    ref = oracle.stp(n, 9, oracle.from_aosoa(n, 9, 12, qs), dt, par=oracle.material_lmr(par[idx].cpu().numpy()))
+    got = oracle.from_aosoa(n, 9, 9, o1.qavg[idx].cpu().numpy())
+    assert O.per_element_rel_diff(ref.qavg, got) <= TOL
+    assert O.per_element_rel_diff(ref.face_f.reshape(5, -1), o1.face_f[idx].cpu().numpy().reshape(5, -1)) <= TOL
+
+
+def test_dense_volume_operator_taylor_series(stp, oracle):
+    """acceptance criterion 2: (N,m) = (4,9) elastic vs the dense V power series."""
+    S = stp
+    from test_oracle import _dense_volume_operator, _elastic_A, _taylor
+    n = 4
+    b = oracle.basis(n)
+    lam, mu, rho = 2.0, 1.0, 1.0
+    rng = np.random.default_rng(2024)
+    qc = rng.uniform(-1, 1, n ** 3 * 9)
+    dt = 0.4 / (3 * 2.0 * 7)
+    want = _taylor(_dense_volume_operator(b, _elastic_A(lam, mu, rho)), qc, n, dt)
+    plan = S.Plan(n, S.elastic_pde(lam, mu, rho), layout=S.LAYOUT_AOSOA)
+    out = plan.predict(torch.from_numpy(oracle.to_aosoa(n, 9, 9, qc[None])).cuda(), dt)
+    got = oracle.from_aosoa(n, 9, 9, out.qavg.cpu().numpy())[0]
+    assert O.rel_diff(want, got) < 1e-11
