@@ -1,19 +1,20 @@
 #!/usr/bin/env python3
 """Benchmark of the B200 linear ADER-DG Space-Time Predictor (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1..c4]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1..c5]
 
 A "step" is one pass of the STP (CK recursion + favg + 12 face arrays) over one batch of
-synthetic elastic elements.  Default workload (N=1): BASELINE config C3 -- order N=7 (nDof 8),
+synthetic elastic elements.  Default workload: BASELINE config C3 -- order N=7 (nDof 8),
 131,072 elements per GPU, padded AoSoA input with nVar padded to 12, per-element random
-material.  Under torchrun (N>1) every rank owns a contiguous element range (weak scaling, no
-collective on the hot path; NCCL only reduces the max step time and a checksum).
+material.  Under torchrun (N > 1) every rank owns a contiguous element range (weak scaling for
+c1-c4, strong scaling for c5) with no collective on the hot path; NCCL only reduces the max
+step time and a checksum after timing.
 
 `value` is device-resident throughput (inputs in HBM, CUDA events, max over ranks);
 `e2e` is the same metric through the public host-buffer API (aderstp_predict_batch_host) with
 pinned host inputs and outputs, copies inside the timed region.  `--impl reference` times the
-reference's own CPU implementation (oracle/_ref, the unmodified reference sources) on the host
-cores over a bounded sample of the same workload.
+reference's own CPU implementation (oracle/_ref = the unmodified reference sources compiled by
+oracle/Makefile) on the host cores over a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -29,19 +30,33 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2003_12787_b200.shard import (barrier, chunks, env_world, max_over_ranks,  # noqa: E402
+                                         strong_shard, sum_over_ranks, weak_shard)
+
 METRIC = "linear STP elements/s & fp64 GFLOP/s (% of roofline) vs order N, 1–8 B200"
 UNIT = "elements/s"
 
 # BASELINE.json configs (order N = polynomial degree, nDof = N+1)
 CONFIGS = {
-    "c1": dict(n=4, elems=64, dist=0, q_stride=9, desc="C1: elastic STP order N=3 (nDof 4), 64 elements, Q~U[-1,1]"),
-    "c2": dict(n=6, elems=32768, dist=2, q_stride=9, desc="C2: elastic STP order N=5 (nDof 6), 32,768 elements "
-               "(32^3 periodic grid), Q = 3 random-phase sinusoids per quantity"),
-    "c3": dict(n=8, elems=131072, dist=0, q_stride=12, desc="C3: elastic STP order N=7 (nDof 8), 131,072 elements/GPU, "
-               "padded AoSoA (nVar padded to 12), Q~U[-1,1], per-element random material"),
-    "c4": dict(n=10, elems=65536, dist=1, q_stride=9, desc="C4: elastic STP order N=9 (nDof 10), 65,536 elements, Q~N(0,1)"),
+    "c1": dict(n=4, elems=64, dist=0, q_stride=9,
+               desc="C1: elastic STP order N=3 (nDof 4), 64 elements, Q~U[-1,1]"),
+    "c2": dict(n=6, elems=32768, dist=2, q_stride=9,
+               desc="C2: elastic STP order N=5 (nDof 6), 32,768 elements (32^3 periodic grid), "
+                    "Q = 3 random-phase sinusoids per quantity"),
+    "c3": dict(n=8, elems=131072, dist=0, q_stride=12,
+               desc="C3: elastic STP order N=7 (nDof 8), 131,072 elements/GPU, padded AoSoA "
+                    "(nVar padded to 12), Q~U[-1,1], per-element random material"),
+    "c4": dict(n=10, elems=65536, dist=1, q_stride=9,
+               desc="C4: elastic STP order N=9 (nDof 10), 65,536 elements, Q~N(0,1)"),
+    # C5: 1,048,576 elements split evenly over the GPUs (strong scaling); a GPU streams its shard
+    # through fixed-size launches (inputs resident in HBM, output buffers reused per launch)
+    "c5": dict(n=8, elems=1048576, dist=0, q_stride=9, strong=True, chunk=131072,
+               desc="C5: elastic STP order N=7 (nDof 8), 1,048,576 elements split over the GPUs"),
+    "c5n6": dict(n=6, elems=1048576, dist=0, q_stride=9, strong=True, chunk=262144,
+                 desc="C5: elastic STP order N=5 (nDof 6), 1,048,576 elements split over the GPUs"),
 }
 SEED = 20031278
+REFERENCE_SAMPLE = {"c1": 64, "c2": 8192, "c3": 4096, "c4": 1024, "c5": 4096, "c5n6": 8192}
 
 
 def fp64_peak():
@@ -53,7 +68,7 @@ def fp64_peak():
 def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["hbm_gbs"]) * 1e9, "MEASURED_PEAKS.json hbm_gbs"
+            return float(json.load(f)["hbm_gbs"]) * 1e9, "MEASURED_PEAKS.json hbm_gbs (measured)"
     except Exception:
         return 6.65e12, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
@@ -110,11 +125,9 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def dist_setup(args):
+def dist_setup():
     import torch
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    world, rank, local = env_world()
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
@@ -124,58 +137,49 @@ def dist_setup(args):
     return world, rank, local
 
 
-def allreduce_max(x):
-    import torch
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized():
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-    return x
-
-
-def allreduce_sum(x):
-    import torch
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized():
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
-    return x
-
-
-def barrier():
-    import torch.distributed as dist
-    if dist.is_available() and dist.is_initialized():
-        dist.barrier()
-
-
 def load_traffic(cfg_name):
     """dram bytes per launch of the STP kernel from the committed ncu --set full summary."""
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
-        with open(path) as f:
-            d = json.load(f)
-        return d.get(cfg_name, {}).get("dram_bytes_per_launch")
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(cfg_name, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
 
-def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
-    """Device-resident timing of one config; returns a dict of per-rank-max numbers."""
-    import torch
-    n, E = cfg["n"], cfg["elems"]
-    grid = round(E ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
-    e0 = rank * E
-    q, par = S.generate(cfg["dist"], SEED, n, e0, E, grid=grid, layout=S.LAYOUT_AOSOA, q_stride=cfg["q_stride"])
-    cp_max = allreduce_max(float(par[:, 1].max().item()))
-    dt = S.stable_dt(n, cp_max, cfl=0.5)
-    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=cfg["q_stride"], out_stride=9,
+def shard_of(cfg, world, rank):
+    if cfg.get("strong"):
+        return strong_shard(cfg["elems"], world, rank)
+    return weak_shard(cfg["elems"], world, rank)
+
+
+def make_plan(S, cfg):
+    return S.Plan(cfg["n"], S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=cfg["q_stride"], out_stride=9,
                   par_kind=S.PAR_RHO_CP_CS, check_inputs=True)
-    out = plan.alloc_output(E)
+
+
+def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
+    """Device-resident timing of one config on this rank's shard (max over ranks)."""
+    import torch
+    n = cfg["n"]
+    sh = shard_of(cfg, world, rank)
+    grid = round(cfg["elems"] ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
+    q, par = S.generate(cfg["dist"], SEED, n, sh.start, sh.count, grid=grid, layout=S.LAYOUT_AOSOA,
+                        q_stride=cfg["q_stride"])
+    cp_max = max_over_ranks(float(par[:, 1].max().item()) if sh.count else 0.0, device="cuda")
+    dt = S.stable_dt(n, cp_max, cfl=0.5)
+    plan = make_plan(S, cfg)
+    chunk = max(1, min(cfg.get("chunk", sh.count), sh.count))
+    out = plan.alloc_output(chunk)
+    ranges = [(s0 - sh.start, c) for s0, c in chunks(sh, chunk)]
+
+    def step():
+        for off, c in ranges:
+            o = S.PredictorOutput(out.qavg[:c], out.favg[:c], out.face_q[:c], out.face_f[:c])
+            plan.predict(q[off:off + c], dt, par=par[off:off + c], out=o)
+
     stream = torch.cuda.current_stream()
     for _ in range(warmup):
-        plan.predict(q, dt, par=par, out=out)
+        step()
     plan.status()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -186,7 +190,7 @@ def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
         sampler.__enter__()
     ev0.record(stream)
     for _ in range(steps):
-        plan.predict(q, dt, par=par, out=out)
+        step()
     ev1.record(stream)
     torch.cuda.synchronize()
     if sampler:
@@ -195,18 +199,25 @@ def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
     ms = ev0.elapsed_time(ev1) / steps
     plan.status()
     checksum = float(out.qavg.sum().item()) + float(out.face_q.sum().item())
-    ms_max = allreduce_max(ms)
-    checksum = allreduce_sum(checksum)
-    return dict(ms=ms_max, dt=dt, checksum=checksum, clocks=sampler.summary() if sampler else None,
-                plan=plan, q=q, par=par, out=out)
+    res = dict(ms=max_over_ranks(ms, device="cuda"), dt=dt,
+               checksum=sum_over_ranks(checksum, device="cuda"),
+               clocks=sampler.summary() if sampler else None, plan=plan, shard=sh,
+               launches_per_step=len(ranges), elements_per_launch=chunk)
+    del q, par, out
+    return res
 
 
 def measure_e2e(S, plan, cfg, world, rank, dt, steps):
-    """Same metric through the host-buffer public API, pinned host memory, copies timed."""
+    """Same metric through the host-buffer public API (aderstp_predict_batch_host): pinned host
+    inputs and outputs, host->device and device->host copies inside the timed region.  One GPU
+    runs its full batch (<= 131,072 elements); with N > 1 ranks each rank uses <= 32,768 elements
+    so that N pinned copies fit in the host's memory."""
     import torch
-    n, E = cfg["n"], cfg["elems"]
-    grid = round(E ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
-    q_d, par_d = S.generate(cfg["dist"], SEED, n, rank * E, E, grid=grid, layout=S.LAYOUT_AOSOA,
+    n = cfg["n"]
+    sh = shard_of(cfg, world, rank)
+    E = min(sh.count, 131072 if world == 1 else 32768)
+    grid = round(cfg["elems"] ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
+    q_d, par_d = S.generate(cfg["dist"], SEED, n, sh.start, E, grid=grid, layout=S.LAYOUT_AOSOA,
                             q_stride=cfg["q_stride"])
     pin = lambda *shape: torch.empty(*shape, dtype=torch.float64, pin_memory=True)  # noqa: E731
     q_h = pin(E, plan.q_size)
@@ -222,19 +233,18 @@ def measure_e2e(S, plan, cfg, world, rank, dt, steps):
     t0 = time.perf_counter()
     for _ in range(steps):
         plan.predict_host(qn, dt, par=pn, out=out_h)
-    sec = (time.perf_counter() - t0) / steps
+    sec = max_over_ranks((time.perf_counter() - t0) / steps, device="cuda")
     barrier()
-    sec = allreduce_max(sec)
     h2d = E * (plan.q_size + 3) * 8
     d2h = E * (plan.out_size * 4 + plan.face_size * 12) * 8
     return dict(value=world * E / sec, unit=UNIT, h2d_bytes_per_step=h2d, d2h_bytes_per_step=d2h,
-                ms_per_step=sec * 1e3, steps=steps, api="aderstp_predict_batch_host (pinned host buffers)")
+                ms_per_step=sec * 1e3, steps=steps, elements_per_rank=E,
+                api="aderstp_predict_batch_host (pinned host buffers, copies pipelined on 3 streams)")
 
 
 def cpu_reference_run(cfg, sample, reps=3, threads=None):
-    """The reference's own CPU path (oracle/_ref) on `sample` elements; best of reps, faster of
+    """The reference's own CPU path (oracle/_ref) on `sample` elements: best of reps, faster of
     splitck / splitck_aosoa.  Falls back to our C port when _ref is absent."""
-    import numpy as np
     import oracle as O
     n = cfg["n"]
     orc = O.Oracle()
@@ -243,8 +253,7 @@ def cpu_reference_run(cfg, sample, reps=3, threads=None):
     lmr = orc.material_lmr(par)
     dt = O.cfl_dt(n, 6.0)
     threads = threads or (os.cpu_count() or 1)
-    best = math.inf
-    variant_used = None
+    best, variant_used = math.inf, None
     if O.reference_available():
         ref = O.Reference()
         kind = "reference"
@@ -261,21 +270,18 @@ def cpu_reference_run(cfg, sample, reps=3, threads=None):
             orc.stp(n, 9, q, dt, par=lmr, threads=threads)
             best = min(best, time.perf_counter() - t0)
         variant_used, lib = "oracle/stp_oracle.c", "libstp_oracle.so"
-    del np
     return dict(value=sample / best, unit=UNIT, cores=threads, kind=kind,
                 sample=f"{sample} elements of {cfg['desc'].split(':')[0]}, best of {reps} reps, "
-                       f"variant {variant_used} ({lib}), {threads} threads")
+                       f"variant {variant_used} ({lib}), {threads} threads, predict loop only")
 
 
 def run_reference_arm(args):
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
+    world, rank, _ = env_world()
     if rank != 0:
         return 0
     cfg = CONFIGS[args.config]
-    sample = {"c1": 64, "c2": 8192, "c3": 4096, "c4": 1024}[args.config]
-    values = []
-    info = None
+    sample = REFERENCE_SAMPLE[args.config]
+    values, info = [], None
     for i in range(args.warmup + args.steps):
         info = cpu_reference_run(cfg, sample, reps=1)
         if i >= args.warmup:
@@ -284,7 +290,8 @@ def run_reference_arm(args):
     info["value"] = value
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sample / value * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak",
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded SplitMix64, same generator as our arm)",
             "config": {"workload": cfg["desc"], "n_dof": cfg["n"], "order": cfg["n"] - 1,
                        "elements_per_step": sample},
@@ -292,6 +299,24 @@ def run_reference_arm(args):
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def roofline_of(S, n, per_gpu, elements_per_launch, traffic):
+    flop_e, byte_e = S.flop_count(n, 9), S.byte_count(n, 9, True)
+    fp64 = fp64_peak()
+    hbm, hbm_src = hbm_peak()
+    tf = per_gpu * flop_e / 1e12
+    gbs = per_gpu * byte_e / 1e9
+    roof = min(fp64 / flop_e, hbm / byte_e)
+    common = {"traffic": traffic, "flop_per_element": flop_e, "byte_per_element": byte_e,
+              "roofline_elements_per_s": roof, "elements_per_launch": elements_per_launch}
+    if fp64 / flop_e < hbm / byte_e:
+        return dict({"bound": "fp64", "achieved": tf, "peak": fp64 / 1e12, "unit": "TFLOP/s",
+                     "frac": tf / (fp64 / 1e12),
+                     "peak_source": "measured DMMA fp64 peak, profiles/fp64_peaks_r01.txt",
+                     "hbm_achieved_gbs": gbs, "hbm_frac": gbs / (hbm / 1e9)}, **common)
+    return dict({"bound": "hbm", "achieved": gbs, "peak": hbm / 1e9, "unit": "GB/s", "frac": gbs / (hbm / 1e9),
+                 "peak_source": hbm_src, "fp64_achieved_tflops": tf, "fp64_frac": tf / (fp64 / 1e12)}, **common)
 
 
 def main():
@@ -310,38 +335,17 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args)
 
-    import torch
     import paper_2003_12787_b200 as S
 
-    world, rank, local = dist_setup(args)
+    world, rank, _ = dist_setup()
     cfg = CONFIGS[args.config]
-    n, E = cfg["n"], cfg["elems"]
+    n = cfg["n"]
     res = measure_device(S, cfg, world, rank, args.steps, args.warmup)
     ms = res["ms"]
-    value = world * E / (ms * 1e-3)
-    flop_e = S.flop_count(n, 9)
-    byte_e = S.byte_count(n, 9, True)
-    per_gpu = E / (ms * 1e-3)
-    fp64 = fp64_peak()
-    hbm, hbm_src = hbm_peak()
-    achieved_tf = per_gpu * flop_e / 1e12
-    achieved_gbs = per_gpu * byte_e / 1e9
-    roof_elem = min(fp64 / flop_e, hbm / byte_e)
-    bound = "fp64" if fp64 / flop_e < hbm / byte_e else "hbm"
-    traffic = load_traffic(args.config)
-    if bound == "fp64":
-        roofline = {"bound": "fp64", "achieved": achieved_tf, "peak": fp64 / 1e12, "unit": "TFLOP/s",
-                    "frac": achieved_tf / (fp64 / 1e12), "traffic": traffic,
-                    "peak_source": "measured DMMA fp64 peak, profiles/fp64_peaks_r01.txt (not in MEASURED_PEAKS.json)",
-                    "flop_per_element": flop_e, "byte_per_element": byte_e,
-                    "hbm_achieved_gbs": achieved_gbs, "hbm_frac": achieved_gbs / (hbm / 1e9),
-                    "roofline_elements_per_s": roof_elem, "elements_per_launch": E}
-    else:
-        roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm / 1e9, "unit": "GB/s",
-                    "frac": achieved_gbs / (hbm / 1e9), "traffic": traffic, "peak_source": hbm_src,
-                    "flop_per_element": flop_e, "byte_per_element": byte_e,
-                    "fp64_achieved_tflops": achieved_tf, "fp64_frac": achieved_tf / (fp64 / 1e12),
-                    "roofline_elements_per_s": roof_elem, "elements_per_launch": E}
+    total = cfg["elems"] if cfg.get("strong") else world * cfg["elems"]
+    value = total / (ms * 1e-3)
+    per_gpu = value / world
+    roofline = roofline_of(S, n, per_gpu, res["elements_per_launch"], load_traffic(args.config))
 
     e2e = None
     if not args.no_e2e:
@@ -353,34 +357,39 @@ def main():
             if name == args.config:
                 continue
             c = CONFIGS[name]
-            r = measure_device(S, c, world, rank, max(5, args.steps // 4), 3, want_clocks=False)
+            r = measure_device(S, c, 1, 0, max(5, args.steps // 4), 3, want_clocks=False)
             pg = c["elems"] / (r["ms"] * 1e-3)
-            fe, be = S.flop_count(c["n"], 9), S.byte_count(c["n"], 9, True)
-            roof = min(fp64 / fe, hbm / be)
+            rf = roofline_of(S, c["n"], pg, c["elems"], load_traffic(name))
             others[name] = {"workload": c["desc"], "elements_per_s": pg, "ms_per_step": r["ms"],
-                            "fp64_gflops": pg * fe / 1e9, "achieved_gbs": pg * be / 1e9,
-                            "roofline_elements_per_s": roof, "frac_of_roofline": pg / roof,
-                            "bound": "fp64" if fp64 / fe < hbm / be else "hbm"}
-            del r
+                            "fp64_gflops": pg * rf["flop_per_element"] / 1e9,
+                            "achieved_gbs": pg * rf["byte_per_element"] / 1e9,
+                            "roofline_elements_per_s": rf["roofline_elements_per_s"],
+                            "frac_of_roofline": pg / rf["roofline_elements_per_s"], "bound": rf["bound"]}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_run(cfg, 16384 if n <= 8 else 4096)
 
     if rank == 0:
+        sh = res["shard"]
+        E = sh.count
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64",
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded SplitMix64 stream, generated on device; per-element rho~U[2,3], "
                         "cp~U[4,6], cs~U[2,3.5])",
                 "config": {"workload": cfg["desc"], "order": n - 1, "n_dof": n, "elements_per_gpu": E,
-                           "global_elements": world * E, "parallelism": f"element shards x{world} (no hot-path collective)",
+                           "global_elements": total,
+                           "parallelism": f"element shards x{world} (no hot-path collective)",
+                           "launches_per_step": res["launches_per_step"],
                            "layout": f"AoSoA [e][k3][k2][s<{cfg['q_stride']}][k1] in, [e][k3][k2][9][k1] out",
                            "dt": res["dt"], "cfl": 0.5,
                            "l2": "no flush needed: inputs %.1f GB and outputs %.1f GB per step >> 126 MB L2" % (
-                               E * n ** 3 * cfg["q_stride"] * 8 / 1e9, E * (4 * n ** 3 * 9 + 12 * n * n * 9) * 8 / 1e9)},
-                "fp64_gflops_per_gpu": achieved_tf * 1e3,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": args.steps,
+                               E * n ** 3 * cfg["q_stride"] * 8 / 1e9,
+                               E * (4 * n ** 3 * 9 + 12 * n * n * 9) * 8 / 1e9)},
+                "fp64_gflops_per_gpu": per_gpu * roofline["flop_per_element"] / 1e9,
+                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": args.steps * res["launches_per_step"],
                 "clocks": res["clocks"], "checksum": res["checksum"], "other_configs": others}
         print(json.dumps(line), flush=True)
     import torch.distributed as dist
