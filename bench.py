@@ -137,11 +137,14 @@ def dist_setup():
     return world, rank, local
 
 
-def load_traffic(cfg_name):
-    """dram bytes per launch of the STP kernel from the committed ncu --set full summary."""
+def load_traffic(cfg_name, elements_per_launch):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the STP kernel, from the
+    committed ncu --set full capture (profiles/ncu_summary.json, measured per element and scaled
+    to this run's launch size)."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f).get(cfg_name, {}).get("dram_bytes_per_launch")
+            per = json.load(f).get(cfg_name, {}).get("dram_bytes_per_element")
+        return None if per is None else per * elements_per_launch
     except Exception:
         return None
 
@@ -345,7 +348,8 @@ def main():
     total = cfg["elems"] if cfg.get("strong") else world * cfg["elems"]
     value = total / (ms * 1e-3)
     per_gpu = value / world
-    roofline = roofline_of(S, n, per_gpu, res["elements_per_launch"], load_traffic(args.config))
+    roofline = roofline_of(S, n, per_gpu, res["elements_per_launch"],
+                           load_traffic("c3" if args.config == "c5" else args.config, res["elements_per_launch"]))
 
     e2e = None
     if not args.no_e2e:
@@ -359,7 +363,7 @@ def main():
             c = CONFIGS[name]
             r = measure_device(S, c, 1, 0, max(5, args.steps // 4), 3, want_clocks=False)
             pg = c["elems"] / (r["ms"] * 1e-3)
-            rf = roofline_of(S, c["n"], pg, c["elems"], load_traffic(name))
+            rf = roofline_of(S, c["n"], pg, c["elems"], load_traffic(name, c["elems"]))
             others[name] = {"workload": c["desc"], "elements_per_s": pg, "ms_per_step": r["ms"],
                             "fp64_gflops": pg * rf["flop_per_element"] / 1e9,
                             "achieved_gbs": pg * rf["byte_per_element"] / 1e9,
