@@ -41,6 +41,8 @@ struct LaunchPlan {
   int force_generic = 0;             // env ADERSTP_FORCE_GENERIC=1: skip specialised kernels
   int dmma8_double_buffer = 0;       // env ADERSTP_DMMA8_DB=1: 2 CTAs/SM double-buffered variant
   int no_dmma8 = 0;                  // env ADERSTP_NO_DMMA8=1: nDof 8 on the line-pass kernel
+  int pass_slots = 6;                // line-pass tasks per line (6 by source, 8 by target)
+  int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel
 };
 
 struct BatchArgs {
@@ -67,6 +69,10 @@ bool kernel_available(int n);
 // stp_dmma8.cu: nDof = 8 elastic kernel on the fp64 tensor cores
 bool dmma8_applicable(const LaunchPlan& p);
 cudaError_t init_dmma8(const LaunchPlan& p);  // once per device, at plan creation
+// stp_dmma.cu: nDof 4..7 on zero-padded 8x8 DMMA tiles
+bool dmmap_applicable(const LaunchPlan& p);
+cudaError_t init_dmmap(const LaunchPlan& p);
+cudaError_t launch_dmmap(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 // stp_pass.cu: line-pass elastic kernel for every order (even/odd split D, uniform operands)
 bool pass_applicable(const LaunchPlan& p);
 cudaError_t init_pass(const LaunchPlan& p);

@@ -160,6 +160,10 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     lp.dmma8_double_buffer = (db && db[0] == '1') ? 1 : 0;
     const char* nd = std::getenv("ADERSTP_NO_DMMA8");
     lp.no_dmma8 = (nd && nd[0] == '1') ? 1 : 0;
+    const char* nq = std::getenv("ADERSTP_NO_DMMAP");
+    lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
+    const char* ps = std::getenv("ADERSTP_PASS_SLOTS");
+    lp.pass_slots = (ps && ps[0] == '8') ? 8 : (ps && ps[0] == '1' && ps[1] == '2') ? 12 : 6;
   }
   aderstp::make_host_basis(n, &lp.basis);
 
@@ -239,6 +243,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   if (e == cudaSuccess) e = cudaMemset(lp.d_status, 0, sizeof(unsigned int));
   if (e == cudaSuccess && aderstp::dmma8_applicable(lp)) e = aderstp::init_dmma8(lp);
   if (e == cudaSuccess && aderstp::pass_applicable(lp)) e = aderstp::init_pass(lp);
+  if (e == cudaSuccess && aderstp::dmmap_applicable(lp)) e = aderstp::init_dmmap(lp);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "plan_create");

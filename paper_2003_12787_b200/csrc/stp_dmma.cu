@@ -1,0 +1,422 @@
+// Elastic STP on the fp64 tensor cores for nDof 4..7: the stp_dmma8.cu scheme on zero-padded
+// 8 x 8 (k2, k1) planes.  (The nDof 8 kernel is the unpadded special case; see that file for the
+// full description.)
+//
+// One CTA = one element, 8 warps; lane (g, t) owns nodes (k2 = g, k1 = 2t, 2t+1) of every k3
+// plane (k3 < N).  Rows and columns k2, k1 >= N and the rows/columns of D beyond N are exact
+// zeros, so every 8x8x4 DMMA (x: A = p slice, B = c D^T; y: A = c D, B = p slice) produces exact
+// zeros on the padding and the real nodes see exactly the N-term sums; N <= 4 needs a single
+// k-step.  z contractions: register DFMA over the N planes with D from the constant cache.
+// Roles (no redundant derivative fields): velocities (warps 0-2), shear (3, 6, 7), normal
+// stresses on two k3 halves sharing Dx u, Dy v, Dz w (4, 5).  Shared memory: p and the qavg
+// accumulator, 2 x 9 x N x 64 doubles, XOR-swizzled rows (bank-conflict free fragment loads).
+#include <cstdint>
+
+#include "../../include/aderstp.h"
+#include "aderstp_internal.h"
+
+// zero-padded 8 x 8 D per order (row k = node, col l), uploaded at plan creation
+extern "C" {
+__constant__ double aderstp_kDP[9 * 64];
+}
+
+namespace aderstp {
+
+namespace {
+
+constexpr int NVP = 9;
+constexpr int NWP = 8;
+constexpr int THREADSP = NWP * 32;
+
+template <int N>
+struct GeoP {
+  static constexpr int PV = N * 64;                  // one quantity: N planes of 8 x 8
+  static constexpr int FACE = N * N * NVP;           // one face array
+  static constexpr int SMEM = 2 * NVP * PV * 8;      // p + qavg accumulator
+  static constexpr int KS = N > 4 ? 2 : 1;           // k-steps of 4
+  static constexpr int H0 = (N + 1) / 2, H1 = N / 2; // normal-stress k3 halves
+};
+
+struct ParamsP {
+  double d[64];      // zero-padded D
+  double phi[2][8];  // zero-padded phi(0), phi(1)
+  int check, par_kind, q_stride;
+};
+
+__constant__ int kRoleP[NWP] = {6, 7, 8, 4, -1, -2, 3, 5};
+__constant__ int kInP[NVP][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
+                                 {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+__constant__ int kCoefP[NVP][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
+                                   {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
+__constant__ int kOutNP[NVP] = {1, 1, 1, 3, 3, 3, 5, 5, 5};
+__constant__ int kOutP[NVP][5][3] = {
+    {{6, 0, 3}}, {{7, 1, 3}}, {{8, 2, 3}},
+    {{6, 1, 3}, {7, 0, 3}, {3, 2, 4}},
+    {{6, 2, 3}, {8, 0, 3}, {4, 1, 4}},
+    {{7, 2, 3}, {8, 1, 3}, {5, 0, 4}},
+    {{0, 0, 0}, {1, 0, 1}, {2, 0, 1}, {3, 1, 2}, {4, 2, 2}},
+    {{0, 1, 1}, {1, 1, 0}, {2, 1, 1}, {3, 0, 2}, {5, 2, 2}},
+    {{0, 2, 1}, {1, 2, 1}, {2, 2, 0}, {4, 0, 2}, {5, 1, 2}}};
+
+__device__ __forceinline__ double ldcp(const double* p) {
+  double v;
+  asm volatile("{\n .reg .u64 ca;\n cvta.to.const.u64 ca, %1;\n ld.const.f64 %0, [ca];\n}\n" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int physp(int k2, int k1) { return k2 * 8 + (k1 ^ ((k2 & 2) << 1)); }
+__device__ __forceinline__ void dmmap(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double selp(const double c[4], int i) {
+  return i == 0 ? c[0] : i == 1 ? c[1] : i == 2 ? c[2] : i == 3 ? c[3] : 0.0;
+}
+__device__ __forceinline__ double2 lds2p(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ void sts2p(double* p, double a, double b) {
+  *reinterpret_cast<double2*>(p) = make_double2(a, b);
+}
+
+template <int N, int NT>
+__device__ __forceinline__ void mma_xp(double (&acc)[NT][2], const double* f, int K0, int g, int t, double b0,
+                                       double b1) {
+  const double* p0 = f + K0 * 64 + physp(g, t);
+  const double* p1 = f + K0 * 64 + physp(g, 4 + t);
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    dmmap(acc[k][0], acc[k][1], p0[k * 64], b0);
+    if (GeoP<N>::KS > 1) dmmap(acc[k][0], acc[k][1], p1[k * 64], b1);
+  }
+}
+
+template <int N, int NT>
+__device__ __forceinline__ void mma_yp(double (&acc)[NT][2], const double* f, int K0, int g, int t, double a0,
+                                       double a1) {
+  const double* p0 = f + K0 * 64 + physp(t, g);
+  const double* p1 = f + K0 * 64 + physp(4 + t, g);
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    dmmap(acc[k][0], acc[k][1], a0, p0[k * 64]);
+    if (GeoP<N>::KS > 1) dmmap(acc[k][0], acc[k][1], a1, p1[k * 64]);
+  }
+}
+
+// acc[k][j] += sum_{l<N} D[K0+k][l] (c f[l]) on the lane's two columns
+template <int N, int NT>
+__device__ __forceinline__ void dfma_zp(double (&acc)[NT][2], const double* f, int K0, int col, double c) {
+  const double* dz = &aderstp_kDP[N * 64];
+#pragma unroll
+  for (int l = 0; l < N; ++l) {
+    const double2 v = lds2p(f + l * 64 + col);
+    const double c0 = c * v.x, c1 = c * v.y;
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double dk = ldcp(dz + (K0 + k) * 8 + l);
+      acc[k][0] = fma(dk, c0, acc[k][0]);
+      acc[k][1] = fma(dk, c1, acc[k][1]);
+    }
+  }
+}
+
+// normal stresses on planes K0 .. K0+NT-1: a = Dx u, b = Dy v, c = Dz w, then
+// t_ii = lambda (a+b+c) + 2 mu {a,b,c}_i; qavg += coeff t; t -> p (after the read barrier)
+template <int N, int NT>
+__device__ __forceinline__ void normal_step(double* P, double* QA, int K0, int g, int t, int col, double d0,
+                                            double d1, double lam, double two_mu, double coeff, bool last) {
+  constexpr int PV = GeoP<N>::PV;
+  double ta[NT][2], tb[NT][2], tc[NT][2];
+#pragma unroll
+  for (int k = 0; k < NT; ++k) ta[k][0] = ta[k][1] = tb[k][0] = tb[k][1] = tc[k][0] = tc[k][1] = 0.0;
+  mma_xp<N, NT>(ta, P + 6 * PV, K0, g, t, d0, d1);
+  mma_yp<N, NT>(tb, P + 7 * PV, K0, g, t, d0, d1);
+  dfma_zp<N, NT>(tc, P + 8 * PV, K0, col, 1.0);
+#pragma unroll
+  for (int k = 0; k < NT; ++k)
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const double sum = lam * (ta[k][j] + tb[k][j] + tc[k][j]);
+      ta[k][j] = fma(two_mu, ta[k][j], sum);
+      tb[k][j] = fma(two_mu, tb[k][j], sum);
+      tc[k][j] = fma(two_mu, tc[k][j], sum);
+    }
+#pragma unroll
+  for (int k = 0; k < NT; ++k) {
+    const int off = (K0 + k) * 64 + col;
+    const double2 va = lds2p(QA + off), vb = lds2p(QA + PV + off), vc = lds2p(QA + 2 * PV + off);
+    sts2p(QA + off, fma(coeff, ta[k][0], va.x), fma(coeff, ta[k][1], va.y));
+    sts2p(QA + PV + off, fma(coeff, tb[k][0], vb.x), fma(coeff, tb[k][1], vb.y));
+    sts2p(QA + 2 * PV + off, fma(coeff, tc[k][0], vc.x), fma(coeff, tc[k][1], vc.y));
+  }
+  __syncthreads();  // every warp has finished reading p (single buffer)
+  if (!last) {
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int off = (K0 + k) * 64 + col;
+      sts2p(P + off, ta[k][0], ta[k][1]);
+      sts2p(P + PV + off, tb[k][0], tb[k][1]);
+      sts2p(P + 2 * PV + off, tc[k][0], tc[k][1]);
+    }
+  }
+}
+
+template <int N>
+__global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsigned int* status) {
+  using G = GeoP<N>;
+  constexpr int PV = G::PV, FACE = G::FACE;
+  extern __shared__ __align__(16) double smq[];
+  double* P = smq;
+  double* QA = smq + NVP * PV;
+  const long long e = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int col = physp(g, 2 * t);
+  unsigned int flags = 0;
+  const double dt = a.dt;
+
+  double c4[4];
+  {
+    const double p0 = a.par[3 * e], p1 = a.par[3 * e + 1], p2 = a.par[3 * e + 2];
+    double lam, mu, rho;
+    if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
+      rho = p0;
+      mu = __dmul_rn(__dmul_rn(p0, p2), p2);
+      lam = __dsub_rn(__dmul_rn(__dmul_rn(p0, p1), p1), __dmul_rn(2.0, mu));
+    } else {
+      lam = p0;
+      mu = p1;
+      rho = p2;
+    }
+    if (!((rho > 0.0) && (mu >= 0.0) && (lam + 2.0 * mu > 0.0))) flags |= 2u;
+    c4[0] = lam + 2.0 * mu;
+    c4[1] = lam;
+    c4[2] = mu;
+    c4[3] = 1.0 / rho;
+  }
+
+  // ---- stage q into the padded planes (padding = 0) and QA = dt q -----------------------
+  // (s, k3, k2 < 8, k1-pair < 4) positions, IT per thread; every load is issued before the
+  // first shared store so the DRAM latencies overlap
+  {
+    const int qs = kp.q_stride;
+    const double* qe = a.q + e * (long long)(N * N * N * qs);
+    constexpr int PAIRS = NVP * N * 32;
+    constexpr int IT = (PAIRS + THREADSP - 1) / THREADSP;
+    double v0[IT], v1[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int i = tid + it * THREADSP;
+      const int kp2 = i & 3, k2 = (i >> 2) & 7, r = i >> 5;  // r = s * N + k3
+      const int s = r / N, k3 = r - s * N;
+      const int k1 = 2 * kp2;
+      v0[it] = v1[it] = 0.0;
+      if (i < PAIRS && k2 < N) {
+        const double* src = qe + ((k3 * N + k2) * qs + s) * N;
+        if (k1 < N) v0[it] = __ldcs(src + k1);
+        if (k1 + 1 < N) v1[it] = __ldcs(src + k1 + 1);
+      }
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int i = tid + it * THREADSP;
+      if (i >= PAIRS) continue;
+      const int kp2 = i & 3, k2 = (i >> 2) & 7, r = i >> 5;
+      const int s = r / N, k3 = r - s * N;
+      if (kp.check && !(isfinite(v0[it]) && isfinite(v1[it]))) flags |= 1u;
+      const int j = s * PV + k3 * 64 + physp(k2, 2 * kp2);
+      sts2p(P + j, v0[it], v1[it]);
+      sts2p(QA + j, dt * v0[it], dt * v1[it]);
+    }
+  }
+  __syncthreads();
+
+  const int role = kRoleP[warp];
+  const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];
+
+  double coeff = dt;
+  if (role >= 0) {
+    const int s = role;
+    const int in_x = kInP[s][0], in_y = kInP[s][1], in_z = kInP[s][2];
+    const double cx = selp(c4, kCoefP[s][0]), cy = selp(c4, kCoefP[s][1]), cz = selp(c4, kCoefP[s][2]);
+    const bool has_x = kCoefP[s][0] != 4, has_y = kCoefP[s][1] != 4, has_z = kCoefP[s][2] != 4;
+    const double bx0 = cx * d0, bx1 = cx * d1, ay0 = cy * d0, ay1 = cy * d1;
+    const int own = s * PV + col;
+#pragma unroll 1
+    for (int o = 1; o < N; ++o) {
+      double tt[N][2];
+#pragma unroll
+      for (int k3 = 0; k3 < N; ++k3) tt[k3][0] = tt[k3][1] = 0.0;
+      if (has_x) mma_xp<N, N>(tt, P + in_x * PV, 0, g, t, bx0, bx1);
+      if (has_y) mma_yp<N, N>(tt, P + in_y * PV, 0, g, t, ay0, ay1);
+      if (has_z) dfma_zp<N, N>(tt, P + in_z * PV, 0, col, cz);
+      coeff *= dt / (o + 1);
+#pragma unroll
+      for (int k3 = 0; k3 < N; ++k3) {
+        const double2 v = lds2p(QA + own + k3 * 64);
+        sts2p(QA + own + k3 * 64, fma(coeff, tt[k3][0], v.x), fma(coeff, tt[k3][1], v.y));
+      }
+      __syncthreads();
+      if (o + 1 < N) {
+#pragma unroll
+        for (int k3 = 0; k3 < N; ++k3) sts2p(P + own + k3 * 64, tt[k3][0], tt[k3][1]);
+      }
+      __syncthreads();
+    }
+  } else {
+    const int h = -role - 1;
+    const double lam = c4[1], two_mu = 2.0 * c4[2];
+#pragma unroll 1
+    for (int o = 1; o < N; ++o) {
+      coeff *= dt / (o + 1);
+      if (h == 0) normal_step<N, G::H0>(P, QA, 0, g, t, col, d0, d1, lam, two_mu, coeff, o + 1 == N);
+      else normal_step<N, G::H1>(P, QA, G::H0, g, t, col, d0, d1, lam, two_mu, coeff, o + 1 == N);
+      __syncthreads();
+    }
+  }
+
+  // ---- epilogue: 9 quantities x k3 planes over the 8 warps ------------------------------
+  double* FQ = smq;  // face staging [6][N][N][9] over the dead p buffer
+  const bool faces = a.face_q || a.face_f;
+  const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0;
+  const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
+  const bool rowok = g < N;
+  const bool k1a = 2 * t < N, k1b = 2 * t + 1 < N;
+  // qavg / favg: units (quantity s, plane k3), 9 N of them round-robin over the 8 warps
+  {
+    double* qout = a.qavg + e * (long long)(N * N * N * NVP);
+    double* fout = a.favg ? a.favg + e * (long long)(3 * N * N * N * NVP) : nullptr;
+#pragma unroll 1
+    for (int u = warp; u < NVP * N; u += NWP) {
+      const int s = u / N, k3 = u - s * N;
+      const double2 v = lds2p(QA + s * PV + k3 * 64 + col);
+      if (rowok) {
+        const int base = ((k3 * N + g) * NVP + s) * N + 2 * t;
+        if (k1a) __stcs(qout + base, v.x);
+        if (k1b) __stcs(qout + base + 1, v.y);
+        if (fout) {
+          const int nout = kOutNP[s];
+          for (int k = 0; k < nout; ++k) {
+            const int so = kOutP[s][k][0], d = kOutP[s][k][1];
+            const double c = selp(c4, kOutP[s][k][2]);
+            const int fb = d * (N * N * N * NVP) + ((k3 * N + g) * NVP + so) * N + 2 * t;
+            if (k1a) __stcs(fout + fb, c * v.x);
+            if (k1b) __stcs(fout + fb + 1, c * v.y);
+          }
+        }
+      }
+    }
+  }
+  if (faces) {
+#pragma unroll 1
+    for (int u = warp; u < NVP * N; u += NWP) {
+      const int s = u / N, k3 = u - s * N;
+      const double* qs = QA + s * PV;
+      double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+      dmmap(x0, x1, qs[k3 * 64 + physp(g, t)], bphi0);
+      if (G::KS > 1) dmmap(x0, x1, qs[k3 * 64 + physp(g, 4 + t)], bphi1);
+      dmmap(y0, y1, bphi0, qs[k3 * 64 + physp(t, g)]);
+      if (G::KS > 1) dmmap(y0, y1, bphi1, qs[k3 * 64 + physp(4 + t, g)]);
+      if (t == 0 && g < N) {
+        FQ[0 * FACE + (k3 * N + g) * NVP + s] = x0;
+        FQ[1 * FACE + (k3 * N + g) * NVP + s] = x1;
+      }
+      if (g < 2) {
+        if (k1a) FQ[(2 + g) * FACE + (k3 * N + 2 * t) * NVP + s] = y0;
+        if (k1b) FQ[(2 + g) * FACE + (k3 * N + 2 * t + 1) * NVP + s] = y1;
+      }
+    }
+#pragma unroll 1
+    for (int s = warp; s < NVP; s += NWP) {
+      const double* qs = QA + s * PV;
+      if (rowok) {
+        double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0};
+#pragma unroll
+        for (int k3 = 0; k3 < N; ++k3) {
+          const double2 v = lds2p(qs + k3 * 64 + col);
+          z0[0] = fma(kp.phi[0][k3], v.x, z0[0]);
+          z0[1] = fma(kp.phi[0][k3], v.y, z0[1]);
+          z1[0] = fma(kp.phi[1][k3], v.x, z1[0]);
+          z1[1] = fma(kp.phi[1][k3], v.y, z1[1]);
+        }
+        if (k1a) {
+          FQ[4 * FACE + (g * N + 2 * t) * NVP + s] = z0[0];
+          FQ[5 * FACE + (g * N + 2 * t) * NVP + s] = z1[0];
+        }
+        if (k1b) {
+          FQ[4 * FACE + (g * N + 2 * t + 1) * NVP + s] = z0[1];
+          FQ[5 * FACE + (g * N + 2 * t + 1) * NVP + s] = z1[1];
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < 252) {
+      const int so = tid % NVP, ab0 = tid / NVP;  // 28 in-face nodes per sweep
+      double* oq = a.face_q ? a.face_q + e * (long long)(6 * FACE) : nullptr;
+      double* of = a.face_f ? a.face_f + e * (long long)(6 * FACE) : nullptr;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const double c = selp(c4, kCoefP[so][d]);
+        const int src = kInP[so][d];
+#pragma unroll
+        for (int sd = 0; sd < 2; ++sd)
+          for (int ab = ab0; ab < N * N; ab += 28) {
+            const int base = (2 * d + sd) * FACE + ab * NVP;
+            if (oq) __stcs(oq + base + so, FQ[base + so]);
+            if (of) __stcs(of + base + so, c * FQ[base + src]);
+          }
+      }
+    }
+  }
+  if (kp.check && flags) atomicOr(status, flags);
+}
+
+template <int N>
+cudaError_t launch_dmmap_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
+  using G = GeoP<N>;
+  ParamsP kp;
+  for (int i = 0; i < 64; ++i) kp.d[i] = 0.0;
+  for (int k = 0; k < N; ++k)
+    for (int l = 0; l < N; ++l) kp.d[k * 8 + l] = p.basis.d[k * N + l];
+  for (int j = 0; j < 8; ++j) {
+    kp.phi[0][j] = j < N ? p.basis.face_left[j] : 0.0;
+    kp.phi[1][j] = j < N ? p.basis.face_right[j] : 0.0;
+  }
+  kp.check = p.check;
+  kp.par_kind = p.par_kind;
+  kp.q_stride = p.q_stride;
+  auto kern = stp_dmmap_kernel<N>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (err != cudaSuccess) return err;
+  if (a.n_elem == 0) return cudaSuccess;
+  if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kern<<<(unsigned)a.n_elem, THREADSP, G::SMEM, stream>>>(kp, a, p.d_status);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool dmmap_applicable(const LaunchPlan& p) {
+  return p.n >= 4 && p.n <= 7 && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
+         p.layout == ADERSTP_LAYOUT_AOSOA && p.out_stride == 9 && p.q_stride >= 9 && p.q_stride <= 64;
+}
+
+cudaError_t init_dmmap(const LaunchPlan& p) {
+  double buf[64] = {0};
+  for (int k = 0; k < p.n; ++k)
+    for (int l = 0; l < p.n; ++l) buf[k * 8 + l] = p.basis.d[k * p.n + l];
+  return cudaMemcpyToSymbol(aderstp_kDP, buf, sizeof(buf), sizeof(double) * 64 * p.n);
+}
+
+cudaError_t launch_dmmap(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
+  switch (p.n) {
+    case 4: return launch_dmmap_n<4>(p, a, stream);
+    case 5: return launch_dmmap_n<5>(p, a, stream);
+    case 6: return launch_dmmap_n<6>(p, a, stream);
+    case 7: return launch_dmmap_n<7>(p, a, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace aderstp

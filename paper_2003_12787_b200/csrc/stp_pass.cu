@@ -30,6 +30,12 @@
 // stored at offset order*80.
 extern "C" {
 __constant__ double aderstp_kEO[11 * 80];
+#ifdef ADERSTP_EXPT_TIMING
+__device__ long long aderstp_dbg_clock[4096 * 8];
+int aderstp_dbg_clock_copy(long long* host, int count) {
+  return (int)cudaMemcpyFromSymbol(host, aderstp_dbg_clock, sizeof(long long) * count);
+}
+#endif
 }
 
 namespace aderstp {
@@ -47,13 +53,22 @@ __constant__ PassSlot kPass[3][6] = {
     {{6, 3, {0, 1, 2}, {0, 1, 1}}, {7, 1, {3}, {2}}, {8, 1, {4}, {2}}, {0, 1, {6}, {3}}, {3, 1, {7}, {3}}, {4, 1, {8}, {3}}},
     {{7, 3, {0, 1, 2}, {1, 0, 1}}, {6, 1, {3}, {2}}, {8, 1, {5}, {2}}, {3, 1, {6}, {3}}, {1, 1, {7}, {3}}, {5, 1, {8}, {3}}},
     {{8, 3, {0, 1, 2}, {1, 1, 0}}, {6, 1, {4}, {2}}, {7, 1, {5}, {2}}, {4, 1, {6}, {3}}, {5, 1, {7}, {3}}, {2, 1, {8}, {3}}}};
+// target-balanced variant: 8 single-target tasks per line and pass (the three normal-stress
+// targets each recompute the derivative of their common source; +1/3 fp64, no divergence)
+struct PassTask {
+  int8_t src, tgt, coef;
+};
+__constant__ PassTask kPass8[3][8] = {
+    {{6, 0, 0}, {6, 1, 1}, {6, 2, 1}, {7, 3, 2}, {8, 4, 2}, {0, 6, 3}, {3, 7, 3}, {4, 8, 3}},
+    {{7, 0, 1}, {7, 1, 0}, {7, 2, 1}, {6, 3, 2}, {8, 5, 2}, {3, 6, 3}, {1, 7, 3}, {5, 8, 3}},
+    {{8, 0, 1}, {8, 1, 1}, {8, 2, 0}, {6, 4, 2}, {7, 5, 2}, {4, 6, 3}, {5, 7, 3}, {2, 8, 3}}};
 // flux table for favg / face_f: F_d(q)_s = coef(s,d) q[in(s,d)], coef 4 = 0
 __constant__ int8_t kInE[NVE][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
                                     {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
 __constant__ int8_t kCoefE[NVE][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
                                       {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
 
-template <int N>
+template <int N, int SL = 6>
 struct Geo {
   static constexpr int H = N / 2;
   static constexpr int RS = (N % 2 == 0) ? N + 1 : N;  // odd row stride: conflict-free lines
@@ -61,7 +76,8 @@ struct Geo {
   static constexpr int VS = N * PL;                    // one quantity
   static constexpr int ES = NVE * VS;                  // one tensor
   static constexpr int LINES = N * N;
-  static constexpr int TASKS = 6 * LINES;              // per element per pass
+  static constexpr int SLOTS = SL;                     // tasks per line and pass (6 or 8)
+  static constexpr int TASKS = SL * LINES;             // per element per pass
   static constexpr int EPB = N <= 2 ? 16 : N == 3 ? 8 : N <= 4 ? 4 : N <= 6 ? 2 : 1;
   static constexpr int THREADS = ((TASKS * EPB + 31) / 32) * 32;
   static constexpr int OUTV = NVE * N * N * N;         // qavg values per element
@@ -73,6 +89,9 @@ struct Geo {
 };
 
 __device__ __forceinline__ double2 ceo2(int i) {
+#ifdef ADERSTP_EXPT_NO_CONST
+  return make_double2(0.01 * (i & 7), 0.02);
+#endif
   double2 v;
   asm volatile("{\n .reg .u64 ca;\n cvta.to.const.u64 ca, %2;\n ld.const.v2.f64 {%0, %1}, [ca];\n}\n"
                : "=d"(v.x), "=d"(v.y)
@@ -133,10 +152,30 @@ __device__ __forceinline__ void eo_apply(const double (&p)[N], double (&out)[N])
 
 // One task of pass D: contract the line (la, lb) of the slot's source field along direction D
 // and write (pass x; pass y's first touch of syz) or accumulate coef * D_D f into each target.
-template <int N, int D>
+template <int N, int D, int SL>
 __device__ __forceinline__ void line_pass(const double* P, double* T, int slot, int la, int lb,
                                           const double (&c4)[4]) {
-  using G = Geo<N>;
+  using G = Geo<N, SL>;
+  if (SL == 8) {
+    constexpr int ST8 = D == 0 ? 1 : D == 1 ? G::RS : G::PL;
+    const int start8 = D == 0 ? la * G::PL + lb * G::RS : D == 1 ? la * G::PL + lb : la * G::RS + lb;
+    const PassTask& pt = kPass8[D][slot];
+    double p8[N], o8[N];
+    const double* src8 = P + pt.src * G::VS + start8;
+#pragma unroll
+    for (int l = 0; l < N; ++l) p8[l] = src8[l * ST8];
+    eo_apply<N>(p8, o8);
+    const double c = pick4(c4, pt.coef);
+    double* dst = T + pt.tgt * G::VS + start8;
+    if (D == 0 || (D == 1 && pt.tgt == 5)) {
+#pragma unroll
+      for (int l = 0; l < N; ++l) dst[l * ST8] = c * o8[l];
+    } else {
+#pragma unroll
+      for (int l = 0; l < N; ++l) dst[l * ST8] = fma(c, o8[l], dst[l * ST8]);
+    }
+    return;
+  }
   constexpr int ST = D == 0 ? 1 : D == 1 ? G::RS : G::PL;
   const int start = D == 0 ? la * G::PL + lb * G::RS : D == 1 ? la * G::PL + lb : la * G::RS + lb;
   const PassSlot& ps = kPass[D][slot];
@@ -182,10 +221,10 @@ __host__ __device__ constexpr int e_coef(int s, int d) {
   return t[s][d];
 }
 
-template <int N>
-__global__ void __launch_bounds__(Geo<N>::THREADS, Geo<N>::MINB)
+template <int N, int SL>
+__global__ void __launch_bounds__(Geo<N, SL>::THREADS, Geo<N, SL>::MINB)
 stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
-  using G = Geo<N>;
+  using G = Geo<N, SL>;
   extern __shared__ __align__(16) double smp[];
   const int tid = threadIdx.x;
   unsigned int flags = 0;
@@ -222,6 +261,14 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     c4[3] = 1.0 / rho;
   }
 
+#ifdef ADERSTP_EXPT_TIMING
+  long long tclk[16];
+  int tn = 0;
+  tclk[tn++] = clock64();
+#define TMARK() tclk[tn++] = clock64()
+#else
+#define TMARK()
+#endif
   // ---- stage q: one node (k3,k2,k1) per task, 9 coalesced loads (AoSoA [k3][k2][s][k1]) --
   {
     const int qs = kp.q_stride;
@@ -252,17 +299,18 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     qa[j] = (ee < G::EPB) ? dt * buf(ee, 0)[i - ee * G::ES] : 0.0;
   }
 
+  TMARK();
   double coeff = dt;
   int cur = 0;  // buffer holding the current iterate p
 #pragma unroll 1
   for (int o = 1; o < N; ++o) {
     const double* P = buf(el < G::EPB ? el : 0, cur);
     double* T = buf(el < G::EPB ? el : 0, cur ^ 1);
-    if (active) line_pass<N, 0>(P, T, slot, la, lb, c4);
+    if (active) line_pass<N, 0, SL>(P, T, slot, la, lb, c4);
     __syncthreads();
-    if (active) line_pass<N, 1>(P, T, slot, la, lb, c4);
+    if (active) line_pass<N, 1, SL>(P, T, slot, la, lb, c4);
     __syncthreads();
-    if (active) line_pass<N, 2>(P, T, slot, la, lb, c4);
+    if (active) line_pass<N, 2, SL>(P, T, slot, la, lb, c4);
     __syncthreads();
     // T = sum_d D_d F_d(p) is the next iterate: qavg += c_o T  (stp_splitck.cpp:64-69)
     coeff *= dt / (o + 1);
@@ -277,6 +325,7 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     // (this step's passes) are all behind the pass-z barrier
   }
   __syncthreads();  // the qavg reads of the last iterate are done
+  TMARK();
 #pragma unroll
   for (int j = 0; j < G::QPT; ++j) {
     const int i = tid + j * G::THREADS;
@@ -398,11 +447,20 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     }
   }
   if (kp.check && flags) atomicOr(status, flags);
+#ifdef ADERSTP_EXPT_TIMING
+  __syncthreads();
+  TMARK();
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned long long* dbg = reinterpret_cast<unsigned long long*>(a.face_f) + 0;  // scratch
+    (void)dbg;
+    for (int i = 0; i < tn; ++i) aderstp_dbg_clock[blockIdx.x * 8 + i] = tclk[i];
+  }
+#endif
 }
 
-template <int N>
+template <int N, int SL>
 cudaError_t launch_pass_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
-  using G = Geo<N>;
+  using G = Geo<N, SL>;
   PassParams<N> kp;
   for (int j = 0; j < N; ++j) {
     kp.phi[0][j] = p.basis.face_left[j];
@@ -411,15 +469,365 @@ cudaError_t launch_pass_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t 
   kp.check = p.check;
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
-  cudaError_t err = cudaFuncSetAttribute(stp_pass_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  auto kern = stp_pass_kernel<N, SL>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err == cudaSuccess)
-    err = cudaFuncSetAttribute(stp_pass_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (err != cudaSuccess) return err;
   const long long blocks = (a.n_elem + G::EPB - 1) / G::EPB;
   if (blocks == 0) return cudaSuccess;
   if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
-  stp_pass_kernel<N><<<(unsigned)blocks, G::THREADS, G::SMEM, stream>>>(kp, a, p.d_status);
+  kern<<<(unsigned)blocks, G::THREADS, G::SMEM, stream>>>(kp, a, p.d_status);
+  return cudaGetLastError();
+}
+
+
+// =============================================================================================
+// Bipartite variant.  The elastic operator couples stresses and velocities only: stress targets
+// read velocity sources and vice versa.  A CK step therefore runs as
+//   phase V: new (u, v, w) from the stress fields            -> TEMP (3 spare field slots)
+//   phase S: new stresses from the OLD (u, v, w)             -> in place over the stresses
+// (the stresses are dead once phase V is done) and the velocity slots swap with TEMP.  Twelve
+// field slots per element instead of eighteen: nDof 10 fits two CTAs per SM.  The time integral
+// qavg accumulates directly in the qavg output array (L2-resident while the element is in
+// flight), which frees the registers the in-register accumulator needed.
+template <int N>
+struct GeoB {
+  static constexpr int RS = (N % 2 == 0) ? N + 1 : N;
+  static constexpr int PL = N * RS;
+  static constexpr int VS = N * PL;
+  static constexpr int EB = 12 * VS;  // field slots: 0-5 stresses, 6-8 / 9-11 velocities
+  static constexpr int LINES = N * N;
+  static constexpr int TASKS = 3 * LINES;
+  static constexpr int EPB = N >= 9 ? 1 : N >= 7 ? 2 : N >= 5 ? 4 : N == 4 ? 8 : N == 3 ? 12 : 32;
+  static constexpr int THREADS = ((TASKS * EPB + 31) / 32) * 32;
+  static constexpr int SMEM = EB * EPB * 8;
+  static constexpr int MINB = N >= 10 ? 2 : N == 9 ? 3 : 2;
+};
+
+// phase-V pass D, slot j: stress source -> velocity target (coefficient 1/rho)
+__constant__ int8_t kBipV[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+// phase-S pass D: slot 0 source (u, v, w)[D] -> sxx, syy, szz with (coef idx); slots 1, 2 shear
+__constant__ int8_t kBipS0[3][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}};
+__constant__ int8_t kBipS12[3][2][2] = {{{7, 3}, {8, 4}}, {{6, 3}, {8, 5}}, {{6, 4}, {7, 5}}};  // (src, tgt)
+
+template <int N, int D>
+__device__ __forceinline__ void bip_line(const double* src, double* const* dst, const double* cf, int nt,
+                                         bool write) {
+  using G = GeoB<N>;
+  constexpr int ST = D == 0 ? 1 : D == 1 ? G::RS : G::PL;
+  double p[N], out[N];
+#pragma unroll
+  for (int l = 0; l < N; ++l) p[l] = src[l * ST];
+  eo_apply<N>(p, out);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k < nt) {
+      double* d = dst[k];
+      const double c = cf[k];
+      if (write) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) d[l * ST] = c * out[l];
+      } else {
+#pragma unroll
+        for (int l = 0; l < N; ++l) d[l * ST] = fma(c, out[l], d[l * ST]);
+      }
+    }
+  }
+}
+
+template <int N, int D>
+__device__ __forceinline__ int bip_start(int la, int lb) {
+  using G = GeoB<N>;
+  return D == 0 ? la * G::PL + lb * G::RS : D == 1 ? la * G::PL + lb : la * G::RS + lb;
+}
+
+template <int N>
+__global__ void __launch_bounds__(GeoB<N>::THREADS, GeoB<N>::MINB)
+stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
+  using G = GeoB<N>;
+  extern __shared__ __align__(16) double smb[];
+  const int tid = threadIdx.x;
+  unsigned int flags = 0;
+  const double dt = a.dt;
+  const long long e0 = (long long)blockIdx.x * G::EPB;
+  constexpr int N3 = N * N * N;
+  constexpr int OUTV = NVE * N3;
+
+  const int el = tid / G::TASKS;
+  const int slot = (tid - el * G::TASKS) / G::LINES;
+  const int line = tid - el * G::TASKS - slot * G::LINES;
+  const bool active = el < G::EPB && e0 + el < a.n_elem;
+  const int la = line / N, lb = line - la * N;
+  double* E = smb + (el < G::EPB ? el : 0) * G::EB;  // this task's element
+
+  double c4[4] = {0.0, 0.0, 0.0, 0.0};
+  if (active) {
+    const double* pr = a.par + 3 * (e0 + el);
+    double lam, mu, rho;
+    if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
+      rho = pr[0];
+      mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
+      lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
+    } else {
+      lam = pr[0];
+      mu = pr[1];
+      rho = pr[2];
+    }
+    if (!((rho > 0.0) && (mu >= 0.0) && (lam + 2.0 * mu > 0.0))) flags |= 2u;
+    c4[0] = lam + 2.0 * mu;
+    c4[1] = lam;
+    c4[2] = mu;
+    c4[3] = 1.0 / rho;
+  }
+
+  // ---- stage q -> slots 0..8; qavg output = dt q ------------------------------------------
+  {
+    const int qs = kp.q_stride;
+    for (int i = tid; i < G::EPB * N3; i += G::THREADS) {
+      const int ee = i / N3, node = i - ee * N3;
+      if (e0 + ee >= a.n_elem) continue;
+      const int k1 = node % N, k32 = node / N;
+      const double* src = a.q + (e0 + ee) * (long long)(N3 * qs) + k32 * qs * N + k1;
+      double* dst = smb + ee * G::EB + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+      double* qo = a.qavg + (e0 + ee) * (long long)OUTV + k32 * NVE * N + k1;
+      double v[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) v[s] = __ldcs(src + s * N);
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) {
+        if (kp.check && !isfinite(v[s])) flags |= 1u;
+        dst[s * G::VS] = v[s];
+        qo[s * N] = dt * v[s];
+      }
+    }
+  }
+  __syncthreads();
+
+  double coeff = dt;
+  int vb = 6;  // slot of u (velocities occupy vb .. vb+2; the other three slots are TEMP)
+#pragma unroll 1
+  for (int o = 1; o < N; ++o) {
+    const int tb = 15 - vb;  // TEMP base: 9 when vb = 6, 6 when vb = 9
+    // phase V: velocity targets from stress sources, into TEMP
+    if (active) {
+      double* dst[3];
+      double cf[3] = {c4[3], 0.0, 0.0};
+      dst[0] = E + (tb + slot) * G::VS + bip_start<N, 0>(la, lb);
+      bip_line<N, 0>(E + kBipV[0][slot] * G::VS + bip_start<N, 0>(la, lb), dst, cf, 1, true);
+    }
+    __syncthreads();
+    if (active) {
+      double* dst[3];
+      double cf[3] = {c4[3], 0.0, 0.0};
+      dst[0] = E + (tb + slot) * G::VS + bip_start<N, 1>(la, lb);
+      bip_line<N, 1>(E + kBipV[1][slot] * G::VS + bip_start<N, 1>(la, lb), dst, cf, 1, false);
+    }
+    __syncthreads();
+    if (active) {
+      double* dst[3];
+      double cf[3] = {c4[3], 0.0, 0.0};
+      dst[0] = E + (tb + slot) * G::VS + bip_start<N, 2>(la, lb);
+      bip_line<N, 2>(E + kBipV[2][slot] * G::VS + bip_start<N, 2>(la, lb), dst, cf, 1, false);
+    }
+    __syncthreads();
+    // phase S: stress targets from the old velocities, in place over the (dead) stresses
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      if (active) {
+        double* dst[3];
+        double cf[3];
+        int srcf, nt;
+        if (slot == 0) {
+          srcf = vb + d;
+          nt = 3;
+#pragma unroll
+          for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[d][k]);
+        } else {
+          const int sv = kBipS12[d][slot - 1][0];  // 6, 7, 8 = u, v, w
+          srcf = vb + (sv - 6);
+          nt = 1;
+          cf[0] = c4[2];
+          cf[1] = cf[2] = 0.0;
+        }
+        const bool write = d == 0 || (d == 1 && slot == 2);
+        if (d == 0) {
+          const int st = bip_start<N, 0>(la, lb);
+          if (slot == 0) { dst[0] = E + st; dst[1] = E + G::VS + st; dst[2] = E + 2 * G::VS + st; }
+          else dst[0] = E + kBipS12[0][slot - 1][1] * G::VS + st;
+          bip_line<N, 0>(E + srcf * G::VS + st, dst, cf, nt, write);
+        } else if (d == 1) {
+          const int st = bip_start<N, 1>(la, lb);
+          if (slot == 0) { dst[0] = E + st; dst[1] = E + G::VS + st; dst[2] = E + 2 * G::VS + st; }
+          else dst[0] = E + kBipS12[1][slot - 1][1] * G::VS + st;
+          bip_line<N, 1>(E + srcf * G::VS + st, dst, cf, nt, write);
+        } else {
+          const int st = bip_start<N, 2>(la, lb);
+          if (slot == 0) { dst[0] = E + st; dst[1] = E + G::VS + st; dst[2] = E + 2 * G::VS + st; }
+          else dst[0] = E + kBipS12[2][slot - 1][1] * G::VS + st;
+          bip_line<N, 2>(E + srcf * G::VS + st, dst, cf, nt, write);
+        }
+      }
+      __syncthreads();
+    }
+    vb = tb;  // the new velocities live in TEMP
+    // qavg += c_o t (stp_splitck.cpp:64-69), accumulated in the output array: flat over
+    // [e][k3][k2][s][k1], consecutive threads = consecutive addresses
+    coeff *= dt / (o + 1);
+    for (int i = tid; i < G::EPB * OUTV; i += G::THREADS) {
+      const int ee = i / OUTV;
+      if (e0 + ee >= a.n_elem) continue;
+      int r = i - ee * OUTV;
+      const int k1 = r % N;
+      r /= N;
+      const int s = r % NVE;
+      const int k32 = r / NVE;
+      const int fs = s < 6 ? s : vb + (s - 6);
+      double* qo = a.qavg + (e0 + ee) * (long long)OUTV + (i - ee * OUTV);
+      *qo = fma(coeff, smb[ee * G::EB + fs * G::VS + (k32 / N) * G::PL + (k32 % N) * G::RS + k1], *qo);
+    }
+    // no barrier: the next phase V pass x reads the stresses (read-only) and writes the old
+    // velocity slots, which nobody reads any more
+  }
+  __syncthreads();
+  // ---- epilogue: qavg (final, in the output array) back into slots 0..8, then favg + faces --
+  for (int i = tid; i < G::EPB * OUTV; i += G::THREADS) {
+    const int ee = i / OUTV;
+    if (e0 + ee >= a.n_elem) continue;
+    int r = i - ee * OUTV;
+    const int k1 = r % N;
+    r /= N;
+    const int s = r % NVE;
+    const int k32 = r / NVE;
+    smb[ee * G::EB + s * G::VS + (k32 / N) * G::PL + (k32 % N) * G::RS + k1] =
+        a.qavg[(e0 + ee) * (long long)OUTV + (i - ee * OUTV)];
+  }
+  __syncthreads();
+  if (a.favg) {
+    for (int i = tid; i < G::EPB * N3; i += G::THREADS) {
+      const int ee = i / N3, node = i - ee * N3;
+      if (e0 + ee >= a.n_elem) continue;
+      const int k1 = node % N, k32 = node / N;
+      const double* qs = smb + ee * G::EB + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+      double v[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) v[s] = qs[s * G::VS];
+      double cc[4];
+      {
+        const double* pr = a.par + 3 * (e0 + ee);
+        if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
+          const double mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
+          const double lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
+          cc[0] = lam + 2.0 * mu;
+          cc[1] = lam;
+          cc[2] = mu;
+          cc[3] = 1.0 / pr[0];
+        } else {
+          cc[0] = pr[0] + 2.0 * pr[1];
+          cc[1] = pr[0];
+          cc[2] = pr[1];
+          cc[3] = 1.0 / pr[2];
+        }
+      }
+      double* fo = a.favg + (e0 + ee) * (long long)(3 * OUTV) + k32 * NVE * N + k1;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+#pragma unroll
+        for (int s = 0; s < NVE; ++s)
+          __stcs(fo + d * OUTV + s * N, e_coef(s, d) == 4 ? 0.0 : cc[e_coef(s, d)] * v[e_in(s, d)]);
+    }
+  }
+  if (a.face_q || a.face_f) {
+    constexpr int FV = N * N * NVE;
+    for (int i = tid; i < G::EPB * 3 * N * N; i += G::THREADS) {
+      const int ee = i / (3 * N * N);
+      if (e0 + ee >= a.n_elem) continue;
+      int r = i - ee * 3 * N * N;
+      const int d = r / (N * N);
+      const int ab = r - d * N * N;
+      const int aa = ab / N, bb = ab - aa * N;
+      const int start = d == 0 ? aa * G::PL + bb * G::RS : d == 1 ? aa * G::PL + bb : aa * G::RS + bb;
+      const int stride = d == 0 ? 1 : d == 1 ? G::RS : G::PL;
+      const double* q0 = smb + ee * G::EB + start;
+      double f0[NVE], f1[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) {
+        double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double x = q0[s * G::VS + j * stride];
+          x0 = fma(kp.phi[0][j], x, x0);
+          x1 = fma(kp.phi[1][j], x, x1);
+        }
+        f0[s] = x0;
+        f1[s] = x1;
+      }
+      const long long fb = (e0 + ee) * 6LL * FV + (2 * d) * FV + ab * NVE;
+      if (a.face_q) {
+#pragma unroll
+        for (int s = 0; s < NVE; ++s) {
+          __stcs(a.face_q + fb + s, f0[s]);
+          __stcs(a.face_q + fb + FV + s, f1[s]);
+        }
+      }
+      if (a.face_f) {
+        double cc[4];
+        const double* pr = a.par + 3 * (e0 + ee);
+        if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
+          const double mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
+          const double lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
+          cc[0] = lam + 2.0 * mu;
+          cc[1] = lam;
+          cc[2] = mu;
+          cc[3] = 1.0 / pr[0];
+        } else {
+          cc[0] = pr[0] + 2.0 * pr[1];
+          cc[1] = pr[0];
+          cc[2] = pr[1];
+          cc[3] = 1.0 / pr[2];
+        }
+#pragma unroll
+        for (int s = 0; s < NVE; ++s) {
+          double g0, g1;
+          if (d == 0) {
+            g0 = e_coef(s, 0) == 4 ? 0.0 : cc[e_coef(s, 0)] * f0[e_in(s, 0)];
+            g1 = e_coef(s, 0) == 4 ? 0.0 : cc[e_coef(s, 0)] * f1[e_in(s, 0)];
+          } else if (d == 1) {
+            g0 = e_coef(s, 1) == 4 ? 0.0 : cc[e_coef(s, 1)] * f0[e_in(s, 1)];
+            g1 = e_coef(s, 1) == 4 ? 0.0 : cc[e_coef(s, 1)] * f1[e_in(s, 1)];
+          } else {
+            g0 = e_coef(s, 2) == 4 ? 0.0 : cc[e_coef(s, 2)] * f0[e_in(s, 2)];
+            g1 = e_coef(s, 2) == 4 ? 0.0 : cc[e_coef(s, 2)] * f1[e_in(s, 2)];
+          }
+          __stcs(a.face_f + fb + s, g0);
+          __stcs(a.face_f + fb + FV + s, g1);
+        }
+      }
+    }
+  }
+  if (kp.check && flags) atomicOr(status, flags);
+}
+
+template <int N>
+cudaError_t launch_bip_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
+  using G = GeoB<N>;
+  PassParams<N> kp;
+  for (int j = 0; j < N; ++j) {
+    kp.phi[0][j] = p.basis.face_left[j];
+    kp.phi[1][j] = p.basis.face_right[j];
+  }
+  kp.check = p.check;
+  kp.par_kind = p.par_kind;
+  kp.q_stride = p.q_stride;
+  auto kern = stp_bip_kernel<N>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (err != cudaSuccess) return err;
+  const long long blocks = (a.n_elem + G::EPB - 1) / G::EPB;
+  if (blocks == 0) return cudaSuccess;
+  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kern<<<(unsigned)blocks, G::THREADS, G::SMEM, stream>>>(kp, a, p.d_status);
   return cudaGetLastError();
 }
 
@@ -450,17 +858,35 @@ cudaError_t init_pass(const LaunchPlan& p) {
 }
 
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
-  switch (p.n) {
-    case 2: return launch_pass_n<2>(p, a, stream);
-    case 3: return launch_pass_n<3>(p, a, stream);
-    case 4: return launch_pass_n<4>(p, a, stream);
-    case 5: return launch_pass_n<5>(p, a, stream);
-    case 6: return launch_pass_n<6>(p, a, stream);
-    case 7: return launch_pass_n<7>(p, a, stream);
-    case 8: return launch_pass_n<8>(p, a, stream);
-    case 9: return launch_pass_n<9>(p, a, stream);
-    case 10: return launch_pass_n<10>(p, a, stream);
+  if (p.pass_slots == 12) {
+    switch (p.n) {
+      case 2: return launch_bip_n<2>(p, a, stream);
+      case 3: return launch_bip_n<3>(p, a, stream);
+      case 4: return launch_bip_n<4>(p, a, stream);
+      case 5: return launch_bip_n<5>(p, a, stream);
+      case 6: return launch_bip_n<6>(p, a, stream);
+      case 7: return launch_bip_n<7>(p, a, stream);
+      case 8: return launch_bip_n<8>(p, a, stream);
+      case 9: return launch_bip_n<9>(p, a, stream);
+      case 10: return launch_bip_n<10>(p, a, stream);
+    }
+    return cudaErrorInvalidValue;
   }
+  const bool eight = p.pass_slots == 8;
+#define ADERSTP_PASS_CASE(NN) \
+  case NN: return eight ? launch_pass_n<NN, 8>(p, a, stream) : launch_pass_n<NN, 6>(p, a, stream);
+  switch (p.n) {
+    ADERSTP_PASS_CASE(2)
+    ADERSTP_PASS_CASE(3)
+    ADERSTP_PASS_CASE(4)
+    ADERSTP_PASS_CASE(5)
+    ADERSTP_PASS_CASE(6)
+    ADERSTP_PASS_CASE(7)
+    ADERSTP_PASS_CASE(8)
+    ADERSTP_PASS_CASE(9)
+    ADERSTP_PASS_CASE(10)
+  }
+#undef ADERSTP_PASS_CASE
   return cudaErrorInvalidValue;
 }
 

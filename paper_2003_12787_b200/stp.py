@@ -25,7 +25,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-library_path = os.path.join(_HERE, "libaderstp.so")
+library_path = os.environ.get("ADERSTP_LIB") or os.path.join(_HERE, "libaderstp.so")
 
 ADERSTP_OK = 0
 ADERSTP_ERR_INVALID_ARG = 1
