@@ -18,6 +18,15 @@
 // zero-padded 8 x 8 D per order (row k = node, col l), uploaded at plan creation
 extern "C" {
 __constant__ double aderstp_kDP[9 * 64];
+#ifdef ADERSTP_EXPT_TIMING
+__device__ long long aderstp_dbg_clock2[4096 * 8];
+int aderstp_dbg_clock2_copy(long long* host, int count) {
+  return (int)cudaMemcpyFromSymbol(host, aderstp_dbg_clock2, sizeof(long long) * count);
+}
+#define TM2(i) if (threadIdx.x == 0 && blockIdx.x < 4096) aderstp_dbg_clock2[blockIdx.x * 8 + (i)] = clock64()
+#else
+#define TM2(i)
+#endif
 }
 
 namespace aderstp {
@@ -174,6 +183,7 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
   unsigned int flags = 0;
   const double dt = a.dt;
 
+  TM2(0);
   double c4[4];
   {
     const double p0 = a.par[3 * e], p1 = a.par[3 * e + 1], p2 = a.par[3 * e + 2];
@@ -230,6 +240,7 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
   }
   __syncthreads();
 
+  TM2(1);
   const int role = kRoleP[warp];
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];
 
@@ -274,6 +285,7 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
     }
   }
 
+  TM2(2);
   // ---- epilogue: 9 quantities x k3 planes over the 8 warps ------------------------------
   double* FQ = smq;  // face staging [6][N][N][9] over the dead p buffer
   const bool faces = a.face_q || a.face_f;
@@ -306,6 +318,7 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
       }
     }
   }
+  TM2(3);
   if (faces) {
 #pragma unroll 1
     for (int u = warp; u < NVP * N; u += NWP) {
@@ -349,6 +362,7 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
       }
     }
     __syncthreads();
+    TM2(4);
     if (tid < 252) {
       const int so = tid % NVP, ab0 = tid / NVP;  // 28 in-face nodes per sweep
       double* oq = a.face_q ? a.face_q + e * (long long)(6 * FACE) : nullptr;
@@ -368,6 +382,7 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
     }
   }
   if (kp.check && flags) atomicOr(status, flags);
+  TM2(5);
 }
 
 template <int N>

@@ -378,13 +378,12 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     }
   }
   if (faces) {
-    __syncthreads();
-    // coalesced copy-out; thread tid handles in-face nodes ab = tid / 9 + 28 i, quantity
-    // so = tid % 9 (252 active threads); face_f[f][ab][so] = coef(so, d) face_q[f][ab][in(so, d)]
-    if (tid < 252) {
-      const int so = tid % NV, ab0 = tid / NV;  // ab0 in 0..27
-      double* oq = a.face_q ? a.face_q + e * (long long)(6 * FACE) : nullptr;
-      double* of = a.face_f ? a.face_f + e * (long long)(6 * FACE) : nullptr;
+    __syncthreads();  // FQ complete; QA no longer read (the face_f staging may overlap it)
+    double* FF = sm8 + 6 * FACE;
+    // face_f[f][ab][so] = coef(so, d) face_q[f][ab][in(so, d)]: thread tid owns quantity
+    // so = tid % 9 for in-face nodes ab = tid / 9 + 28 i (252 active threads)
+    if (a.face_f && tid < 252) {
+      const int so = tid % NV, ab0 = tid / NV;
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         const double c = sel4(c4, kCoef[so][d]);
@@ -396,11 +395,28 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
             const int ab = ab0 + 28 * i;
             if (ab < 64) {
               const int base = (2 * d + sd) * FACE + ab * NV;
-              if (oq) __stcs(oq + base + so, FQ[base + so]);
-              if (of) __stcs(of + base + so, c * FQ[base + src]);
+              FF[base + so] = c * FQ[base + src];
             }
           }
       }
+    }
+    // face_q / face_f leave as two TMA bulk stores (cp.async.bulk, SASS UBLKCP)
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned bytes = 6 * FACE * 8;
+      if (a.face_q)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                         a.face_q + e * (long long)(6 * FACE)),
+                     "r"((unsigned)__cvta_generic_to_shared(FQ)), "r"(bytes)
+                     : "memory");
+      if (a.face_f)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                         a.face_f + e * (long long)(6 * FACE)),
+                     "r"((unsigned)__cvta_generic_to_shared(FF)), "r"(bytes)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
   }
   if (kp.check && flags) atomicOr(status, flags);
