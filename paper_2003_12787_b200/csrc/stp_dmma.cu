@@ -86,6 +86,18 @@ __device__ __forceinline__ void sts2p(double* p, double a, double b) {
   *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
 
+// node pair (k1 = 2t, 2t+1) of an output row; one 16-byte streaming store when N is even (the
+// pair is then 16-byte aligned), scalar stores otherwise
+template <int N>
+__device__ __forceinline__ void st_pair(double* p, double x, double y, bool ok0, bool ok1) {
+  if (N % 2 == 0) {
+    if (ok0) asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};\n" ::"l"(p), "d"(x), "d"(y) : "memory");
+  } else {
+    if (ok0) __stcs(p, x);
+    if (ok1) __stcs(p + 1, y);
+  }
+}
+
 template <int N, int NT>
 __device__ __forceinline__ void mma_xp(double (&acc)[NT][2], const double* f, int K0, int g, int t, double b0,
                                        double b1) {
@@ -169,7 +181,7 @@ __device__ __forceinline__ void normal_step(double* P, double* QA, int K0, int g
 }
 
 template <int N>
-__global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsigned int* status) {
+__global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsigned int* status) {
   using G = GeoP<N>;
   constexpr int PV = G::PV, FACE = G::FACE;
   extern __shared__ __align__(16) double smq[];
@@ -303,16 +315,14 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
       const double2 v = lds2p(QA + s * PV + k3 * 64 + col);
       if (rowok) {
         const int base = ((k3 * N + g) * NVP + s) * N + 2 * t;
-        if (k1a) __stcs(qout + base, v.x);
-        if (k1b) __stcs(qout + base + 1, v.y);
+        st_pair<N>(qout + base, v.x, v.y, k1a, k1b);
         if (fout) {
           const int nout = kOutNP[s];
           for (int k = 0; k < nout; ++k) {
             const int so = kOutP[s][k][0], d = kOutP[s][k][1];
             const double c = selp(c4, kOutP[s][k][2]);
             const int fb = d * (N * N * N * NVP) + ((k3 * N + g) * NVP + so) * N + 2 * t;
-            if (k1a) __stcs(fout + fb, c * v.x);
-            if (k1b) __stcs(fout + fb + 1, c * v.y);
+            st_pair<N>(fout + fb, c * v.x, c * v.y, k1a, k1b);
           }
         }
       }
@@ -363,10 +373,10 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
     }
     __syncthreads();
     TM2(4);
-    if (tid < 252) {
+    // face_f = F_d(face_q) staged next to face_q; both leave as TMA bulk stores (UBLKCP)
+    double* FF = smq + 6 * FACE;
+    if (a.face_f && tid < 252) {
       const int so = tid % NVP, ab0 = tid / NVP;  // 28 in-face nodes per sweep
-      double* oq = a.face_q ? a.face_q + e * (long long)(6 * FACE) : nullptr;
-      double* of = a.face_f ? a.face_f + e * (long long)(6 * FACE) : nullptr;
 #pragma unroll
       for (int d = 0; d < 3; ++d) {
         const double c = selp(c4, kCoefP[so][d]);
@@ -375,10 +385,26 @@ __global__ void __maxnreg__(80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsign
         for (int sd = 0; sd < 2; ++sd)
           for (int ab = ab0; ab < N * N; ab += 28) {
             const int base = (2 * d + sd) * FACE + ab * NVP;
-            if (oq) __stcs(oq + base + so, FQ[base + so]);
-            if (of) __stcs(of + base + so, c * FQ[base + src]);
+            FF[base + so] = c * FQ[base + src];
           }
       }
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      const unsigned bytes = 6 * FACE * 8;
+      if (a.face_q)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                         a.face_q + e * (long long)(6 * FACE)),
+                     "r"((unsigned)__cvta_generic_to_shared(FQ)), "r"(bytes)
+                     : "memory");
+      if (a.face_f)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                         a.face_f + e * (long long)(6 * FACE)),
+                     "r"((unsigned)__cvta_generic_to_shared(FF)), "r"(bytes)
+                     : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
   }
   if (kp.check && flags) atomicOr(status, flags);

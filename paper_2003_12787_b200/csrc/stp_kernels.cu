@@ -469,7 +469,7 @@ cudaError_t launch_stp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t str
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   const bool aligned = al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) && al16(a.face_f);
   if (!p.force_generic && !p.no_dmma8 && aligned && dmma8_applicable(p)) return launch_dmma8(p, a, stream);
-  if (!p.force_generic && !p.no_dmmap && dmmap_applicable(p)) return launch_dmmap(p, a, stream);
+  if (!p.force_generic && !p.no_dmmap && aligned && dmmap_applicable(p)) return launch_dmmap(p, a, stream);
   if (!p.force_generic && pass_applicable(p)) return launch_pass(p, a, stream);
   if (p.kind == ADERSTP_PDE_ELASTIC) return dispatch<true>(p, a, stream);
   return dispatch<false>(p, a, stream);
