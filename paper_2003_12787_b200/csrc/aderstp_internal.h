@@ -43,6 +43,7 @@ struct LaunchPlan {
   int no_dmma8 = 0;                  // env ADERSTP_NO_DMMA8=1: nDof 8 on the line-pass kernel
   int pass_slots = 6;                // line-pass tasks per line (6 by source, 8 by target)
   int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel
+  int dmmap_persist = 0;             // env ADERSTP_PERSIST=1: persistent CTAs with TMA prefetch
 };
 
 struct BatchArgs {

@@ -160,6 +160,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     lp.dmma8_double_buffer = (db && db[0] == '1') ? 1 : 0;
     const char* nd = std::getenv("ADERSTP_NO_DMMA8");
     lp.no_dmma8 = (nd && nd[0] == '1') ? 1 : 0;
+    const char* pe = std::getenv("ADERSTP_PERSIST");
+    lp.dmmap_persist = (pe && pe[0] == '1') ? 1 : 0;
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");
     lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
     const char* ps = std::getenv("ADERSTP_PASS_SLOTS");
