@@ -23,6 +23,7 @@
 // arrays are contracted by DMMA (x, y normals) and DFMA (z normal) from the qavg accumulator,
 // staged in the reference's [f][a][b][s] order and written coalesced, face_f = F_d(face_q).
 #include <cstdint>
+#include <cstdlib>
 
 #include "../../include/aderstp.h"
 #include "aderstp_internal.h"
@@ -32,6 +33,15 @@
 // broadcast), so ptxas cannot hoist 64 doubles of D into registers and spill.
 extern "C" {
 __constant__ double aderstp_kD8[64];
+#ifdef ADERSTP_EXPT_TIMING
+__device__ long long aderstp_dbg_clock3[4096 * 8];
+int aderstp_dbg_clock3_copy(long long* host, int count) {
+  return (int)cudaMemcpyFromSymbol(host, aderstp_dbg_clock3, sizeof(long long) * count);
+}
+#define TM3(i) if (threadIdx.x == 0 && blockIdx.x < 4096) aderstp_dbg_clock3[blockIdx.x * 8 + (i)] = clock64()
+#else
+#define TM3(i)
+#endif
 }
 
 namespace aderstp {
@@ -172,6 +182,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   const int col = phys(g, 2 * t);  // + k3*64: this lane's node pair within a quantity plane
   unsigned int flags = 0;
   const double dt = a.dt;
+  TM3(0);
 
   // ---- material (proj/src/pde.cpp:171-178) -------------------------------------------
   double c4[4];
@@ -218,6 +229,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   }
   __syncthreads();
 
+  TM3(1);
   // ---- per-warp constants ---------------------------------------------------------------
   const int role = kRole[warp];
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];  // D[g][kh*4 + t]
@@ -304,6 +316,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     }
   }
 
+  TM3(2);
   // ---- epilogue ------------------------------------------------------------------------
   // 18 units (quantity s, k3 half h) over the 8 warps: qavg and favg from registers, x/y faces
   // by DMMA from the accumulator (staged into the dead p buffers); the unit with h = 0 also does
@@ -379,6 +392,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   }
   if (faces) {
     __syncthreads();  // FQ complete; QA no longer read (the face_f staging may overlap it)
+    TM3(3);
     double* FF = sm8 + 6 * FACE;
     // face_f[f][ab][so] = coef(so, d) face_q[f][ab][in(so, d)]: thread tid owns quantity
     // so = tid % 9 for in-face nodes ab = tid / 9 + 28 i (252 active threads)
@@ -420,6 +434,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     }
   }
   if (kp.check && flags) atomicOr(status, flags);
+  TM3(4);
 }
 
 }  // namespace
@@ -445,7 +460,10 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   kp.q_stride = p.q_stride;
   const bool db = p.dmma8_double_buffer;
   auto kern = db ? stp_dmma8_kernel<true> : stp_dmma8_kernel<false>;
-  const int smem = smem8(db);
+  int smem = smem8(db);
+#ifdef ADERSTP_EXPT_TIMING
+  if (const char* x = std::getenv("ADERSTP_EXPT_SMEM")) smem += std::atoi(x);  // occupancy experiments
+#endif
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err == cudaSuccess)
     err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
