@@ -39,7 +39,6 @@ struct LaunchPlan {
   double src_proj[3][kMaxOrder];
   unsigned int* d_status = nullptr;  // device word: bit0 non-finite q, bit1 bad material
   int force_generic = 0;             // env ADERSTP_FORCE_GENERIC=1: skip specialised kernels
-  int dmma8_double_buffer = 0;       // env ADERSTP_DMMA8_DB=1: 2 CTAs/SM double-buffered variant
   int no_dmma8 = 0;                  // env ADERSTP_NO_DMMA8=1: nDof 8 on the line-pass kernel
   int pass_slots = 6;                // line-pass tasks per line (6 by source, 8 by target)
   int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel

@@ -156,8 +156,6 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   {
     const char* env = std::getenv("ADERSTP_FORCE_GENERIC");
     lp.force_generic = (env && env[0] == '1') ? 1 : 0;
-    const char* db = std::getenv("ADERSTP_DMMA8_DB");
-    lp.dmma8_double_buffer = (db && db[0] == '1') ? 1 : 0;
     const char* nd = std::getenv("ADERSTP_NO_DMMA8");
     lp.no_dmma8 = (nd && nd[0] == '1') ? 1 : 0;
     const char* pe = std::getenv("ADERSTP_PERSIST");

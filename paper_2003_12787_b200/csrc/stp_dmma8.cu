@@ -16,12 +16,14 @@
 // paired on the SM sub-partitions (warp % 4) so that every SMSP carries about the same fp64 work.
 // Flux-first exactly like the reference's D_d * F_d(p) (proj/src/stp_splitck.cpp:53-55).
 //
-// Shared memory (110,592 B, 2 CTAs per SM): p and p_next (double buffer, one barrier per CK step)
-// and the qavg accumulator, each 9 x 8 x 8 x 8 fp64 with an XOR swizzle on k1 (bit 2 flipped on
-// rows with k2 & 2) that makes every fragment load, column load and store bank-conflict free.
-// Epilogue: qavg and favg go out from registers (st.global.cs, 64-byte segments); the 12 face
-// arrays are contracted by DMMA (x, y normals) and DFMA (z normal) from the qavg accumulator,
-// staged in the reference's [f][a][b][s] order and written coalesced, face_f = F_d(face_q).
+// The series is evaluated in Horner form (see ck_quantity below).
+//
+// Shared memory (73,728 B, 3 CTAs per SM): the Horner iterate r and q, each 9 x 8 x 8 x 8 fp64
+// with an XOR swizzle on k1 (bit 2 flipped on rows with k2 & 2) that makes every fragment load,
+// column load and store bank-conflict free.  Epilogue: qavg and favg go out from registers
+// (st.global.cs, 64-byte segments); the 12 face arrays are contracted by DMMA (x, y normals) and
+// DFMA (z normal) from qavg, staged in the reference's [f][a][b][s] order and leave as TMA bulk
+// stores, face_f = F_d(face_q).
 #include <cstdint>
 #include <cstdlib>
 
@@ -50,17 +52,16 @@ namespace {
 
 constexpr int N8 = 8;
 constexpr int NV = 9;
-constexpr int NWARP = 8;
-constexpr int THREADS8 = NWARP * 32;
+constexpr int NWARP = 8;  // default CTA: 8 warps, 3 CTAs/SM
 constexpr int PV = N8 * N8 * N8;    // doubles per quantity plane
 constexpr int FACE = N8 * N8 * NV;  // doubles per face array (576)
-// DB = true: p / p_next double buffer (110,592 B, 2 CTAs/SM, one barrier per CK step);
-// DB = false: single p buffer (73,728 B, 3 CTAs/SM, two barriers per CK step).
-constexpr int smem8(bool db) { return (db ? 3 : 2) * NV * PV * 8; }
+// r and q, 73,728 B: 3 CTAs/SM, two barriers per CK step.
+constexpr int kSmem8 = 2 * NV * PV * 8;
 
 struct Params8 {
   double d[64];      // d[k*8+l] = phi_l'(x_k)
   double phi[2][8];  // phi(0), phi(1)
+  double cf[8];      // cf[o] = dt^(o+1)/(o+1)!, the reference's running coefficient
   int check;
   int par_kind;
   int q_stride;
@@ -168,20 +169,96 @@ __device__ __forceinline__ void dfma_z(double (&acc)[NT][2], const double* f, in
   }
 }
 
-template <bool DB>
+
+// The CK series qavg = sum_o c_o L^o q (c_o = dt^(o+1)/(o+1)!, L q = sum_d D_d F_d(q)) evaluated
+// in Horner form, r <- c_o q + L r for o = n-2 .. 0 from r = c_(n-1) q: the same n-1 applications
+// of L as the reference's forward recursion (proj/src/stp_splitck.cpp:46-70), but each step reads
+// the constant q instead of read-modify-writing a qavg accumulator -- 20% less shared-memory
+// traffic, which is what bounds this kernel.  P holds r (updated in place between two barriers),
+// Q holds q.
+
+// One Horner step loop for output quantity s on k3 tiles K0 .. K0+NT-1.
+template <int NT>
+__device__ __forceinline__ void ck_quantity(double* P, const double* Q, const double* cf, int s, int K0, int g,
+                                            int t, int col, double d0, double d1, const double (&c4)[4]) {
+  const int in_x = kIn[s][0], in_y = kIn[s][1], in_z = kIn[s][2];
+  const double cx = sel4(c4, kCoef[s][0]), cy = sel4(c4, kCoef[s][1]), cz = sel4(c4, kCoef[s][2]);
+  const bool has_x = kCoef[s][0] != 4, has_y = kCoef[s][1] != 4, has_z = kCoef[s][2] != 4;
+  const double bx0 = cx * d0, bx1 = cx * d1;  // B-fragments of c_x D^T
+  const double ay0 = cy * d0, ay1 = cy * d1;  // A-fragments of c_y D
+  const int own = s * PV + K0 * 64 + col;
+#pragma unroll 1
+  for (int o = N8 - 2; o >= 0; --o) {
+    const double co = cf[o];
+    double tt[NT][2];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const double2 v = lds2(Q + own + k * 64);
+      tt[k][0] = co * v.x;
+      tt[k][1] = co * v.y;
+    }
+    if (has_x) mma_x<NT>(tt, P + in_x * PV, K0, g, t, bx0, bx1);
+    if (has_y) mma_y<NT>(tt, P + in_y * PV, K0, g, t, ay0, ay1);
+    if (has_z) dfma_z<NT>(tt, P + in_z * PV, K0, col, cz);
+    __syncthreads();  // every warp has finished reading r
+#pragma unroll
+    for (int k = 0; k < NT; ++k) sts2(P + own + k * 64, tt[k][0], tt[k][1]);
+    __syncthreads();  // new r complete
+  }
+}
+
+// Normal stresses on k3 tiles K0 .. K0+NT-1: a = Dx u, b = Dy v, c = Dz w (unscaled), then
+// t_sxx = lambda (a+b+c) + 2 mu a, etc. (proj/src/pde.cpp:180-190)
+template <int NT>
+__device__ __forceinline__ void ck_normal(double* P, const double* Q, const double* cf, int K0, int g, int t,
+                                          int col, double d0, double d1, const double (&c4)[4]) {
+  const double lam = c4[1], two_mu = 2.0 * c4[2];
+#pragma unroll 1
+  for (int o = N8 - 2; o >= 0; --o) {
+    const double co = cf[o];
+    double ta[NT][2], tb[NT][2], tc[NT][2];
+#pragma unroll
+    for (int k = 0; k < NT; ++k) ta[k][0] = ta[k][1] = tb[k][0] = tb[k][1] = tc[k][0] = tc[k][1] = 0.0;
+    mma_x<NT>(ta, P + 6 * PV, K0, g, t, d0, d1);
+    mma_y<NT>(tb, P + 7 * PV, K0, g, t, d0, d1);
+    dfma_z<NT>(tc, P + 8 * PV, K0, col, 1.0);
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int off = (K0 + k) * 64 + col;
+      const double2 qa = lds2(Q + off), qb = lds2(Q + PV + off), qc = lds2(Q + 2 * PV + off);
+      const double qv[3][2] = {{qa.x, qa.y}, {qb.x, qb.y}, {qc.x, qc.y}};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const double sum = lam * (ta[k][j] + tb[k][j] + tc[k][j]);
+        ta[k][j] = fma(co, qv[0][j], fma(two_mu, ta[k][j], sum));
+        tb[k][j] = fma(co, qv[1][j], fma(two_mu, tb[k][j], sum));
+        tc[k][j] = fma(co, qv[2][j], fma(two_mu, tc[k][j], sum));
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NT; ++k) {
+      const int off = (K0 + k) * 64 + col;
+      sts2(P + off, ta[k][0], ta[k][1]);
+      sts2(P + PV + off, tb[k][0], tb[k][1]);
+      sts2(P + 2 * PV + off, tc[k][0], tc[k][1]);
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __maxnreg__(80)
 stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
+  constexpr int THREADS8 = NWARP * 32;
   extern __shared__ __align__(16) double sm8[];
-  double* P = sm8;                            // current iterate p   [9][8][8][8] swizzled
-  double* PN = DB ? sm8 + NV * PV : sm8;      // next iterate
-  double* QA = sm8 + (DB ? 2 : 1) * NV * PV;  // qavg accumulator
+  double* P = sm8;            // Horner iterate r   [9][8][8][8] swizzled; qavg at the end
+  double* Q = sm8 + NV * PV;  // q (constant during the recursion)
   const long long e = blockIdx.x;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int col = phys(g, 2 * t);  // + k3*64: this lane's node pair within a quantity plane
   unsigned int flags = 0;
-  const double dt = a.dt;
   TM3(0);
 
   // ---- material (proj/src/pde.cpp:171-178) -------------------------------------------
@@ -205,115 +282,43 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     c4[3] = 1.0 / rho;
   }
 
-  // ---- stage q: AoSoA [k3][k2][s < QS][k1] -> P and QA = dt q -------------------------
+  // ---- stage q: AoSoA [k3][k2][s < QS][k1] -> Q = q and P = c_(n-1) q ------------------
   // 64 rows (k3,k2) x 9 quantities x 4 k1-pairs = 2304 pairs = 9 per thread; every load is
   // issued before the first shared store so their latencies overlap.
   {
     const double* qe = a.q + e * (long long)(PV * kp.q_stride);
-    double2 v[9];
+    constexpr int IT = (2304 + THREADS8 - 1) / THREADS8;
+    double2 v[IT];
 #pragma unroll
-    for (int it = 0; it < 9; ++it) {
+    for (int it = 0; it < IT; ++it) {
       const int i = tid + it * THREADS8;
       const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
-      v[it] = ld_nc2(qe + (k32 * kp.q_stride + si) * 8 + 2 * (i & 3));
+      if (2304 % THREADS8 == 0 || i < 2304) v[it] = ld_nc2(qe + (k32 * kp.q_stride + si) * 8 + 2 * (i & 3));
     }
 #pragma unroll
-    for (int it = 0; it < 9; ++it) {
+    for (int it = 0; it < IT; ++it) {
       const int i = tid + it * THREADS8;
+      if (2304 % THREADS8 != 0 && i >= 2304) break;
       const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
       if (kp.check && !(isfinite(v[it].x) && isfinite(v[it].y))) flags |= 1u;
       const int j = si * PV + (k32 >> 3) * 64 + phys(k32 & 7, 2 * (i & 3));
-      sts2(P + j, v[it].x, v[it].y);
-      sts2(QA + j, dt * v[it].x, dt * v[it].y);
+      sts2(Q + j, v[it].x, v[it].y);
+      sts2(P + j, kp.cf[N8 - 1] * v[it].x, kp.cf[N8 - 1] * v[it].y);
     }
   }
   __syncthreads();
 
   TM3(1);
   // ---- per-warp constants ---------------------------------------------------------------
-  const int role = kRole[warp];
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];  // D[g][kh*4 + t]
 
-  // ---- Cauchy-Kowalewsky recursion (proj/src/stp_splitck.cpp:46-70) -------------------
-  double coeff = dt;
-  if (role >= 0) {
-    const int s = role;
-    const int in_x = kIn[s][0], in_y = kIn[s][1], in_z = kIn[s][2];
-    const double cx = sel4(c4, kCoef[s][0]), cy = sel4(c4, kCoef[s][1]), cz = sel4(c4, kCoef[s][2]);
-    const bool has_x = kCoef[s][0] != 4, has_y = kCoef[s][1] != 4, has_z = kCoef[s][2] != 4;
-    const double bx0 = cx * d0, bx1 = cx * d1;  // B-fragments of c_x D^T
-    const double ay0 = cy * d0, ay1 = cy * d1;  // A-fragments of c_y D
-    const int own = s * PV + col;
-#pragma unroll 1
-    for (int o = 1; o < N8; ++o) {
-      double tt[8][2];
-#pragma unroll
-      for (int k3 = 0; k3 < 8; ++k3) tt[k3][0] = tt[k3][1] = 0.0;
-      if (has_x) mma_x<8>(tt, P + in_x * PV, 0, g, t, bx0, bx1);
-      if (has_y) mma_y<8>(tt, P + in_y * PV, 0, g, t, ay0, ay1);
-      if (has_z) dfma_z<8>(tt, P + in_z * PV, 0, col, cz);
-      coeff *= dt / (o + 1);  // dt^(o+1)/(o+1)!
-#pragma unroll
-      for (int k3 = 0; k3 < 8; ++k3) {  // qavg += c_o t on this lane's own nodes (no race)
-        const double2 v = lds2(QA + own + k3 * 64);
-        sts2(QA + own + k3 * 64, fma(coeff, tt[k3][0], v.x), fma(coeff, tt[k3][1], v.y));
-      }
-      if (o + 1 < N8) {
-        if (!DB) __syncthreads();  // single buffer: every warp has finished reading p
-#pragma unroll
-        for (int k3 = 0; k3 < 8; ++k3) sts2(PN + own + k3 * 64, tt[k3][0], tt[k3][1]);
-      }
-      __syncthreads();  // p_next complete; every warp has finished reading p
-      double* sw = P;
-      P = PN;
-      PN = sw;
-    }
-  } else {
-    // normal stresses on k3 half h: a = Dx u, b = Dy v, c = Dz w (unscaled), then
-    // t_sxx = lambda (a+b+c) + 2 mu a, etc.
-    const int h = -role - 1, K0 = 4 * h;
-    const double lam = c4[1], two_mu = 2.0 * c4[2];
-#pragma unroll 1
-    for (int o = 1; o < N8; ++o) {
-      double ta[4][2], tb[4][2], tc[4][2];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) ta[k][0] = ta[k][1] = tb[k][0] = tb[k][1] = tc[k][0] = tc[k][1] = 0.0;
-      mma_x<4>(ta, P + 6 * PV, K0, g, t, d0, d1);
-      mma_y<4>(tb, P + 7 * PV, K0, g, t, d0, d1);
-      dfma_z<4>(tc, P + 8 * PV, K0, col, 1.0);
-      coeff *= dt / (o + 1);
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const double sum = lam * (ta[k][j] + tb[k][j] + tc[k][j]);
-          ta[k][j] = fma(two_mu, ta[k][j], sum);
-          tb[k][j] = fma(two_mu, tb[k][j], sum);
-          tc[k][j] = fma(two_mu, tc[k][j], sum);
-        }
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int off = (K0 + k) * 64 + col;
-        const double2 va = lds2(QA + off), vb = lds2(QA + PV + off), vc = lds2(QA + 2 * PV + off);
-        sts2(QA + off, fma(coeff, ta[k][0], va.x), fma(coeff, ta[k][1], va.y));
-        sts2(QA + PV + off, fma(coeff, tb[k][0], vb.x), fma(coeff, tb[k][1], vb.y));
-        sts2(QA + 2 * PV + off, fma(coeff, tc[k][0], vc.x), fma(coeff, tc[k][1], vc.y));
-      }
-      if (o + 1 < N8) {
-        if (!DB) __syncthreads();
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int off = (K0 + k) * 64 + col;
-          sts2(PN + off, ta[k][0], ta[k][1]);
-          sts2(PN + PV + off, tb[k][0], tb[k][1]);
-          sts2(PN + 2 * PV + off, tc[k][0], tc[k][1]);
-        }
-      }
-      __syncthreads();
-      double* sw = P;
-      P = PN;
-      PN = sw;
-    }
+  // ---- Cauchy-Kowalewsky recursion, Horner form ------------------------------------------
+  {
+    const int role = kRole[warp];
+    if (role >= 0)
+      ck_quantity<8>(P, Q, kp.cf, role, 0, g, t, col, d0, d1, c4);
+    else
+      ck_normal<4>(P, Q, kp.cf, 4 * (-role - 1), g, t, col, d0, d1, c4);
   }
 
   TM3(2);
@@ -321,14 +326,14 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   // 18 units (quantity s, k3 half h) over the 8 warps: qavg and favg from registers, x/y faces
   // by DMMA from the accumulator (staged into the dead p buffers); the unit with h = 0 also does
   // the z faces, which need the whole column.
-  double* FQ = sm8;  // face_q staging [6][8][8][9] (the p buffer is dead after the last barrier)
+  double* FQ = Q;  // face_q staging [6][8][8][9] (q is dead after the last barrier)
   const bool faces = a.face_q || a.face_f;
   const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0;  // padded phi (rows / cols = side)
   const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
 #pragma unroll 1
   for (int unit = warp; unit < 2 * NV; unit += NWARP) {
     const int s = unit >> 1, h = unit & 1, K0 = 4 * h;
-    const double* qs = QA + s * PV;
+    const double* qs = P + s * PV;
     double qa[4][2];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -391,9 +396,9 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     }
   }
   if (faces) {
-    __syncthreads();  // FQ complete; QA no longer read (the face_f staging may overlap it)
+    __syncthreads();  // FQ complete; qavg (P) no longer read, so face_f is staged over it
     TM3(3);
-    double* FF = sm8 + 6 * FACE;
+    double* FF = P;
     // face_f[f][ab][so] = coef(so, d) face_q[f][ab][in(so, d)]: thread tid owns quantity
     // so = tid % 9 for in-face nodes ab = tid / 9 + 28 i (252 active threads)
     if (a.face_f && tid < 252) {
@@ -458,9 +463,16 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   kp.check = p.check;
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
-  const bool db = p.dmma8_double_buffer;
-  auto kern = db ? stp_dmma8_kernel<true> : stp_dmma8_kernel<false>;
-  int smem = smem8(db);
+  {
+    double c = a.dt;  // same operation sequence as proj/src/stp_splitck.cpp:45,64
+    kp.cf[0] = c;
+    for (int o = 1; o < N8; ++o) {
+      c *= a.dt / (o + 1);
+      kp.cf[o] = c;
+    }
+  }
+  auto kern = stp_dmma8_kernel;
+  int smem = kSmem8;
 #ifdef ADERSTP_EXPT_TIMING
   if (const char* x = std::getenv("ADERSTP_EXPT_SMEM")) smem += std::atoi(x);  // occupancy experiments
 #endif
@@ -470,7 +482,7 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   if (err != cudaSuccess) return err;
   if (a.n_elem == 0) return cudaSuccess;
   if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
-  kern<<<(unsigned)a.n_elem, THREADS8, smem, stream>>>(kp, a, p.d_status);
+  kern<<<(unsigned)a.n_elem, NWARP * 32, smem, stream>>>(kp, a, p.d_status);
   return cudaGetLastError();
 }
 

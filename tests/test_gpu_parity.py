@@ -85,8 +85,8 @@ def test_kernel_variants_agree(stp, oracle, monkeypatch, n):
     par_h = par.cpu().numpy()
     dt = O.cfl_dt(n, par_h[:, 1].max())
     ref = oracle.stp(n, 9, oracle.from_aosoa(n, 9, 9, q.cpu().numpy()), dt, par=oracle.material_lmr(par_h))
-    for env in ({"ADERSTP_NO_DMMA8": "1"}, {"ADERSTP_FORCE_GENERIC": "1"}, {"ADERSTP_DMMA8_DB": "1"}):
-        for k in ("ADERSTP_NO_DMMA8", "ADERSTP_FORCE_GENERIC", "ADERSTP_DMMA8_DB"):
+    for env in ({"ADERSTP_NO_DMMA8": "1"}, {"ADERSTP_FORCE_GENERIC": "1"}):
+        for k in ("ADERSTP_NO_DMMA8", "ADERSTP_FORCE_GENERIC"):
             monkeypatch.setenv(k, env.get(k, "0"))
         plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
         out = plan.predict(q, dt, par=par)
