@@ -163,7 +163,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");
     lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
     const char* ps = std::getenv("ADERSTP_PASS_SLOTS");
-    lp.pass_slots = (ps && ps[0] == '8') ? 8 : (ps && ps[0] == '1' && ps[1] == '2') ? 12 : 6;
+    lp.pass_slots = !ps ? 0 : (ps[0] == '6') ? 6 : (ps[0] == '8') ? 8 : (ps[0] == '1' && ps[1] == '2') ? 12 : 0;
   }
   aderstp::make_host_basis(n, &lp.basis);
 

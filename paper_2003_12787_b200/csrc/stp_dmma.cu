@@ -17,7 +17,7 @@
 
 // zero-padded 8 x 8 D per order (row k = node, col l), uploaded at plan creation
 extern "C" {
-__constant__ double aderstp_kDP[9 * 64];
+__constant__ __align__(16) double aderstp_kDP[9 * 64];
 #ifdef ADERSTP_EXPT_TIMING
 __device__ long long aderstp_dbg_clock2[4096 * 8];
 int aderstp_dbg_clock2_copy(long long* host, int count) {

@@ -34,7 +34,7 @@
 // The z-contraction reads it at the point of use through volatile ld.const (constant cache,
 // broadcast), so ptxas cannot hoist 64 doubles of D into registers and spill.
 extern "C" {
-__constant__ double aderstp_kD8[64];
+__constant__ __align__(16) double aderstp_kD8[64];
 #ifdef ADERSTP_EXPT_TIMING
 __device__ long long aderstp_dbg_clock3[4096 * 8];
 int aderstp_dbg_clock3_copy(long long* host, int count) {

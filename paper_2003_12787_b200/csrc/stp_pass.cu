@@ -29,7 +29,7 @@
 // padded to 6 doubles so they load as 16-byte pairs: [A: h x 6][B: h x 6][M: 6], h = n/2,
 // stored at offset order*80.
 extern "C" {
-__constant__ double aderstp_kEO[11 * 80];
+__constant__ __align__(16) double aderstp_kEO[11 * 80];
 #ifdef ADERSTP_EXPT_TIMING
 __device__ long long aderstp_dbg_clock[4096 * 8];
 int aderstp_dbg_clock_copy(long long* host, int count) {
@@ -205,8 +205,26 @@ __device__ __forceinline__ void line_pass(const double* P, double* T, int slot, 
 template <int N>
 struct PassParams {
   double phi[2][N];
+  double cf[N];  // cf[o] = dt^(o+1)/(o+1)! (Horner coefficients, stp_splitck.cpp:45,64)
   int check, par_kind, q_stride;
 };
+
+template <int N>
+void fill_pass_params(const LaunchPlan& p, const BatchArgs& a, PassParams<N>& kp) {
+  for (int j = 0; j < N; ++j) {
+    kp.phi[0][j] = p.basis.face_left[j];
+    kp.phi[1][j] = p.basis.face_right[j];
+  }
+  double c = a.dt;
+  kp.cf[0] = c;
+  for (int o = 1; o < N; ++o) {
+    c *= a.dt / (o + 1);
+    kp.cf[o] = c;
+  }
+  kp.check = p.check;
+  kp.par_kind = p.par_kind;
+  kp.q_stride = p.q_stride;
+}
 
 // Node-wise epilogue helpers: the elastic flux F_d(q)_s = coef(s,d) q[in(s,d)] with
 // compile-time (s, d), so every index below folds to a constant.
@@ -462,13 +480,7 @@ template <int N, int SL>
 cudaError_t launch_pass_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
   using G = Geo<N, SL>;
   PassParams<N> kp;
-  for (int j = 0; j < N; ++j) {
-    kp.phi[0][j] = p.basis.face_left[j];
-    kp.phi[1][j] = p.basis.face_right[j];
-  }
-  kp.check = p.check;
-  kp.par_kind = p.par_kind;
-  kp.q_stride = p.q_stride;
+  fill_pass_params(p, a, kp);
   auto kern = stp_pass_kernel<N, SL>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err == cudaSuccess)
@@ -483,27 +495,92 @@ cudaError_t launch_pass_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t 
 
 
 // =============================================================================================
-// Bipartite variant.  The elastic operator couples stresses and velocities only: stress targets
-// read velocity sources and vice versa.  A CK step therefore runs as
+// Bipartite + tensor-memory variant (nDof 9, 10).
+//
+// The elastic operator couples stresses and velocities only (proj/src/pde.cpp:180-218): stress
+// targets read velocity sources and vice versa.  A CK step therefore runs as
 //   phase V: new (u, v, w) from the stress fields            -> TEMP (3 spare field slots)
 //   phase S: new stresses from the OLD (u, v, w)             -> in place over the stresses
-// (the stresses are dead once phase V is done) and the velocity slots swap with TEMP.  Twelve
-// field slots per element instead of eighteen: nDof 10 fits two CTAs per SM.  The time integral
-// qavg accumulates directly in the qavg output array (L2-resident while the element is in
-// flight), which frees the registers the in-register accumulator needed.
+// (the stresses are dead once phase V is done) and the velocity slots swap with TEMP: twelve
+// field slots per element instead of eighteen, so nDof 10 fits two CTAs per SM.
+// The series is evaluated in Horner form, r <- c_o q + L r (as in stp_dmma8.cu), so there is no
+// qavg accumulator at all -- the last iterate IS qavg.  The c_o q term is added by the thread
+// that finishes a target line (its z pass); that thread keeps the q values of exactly those
+// z-lines in tensor memory (thread-private TMEM columns, tcgen05.ld), off the shared-memory pipe
+// and out of the register file.
 template <int N>
 struct GeoB {
+  static_assert(N >= 8 && N <= 10, "TMEM column layout below assumes 8 <= nDof <= 10");
   static constexpr int RS = (N % 2 == 0) ? N + 1 : N;
   static constexpr int PL = N * RS;
   static constexpr int VS = N * PL;
   static constexpr int EB = 12 * VS;  // field slots: 0-5 stresses, 6-8 / 9-11 velocities
   static constexpr int LINES = N * N;
   static constexpr int TASKS = 3 * LINES;
-  static constexpr int EPB = N >= 9 ? 1 : N >= 7 ? 2 : N >= 5 ? 4 : N == 4 ? 8 : N == 3 ? 12 : 32;
-  static constexpr int THREADS = ((TASKS * EPB + 31) / 32) * 32;
-  static constexpr int SMEM = EB * EPB * 8;
-  static constexpr int MINB = N >= 10 ? 2 : N == 9 ? 3 : 2;
+  static constexpr int THREADS = ((TASKS + 31) / 32) * 32;
+  static constexpr int NW = THREADS / 32;
+  static constexpr int SMEM = EB * 8;
+  // TMEM columns of one warp: the q z-lines of 4 targets (phase V + up to three in phase S);
+  // nodes 0..7 of target k in the 16-column block k, nodes 8, 9 at column 64 + 4k
+  static constexpr int WCOLS = N == 8 ? 64 : 80;
+  static constexpr int TC = ((NW + 3) / 4) * WCOLS;
+  static constexpr int TCOLS = TC <= 32 ? 32 : TC <= 64 ? 64 : TC <= 128 ? 128 : TC <= 256 ? 256 : 512;
 };
+
+__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(ta));
+}
+__device__ __forceinline__ void tm_ld4(uint32_t ta, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(ta));
+}
+__device__ __forceinline__ void tm_ld2(uint32_t ta, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(ta));
+}
+__device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};\n" ::"r"(ta),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
+}
+__device__ __forceinline__ void tm_st4(uint32_t ta, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(ta), "r"(r[0]), "r"(r[1]),
+               "r"(r[2]), "r"(r[3]));
+}
+__device__ __forceinline__ void tm_st2(uint32_t ta, const uint32_t* r) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(ta), "r"(r[0]), "r"(r[1]));
+}
+
+// q z-line of TMEM target k (warp-collective: every lane of the warp executes it)
+template <int N>
+__device__ __forceinline__ void tm_load_q(uint32_t ta, int k, double (&q)[N]) {
+  uint32_t r[2 * N];
+  tm_ld16(ta + 16 * k, r);
+  if constexpr (N == 10) tm_ld4(ta + 64 + 4 * k, r + 16);
+  if constexpr (N == 9) tm_ld2(ta + 64 + 4 * k, r + 16);
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) q[i] = __hiloint2double(r[2 * i + 1], r[2 * i]);
+}
+template <int N>
+__device__ __forceinline__ void tm_store_q(uint32_t ta, int k, const double (&q)[N]) {
+  uint32_t r[2 * N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    r[2 * i] = __double2loint(q[i]);
+    r[2 * i + 1] = __double2hiint(q[i]);
+  }
+  tm_st16(ta + 16 * k, r);
+  if constexpr (N == 10) tm_st4(ta + 64 + 4 * k, r + 16);
+  if constexpr (N == 9) tm_st2(ta + 64 + 4 * k, r + 16);
+}
 
 // phase-V pass D, slot j: stress source -> velocity target (coefficient 1/rho)
 __constant__ int8_t kBipV[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
@@ -511,6 +588,13 @@ __constant__ int8_t kBipV[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
 __constant__ int8_t kBipS0[3][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}};
 __constant__ int8_t kBipS12[3][2][2] = {{{7, 3}, {8, 4}}, {{6, 3}, {8, 5}}, {{6, 4}, {7, 5}}};  // (src, tgt)
 
+template <int N, int D>
+__device__ __forceinline__ int bip_start(int la, int lb) {
+  using G = GeoB<N>;
+  return D == 0 ? la * G::PL + lb * G::RS : D == 1 ? la * G::PL + lb : la * G::RS + lb;
+}
+
+// Passes x and y: contract the source line and write (first touch) or accumulate into targets.
 template <int N, int D>
 __device__ __forceinline__ void bip_line(const double* src, double* const* dst, const double* cf, int nt,
                                          bool write) {
@@ -536,34 +620,64 @@ __device__ __forceinline__ void bip_line(const double* src, double* const* dst, 
   }
 }
 
-template <int N, int D>
-__device__ __forceinline__ int bip_start(int la, int lb) {
+// Pass z: the last contribution to each target line, plus the Horner term c_o q (TMEM target
+// k0 + k).  Warp-collective (the TMEM loads): every thread of the CTA calls it; ntw is the
+// warp-uniform maximum target count, nt this thread's (0 for idle threads).
+template <int N>
+__device__ __forceinline__ void bip_line_z(const double* src, double* const* dst, const double* cf, int nt,
+                                           int ntw, uint32_t ta, int k0, double co) {
   using G = GeoB<N>;
-  return D == 0 ? la * G::PL + lb * G::RS : D == 1 ? la * G::PL + lb : la * G::RS + lb;
+  double out[N];
+  if (nt > 0) {
+    double p[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) p[l] = src[l * G::PL];
+    eo_apply<N>(p, out);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k >= ntw) break;
+    double q[N];
+    tm_load_q<N>(ta, k0 + k, q);
+    if (k < nt) {
+      double* d = dst[k];
+      const double c = cf[k];
+#pragma unroll
+      for (int l = 0; l < N; ++l) d[l * G::PL] = fma(co, q[l], fma(c, out[l], d[l * G::PL]));
+    }
+  }
 }
 
 template <int N>
-__global__ void __launch_bounds__(GeoB<N>::THREADS, GeoB<N>::MINB)
+__global__ void __launch_bounds__(GeoB<N>::THREADS, 2)
 stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   using G = GeoB<N>;
   extern __shared__ __align__(16) double smb[];
-  const int tid = threadIdx.x;
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
   unsigned int flags = 0;
-  const double dt = a.dt;
-  const long long e0 = (long long)blockIdx.x * G::EPB;
+  const long long e = blockIdx.x;
   constexpr int N3 = N * N * N;
   constexpr int OUTV = NVE * N3;
+  double* E = smb;
 
-  const int el = tid / G::TASKS;
-  const int slot = (tid - el * G::TASKS) / G::LINES;
-  const int line = tid - el * G::TASKS - slot * G::LINES;
-  const bool active = el < G::EPB && e0 + el < a.n_elem;
+  const int slot = tid / G::LINES;  // 0..2; 3 = padding thread
+  const int line = tid - slot * G::LINES;
+  const bool active = slot < 3;
+  const int sl = active ? slot : 0;
   const int la = line / N, lb = line - la * N;
-  double* E = smb + (el < G::EPB ? el : 0) * G::EB;  // this task's element
 
-  double c4[4] = {0.0, 0.0, 0.0, 0.0};
-  if (active) {
-    const double* pr = a.par + 3 * (e0 + el);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_base_s)),
+                 "n"(G::TCOLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+
+  double c4[4];
+  {
+    const double* pr = a.par + 3 * e;
     double lam, mu, rho;
     if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
       rho = pr[0];
@@ -581,16 +695,13 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     c4[3] = 1.0 / rho;
   }
 
-  // ---- stage q -> slots 0..8; qavg output = dt q ------------------------------------------
+  // ---- stage q -> field slots 0..8 (node-wise, coalesced AoSoA loads) ---------------------
   {
     const int qs = kp.q_stride;
-    for (int i = tid; i < G::EPB * N3; i += G::THREADS) {
-      const int ee = i / N3, node = i - ee * N3;
-      if (e0 + ee >= a.n_elem) continue;
-      const int k1 = node % N, k32 = node / N;
-      const double* src = a.q + (e0 + ee) * (long long)(N3 * qs) + k32 * qs * N + k1;
-      double* dst = smb + ee * G::EB + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
-      double* qo = a.qavg + (e0 + ee) * (long long)OUTV + k32 * NVE * N + k1;
+    for (int i = tid; i < N3; i += G::THREADS) {
+      const int k1 = i % N, k32 = i / N;
+      const double* src = a.q + e * (long long)(N3 * qs) + k32 * qs * N + k1;
+      double* dst = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
       double v[NVE];
 #pragma unroll
       for (int s = 0; s < NVE; ++s) v[s] = __ldcs(src + s * N);
@@ -598,171 +709,195 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
       for (int s = 0; s < NVE; ++s) {
         if (kp.check && !isfinite(v[s])) flags |= 1u;
         dst[s * G::VS] = v[s];
-        qo[s * N] = dt * v[s];
       }
     }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * G::WCOLS);
+
+  // ---- q of the target lines this thread finishes (its z pass) -> TMEM:
+  //   block 0: the phase-V velocity 6 + slot
+  //   blocks 1..: phase-S stresses -- slot 0: sxx, syy, szz; slot 1: sxz and sxy (sxy has no
+  //   z term: the slot-1 z pass adds only its Horner term); slot 2: syz
+  const int ntS = active ? (slot == 0 ? 3 : slot == 1 ? 2 : 1) : 0;
+  const int ntS_w = __reduce_max_sync(0xffffffffu, (unsigned)ntS);
+  const int zst = la * G::RS + lb;  // z-line (k2, k1) = (la, lb)
+  {
+    double v[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) v[l] = active ? E[(6 + sl) * G::VS + zst + l * G::PL] : 0.0;
+    tm_store_q<N>(ta, 0, v);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k >= ntS_w) break;
+      const int f = slot == 0 ? k : slot == 1 ? (k == 0 ? 4 : 3) : 5;
+#pragma unroll
+      for (int l = 0; l < N; ++l) v[l] = (k < ntS) ? E[f * G::VS + zst + l * G::PL] : 0.0;
+      tm_store_q<N>(ta, 1 + k, v);
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+  }
+  __syncthreads();
+  // Horner start r = c_(n-1) q
+  {
+    const double c = kp.cf[N - 1];
+    for (int i = tid; i < NVE * G::VS; i += G::THREADS) E[i] *= c;
   }
   __syncthreads();
 
-  double coeff = dt;
   int vb = 6;  // slot of u (velocities occupy vb .. vb+2; the other three slots are TEMP)
 #pragma unroll 1
-  for (int o = 1; o < N; ++o) {
+  for (int o = N - 2; o >= 0; --o) {
+    const double co = kp.cf[o];
     const int tb = 15 - vb;  // TEMP base: 9 when vb = 6, 6 when vb = 9
+    const double crho[3] = {c4[3], 0.0, 0.0};
     // phase V: velocity targets from stress sources, into TEMP
     if (active) {
-      double* dst[3];
-      double cf[3] = {c4[3], 0.0, 0.0};
-      dst[0] = E + (tb + slot) * G::VS + bip_start<N, 0>(la, lb);
-      bip_line<N, 0>(E + kBipV[0][slot] * G::VS + bip_start<N, 0>(la, lb), dst, cf, 1, true);
+      double* dst[3] = {E + (tb + sl) * G::VS + bip_start<N, 0>(la, lb), nullptr, nullptr};
+      bip_line<N, 0>(E + kBipV[0][sl] * G::VS + bip_start<N, 0>(la, lb), dst, crho, 1, true);
     }
     __syncthreads();
     if (active) {
-      double* dst[3];
-      double cf[3] = {c4[3], 0.0, 0.0};
-      dst[0] = E + (tb + slot) * G::VS + bip_start<N, 1>(la, lb);
-      bip_line<N, 1>(E + kBipV[1][slot] * G::VS + bip_start<N, 1>(la, lb), dst, cf, 1, false);
+      double* dst[3] = {E + (tb + sl) * G::VS + bip_start<N, 1>(la, lb), nullptr, nullptr};
+      bip_line<N, 1>(E + kBipV[1][sl] * G::VS + bip_start<N, 1>(la, lb), dst, crho, 1, false);
     }
     __syncthreads();
-    if (active) {
-      double* dst[3];
-      double cf[3] = {c4[3], 0.0, 0.0};
-      dst[0] = E + (tb + slot) * G::VS + bip_start<N, 2>(la, lb);
-      bip_line<N, 2>(E + kBipV[2][slot] * G::VS + bip_start<N, 2>(la, lb), dst, cf, 1, false);
+    {
+      double* dst[3] = {E + (tb + sl) * G::VS + zst, nullptr, nullptr};
+      bip_line_z<N>(E + kBipV[2][sl] * G::VS + zst, dst, crho, active ? 1 : 0, 1, ta, 0, co);
     }
     __syncthreads();
     // phase S: stress targets from the old velocities, in place over the (dead) stresses
+    {
+      double cf[3];
+      double* dst[3];
+      int srcf, nt;
+      if (slot == 0) {
+        srcf = vb;
+        nt = 3;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      if (active) {
-        double* dst[3];
-        double cf[3];
-        int srcf, nt;
-        if (slot == 0) {
-          srcf = vb + d;
-          nt = 3;
-#pragma unroll
-          for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[d][k]);
-        } else {
-          const int sv = kBipS12[d][slot - 1][0];  // 6, 7, 8 = u, v, w
-          srcf = vb + (sv - 6);
-          nt = 1;
-          cf[0] = c4[2];
-          cf[1] = cf[2] = 0.0;
-        }
-        const bool write = d == 0 || (d == 1 && slot == 2);
-        if (d == 0) {
-          const int st = bip_start<N, 0>(la, lb);
-          if (slot == 0) { dst[0] = E + st; dst[1] = E + G::VS + st; dst[2] = E + 2 * G::VS + st; }
-          else dst[0] = E + kBipS12[0][slot - 1][1] * G::VS + st;
-          bip_line<N, 0>(E + srcf * G::VS + st, dst, cf, nt, write);
-        } else if (d == 1) {
-          const int st = bip_start<N, 1>(la, lb);
-          if (slot == 0) { dst[0] = E + st; dst[1] = E + G::VS + st; dst[2] = E + 2 * G::VS + st; }
-          else dst[0] = E + kBipS12[1][slot - 1][1] * G::VS + st;
-          bip_line<N, 1>(E + srcf * G::VS + st, dst, cf, nt, write);
-        } else {
-          const int st = bip_start<N, 2>(la, lb);
-          if (slot == 0) { dst[0] = E + st; dst[1] = E + G::VS + st; dst[2] = E + 2 * G::VS + st; }
-          else dst[0] = E + kBipS12[2][slot - 1][1] * G::VS + st;
-          bip_line<N, 2>(E + srcf * G::VS + st, dst, cf, nt, write);
-        }
+        for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[0][k]);
+      } else {
+        srcf = vb + (kBipS12[0][sl > 0 ? sl - 1 : 0][0] - 6);
+        nt = 1;
+        cf[0] = c4[2];
+        cf[1] = cf[2] = 0.0;
       }
-      __syncthreads();
+      const int st = bip_start<N, 0>(la, lb);
+      if (slot == 0) {
+        dst[0] = E + st;
+        dst[1] = E + G::VS + st;
+        dst[2] = E + 2 * G::VS + st;
+      } else {
+        dst[0] = E + kBipS12[0][sl > 0 ? sl - 1 : 0][1] * G::VS + st;
+        dst[1] = dst[2] = nullptr;
+      }
+      if (active) bip_line<N, 0>(E + srcf * G::VS + st, dst, cf, nt, true);
     }
+    __syncthreads();
+    {
+      double cf[3];
+      double* dst[3];
+      int srcf, nt;
+      if (slot == 0) {
+        srcf = vb + 1;
+        nt = 3;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[1][k]);
+      } else {
+        srcf = vb + (kBipS12[1][sl > 0 ? sl - 1 : 0][0] - 6);
+        nt = 1;
+        cf[0] = c4[2];
+        cf[1] = cf[2] = 0.0;
+      }
+      const int st = bip_start<N, 1>(la, lb);
+      if (slot == 0) {
+        dst[0] = E + st;
+        dst[1] = E + G::VS + st;
+        dst[2] = E + 2 * G::VS + st;
+      } else {
+        dst[0] = E + kBipS12[1][sl > 0 ? sl - 1 : 0][1] * G::VS + st;
+        dst[1] = dst[2] = nullptr;
+      }
+      // syz (slot 2) gets its first contribution here
+      if (active) bip_line<N, 1>(E + srcf * G::VS + st, dst, cf, nt, slot == 2);
+    }
+    __syncthreads();
+    {
+      double cf[3];
+      double* dst[3];
+      int srcf;
+      if (slot == 0) {
+        srcf = vb + 2;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[2][k]);
+        dst[0] = E + zst;
+        dst[1] = E + G::VS + zst;
+        dst[2] = E + 2 * G::VS + zst;
+      } else {
+        srcf = vb + (kBipS12[2][sl > 0 ? sl - 1 : 0][0] - 6);
+        cf[0] = c4[2];
+        cf[1] = cf[2] = 0.0;  // slot 1, target 1 = sxy: coefficient 0, Horner term only
+        dst[0] = E + kBipS12[2][sl > 0 ? sl - 1 : 0][1] * G::VS + zst;
+        dst[1] = E + 3 * G::VS + zst;
+        dst[2] = nullptr;
+      }
+      bip_line_z<N>(E + srcf * G::VS + zst, dst, cf, ntS, ntS_w, ta, 1, co);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     vb = tb;  // the new velocities live in TEMP
-    // qavg += c_o t (stp_splitck.cpp:64-69), accumulated in the output array: flat over
-    // [e][k3][k2][s][k1], consecutive threads = consecutive addresses
-    coeff *= dt / (o + 1);
-    for (int i = tid; i < G::EPB * OUTV; i += G::THREADS) {
-      const int ee = i / OUTV;
-      if (e0 + ee >= a.n_elem) continue;
-      int r = i - ee * OUTV;
-      const int k1 = r % N;
-      r /= N;
-      const int s = r % NVE;
-      const int k32 = r / NVE;
-      const int fs = s < 6 ? s : vb + (s - 6);
-      double* qo = a.qavg + (e0 + ee) * (long long)OUTV + (i - ee * OUTV);
-      *qo = fma(coeff, smb[ee * G::EB + fs * G::VS + (k32 / N) * G::PL + (k32 % N) * G::RS + k1], *qo);
-    }
-    // no barrier: the next phase V pass x reads the stresses (read-only) and writes the old
-    // velocity slots, which nobody reads any more
   }
-  __syncthreads();
-  // ---- epilogue: qavg (final, in the output array) back into slots 0..8, then favg + faces --
-  for (int i = tid; i < G::EPB * OUTV; i += G::THREADS) {
-    const int ee = i / OUTV;
-    if (e0 + ee >= a.n_elem) continue;
-    int r = i - ee * OUTV;
-    const int k1 = r % N;
-    r /= N;
-    const int s = r % NVE;
-    const int k32 = r / NVE;
-    smb[ee * G::EB + s * G::VS + (k32 / N) * G::PL + (k32 % N) * G::RS + k1] =
-        a.qavg[(e0 + ee) * (long long)OUTV + (i - ee * OUTV)];
-  }
-  __syncthreads();
-  if (a.favg) {
-    for (int i = tid; i < G::EPB * N3; i += G::THREADS) {
-      const int ee = i / N3, node = i - ee * N3;
-      if (e0 + ee >= a.n_elem) continue;
-      const int k1 = node % N, k32 = node / N;
-      const double* qs = smb + ee * G::EB + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
-      double v[NVE];
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base_s), "n"(G::TCOLS)
+                 : "memory");
+
+  // ---- epilogue: qavg = the last iterate (fields 0..5 and vb..vb+2) -----------------------
+  auto fld = [&](int s) { return s < 6 ? s : vb + (s - 6); };
+  for (int i = tid; i < N3; i += G::THREADS) {
+    const int k1 = i % N, k32 = i / N;
+    const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+    double v[NVE];
 #pragma unroll
-      for (int s = 0; s < NVE; ++s) v[s] = qs[s * G::VS];
-      double cc[4];
-      {
-        const double* pr = a.par + 3 * (e0 + ee);
-        if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
-          const double mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
-          const double lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
-          cc[0] = lam + 2.0 * mu;
-          cc[1] = lam;
-          cc[2] = mu;
-          cc[3] = 1.0 / pr[0];
-        } else {
-          cc[0] = pr[0] + 2.0 * pr[1];
-          cc[1] = pr[0];
-          cc[2] = pr[1];
-          cc[3] = 1.0 / pr[2];
-        }
-      }
-      double* fo = a.favg + (e0 + ee) * (long long)(3 * OUTV) + k32 * NVE * N + k1;
+    for (int s = 0; s < NVE; ++s) v[s] = qs[fld(s) * G::VS];
+    const long long ob = e * (long long)OUTV + k32 * NVE * N + k1;
+#pragma unroll
+    for (int s = 0; s < NVE; ++s) __stcs(a.qavg + ob + s * N, v[s]);
+    if (a.favg) {
+      double* fo = a.favg + e * (long long)(3 * OUTV) + k32 * NVE * N + k1;
 #pragma unroll
       for (int d = 0; d < 3; ++d)
 #pragma unroll
         for (int s = 0; s < NVE; ++s)
-          __stcs(fo + d * OUTV + s * N, e_coef(s, d) == 4 ? 0.0 : cc[e_coef(s, d)] * v[e_in(s, d)]);
+          __stcs(fo + d * OUTV + s * N, e_coef(s, d) == 4 ? 0.0 : c4[e_coef(s, d)] * v[e_in(s, d)]);
     }
   }
   if (a.face_q || a.face_f) {
     constexpr int FV = N * N * NVE;
-    for (int i = tid; i < G::EPB * 3 * N * N; i += G::THREADS) {
-      const int ee = i / (3 * N * N);
-      if (e0 + ee >= a.n_elem) continue;
-      int r = i - ee * 3 * N * N;
-      const int d = r / (N * N);
-      const int ab = r - d * N * N;
+    for (int i = tid; i < 3 * N * N; i += G::THREADS) {
+      const int d = i / (N * N);
+      const int ab = i - d * N * N;
       const int aa = ab / N, bb = ab - aa * N;
       const int start = d == 0 ? aa * G::PL + bb * G::RS : d == 1 ? aa * G::PL + bb : aa * G::RS + bb;
       const int stride = d == 0 ? 1 : d == 1 ? G::RS : G::PL;
-      const double* q0 = smb + ee * G::EB + start;
       double f0[NVE], f1[NVE];
 #pragma unroll
       for (int s = 0; s < NVE; ++s) {
+        const double* q0 = E + fld(s) * G::VS + start;
         double x0 = 0.0, x1 = 0.0;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-          const double x = q0[s * G::VS + j * stride];
+          const double x = q0[j * stride];
           x0 = fma(kp.phi[0][j], x, x0);
           x1 = fma(kp.phi[1][j], x, x1);
         }
         f0[s] = x0;
         f1[s] = x1;
       }
-      const long long fb = (e0 + ee) * 6LL * FV + (2 * d) * FV + ab * NVE;
+      const long long fb = e * 6LL * FV + (2 * d) * FV + ab * NVE;
       if (a.face_q) {
 #pragma unroll
         for (int s = 0; s < NVE; ++s) {
@@ -771,33 +906,18 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
         }
       }
       if (a.face_f) {
-        double cc[4];
-        const double* pr = a.par + 3 * (e0 + ee);
-        if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
-          const double mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
-          const double lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
-          cc[0] = lam + 2.0 * mu;
-          cc[1] = lam;
-          cc[2] = mu;
-          cc[3] = 1.0 / pr[0];
-        } else {
-          cc[0] = pr[0] + 2.0 * pr[1];
-          cc[1] = pr[0];
-          cc[2] = pr[1];
-          cc[3] = 1.0 / pr[2];
-        }
 #pragma unroll
         for (int s = 0; s < NVE; ++s) {
           double g0, g1;
           if (d == 0) {
-            g0 = e_coef(s, 0) == 4 ? 0.0 : cc[e_coef(s, 0)] * f0[e_in(s, 0)];
-            g1 = e_coef(s, 0) == 4 ? 0.0 : cc[e_coef(s, 0)] * f1[e_in(s, 0)];
+            g0 = e_coef(s, 0) == 4 ? 0.0 : c4[e_coef(s, 0)] * f0[e_in(s, 0)];
+            g1 = e_coef(s, 0) == 4 ? 0.0 : c4[e_coef(s, 0)] * f1[e_in(s, 0)];
           } else if (d == 1) {
-            g0 = e_coef(s, 1) == 4 ? 0.0 : cc[e_coef(s, 1)] * f0[e_in(s, 1)];
-            g1 = e_coef(s, 1) == 4 ? 0.0 : cc[e_coef(s, 1)] * f1[e_in(s, 1)];
+            g0 = e_coef(s, 1) == 4 ? 0.0 : c4[e_coef(s, 1)] * f0[e_in(s, 1)];
+            g1 = e_coef(s, 1) == 4 ? 0.0 : c4[e_coef(s, 1)] * f1[e_in(s, 1)];
           } else {
-            g0 = e_coef(s, 2) == 4 ? 0.0 : cc[e_coef(s, 2)] * f0[e_in(s, 2)];
-            g1 = e_coef(s, 2) == 4 ? 0.0 : cc[e_coef(s, 2)] * f1[e_in(s, 2)];
+            g0 = e_coef(s, 2) == 4 ? 0.0 : c4[e_coef(s, 2)] * f0[e_in(s, 2)];
+            g1 = e_coef(s, 2) == 4 ? 0.0 : c4[e_coef(s, 2)] * f1[e_in(s, 2)];
           }
           __stcs(a.face_f + fb + s, g0);
           __stcs(a.face_f + fb + FV + s, g1);
@@ -812,22 +932,15 @@ template <int N>
 cudaError_t launch_bip_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
   using G = GeoB<N>;
   PassParams<N> kp;
-  for (int j = 0; j < N; ++j) {
-    kp.phi[0][j] = p.basis.face_left[j];
-    kp.phi[1][j] = p.basis.face_right[j];
-  }
-  kp.check = p.check;
-  kp.par_kind = p.par_kind;
-  kp.q_stride = p.q_stride;
+  fill_pass_params(p, a, kp);
   auto kern = stp_bip_kernel<N>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err == cudaSuccess)
     err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (err != cudaSuccess) return err;
-  const long long blocks = (a.n_elem + G::EPB - 1) / G::EPB;
-  if (blocks == 0) return cudaSuccess;
-  if (blocks > 0x7fffffffLL) return cudaErrorInvalidValue;
-  kern<<<(unsigned)blocks, G::THREADS, G::SMEM, stream>>>(kp, a, p.d_status);
+  if (a.n_elem == 0) return cudaSuccess;
+  if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kern<<<(unsigned)a.n_elem, G::THREADS, G::SMEM, stream>>>(kp, a, p.d_status);
   return cudaGetLastError();
 }
 
@@ -858,19 +971,12 @@ cudaError_t init_pass(const LaunchPlan& p) {
 }
 
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
-  if (p.pass_slots == 12) {
+  // bipartite + TMEM kernel: default for nDof 10, ADERSTP_PASS_SLOTS=12 forces it for nDof 9
+  if (p.pass_slots == 12 || (p.pass_slots == 0 && p.n == 10)) {
     switch (p.n) {
-      case 2: return launch_bip_n<2>(p, a, stream);
-      case 3: return launch_bip_n<3>(p, a, stream);
-      case 4: return launch_bip_n<4>(p, a, stream);
-      case 5: return launch_bip_n<5>(p, a, stream);
-      case 6: return launch_bip_n<6>(p, a, stream);
-      case 7: return launch_bip_n<7>(p, a, stream);
-      case 8: return launch_bip_n<8>(p, a, stream);
       case 9: return launch_bip_n<9>(p, a, stream);
       case 10: return launch_bip_n<10>(p, a, stream);
     }
-    return cudaErrorInvalidValue;
   }
   const bool eight = p.pass_slots == 8;
 #define ADERSTP_PASS_CASE(NN) \

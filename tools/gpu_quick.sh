@@ -5,3 +5,4 @@ for c in ${CONFIGS:-c3}; do
   python bench.py --config $c --steps 20 --no-e2e --no-cpu-baseline --no-other-configs 2>&1 | tail -1 | \
     python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', d['value'], d['roofline']['frac'], d['clocks'])"
 done
+[ -n "$EXPT" ] && python tools/expt_timing.py
