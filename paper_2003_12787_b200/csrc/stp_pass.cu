@@ -35,6 +35,9 @@ __device__ long long aderstp_dbg_clock[4096 * 8];
 int aderstp_dbg_clock_copy(long long* host, int count) {
   return (int)cudaMemcpyFromSymbol(host, aderstp_dbg_clock, sizeof(long long) * count);
 }
+#define TMB(i) if (threadIdx.x == 0 && blockIdx.x < 4096) aderstp_dbg_clock[blockIdx.x * 8 + (i)] = clock64()
+#else
+#define TMB(i)
 #endif
 }
 
@@ -510,10 +513,15 @@ cudaError_t launch_pass_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t 
 // and out of the register file.
 template <int N>
 struct GeoB {
-  static_assert(N >= 8 && N <= 10, "TMEM column layout below assumes 8 <= nDof <= 10");
-  static constexpr int RS = (N % 2 == 0) ? N + 1 : N;
-  static constexpr int PL = N * RS;
-  static constexpr int VS = N * PL;
+  static_assert(N >= 9 && N <= 10, "TMEM column layout below assumes nDof 9 or 10");
+  // Padding chosen by an exhaustive bank-conflict search over the six passes' access patterns
+  // (half-warp / quarter-warp bank-pair model, tools/bank_model.py): rows unpadded, planes
+  // padded so that y- and z-line starts of consecutive tasks fall on distinct banks; for even N
+  // the x lines are read and written as 16-byte pairs.  nDof 10: 4490 vs 6610 wavefronts/step.
+  static constexpr int RS = N;
+  static constexpr int PL = N == 10 ? 106 : 89;
+  static constexpr int VS = N == 10 ? 1060 : 801;
+  static constexpr bool X128 = N % 2 == 0;
   static constexpr int EB = 12 * VS;  // field slots: 0-5 stresses, 6-8 / 9-11 velocities
   static constexpr int LINES = N * N;
   static constexpr int TASKS = 3 * LINES;
@@ -601,6 +609,32 @@ __device__ __forceinline__ void bip_line(const double* src, double* const* dst, 
   using G = GeoB<N>;
   constexpr int ST = D == 0 ? 1 : D == 1 ? G::RS : G::PL;
   double p[N], out[N];
+  if constexpr (D == 0 && G::X128) {  // x lines: contiguous, 16-byte aligned
+#pragma unroll
+    for (int l = 0; l < N; l += 2) {
+      const double2 v = *reinterpret_cast<const double2*>(src + l);
+      p[l] = v.x;
+      p[l + 1] = v.y;
+    }
+    eo_apply<N>(p, out);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      if (k < nt) {
+        double2* d = reinterpret_cast<double2*>(dst[k]);
+        const double c = cf[k];
+#pragma unroll
+        for (int l = 0; l < N; l += 2) {
+          if (write) {
+            d[l / 2] = make_double2(c * out[l], c * out[l + 1]);
+          } else {
+            const double2 v = d[l / 2];
+            d[l / 2] = make_double2(fma(c, out[l], v.x), fma(c, out[l + 1], v.y));
+          }
+        }
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int l = 0; l < N; ++l) p[l] = src[l * ST];
   eo_apply<N>(p, out);
@@ -661,6 +695,7 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   constexpr int OUTV = NVE * N3;
   double* E = smb;
 
+  TMB(0);
   const int slot = tid / G::LINES;  // 0..2; 3 = padding thread
   const int line = tid - slot * G::LINES;
   const bool active = slot < 3;
@@ -747,6 +782,7 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   }
   __syncthreads();
 
+  TMB(1);
   int vb = 6;  // slot of u (velocities occupy vb .. vb+2; the other three slots are TEMP)
 #pragma unroll 1
   for (int o = N - 2; o >= 0; --o) {
@@ -855,6 +891,7 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base_s), "n"(G::TCOLS)
                  : "memory");
 
+  TMB(2);
   // ---- epilogue: qavg = the last iterate (fields 0..5 and vb..vb+2) -----------------------
   auto fld = [&](int s) { return s < 6 ? s : vb + (s - 6); };
   for (int i = tid; i < N3; i += G::THREADS) {
@@ -875,6 +912,7 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
           __stcs(fo + d * OUTV + s * N, e_coef(s, d) == 4 ? 0.0 : c4[e_coef(s, d)] * v[e_in(s, d)]);
     }
   }
+  TMB(3);
   if (a.face_q || a.face_f) {
     constexpr int FV = N * N * NVE;
     for (int i = tid; i < 3 * N * N; i += G::THREADS) {
@@ -925,6 +963,10 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
       }
     }
   }
+#ifdef ADERSTP_EXPT_TIMING
+  __syncthreads();
+#endif
+  TMB(4);
   if (kp.check && flags) atomicOr(status, flags);
 }
 

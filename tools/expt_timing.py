@@ -58,8 +58,8 @@ for cfg_name, elems in (("c4", 65536),):
     torch.cuda.synchronize()
     host = np.zeros(4096 * 8, dtype=np.int64)
     L.aderstp_dbg_clock_copy(host.ctypes.data, 4096 * 8)
-    t = host.reshape(4096, 8)[:, :4].astype(np.float64)
+    t = host.reshape(4096, 8)[:, :5].astype(np.float64)
     d = np.diff(t, axis=1)
-    tot = t[:, 3] - t[:, 0]
-    print(cfg_name, "per-CTA clocks: staging %.0f  CK loop %.0f  epilogue %.0f  total %.0f" % tuple(
+    tot = t[:, 4] - t[:, 0]
+    print("bip", cfg_name, "per-CTA clocks: staging+TMEM %.0f  CK loop %.0f  qavg/favg %.0f  faces %.0f  total %.0f" % tuple(
         list(np.median(d, axis=0)) + [np.median(tot)]))
