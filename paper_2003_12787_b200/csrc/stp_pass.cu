@@ -1013,8 +1013,9 @@ cudaError_t init_pass(const LaunchPlan& p) {
 }
 
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
-  // bipartite + TMEM kernel: default for nDof 10, ADERSTP_PASS_SLOTS=12 forces it for nDof 9
-  if (p.pass_slots == 12 || (p.pass_slots == 0 && p.n == 10)) {
+  // bipartite + TMEM kernel: the default for nDof 9 and 10 (ADERSTP_PASS_SLOTS=6/8 select the
+  // older line-pass kernel)
+  if (p.pass_slots == 12 || (p.pass_slots == 0 && p.n >= 9)) {
     switch (p.n) {
       case 9: return launch_bip_n<9>(p, a, stream);
       case 10: return launch_bip_n<10>(p, a, stream);
