@@ -730,20 +730,32 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     c4[3] = 1.0 / rho;
   }
 
-  // ---- stage q -> field slots 0..8 (node-wise, coalesced AoSoA loads) ---------------------
+  // ---- stage q -> field slots 0..8 (node-wise, coalesced AoSoA loads; k1 pairs for even N) --
   {
     const int qs = kp.q_stride;
-    for (int i = tid; i < N3; i += G::THREADS) {
-      const int k1 = i % N, k32 = i / N;
+    constexpr int V = N % 2 == 0 ? 2 : 1;  // nodes per task
+    for (int i = tid; i < N3 / V; i += G::THREADS) {
+      const int k1 = V * (i % (N / V)), k32 = i / (N / V);
       const double* src = a.q + e * (long long)(N3 * qs) + k32 * qs * N + k1;
       double* dst = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
-      double v[NVE];
+      if constexpr (V == 2) {
+        double2 v[NVE];
 #pragma unroll
-      for (int s = 0; s < NVE; ++s) v[s] = __ldcs(src + s * N);
+        for (int s = 0; s < NVE; ++s) v[s] = __ldcs(reinterpret_cast<const double2*>(src + s * N));
 #pragma unroll
-      for (int s = 0; s < NVE; ++s) {
-        if (kp.check && !isfinite(v[s])) flags |= 1u;
-        dst[s * G::VS] = v[s];
+        for (int s = 0; s < NVE; ++s) {
+          if (kp.check && !(isfinite(v[s].x) && isfinite(v[s].y))) flags |= 1u;
+          *reinterpret_cast<double2*>(dst + s * G::VS) = v[s];
+        }
+      } else {
+        double v[NVE];
+#pragma unroll
+        for (int s = 0; s < NVE; ++s) v[s] = __ldcs(src + s * N);
+#pragma unroll
+        for (int s = 0; s < NVE; ++s) {
+          if (kp.check && !isfinite(v[s])) flags |= 1u;
+          dst[s * G::VS] = v[s];
+        }
       }
     }
   }
@@ -759,26 +771,33 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   const int ntS = active ? (slot == 0 ? 3 : slot == 1 ? 2 : 1) : 0;
   const int ntS_w = __reduce_max_sync(0xffffffffu, (unsigned)ntS);
   const int zst = la * G::RS + lb;  // z-line (k2, k1) = (la, lb)
+  // These z-lines cover every node of the nine fields exactly once, so the same loop also
+  // writes the Horner start r = c_(n-1) q back in place.
   {
+    const double c = kp.cf[N - 1];
     double v[N];
+    double* z0 = E + (6 + sl) * G::VS + zst;
 #pragma unroll
-    for (int l = 0; l < N; ++l) v[l] = active ? E[(6 + sl) * G::VS + zst + l * G::PL] : 0.0;
+    for (int l = 0; l < N; ++l) v[l] = active ? z0[l * G::PL] : 0.0;
     tm_store_q<N>(ta, 0, v);
+    if (active) {
+#pragma unroll
+      for (int l = 0; l < N; ++l) z0[l * G::PL] = c * v[l];
+    }
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       if (k >= ntS_w) break;
       const int f = slot == 0 ? k : slot == 1 ? (k == 0 ? 4 : 3) : 5;
+      double* zk = E + f * G::VS + zst;
 #pragma unroll
-      for (int l = 0; l < N; ++l) v[l] = (k < ntS) ? E[f * G::VS + zst + l * G::PL] : 0.0;
+      for (int l = 0; l < N; ++l) v[l] = (k < ntS) ? zk[l * G::PL] : 0.0;
       tm_store_q<N>(ta, 1 + k, v);
+      if (k < ntS) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) zk[l * G::PL] = c * v[l];
+      }
     }
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-  }
-  __syncthreads();
-  // Horner start r = c_(n-1) q
-  {
-    const double c = kp.cf[N - 1];
-    for (int i = tid; i < NVE * G::VS; i += G::THREADS) E[i] *= c;
   }
   __syncthreads();
 
@@ -894,22 +913,47 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   TMB(2);
   // ---- epilogue: qavg = the last iterate (fields 0..5 and vb..vb+2) -----------------------
   auto fld = [&](int s) { return s < 6 ? s : vb + (s - 6); };
-  for (int i = tid; i < N3; i += G::THREADS) {
-    const int k1 = i % N, k32 = i / N;
-    const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
-    double v[NVE];
+  if constexpr (N % 2 == 0) {  // k1 pairs: 16-byte shared loads and global stores
+    for (int i = tid; i < N3 / 2; i += G::THREADS) {
+      const int k1 = 2 * (i % (N / 2)), k32 = i / (N / 2);
+      const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+      double2 v[NVE];
 #pragma unroll
-    for (int s = 0; s < NVE; ++s) v[s] = qs[fld(s) * G::VS];
-    const long long ob = e * (long long)OUTV + k32 * NVE * N + k1;
+      for (int s = 0; s < NVE; ++s) v[s] = *reinterpret_cast<const double2*>(qs + fld(s) * G::VS);
+      const long long ob = e * (long long)OUTV + k32 * NVE * N + k1;
 #pragma unroll
-    for (int s = 0; s < NVE; ++s) __stcs(a.qavg + ob + s * N, v[s]);
-    if (a.favg) {
-      double* fo = a.favg + e * (long long)(3 * OUTV) + k32 * NVE * N + k1;
+      for (int s = 0; s < NVE; ++s) __stcs(reinterpret_cast<double2*>(a.qavg + ob + s * N), v[s]);
+      if (a.favg) {
+        double* fo = a.favg + e * (long long)(3 * OUTV) + k32 * NVE * N + k1;
 #pragma unroll
-      for (int d = 0; d < 3; ++d)
+        for (int d = 0; d < 3; ++d)
 #pragma unroll
-        for (int s = 0; s < NVE; ++s)
-          __stcs(fo + d * OUTV + s * N, e_coef(s, d) == 4 ? 0.0 : c4[e_coef(s, d)] * v[e_in(s, d)]);
+          for (int s = 0; s < NVE; ++s) {
+            const double c = c4[e_coef(s, d) == 4 ? 0 : e_coef(s, d)];
+            const double2 x = v[e_in(s, d)];
+            __stcs(reinterpret_cast<double2*>(fo + d * OUTV + s * N),
+                   e_coef(s, d) == 4 ? make_double2(0.0, 0.0) : make_double2(c * x.x, c * x.y));
+          }
+      }
+    }
+  } else {
+    for (int i = tid; i < N3; i += G::THREADS) {
+      const int k1 = i % N, k32 = i / N;
+      const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+      double v[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) v[s] = qs[fld(s) * G::VS];
+      const long long ob = e * (long long)OUTV + k32 * NVE * N + k1;
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) __stcs(a.qavg + ob + s * N, v[s]);
+      if (a.favg) {
+        double* fo = a.favg + e * (long long)(3 * OUTV) + k32 * NVE * N + k1;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int s = 0; s < NVE; ++s)
+            __stcs(fo + d * OUTV + s * N, e_coef(s, d) == 4 ? 0.0 : c4[e_coef(s, d)] * v[e_in(s, d)]);
+      }
     }
   }
   TMB(3);
@@ -1015,7 +1059,9 @@ cudaError_t init_pass(const LaunchPlan& p) {
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
   // bipartite + TMEM kernel: the default for nDof 9 and 10 (ADERSTP_PASS_SLOTS=6/8 select the
   // older line-pass kernel)
-  if (p.pass_slots == 12 || (p.pass_slots == 0 && p.n >= 9)) {
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  const bool vec_ok = (p.n % 2) || (al16(a.q) && al16(a.qavg) && al16(a.favg));  // 16-byte accesses
+  if (vec_ok && (p.pass_slots == 12 || (p.pass_slots == 0 && p.n >= 9))) {
     switch (p.n) {
       case 9: return launch_bip_n<9>(p, a, stream);
       case 10: return launch_bip_n<10>(p, a, stream);

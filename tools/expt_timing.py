@@ -46,7 +46,7 @@ for cfg_name, elems in (("c2", 32768),):
     t = host.reshape(4096, 8)[:, :6].astype(np.float64)
     d = np.diff(t, axis=1)
     print("dmmap", cfg_name, "per-CTA clocks: staging %.0f  CK %.0f  qavg/favg %.0f  faces %.0f  copy-out %.0f" % tuple(np.median(d, axis=0)), "total %.0f" % np.median(t[:, 5] - t[:, 0]))
-for cfg_name, elems in (("c4", 65536),):
+for cfg_name, elems in (("c4", 65536), ("n9", 65536)):
     cfg = bench.CONFIGS[cfg_name]
     n = cfg["n"]
     q, par = S.generate(cfg["dist"], 1, n, 0, elems, grid=32, layout=S.LAYOUT_AOSOA, q_stride=cfg["q_stride"])
