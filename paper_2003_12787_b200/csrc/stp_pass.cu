@@ -519,6 +519,8 @@ struct GeoB {
   // padded so that y- and z-line starts of consecutive tasks fall on distinct banks; for even N
   // the x lines are read and written as 16-byte pairs.  nDof 10: 4490 vs 6610 wavefronts/step.
   static constexpr int RS = N;
+  // (nDof 9 with three CTAs per SM -- 12 x 737 doubles -- measured 4 % slower: the kernel is
+  // bound by the shared-memory pipe, not by latency)
   static constexpr int PL = N == 10 ? 106 : 89;
   static constexpr int VS = N == 10 ? 1060 : 801;
   static constexpr bool X128 = N % 2 == 0;
@@ -528,11 +530,26 @@ struct GeoB {
   static constexpr int THREADS = ((TASKS + 31) / 32) * 32;
   static constexpr int NW = THREADS / 32;
   static constexpr int SMEM = EB * 8;
-  // TMEM columns of one warp: the q z-lines of 4 targets (phase V + up to three in phase S);
-  // nodes 0..7 of target k in the 16-column block k, nodes 8, 9 at column 64 + 4k
-  static constexpr int WCOLS = N == 8 ? 64 : 80;
-  static constexpr int TC = ((NW + 3) / 4) * WCOLS;
-  static constexpr int TCOLS = TC <= 32 ? 32 : TC <= 64 ? 64 : TC <= 128 ? 128 : TC <= 256 ? 256 : 512;
+  static constexpr int MINB = 2;  // CTAs per SM
+  // TMEM: block k of a thread = the 2N columns [2N k, 2N k + 2N) of its warp's range; warp w
+  // needs nb(w) blocks (1 + the phase-S targets of its first lane's slot: 3, 2, 1), and the warps
+  // of one lane quarter (w % 4) take consecutive column ranges.
+  static constexpr int QC = 2 * N;
+  static constexpr int nb(int w) {
+    return 32 * w >= TASKS ? 1 : 1 + (3 - (32 * w) / LINES);
+  }
+  static constexpr int base(int w) {
+    int b = 0;
+    for (int v = w % 4; v < w; v += 4) b += nb(v) * QC;
+    return b;
+  }
+  static constexpr int tc() {
+    int m = 0;
+    for (int w = 0; w < NW; ++w) m = base(w) + nb(w) * QC > m ? base(w) + nb(w) * QC : m;
+    return m;
+  }
+  static constexpr int TCOLS = tc() <= 32 ? 32 : tc() <= 64 ? 64 : tc() <= 128 ? 128 : tc() <= 256 ? 256 : 512;
+  static_assert(MINB * TCOLS <= 512, "tensor memory of the resident CTAs");
 };
 
 __device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t* r) {
@@ -570,9 +587,9 @@ __device__ __forceinline__ void tm_st2(uint32_t ta, const uint32_t* r) {
 template <int N>
 __device__ __forceinline__ void tm_load_q(uint32_t ta, int k, double (&q)[N]) {
   uint32_t r[2 * N];
-  tm_ld16(ta + 16 * k, r);
-  if constexpr (N == 10) tm_ld4(ta + 64 + 4 * k, r + 16);
-  if constexpr (N == 9) tm_ld2(ta + 64 + 4 * k, r + 16);
+  tm_ld16(ta + 2 * N * k, r);
+  if constexpr (N == 10) tm_ld4(ta + 2 * N * k + 16, r + 16);
+  if constexpr (N == 9) tm_ld2(ta + 2 * N * k + 16, r + 16);
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
   for (int i = 0; i < N; ++i) q[i] = __hiloint2double(r[2 * i + 1], r[2 * i]);
@@ -585,9 +602,9 @@ __device__ __forceinline__ void tm_store_q(uint32_t ta, int k, const double (&q)
     r[2 * i] = __double2loint(q[i]);
     r[2 * i + 1] = __double2hiint(q[i]);
   }
-  tm_st16(ta + 16 * k, r);
-  if constexpr (N == 10) tm_st4(ta + 64 + 4 * k, r + 16);
-  if constexpr (N == 9) tm_st2(ta + 64 + 4 * k, r + 16);
+  tm_st16(ta + 2 * N * k, r);
+  if constexpr (N == 10) tm_st4(ta + 2 * N * k + 16, r + 16);
+  if constexpr (N == 9) tm_st2(ta + 2 * N * k + 16, r + 16);
 }
 
 // phase-V pass D, slot j: stress source -> velocity target (coefficient 1/rho)
@@ -683,7 +700,7 @@ __device__ __forceinline__ void bip_line_z(const double* src, double* const* dst
 }
 
 template <int N>
-__global__ void __launch_bounds__(GeoB<N>::THREADS, 2)
+__global__ void __launch_bounds__(GeoB<N>::THREADS, GeoB<N>::MINB)
 stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   using G = GeoB<N>;
   extern __shared__ __align__(16) double smb[];
@@ -762,7 +779,9 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-  const uint32_t ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * G::WCOLS);
+  int wbase = 0;  // G::base(warp), evaluated at run time
+  for (int v = warp & 3; v < warp; v += 4) wbase += G::nb(v) * G::QC;
+  const uint32_t ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)wbase;
 
   // ---- q of the target lines this thread finishes (its z pass) -> TMEM:
   //   block 0: the phase-V velocity 6 + slot
