@@ -24,6 +24,7 @@
 
 #include "../../include/aderstp.h"
 #include "aderstp_internal.h"
+#include "tmem.cuh"
 
 // Even/odd derivative operator per order (uploaded once per device at plan creation), rows
 // padded to 6 doubles so they load as 16-byte pairs: [A: h x 6][B: h x 6][M: 6], h = n/2,
@@ -551,37 +552,6 @@ struct GeoB {
   static constexpr int TCOLS = tc() <= 32 ? 32 : tc() <= 64 ? 64 : tc() <= 128 ? 128 : tc() <= 256 ? 256 : 512;
   static_assert(MINB * TCOLS <= 512, "tensor memory of the resident CTAs");
 };
-
-__device__ __forceinline__ void tm_ld16(uint32_t ta, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-      "%14, %15}, [%16];\n"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(ta));
-}
-__device__ __forceinline__ void tm_ld4(uint32_t ta, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];\n"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(ta));
-}
-__device__ __forceinline__ void tm_ld2(uint32_t ta, uint32_t* r) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];\n" : "=r"(r[0]), "=r"(r[1]) : "r"(ta));
-}
-__device__ __forceinline__ void tm_st16(uint32_t ta, const uint32_t* r) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-      "%14, %15, %16};\n" ::"r"(ta),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-      "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]));
-}
-__device__ __forceinline__ void tm_st4(uint32_t ta, const uint32_t* r) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(ta), "r"(r[0]), "r"(r[1]),
-               "r"(r[2]), "r"(r[3]));
-}
-__device__ __forceinline__ void tm_st2(uint32_t ta, const uint32_t* r) {
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(ta), "r"(r[0]), "r"(r[1]));
-}
 
 // q z-line of TMEM target k (warp-collective: every lane of the warp executes it)
 template <int N>
