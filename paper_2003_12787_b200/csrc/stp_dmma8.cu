@@ -70,6 +70,11 @@ struct Params8 {
 // role of each warp: a single output quantity (0..8), or -1 / -2 for the normal-stress warps on
 // k3 half 0 / 1.  SMSP pairs (w, w+4): {u, N0}, {v, N1}, {w, sxy}, {sxz, syz}.
 __constant__ int kRole[NWARP] = {6, 7, 8, 4, -1, -2, 3, 5};
+// epilogue units (quantity s, k3 half h) -> unit id 2s + h, per warp, balanced by cost (favg
+// stores 1/3/5 planes per unit, z faces on h = 0): the natural round-robin put three z-face
+// units on warp 0 (cost model 318 vs 204 for this table, ideal 189)
+__constant__ int kUnits[NWARP][3] = {{5, 11, 1}, {16, 13, -1}, {12, 15, -1}, {2, 8, -1},
+                                     {10, 0, -1}, {4, 6, -1}, {7, 17, 3}, {14, 9, -1}};
 // elastic flux table F_d(q)_s = coef(s,d) q[in(s,d)]; coef 0: lambda+2mu, 1: lambda, 2: mu,
 // 3: 1/rho, 4: 0
 __constant__ int kIn[NV][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
@@ -323,7 +328,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
 
   TM3(2);
   // ---- epilogue ------------------------------------------------------------------------
-  // 18 units (quantity s, k3 half h) over the 8 warps: qavg and favg from registers, x/y faces
+  // 18 units (quantity s, k3 half h) over the 8 warps (kUnits): qavg and favg from registers, x/y faces
   // by DMMA from the accumulator (staged into the dead p buffers); the unit with h = 0 also does
   // the z faces, which need the whole column.
   double* FQ = Q;  // face_q staging [6][8][8][9] (q is dead after the last barrier)
@@ -331,7 +336,9 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0;  // padded phi (rows / cols = side)
   const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
 #pragma unroll 1
-  for (int unit = warp; unit < 2 * NV; unit += NWARP) {
+  for (int ku = 0; ku < 3; ++ku) {
+    const int unit = kUnits[warp][ku];
+    if (unit < 0) break;
     const int s = unit >> 1, h = unit & 1, K0 = 4 * h;
     const double* qs = P + s * PV;
     double qa[4][2];
