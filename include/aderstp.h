@@ -22,6 +22,12 @@
  *   aderstp_basis               <- ader::make_basis (src/basis.cpp:110-122), host side.
  *   aderstp_flop_count          <- ader::flop_count (include/ader/predictor.hpp:86), reporting the
  *                                  algorithmic count of this implementation.
+ *   aderstp_correct_batch       <- ader::corrector_step(Mesh&, std::vector<PredictorOutput>&,
+ *                                  const LinearPde&, const BasisOperators&, double dt, double t,
+ *                                  int workers)  include/ader/solver.hpp:87-93, src/solver.cpp:257-311
+ *   aderstp_run_simulation      <- ader::run_simulation(const LinearPde&, const SolverConfig&, Mesh&,
+ *                                  double t_end, Variant, const AnalyticFn*, int workers)
+ *                                  include/ader/solver.hpp:102-104, src/solver.cpp:313-359
  *   aderstp_last_error          <- the std::invalid_argument messages of validate_stp
  *                                  (src/predictor_common.cpp:129-146); nothing is thrown across
  *                                  the ABI.
@@ -137,6 +143,38 @@ int aderstp_convert_layout(int order, int quantities, int64_t n_elem, int src_la
  * (rho, cp, cs) per element.  q uses the plan-independent layout given here, m = 9. */
 int aderstp_generate(int dist, uint64_t seed, int order, int64_t e0, int64_t n_elem, int grid,
                      int layout, int q_stride, double* q, double* par, void* stream);
+
+/* ---- the GPU time loop around the predictor --------------------
+ * Uniform periodic Cartesian mesh on [0, domain_len]^3 with e elements per dimension (ader::Mesh,
+ * include/ader/solver.hpp:16-32): element (ix, iy, iz) is (iz*e + iy)*e + ix and its state is one
+ * q-layout tensor of the plan (layout, q_stride). */
+typedef struct aderstp_mesh {
+  int elements_per_dim;
+  double domain_len;
+} aderstp_mesh;
+
+/* corrector_step (src/solver.cpp:257-311; correct_cell :184-253): u += V(qavg) + the Rusanov
+ * surface fluctuations lifted through the inverse mass, from this step's predictor outputs of every
+ * element (qavg in the plan's output layout, face_q / face_f).  The predictor outputs must come
+ * from the PDE scaled by 1/h (ScaledPde, src/solver.cpp:111-156), as aderstp_run_simulation does.
+ * max_wavespeed: the PDE's unscaled max_wavespeed(); for ADERSTP_PDE_ELASTIC a negative value means
+ * "per face, the larger cp of its two elements" (per-element material has no reference
+ * counterpart; with one material it equals the reference).  Point-source kinds are unsupported.
+ * Device buffers, asynchronous; a non-finite update is reported by aderstp_plan_status as
+ * ADERSTP_ERR_NONFINITE (the reference throws "corrector_step: non-finite update"). */
+int aderstp_correct_batch(const aderstp_plan* plan, const aderstp_mesh* mesh, double* u,
+                          const double* par, const double* qavg, const double* face_q,
+                          const double* face_f, double max_wavespeed, void* stream);
+
+/* run_simulation (src/solver.cpp:313-359): steps of dt = min(stable_dt, t_end - t) until t_end,
+ * each = aderstp_predict_batch on the 1/h-scaled PDE + aderstp_correct_batch, with
+ * stable_dt = cfl h / (3 smax (2n - 1)) (:170-174).  u: device state (in/out); par: per-element
+ * material (elastic) or NULL.  max_wavespeed as above (elastic, negative: the max over elements
+ * of cp).  Synchronous.  Returns ADERSTP_ERR_NONFINITE when a step produced a non-finite state
+ * (RunResult.stable = false); *steps and *t_final report the completed steps. */
+int aderstp_run_simulation(const aderstp_plan* plan, const aderstp_mesh* mesh, double* u,
+                           const double* par, double cfl, double t_end, double max_wavespeed,
+                           int64_t* steps, double* t_final, void* stream);
 
 /* ---- host helpers -------------------------------------------------------------------- */
 int aderstp_basis(int order, double* nodes, double* weights, double* d, double* face_left,

@@ -169,6 +169,14 @@ class Reference:
         lib.ref_flop_count.restype = ctypes.c_uint64
         lib.ref_flop_count.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int]
         lib.ref_volume_operator.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _dp, _dp, _dp]
+        _i = ctypes.c_int
+        lib.ref_corrector_step.argtypes = [_i, _i, _i, ctypes.c_double, _i, _dp, _dp, ctypes.c_double,
+                                           ctypes.c_double, _dp, _dp, _dp, _dp, _i]
+        lib.ref_run_simulation.argtypes = [_i, _i, _i, ctypes.c_double, _i, _dp, _dp, ctypes.c_double,
+                                           ctypes.c_double, _i, _dp, _i, ctypes.POINTER(_i), ctypes.POINTER(_i),
+                                           _dp]
+        lib.ref_max_wavespeed.restype = ctypes.c_double
+        lib.ref_max_wavespeed.argtypes = [_i, _i, _dp, _dp]
         self.lib = lib
         self.isa = isa
         self.path = path
@@ -208,6 +216,43 @@ class Reference:
         if rc != 0:
             raise ValueError(self.lib.ref_last_error().decode())
         return Outputs(qavg, favg, fq, ff, secs.value)
+
+
+    # ---- corrector / time loop (proj/src/solver.cpp); mesh state canonical [c][k3][k2][k1][s] ----
+    def corrector_step(self, n, m, e, domain_len, u, qavg, face_q, face_f, dt, par=None,
+                       pde_kind=PDE_ELASTIC, args=None, t=0.0, workers=None):
+        """ader::corrector_step with ONE shared PDE (par = (lambda, mu, rho)); returns (u, ok)."""
+        u = np.ascontiguousarray(u, dtype=np.float64).copy()
+        qavg = np.ascontiguousarray(qavg, dtype=np.float64)
+        face_q = np.ascontiguousarray(face_q, dtype=np.float64)
+        face_f = np.ascontiguousarray(face_f, dtype=np.float64)
+        par_a = None if par is None else np.ascontiguousarray(par, dtype=np.float64).reshape(3)
+        args_a = np.zeros(8) if args is None else np.ascontiguousarray(args, dtype=np.float64)
+        rc = self.lib.ref_corrector_step(n, m, e, domain_len, pde_kind, _ptr(par_a), _ptr(args_a), dt, t,
+                                         _ptr(u), _ptr(qavg), _ptr(face_q), _ptr(face_f),
+                                         workers or (os.cpu_count() or 1))
+        if rc == -1:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return u, rc == 0
+
+    def run_simulation(self, n, m, e, domain_len, u, cfl, t_end, par=None, pde_kind=PDE_ELASTIC,
+                       args=None, variant="splitck", workers=None):
+        """ader::run_simulation; returns (u, stable, steps, t_final)."""
+        u = np.ascontiguousarray(u, dtype=np.float64).copy()
+        par_a = None if par is None else np.ascontiguousarray(par, dtype=np.float64).reshape(3)
+        args_a = np.zeros(8) if args is None else np.ascontiguousarray(args, dtype=np.float64)
+        stable, steps, t_final = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_double(0.0)
+        rc = self.lib.ref_run_simulation(n, m, e, domain_len, pde_kind, _ptr(par_a), _ptr(args_a), cfl,
+                                         t_end, VARIANTS[variant], _ptr(u), workers or (os.cpu_count() or 1),
+                                         ctypes.byref(stable), ctypes.byref(steps), ctypes.byref(t_final))
+        if rc != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return u, bool(stable.value), steps.value, t_final.value
+
+    def max_wavespeed(self, pde_kind, m, par=None, args=None):
+        par_a = None if par is None else np.ascontiguousarray(par, dtype=np.float64).reshape(3)
+        args_a = np.zeros(8) if args is None else np.ascontiguousarray(args, dtype=np.float64)
+        return self.lib.ref_max_wavespeed(pde_kind, m, _ptr(par_a), _ptr(args_a))
 
 
 def rel_diff(a, b) -> float:

@@ -25,6 +25,7 @@
 #include "ader/layout.hpp"
 #include "ader/pde.hpp"
 #include "ader/predictor.hpp"
+#include "ader/solver.hpp"
 #include "ader/util.hpp"
 
 namespace {
@@ -195,6 +196,109 @@ int ref_volume_operator(int n, int m, int pde_kind, const double* par, const dou
   } catch (const std::exception& ex) {
     g_err = ex.what();
     return -1;
+  }
+}
+
+// ---- corrector and time loop (proj/src/solver.cpp), mesh state canonical [c][k3][k2][k1][s] ----
+
+namespace {
+
+void load_mesh(ader::Mesh& mesh, const double* u) {
+  const ader::LayoutSpec& sp = mesh.spec;
+  const long nn = static_cast<long>(sp.n) * sp.n * sp.n;
+  for (std::size_t c = 0; c < mesh.cells.size(); ++c)
+    for (long k = 0; k < nn; ++k)
+      std::memcpy(mesh.cells[c].data() + k * sp.m_pad, u + (c * nn + k) * sp.m, sizeof(double) * sp.m);
+}
+
+void store_mesh(const ader::Mesh& mesh, double* u) {
+  const ader::LayoutSpec& sp = mesh.spec;
+  const long nn = static_cast<long>(sp.n) * sp.n * sp.n;
+  for (std::size_t c = 0; c < mesh.cells.size(); ++c)
+    for (long k = 0; k < nn; ++k)
+      std::memcpy(u + (c * nn + k) * sp.m, mesh.cells[c].data() + k * sp.m_pad, sizeof(double) * sp.m);
+}
+
+}  // namespace
+
+// ader::corrector_step on an e^3 periodic mesh (one shared PDE: par = (lambda, mu, rho) for the
+// elastic kind, args otherwise) from given predictor outputs (qavg canonical, faces
+// [c][f][a][b][s]).  u is updated in place.  Returns 0, -1 on a reference exception, -2 when
+// the reference reports a non-finite update.
+int ref_corrector_step(int n, int m, int e, double domain_len, int pde_kind, const double* par,
+                       const double* args, double dt, double t, double* u, const double* qavg,
+                       const double* face_q, const double* face_f, int workers) {
+  try {
+    ader::SolverConfig cfg;
+    cfg.order = n;
+    cfg.quantities = m;
+    cfg.vec_width = 8;
+    ader::Mesh mesh(e, cfg, domain_len);
+    const ader::BasisOperators ops = ader::make_basis(n);
+    auto pde = make_pde(pde_kind, m, par, args);
+    load_mesh(mesh, u);
+    const ader::LayoutSpec& sp = mesh.spec;
+    const long nn = static_cast<long>(n) * n * n, face = static_cast<long>(n) * n * m;
+    std::vector<ader::PredictorOutput> outs;
+    outs.reserve(mesh.cells.size());
+    for (std::size_t c = 0; c < mesh.cells.size(); ++c) {
+      outs.emplace_back(sp);
+      for (long k = 0; k < nn; ++k)
+        std::memcpy(outs[c].qavg.data() + k * sp.m_pad, qavg + (c * nn + k) * m, sizeof(double) * m);
+      for (int f = 0; f < 6; ++f) {
+        std::memcpy(outs[c].face_q[f].data(), face_q + (c * 6 + f) * face, sizeof(double) * face);
+        std::memcpy(outs[c].face_f[f].data(), face_f + (c * 6 + f) * face, sizeof(double) * face);
+      }
+    }
+    try {
+      ader::corrector_step(mesh, outs, *pde, ops, dt, t, workers > 0 ? workers : 1);
+    } catch (const std::runtime_error& ex) {
+      g_err = ex.what();
+      store_mesh(mesh, u);
+      return -2;
+    }
+    store_mesh(mesh, u);
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return -1;
+  }
+}
+
+// ader::run_simulation (splitck unless variant says otherwise) on an e^3 periodic mesh with
+// one shared PDE; u (canonical) in/out.  stable / steps / t_final mirror RunResult.
+int ref_run_simulation(int n, int m, int e, double domain_len, int pde_kind, const double* par,
+                       const double* args, double cfl, double t_end, int variant, double* u,
+                       int workers, int* stable, int* steps, double* t_final) {
+  try {
+    ader::SolverConfig cfg;
+    cfg.order = n;
+    cfg.quantities = m;
+    cfg.vec_width = 8;
+    cfg.cfl = cfl;
+    ader::Mesh mesh(e, cfg, domain_len);
+    auto pde = make_pde(pde_kind, m, par, args);
+    load_mesh(mesh, u);
+    const ader::RunResult r = ader::run_simulation(*pde, cfg, mesh, t_end, static_cast<ader::Variant>(variant),
+                                                   nullptr, workers > 0 ? workers : 1);
+    store_mesh(mesh, u);
+    if (stable) *stable = r.stable ? 1 : 0;
+    if (steps) *steps = r.steps;
+    if (t_final) *t_final = r.t_final;
+    return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return -1;
+  }
+}
+
+// PDE max_wavespeed of the reference factories (include/ader/pde.hpp:38)
+double ref_max_wavespeed(int pde_kind, int m, const double* par, const double* args) {
+  try {
+    return make_pde(pde_kind, m, par, args)->max_wavespeed();
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return -1.0;
   }
 }
 

@@ -57,6 +57,23 @@ struct BatchArgs {
   double t_start;
 };
 
+// corrector.cu: GPU corrector step (proj/src/solver.cpp:184-311) and time-loop helpers
+struct CorrArgs {
+  double* u;             // mesh state, the plan's q layout, element (iz*e + iy)*e + ix
+  const double* par;     // per-element material (elastic)
+  const double* qavg;
+  const double* face_q;
+  const double* face_f;
+  int e;                 // elements per dimension (periodic)
+  double inv_h;          // 1 / h
+  double smax;           // scaled max wave speed, < 0: elastic per-face max(cp) / h
+};
+cudaError_t launch_correct(const LaunchPlan& p, const CorrArgs& a, cudaStream_t stream);
+cudaError_t launch_scale_par(const double* in, int par_kind, double s, long long n, double* out,
+                             cudaStream_t stream);
+cudaError_t launch_max_cp(const double* par, int par_kind, long long n, unsigned long long* out,
+                          cudaStream_t stream);
+
 // stp_kernels.cu
 cudaError_t launch_stp(const LaunchPlan& plan, const BatchArgs& args, cudaStream_t stream);
 cudaError_t launch_convert(int n, int m, long long n_elem, int src_layout, int src_stride,

@@ -1,7 +1,9 @@
 // Host side of the C ABI (include/aderstp.h): plans, argument validation with the reference's
 // validate_stp semantics (proj/src/predictor_common.cpp:129-146), PDE term tables from the
 // reference's LinearPde factories (proj/src/pde.cpp), and the pipelined host-buffer path.
+#include <algorithm>
 #include <cmath>
+#include <limits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -448,3 +450,135 @@ int aderstp_generate(int dist, uint64_t seed, int order, int64_t e0, int64_t n_e
 }
 
 }  // extern "C"
+
+// ---- GPU corrector and time loop ------------------------------------
+
+namespace {
+
+int validate_mesh(const aderstp_plan* p, const aderstp_mesh* mesh, const double* u, const double* par,
+                  const char* who) {
+  if (!p || !mesh || !u) return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": null argument");
+  if (mesh->elements_per_dim < 1)
+    return fail(ADERSTP_ERR_INVALID_ARG, "Mesh: need at least one element per dimension");
+  if (!(mesh->domain_len > 0.0)) return fail(ADERSTP_ERR_INVALID_ARG, "Mesh: domain length must be positive");
+  if ((double)mesh->elements_per_dim * mesh->elements_per_dim * mesh->elements_per_dim > 2147483647.0)
+    return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": mesh too large");
+  if (p->lp.src_comp >= 0)
+    return fail(ADERSTP_ERR_UNSUPPORTED, std::string(who) + ": point sources are not supported by the GPU corrector");
+  if (p->lp.kind == ADERSTP_PDE_ELASTIC && !par)
+    return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": elastic kinds need per-element parameters");
+  return ADERSTP_OK;
+}
+
+}  // namespace
+
+int aderstp_correct_batch(const aderstp_plan* p, const aderstp_mesh* mesh, double* u, const double* par,
+                          const double* qavg, const double* face_q, const double* face_f,
+                          double max_wavespeed, void* stream) {
+  int rc = validate_mesh(p, mesh, u, par, "corrector_step");
+  if (rc != ADERSTP_OK) return rc;
+  if (!qavg || !face_q || !face_f)
+    return fail(ADERSTP_ERR_INVALID_ARG, "corrector_step: one predictor output per element required");
+  if (p->lp.kind != ADERSTP_PDE_ELASTIC && !(max_wavespeed >= 0.0))
+    return fail(ADERSTP_ERR_INVALID_ARG, "corrector_step: max_wavespeed required for table PDEs");
+  const double inv_h = mesh->elements_per_dim / mesh->domain_len;
+  aderstp::CorrArgs a{u, par, qavg, face_q, face_f, mesh->elements_per_dim, inv_h,
+                      max_wavespeed >= 0.0 ? max_wavespeed * inv_h : -1.0};
+  cudaError_t e = aderstp::launch_correct(p->lp, a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "correct_batch launch");
+  return ADERSTP_OK;
+}
+
+int aderstp_run_simulation(const aderstp_plan* p, const aderstp_mesh* mesh, double* u, const double* par,
+                           double cfl, double t_end, double max_wavespeed, int64_t* steps, double* t_final,
+                           void* stream) {
+  if (steps) *steps = 0;
+  if (t_final) *t_final = 0.0;
+  int rc = validate_mesh(p, mesh, u, par, "run_simulation");
+  if (rc != ADERSTP_OK) return rc;
+  if (!(cfl > 0.0) || !(t_end >= 0.0)) return fail(ADERSTP_ERR_INVALID_ARG, "run_simulation: bad cfl or t_end");
+  const bool elastic = p->lp.kind == ADERSTP_PDE_ELASTIC;
+  if (!elastic && !(max_wavespeed >= 0.0))
+    return fail(ADERSTP_ERR_INVALID_ARG, "run_simulation: max_wavespeed required for table PDEs");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int e = mesh->elements_per_dim;
+  const long long E = (long long)e * e * e;
+  const int n = p->lp.n, m = p->lp.m;
+  const double h = mesh->domain_len / e, s = 1.0 / h;
+
+  // the predictor on ScaledPde(1/h): table terms x s, elastic material (s lambda, s mu, rho / s)
+  aderstp::LaunchPlan sp = p->lp;
+  if (!elastic)
+    for (int q = 0; q < aderstp::kMaxM; ++q)
+      for (int d = 0; d < 3; ++d)
+        for (int k = 0; k < aderstp::kMaxTerms; ++k) {
+          sp.tc[q][d][k] *= s;
+          sp.fc[q][d][k] *= s;
+        }
+  double *par_s = nullptr, *qavg = nullptr, *faces = nullptr;
+  unsigned long long* d_cp = nullptr;
+  auto cleanup = [&]() {
+    if (par_s) cudaFree(par_s);
+    if (qavg) cudaFree(qavg);
+    if (faces) cudaFree(faces);
+    if (d_cp) cudaFree(d_cp);
+  };
+  const size_t n3 = (size_t)n * n * n, face = 6 * (size_t)n * n * m;
+  cudaError_t err = cudaMalloc(&qavg, sizeof(double) * n3 * p->lp.out_stride * E);
+  if (err == cudaSuccess) err = cudaMalloc(&faces, sizeof(double) * 2 * face * E);
+  double smax = max_wavespeed;
+  if (err == cudaSuccess && elastic) {
+    err = cudaMalloc(&par_s, sizeof(double) * 3 * E);
+    if (err == cudaSuccess) err = aderstp::launch_scale_par(par, p->lp.par_kind, s, E, par_s, st);
+    sp.par_kind = ADERSTP_PAR_LAMBDA_MU_RHO;
+    if (err == cudaSuccess && !(smax >= 0.0)) {
+      unsigned long long bits = 0;
+      err = cudaMalloc(&d_cp, sizeof bits);
+      if (err == cudaSuccess) err = aderstp::launch_max_cp(par, p->lp.par_kind, E, d_cp, st);
+      if (err == cudaSuccess) err = cudaMemcpyAsync(&bits, d_cp, sizeof bits, cudaMemcpyDeviceToHost, st);
+      if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+      double v;
+      std::memcpy(&v, &bits, sizeof v);
+      smax = v;
+    }
+  }
+  if (err != cudaSuccess) {
+    cleanup();
+    return cuda_fail(err, "run_simulation setup");
+  }
+  // stable_dt (src/solver.cpp:170-174)
+  const double dt0 = smax > 0.0 ? cfl * h / (3.0 * smax * (2.0 * n - 1.0)) : std::numeric_limits<double>::infinity();
+  double* face_q = faces;
+  double* face_f = faces + face * E;
+  double t = 0.0;
+  int64_t done = 0;
+  rc = ADERSTP_OK;
+  while (t < t_end - 1e-14 * std::max(1.0, t_end)) {
+    const double dt = std::min(dt0, t_end - t);
+    aderstp::BatchArgs ba{u, elastic ? par_s : par, qavg, nullptr, face_q, face_f, E, dt, t};
+    err = aderstp::launch_stp(sp, ba, st);
+    aderstp::CorrArgs ca{u, par, qavg, face_q, face_f, e, s, (elastic && max_wavespeed < 0.0) ? -1.0 : smax * s};
+    if (err == cudaSuccess) err = aderstp::launch_correct(p->lp, ca, st);
+    unsigned int flags = 0;
+    if (err == cudaSuccess) err = cudaMemcpyAsync(&flags, p->lp.d_status, sizeof flags, cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) {
+      rc = cuda_fail(err, "run_simulation step");
+      break;
+    }
+    if (flags) {
+      cudaMemsetAsync(p->lp.d_status, 0, sizeof flags, st);
+      cudaStreamSynchronize(st);
+      rc = fail((flags & 2u) ? ADERSTP_ERR_MATERIAL : ADERSTP_ERR_NONFINITE,
+                (flags & 2u) ? "elastic_pde: need rho > 0, mu >= 0, lambda + 2mu > 0"
+                             : "corrector_step: non-finite update (unstable)");
+      break;
+    }
+    t += dt;
+    ++done;
+  }
+  if (steps) *steps = done;
+  if (t_final) *t_final = t;
+  cleanup();
+  return rc;
+}

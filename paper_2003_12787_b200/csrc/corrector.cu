@@ -1,0 +1,320 @@
+// GPU corrector step and the small device helpers of the GPU time loop.
+//
+// The reference advances its periodic Cartesian mesh (proj/include/ader/solver.hpp:16-32) after
+// the predictor with corrector_step (proj/src/solver.cpp:257-311), one correct_cell per element
+// (:184-253):
+//   u += V(qavg)                          volume term: one application of the element operator
+//                                         Σ_d D_d F_d + B_d D_d (apply_volume_once,
+//                                         proj/src/predictor_common.cpp:243-259) on the scaled PDE
+//   for d, side:  fhat = ½(f⁺ + f⁻) − ½ smax (q⁻ − q⁺)          (the plus side is the element in
+//                 u[line j] += sign φ_side[j] / w_j · (fhat − f_self)   the +d direction)
+// with the ScaledPde of an element of size h (flux and ncp × 1/h, smax = max_wavespeed / h,
+// solver.cpp:111-156).  Here one CTA corrects one element: qavg is staged in shared memory for the
+// volume contraction, the 6 face fluctuations (fhat − f_self) are formed once per face node from
+// the element's and its neighbours' predictor faces (L2-resident: every face array is read by its
+// owner and one neighbour), and every state entry is updated by one coalesced read-modify-write in
+// the state's own layout.  Per-element elastic material (the reference has one material per mesh)
+// is supported; smax is then max(cp) of the two elements of a face unless the caller passes one.
+// Point sources are not supported on this path (the caller is told ADERSTP_ERR_UNSUPPORTED).
+#include <cstdint>
+
+#include "../../include/aderstp.h"
+#include "aderstp_internal.h"
+
+namespace aderstp {
+
+namespace {
+
+constexpr int NVC = 9;
+
+struct CorrParams {
+  double d[kMaxOrder * kMaxOrder];
+  double phi[2][kMaxOrder];
+  double inv_w[kMaxOrder];
+  signed char tr[kMaxM][3][kMaxTerms];
+  double tc[kMaxM][3][kMaxTerms];
+  int m, q_stride, out_stride, layout, par_kind, n_terms;
+  int e;         // elements per dimension
+  double inv_h;  // grad scale 1 / h
+  double smax;   // scaled max wave speed; < 0: elastic, per face from the material
+};
+
+// elastic flux table (proj/src/pde.cpp:180-218): F_d(q)_s = coef(s,d) q[in(s,d)]
+__constant__ int8_t kInC[NVC][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
+                                    {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+__constant__ int8_t kCoefC[NVC][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
+                                      {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
+
+struct Material {
+  double c4[5];  // lambda+2mu, lambda, mu, 1/rho, 0
+  double cp;
+};
+
+__device__ __forceinline__ Material material(const double* pr, int par_kind) {
+  double lam, mu, rho;
+  if (par_kind == ADERSTP_PAR_RHO_CP_CS) {
+    rho = pr[0];
+    mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
+    lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
+  } else {
+    lam = pr[0];
+    mu = pr[1];
+    rho = pr[2];
+  }
+  Material mt;
+  mt.c4[0] = lam + 2.0 * mu;
+  mt.c4[1] = lam;
+  mt.c4[2] = mu;
+  mt.c4[3] = 1.0 / rho;
+  mt.c4[4] = 0.0;
+  mt.cp = sqrt((lam + 2.0 * mu) / rho);  // ElasticPde::cp_ (pde.cpp:177)
+  return mt;
+}
+
+__device__ __forceinline__ long long wrap_index(int ix, int iy, int iz, int e) {  // Mesh::cell_index
+  ix = (ix % e + e) % e;
+  iy = (iy % e + e) % e;
+  iz = (iz % e + e) % e;
+  return ((long long)iz * e + iy) * e + ix;
+}
+
+template <int N, bool ELASTIC>
+__global__ void __launch_bounds__(256) correct_kernel(CorrParams kp, double* __restrict__ u,
+                                                      const double* __restrict__ par,
+                                                      const double* __restrict__ qavg,
+                                                      const double* __restrict__ face_q,
+                                                      const double* __restrict__ face_f,
+                                                      unsigned int* status) {
+  constexpr int N2 = N * N, N3 = N * N * N;
+  const int m = ELASTIC ? NVC : kp.m;
+  extern __shared__ __align__(16) double smc[];
+  double* QA = smc;           // qavg [s][k3][k2][k1]
+  double* DL = smc + m * N3;  // fhat - f_self  [f][a][b][s]
+  const int e = kp.e;
+  const long long c = blockIdx.x;
+  const int ix = (int)(c % e), iy = (int)((c / e) % e), iz = (int)(c / ((long long)e * e));
+  const int tid = threadIdx.x;
+
+  Material mine;
+  if (ELASTIC) {
+    mine = material(par + 3 * c, kp.par_kind);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mine.c4[i] *= kp.inv_h;  // ScaledPde: flux x 1/h
+  }
+
+  // ---- qavg -> shared (flat over the output layout: coalesced) ----------------------------
+  {
+    const int os = kp.out_stride;
+    const double* qa = qavg + c * (long long)(N3 * os);
+    for (int j = tid; j < N3 * os; j += blockDim.x) {
+      int s, node;
+      if (kp.layout == ADERSTP_LAYOUT_AOSOA) {
+        const int k1 = j % N, r = j / N;
+        s = r % os;
+        node = (r / os) * N + k1;
+      } else {
+        s = j % os;
+        node = j / os;
+      }
+      if (s < m) QA[s * N3 + node] = qa[j];
+    }
+  }
+  // ---- face fluctuations (solver.cpp:218-226) --------------------------------------------
+  {
+    const int FV = N2 * m;
+    const double* mq = face_q + c * 6LL * FV;
+    const double* mf = face_f + c * 6LL * FV;
+    for (int i = tid; i < 6 * FV; i += blockDim.x) {
+      const int f = i / FV, r = i - f * FV;
+      const int d = f >> 1, side = f & 1, step = side ? 1 : -1;
+      const long long nb =
+          wrap_index(ix + (d == 0 ? step : 0), iy + (d == 1 ? step : 0), iz + (d == 2 ? step : 0), e);
+      const double* tq = face_q + nb * 6LL * FV;
+      const double* tf = face_f + nb * 6LL * FV;
+      double q_plus, q_minus, f_plus, f_minus;
+      if (side == 1) {
+        q_plus = tq[(2 * d) * FV + r];
+        q_minus = mq[(2 * d + 1) * FV + r];
+        f_plus = tf[(2 * d) * FV + r];
+        f_minus = mf[(2 * d + 1) * FV + r];
+      } else {
+        q_plus = mq[(2 * d) * FV + r];
+        q_minus = tq[(2 * d + 1) * FV + r];
+        f_plus = mf[(2 * d) * FV + r];
+        f_minus = tf[(2 * d + 1) * FV + r];
+      }
+      double smax = kp.smax;
+      if (ELASTIC && smax < 0.0) smax = fmax(mine.cp, material(par + 3 * nb, kp.par_kind).cp) * kp.inv_h;
+      const double fh = 0.5 * (f_plus + f_minus) - 0.5 * smax * (q_minus - q_plus);
+      DL[i] = fh - mf[f * FV + r];
+    }
+  }
+  __syncthreads();
+
+  // ---- u += V(qavg) + surface terms, in the state's layout ---------------------------------
+  unsigned int flags = 0;
+  const int qs = kp.q_stride;
+  double* ue = u + c * (long long)(N3 * qs);
+  for (int j = tid; j < N3 * qs; j += blockDim.x) {
+    int s, k1, k2, k3;
+    if (kp.layout == ADERSTP_LAYOUT_AOSOA) {
+      k1 = j % N;
+      const int r = j / N;
+      s = r % qs;
+      const int k32 = r / qs;
+      k2 = k32 % N;
+      k3 = k32 / N;
+    } else {
+      s = j % qs;
+      const int node = j / qs;
+      k1 = node % N;
+      k2 = (node / N) % N;
+      k3 = node / N2;
+    }
+    if (s >= m) continue;
+    // volume (apply_volume_once): sum over d of D_d applied to the scaled flux / ncp terms
+    double vol = 0.0;
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int kd = d == 0 ? k1 : d == 1 ? k2 : k3;
+      const int stride = d == 0 ? 1 : d == 1 ? N : N2;
+      const int base = k3 * N2 + k2 * N + k1 - kd * stride;
+      if (ELASTIC) {
+        const int cf = kCoefC[s][d];
+        if (cf == 4) continue;
+        const double cc = mine.c4[cf];
+        const double* src = QA + kInC[s][d] * N3 + base;
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) acc = fma(kp.d[kd * N + l], cc * src[l * stride], acc);
+        vol += acc;
+      } else {
+        for (int k = 0; k < kp.n_terms; ++k) {
+          const double cc = kp.tc[s][d][k] * kp.inv_h;
+          if (cc == 0.0) continue;
+          const double* src = QA + kp.tr[s][d][k] * N3 + base;
+          double acc = 0.0;
+#pragma unroll
+          for (int l = 0; l < N; ++l) acc = fma(kp.d[kd * N + l], cc * src[l * stride], acc);
+          vol += acc;
+        }
+      }
+    }
+    double val = ue[j] + vol;
+    // surface (solver.cpp:228-249): in-face (a, b) in (z, y, x) order without dimension d
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const int kd = d == 0 ? k1 : d == 1 ? k2 : k3;
+      const int ab = d == 0 ? k3 * N + k2 : d == 1 ? k3 * N + k1 : k2 * N + k1;
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const double scale = (side == 0 ? -1.0 : 1.0) * kp.phi[side][kd] * kp.inv_w[kd];
+        val += scale * DL[((2 * d + side) * N2 + ab) * m + s];
+      }
+    }
+    if (!isfinite(val)) flags |= 1u;
+    ue[j] = val;
+  }
+  if (flags) atomicOr(status, flags);
+}
+
+// (lambda, mu, rho) scaled like ScaledPde(1/h): every flux coefficient x s  ->  (s lambda, s mu, rho / s)
+__global__ void scale_par_kernel(const double* __restrict__ in, int par_kind, double s, long long n,
+                                 double* __restrict__ out) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const double* pr = in + 3 * i;
+    double lam, mu, rho;
+    if (par_kind == ADERSTP_PAR_RHO_CP_CS) {
+      rho = pr[0];
+      mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
+      lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
+    } else {
+      lam = pr[0];
+      mu = pr[1];
+      rho = pr[2];
+    }
+    out[3 * i] = lam * s;
+    out[3 * i + 1] = mu * s;
+    out[3 * i + 2] = rho / s;
+  }
+}
+
+// max over elements of the P-wave speed, for the time step (stable_dt, solver.cpp:170-174)
+__global__ void max_cp_kernel(const double* __restrict__ par, int par_kind, long long n, unsigned long long* out) {
+  double best = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    best = fmax(best, material(par + 3 * i, par_kind).cp);
+  // non-negative doubles order like their bit patterns
+  atomicMax(out, (unsigned long long)__double_as_longlong(best));
+}
+
+template <int N>
+cudaError_t launch_correct_n(const LaunchPlan& p, const CorrArgs& a, cudaStream_t stream) {
+  CorrParams kp;
+  const int n = p.n;
+  for (int i = 0; i < n * n; ++i) kp.d[i] = p.basis.d[i];
+  for (int j = 0; j < n; ++j) {
+    kp.phi[0][j] = p.basis.face_left[j];
+    kp.phi[1][j] = p.basis.face_right[j];
+    kp.inv_w[j] = 1.0 / p.basis.weights[j];
+  }
+  for (int s = 0; s < kMaxM; ++s)
+    for (int d = 0; d < 3; ++d)
+      for (int k = 0; k < kMaxTerms; ++k) {
+        kp.tr[s][d][k] = p.tr[s][d][k];
+        kp.tc[s][d][k] = p.tc[s][d][k];
+      }
+  kp.m = p.m;
+  kp.q_stride = p.q_stride;
+  kp.out_stride = p.out_stride;
+  kp.layout = p.layout;
+  kp.par_kind = p.par_kind;
+  kp.n_terms = p.n_terms;
+  kp.e = a.e;
+  kp.inv_h = a.inv_h;
+  kp.smax = a.smax;
+  const bool elastic = p.kind == ADERSTP_PDE_ELASTIC;
+  const size_t smem = sizeof(double) * (size_t)p.m * (N * N * N + 6 * N * N);
+  auto kern = elastic ? correct_kernel<N, true> : correct_kernel<N, false>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  const long long cells = (long long)a.e * a.e * a.e;
+  kern<<<(unsigned)cells, 256, smem, stream>>>(kp, a.u, a.par, a.qavg, a.face_q, a.face_f, p.d_status);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_correct(const LaunchPlan& p, const CorrArgs& a, cudaStream_t stream) {
+  switch (p.n) {
+    case 2: return launch_correct_n<2>(p, a, stream);
+    case 3: return launch_correct_n<3>(p, a, stream);
+    case 4: return launch_correct_n<4>(p, a, stream);
+    case 5: return launch_correct_n<5>(p, a, stream);
+    case 6: return launch_correct_n<6>(p, a, stream);
+    case 7: return launch_correct_n<7>(p, a, stream);
+    case 8: return launch_correct_n<8>(p, a, stream);
+    case 9: return launch_correct_n<9>(p, a, stream);
+    case 10: return launch_correct_n<10>(p, a, stream);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_scale_par(const double* in, int par_kind, double s, long long n, double* out,
+                             cudaStream_t stream) {
+  if (n == 0) return cudaSuccess;
+  const long long blocks = (n + 255) / 256;
+  scale_par_kernel<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, stream>>>(in, par_kind, s, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_max_cp(const double* par, int par_kind, long long n, unsigned long long* out,
+                          cudaStream_t stream) {
+  cudaError_t err = cudaMemsetAsync(out, 0, sizeof(unsigned long long), stream);
+  if (err != cudaSuccess || n == 0) return err;
+  const long long blocks = (n + 255) / 256;
+  max_cp_kernel<<<(unsigned)(blocks < 1024 ? blocks : 1024), 256, 0, stream>>>(par, par_kind, n, out);
+  return cudaGetLastError();
+}
+
+}  // namespace aderstp

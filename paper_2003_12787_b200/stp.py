@@ -65,6 +65,10 @@ _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
 
 
+class _Mesh(ctypes.Structure):
+    _fields_ = [("elements_per_dim", ctypes.c_int), ("domain_len", ctypes.c_double)]
+
+
 def _load():
     if not os.path.exists(library_path):
         raise ImportError(
@@ -84,6 +88,9 @@ def _load():
                                          _vp, ctypes.c_int, ctypes.c_int, _vp, _vp]
     L.aderstp_generate.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, _i64, _i64, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]
+    L.aderstp_correct_batch.argtypes = [_vp, ctypes.POINTER(_Mesh), _vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp]
+    L.aderstp_run_simulation.argtypes = [_vp, ctypes.POINTER(_Mesh), _vp, _vp, ctypes.c_double, ctypes.c_double,
+                                         ctypes.c_double, ctypes.POINTER(_i64), _dp, _vp]
     L.aderstp_basis.argtypes = [ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
     L.aderstp_flop_count.restype = ctypes.c_double
     L.aderstp_flop_count.argtypes = [ctypes.c_int, ctypes.c_int]
@@ -334,6 +341,53 @@ class Plan:
         _check(lib.aderstp_predict_batch(self._h, n_elem, ptr(q), ptr(par), dt, t_start, ptr(out.qavg),
                                          ptr(out.favg), ptr(out.face_q), ptr(out.face_f), _stream_handle(stream)))
         return out
+
+    # ---- GPU corrector and time loop (proj/src/solver.cpp) ---------------------------------
+    def correct(self, u, elements_per_dim: int, out: PredictorOutput, par=None, domain_len: float = 1.0,
+                max_wavespeed: float | None = None, stream=None):
+        """corrector_step (solver.cpp:257-311) in place on the device mesh state u [e^3, q_size]
+        from this step's predictor outputs (computed on the 1/h-scaled PDE).  max_wavespeed: the
+        PDE's unscaled max_wavespeed(); None = the PDE's own (elastic: per face from the material)."""
+        import torch
+        E = elements_per_dim ** 3
+        if not (isinstance(u, torch.Tensor) and u.is_cuda and u.dtype == torch.float64 and u.is_contiguous()
+                and u.numel() == E * self.q_size):
+            raise StpError(ADERSTP_ERR_INVALID_ARG, "correct: u must be a contiguous CUDA float64 [e^3, q_size] tensor")
+        if self.pde.kind in (PDE_ELASTIC, PDE_ELASTIC_SOURCE) and par is None:
+            par = self._uniform_par(E, u)
+        smax = self._smax(max_wavespeed)
+        mesh = _Mesh(elements_per_dim, domain_len)
+        ptr = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _check(lib.aderstp_correct_batch(self._h, ctypes.byref(mesh), ptr(u), ptr(par), ptr(out.qavg),
+                                         ptr(out.face_q), ptr(out.face_f), smax, _stream_handle(stream)))
+
+    def _smax(self, max_wavespeed):
+        if max_wavespeed is not None:
+            return float(max_wavespeed)
+        if self.pde.kind in (PDE_ELASTIC, PDE_ELASTIC_SOURCE):
+            return -1.0
+        return float(self.pde.max_wavespeed())
+
+    def run_simulation(self, u, elements_per_dim: int, t_end: float, par=None, cfl: float = 0.35,
+                       domain_len: float = 1.0, max_wavespeed: float | None = None, stream=None):
+        """run_simulation (solver.cpp:313-359) on the device mesh state u (in place).  Returns
+        (stable, steps, t_final) like RunResult; raises on argument / CUDA errors."""
+        import torch
+        E = elements_per_dim ** 3
+        if not (isinstance(u, torch.Tensor) and u.is_cuda and u.dtype == torch.float64 and u.is_contiguous()
+                and u.numel() == E * self.q_size):
+            raise StpError(ADERSTP_ERR_INVALID_ARG, "run_simulation: u must be a contiguous CUDA float64 tensor")
+        if self.pde.kind in (PDE_ELASTIC, PDE_ELASTIC_SOURCE) and par is None:
+            par = self._uniform_par(E, u)
+        smax = self._smax(max_wavespeed)
+        mesh = _Mesh(elements_per_dim, domain_len)
+        steps, t_final = _i64(0), ctypes.c_double(0.0)
+        ptr = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        rc = lib.aderstp_run_simulation(self._h, ctypes.byref(mesh), ptr(u), ptr(par), cfl, t_end, smax,
+                                        ctypes.byref(steps), ctypes.byref(t_final), _stream_handle(stream))
+        if rc not in (ADERSTP_OK, ADERSTP_ERR_NONFINITE):
+            _check(rc)
+        return rc == ADERSTP_OK, steps.value, t_final.value
 
     def status(self, stream=None):
         """Synchronise and raise on flagged inputs (validate_stp's non-finite / material checks)."""

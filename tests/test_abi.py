@@ -99,3 +99,16 @@ def test_stable_dt_matches_reference_formula(S):
     # proj/src/solver.cpp:170-174
     assert S.stable_dt(8, 6.0, cfl=0.5) == 0.5 / (3.0 * 6.0 * 15.0)
     assert S.stable_dt(4, 0.0) == float("inf")
+
+
+def test_corrector_entry_points_validate_arguments(S):
+    """aderstp_correct_batch / aderstp_run_simulation reject bad arguments before any device work."""
+    L = S.lib
+    mesh = S.stp._Mesh(2, 1.0)
+    rc = L.aderstp_correct_batch(None, ctypes.byref(mesh), None, None, None, None, None, 1.0, None)
+    assert rc == S.ADERSTP_ERR_INVALID_ARG
+    steps, t_final = ctypes.c_int64(7), ctypes.c_double(7.0)
+    rc = L.aderstp_run_simulation(None, ctypes.byref(mesh), None, None, 0.35, 1.0, 1.0,
+                                  ctypes.byref(steps), ctypes.byref(t_final), None)
+    assert rc == S.ADERSTP_ERR_INVALID_ARG and steps.value == 0 and t_final.value == 0.0
+    assert b"null" in L.aderstp_last_error()
