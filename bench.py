@@ -214,6 +214,55 @@ def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
     return res
 
 
+def measure_timestep(S, n, e, steps, warmup):
+    """One full time step of the GPU solver on an e^3 periodic mesh: the
+    predictor on the 1/h-scaled PDE without favg (the corrector never reads it, solver.cpp:184-253)
+    followed by the corrector, per-element elastic material.  Device timing of each part."""
+    import torch
+    E = e ** 3
+    q, par = S.generate(0, SEED, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
+    rho, cp, cs = par[:, 0], par[:, 1], par[:, 2]
+    mu = rho * cs * cs
+    lam = rho * cp * cp - 2.0 * mu
+    s = float(e)  # 1 / h on the unit domain
+    par_s = torch.stack([lam * s, mu * s, rho / s], 1).contiguous()
+    pred = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_LAMBDA_MU_RHO)
+    corr = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
+    out = pred.alloc_output(E, want_favg=False)
+    dt = 0.35 / e / (3.0 * float(cp.max()) * (2 * n - 1))
+
+    def p_step():
+        pred.predict(q, dt, par=par_s, out=out, want_favg=False)
+
+    def c_step():
+        corr.correct(q, e, out, par=par)
+
+    stream = torch.cuda.current_stream()
+    res = {}
+    for name, fn in (("predictor", p_step), ("corrector", c_step), ("step", lambda: (p_step(), c_step()))):
+        for _ in range(warmup):
+            fn()
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(steps):
+            fn()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        res[name] = ev0.elapsed_time(ev1) / steps
+    pred.status()
+    m = 9
+    corr_bytes = 8 * (3 * n ** 3 * m + 24 * n * n * m + 3)  # u in/out, qavg, own + neighbour faces, par
+    peak = hbm_peak()[0] / 1e9
+    return {"workload": f"GPU time step, elastic nDof {n}, periodic {e}^3 mesh ({E} elements), per-element material",
+            "elements_per_s": E / (res["step"] * 1e-3), "ms_per_step": res["step"],
+            "predictor_ms": res["predictor"], "corrector_ms": res["corrector"],
+            "corrector_bytes_per_element": corr_bytes,
+            "corrector_achieved_gbs": E * corr_bytes / (res["corrector"] * 1e-3) / 1e9,
+            "corrector_hbm_frac": E * corr_bytes / (res["corrector"] * 1e-3) / 1e9 / peak,
+            "bound": "predictor fp64, corrector hbm"}
+
+
 def measure_e2e(S, plan, cfg, world, rank, dt, steps):
     """Same metric through the host-buffer public API (aderstp_predict_batch_host): pinned host
     inputs and outputs, host->device and device->host copies inside the timed region.  One GPU
@@ -373,6 +422,7 @@ def main():
                             "achieved_gbs": pg * rf["byte_per_element"] / 1e9,
                             "roofline_elements_per_s": rf["roofline_elements_per_s"],
                             "frac_of_roofline": pg / rf["roofline_elements_per_s"], "bound": rf["bound"]}
+        others["timestep_n8"] = measure_timestep(S, 8, 50, max(5, args.steps // 4), 3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

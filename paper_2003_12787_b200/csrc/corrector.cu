@@ -78,8 +78,10 @@ __device__ __forceinline__ long long wrap_index(int ix, int iy, int iz, int e) {
   return ((long long)iz * e + iy) * e + ix;
 }
 
+constexpr int kCorrThreads = 512;
+
 template <int N, bool ELASTIC>
-__global__ void __launch_bounds__(256) correct_kernel(CorrParams kp, double* __restrict__ u,
+__global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, double* __restrict__ u,
                                                       const double* __restrict__ par,
                                                       const double* __restrict__ qavg,
                                                       const double* __restrict__ face_q,
@@ -90,6 +92,9 @@ __global__ void __launch_bounds__(256) correct_kernel(CorrParams kp, double* __r
   extern __shared__ __align__(16) double smc[];
   double* QA = smc;           // qavg [s][k3][k2][k1]
   double* DL = smc + m * N3;  // fhat - f_self  [f][a][b][s]
+  __shared__ double Ds[N * N];     // D (per-thread row indices: shared, not the constant bank)
+  __shared__ double SC[2][N];      // sign * phi_side[j] / w_j
+  __shared__ double SMAX[6];       // per face
   const int e = kp.e;
   const long long c = blockIdx.x;
   const int ix = (int)(c % e), iy = (int)((c / e) % e), iz = (int)(c / ((long long)e * e));
@@ -101,6 +106,22 @@ __global__ void __launch_bounds__(256) correct_kernel(CorrParams kp, double* __r
 #pragma unroll
     for (int i = 0; i < 4; ++i) mine.c4[i] *= kp.inv_h;  // ScaledPde: flux x 1/h
   }
+  for (int i = tid; i < N * N; i += blockDim.x) Ds[i] = kp.d[i];
+  if (tid < 2 * N) {
+    const int side = tid / N, j = tid - side * N;
+    SC[side][j] = (side == 0 ? -1.0 : 1.0) * kp.phi[side][j] * kp.inv_w[j];
+  }
+  if (tid < 6) {
+    const int d = tid >> 1, step = (tid & 1) ? 1 : -1;
+    double smax = kp.smax;
+    if (ELASTIC && smax < 0.0) {
+      const long long nb =
+          wrap_index(ix + (d == 0 ? step : 0), iy + (d == 1 ? step : 0), iz + (d == 2 ? step : 0), e);
+      smax = fmax(material(par + 3 * c, kp.par_kind).cp, material(par + 3 * nb, kp.par_kind).cp) * kp.inv_h;
+    }
+    SMAX[tid] = smax;
+  }
+  __syncthreads();
 
   // ---- qavg -> shared (flat over the output layout: coalesced) ----------------------------
   {
@@ -143,9 +164,7 @@ __global__ void __launch_bounds__(256) correct_kernel(CorrParams kp, double* __r
         f_plus = mf[(2 * d) * FV + r];
         f_minus = tf[(2 * d + 1) * FV + r];
       }
-      double smax = kp.smax;
-      if (ELASTIC && smax < 0.0) smax = fmax(mine.cp, material(par + 3 * nb, kp.par_kind).cp) * kp.inv_h;
-      const double fh = 0.5 * (f_plus + f_minus) - 0.5 * smax * (q_minus - q_plus);
+      const double fh = 0.5 * (f_plus + f_minus) - 0.5 * SMAX[f] * (q_minus - q_plus);
       DL[i] = fh - mf[f * FV + r];
     }
   }
@@ -182,11 +201,11 @@ __global__ void __launch_bounds__(256) correct_kernel(CorrParams kp, double* __r
       if (ELASTIC) {
         const int cf = kCoefC[s][d];
         if (cf == 4) continue;
-        const double cc = mine.c4[cf];
+        const double cc = cf == 0 ? mine.c4[0] : cf == 1 ? mine.c4[1] : cf == 2 ? mine.c4[2] : mine.c4[3];
         const double* src = QA + kInC[s][d] * N3 + base;
         double acc = 0.0;
 #pragma unroll
-        for (int l = 0; l < N; ++l) acc = fma(kp.d[kd * N + l], cc * src[l * stride], acc);
+        for (int l = 0; l < N; ++l) acc = fma(Ds[kd * N + l], cc * src[l * stride], acc);
         vol += acc;
       } else {
         for (int k = 0; k < kp.n_terms; ++k) {
@@ -195,7 +214,7 @@ __global__ void __launch_bounds__(256) correct_kernel(CorrParams kp, double* __r
           const double* src = QA + kp.tr[s][d][k] * N3 + base;
           double acc = 0.0;
 #pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(kp.d[kd * N + l], cc * src[l * stride], acc);
+          for (int l = 0; l < N; ++l) acc = fma(Ds[kd * N + l], cc * src[l * stride], acc);
           vol += acc;
         }
       }
@@ -208,8 +227,7 @@ __global__ void __launch_bounds__(256) correct_kernel(CorrParams kp, double* __r
       const int ab = d == 0 ? k3 * N + k2 : d == 1 ? k3 * N + k1 : k2 * N + k1;
 #pragma unroll
       for (int side = 0; side < 2; ++side) {
-        const double scale = (side == 0 ? -1.0 : 1.0) * kp.phi[side][kd] * kp.inv_w[kd];
-        val += scale * DL[((2 * d + side) * N2 + ab) * m + s];
+        val += SC[side][kd] * DL[((2 * d + side) * N2 + ab) * m + s];
       }
     }
     if (!isfinite(val)) flags |= 1u;
@@ -279,7 +297,7 @@ cudaError_t launch_correct_n(const LaunchPlan& p, const CorrArgs& a, cudaStream_
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const long long cells = (long long)a.e * a.e * a.e;
-  kern<<<(unsigned)cells, 256, smem, stream>>>(kp, a.u, a.par, a.qavg, a.face_q, a.face_f, p.d_status);
+  kern<<<(unsigned)cells, kCorrThreads, smem, stream>>>(kp, a.u, a.par, a.qavg, a.face_q, a.face_f, p.d_status);
   return cudaGetLastError();
 }
 
