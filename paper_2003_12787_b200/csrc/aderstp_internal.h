@@ -55,6 +55,10 @@ struct BatchArgs {
   long long n_elem;
   double dt;
   double t_start;
+  // fused time-step mode (GPU time loop): also write u_next = q + L(qavg) in q's layout, i.e. the
+  // corrector's volume term (solver.cpp:199-207) applied by one more Horner step; qavg may then be
+  // null.  Only kernels with fused_supported() honour it.
+  double* u_next = nullptr;
 };
 
 // corrector.cu: GPU corrector step (proj/src/solver.cpp:184-311) and time-loop helpers
@@ -76,6 +80,7 @@ cudaError_t launch_max_cp(const double* par, int par_kind, long long n, unsigned
 
 // stp_kernels.cu
 cudaError_t launch_stp(const LaunchPlan& plan, const BatchArgs& args, cudaStream_t stream);
+bool fused_supported(const LaunchPlan& plan, const BatchArgs& args);  // u_next honoured by the dispatch
 cudaError_t launch_convert(int n, int m, long long n_elem, int src_layout, int src_stride,
                            const double* src, int dst_layout, int dst_stride, double* dst,
                            cudaStream_t stream);

@@ -553,11 +553,19 @@ int aderstp_run_simulation(const aderstp_plan* p, const aderstp_mesh* mesh, doub
   double t = 0.0;
   int64_t done = 0;
   rc = ADERSTP_OK;
+  // fused step where the predictor supports it: the predictor writes u + L(qavg) in place (one more
+  // Horner step with coefficient 1, the corrector's volume term) and the corrector adds only the
+  // surface terms; elsewhere qavg goes through HBM to the full corrector
+  aderstp::BatchArgs probe{u, elastic ? par_s : par, nullptr, nullptr, face_q, face_f, E, 1.0, 0.0};
+  probe.u_next = u;
+  const bool fused = aderstp::fused_supported(sp, probe);
   while (t < t_end - 1e-14 * std::max(1.0, t_end)) {
     const double dt = std::min(dt0, t_end - t);
-    aderstp::BatchArgs ba{u, elastic ? par_s : par, qavg, nullptr, face_q, face_f, E, dt, t};
+    aderstp::BatchArgs ba{u, elastic ? par_s : par, fused ? nullptr : qavg, nullptr, face_q, face_f, E, dt, t};
+    if (fused) ba.u_next = u;
     err = aderstp::launch_stp(sp, ba, st);
-    aderstp::CorrArgs ca{u, par, qavg, face_q, face_f, e, s, (elastic && max_wavespeed < 0.0) ? -1.0 : smax * s};
+    aderstp::CorrArgs ca{u, par, fused ? nullptr : qavg, face_q, face_f, e, s,
+                         (elastic && max_wavespeed < 0.0) ? -1.0 : smax * s};
     if (err == cudaSuccess) err = aderstp::launch_correct(p->lp, ca, st);
     unsigned int flags = 0;
     if (err == cudaSuccess) err = cudaMemcpyAsync(&flags, p->lp.d_status, sizeof flags, cudaMemcpyDeviceToHost, st);

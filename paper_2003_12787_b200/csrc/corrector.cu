@@ -80,7 +80,9 @@ __device__ __forceinline__ long long wrap_index(int ix, int iy, int iz, int e) {
 
 constexpr int kCorrThreads = 512;
 
-template <int N, bool ELASTIC>
+// VOL = false: the volume term was already applied by the fused predictor (BatchArgs::u_next),
+// only the surface fluctuations remain.
+template <int N, bool ELASTIC, bool VOL>
 __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, double* __restrict__ u,
                                                       const double* __restrict__ par,
                                                       const double* __restrict__ qavg,
@@ -91,7 +93,7 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, do
   const int m = ELASTIC ? NVC : kp.m;
   extern __shared__ __align__(16) double smc[];
   double* QA = smc;           // qavg [s][k3][k2][k1]
-  double* DL = smc + m * N3;  // fhat - f_self  [f][a][b][s]
+  double* DL = smc + (VOL ? m * N3 : 0);  // fhat - f_self  [f][a][b][s]
   __shared__ double Ds[N * N];     // D (per-thread row indices: shared, not the constant bank)
   __shared__ double SC[2][N];      // sign * phi_side[j] / w_j
   __shared__ double SMAX[6];       // per face
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, do
   __syncthreads();
 
   // ---- qavg -> shared (flat over the output layout: coalesced) ----------------------------
-  {
+  if (VOL) {
     const int os = kp.out_stride;
     const double* qa = qavg + c * (long long)(N3 * os);
     for (int j = tid; j < N3 * os; j += blockDim.x) {
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, do
     // volume (apply_volume_once): sum over d of D_d applied to the scaled flux / ncp terms
     double vol = 0.0;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
+    for (int d = 0; d < 3 && VOL; ++d) {
       const int kd = d == 0 ? k1 : d == 1 ? k2 : k3;
       const int stride = d == 0 ? 1 : d == 1 ? N : N2;
       const int base = k3 * N2 + k2 * N + k1 - kd * stride;
@@ -292,8 +294,10 @@ cudaError_t launch_correct_n(const LaunchPlan& p, const CorrArgs& a, cudaStream_
   kp.inv_h = a.inv_h;
   kp.smax = a.smax;
   const bool elastic = p.kind == ADERSTP_PDE_ELASTIC;
-  const size_t smem = sizeof(double) * (size_t)p.m * (N * N * N + 6 * N * N);
-  auto kern = elastic ? correct_kernel<N, true> : correct_kernel<N, false>;
+  const bool vol = a.qavg != nullptr;
+  const size_t smem = sizeof(double) * (size_t)p.m * ((vol ? N * N * N : 0) + 6 * N * N);
+  auto kern = elastic ? (vol ? correct_kernel<N, true, true> : correct_kernel<N, true, false>)
+                      : (vol ? correct_kernel<N, false, true> : correct_kernel<N, false, false>);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const long long cells = (long long)a.e * a.e * a.e;

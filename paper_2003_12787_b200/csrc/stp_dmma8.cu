@@ -183,18 +183,23 @@ __device__ __forceinline__ void dfma_z(double (&acc)[NT][2], const double* f, in
 // Q holds q.
 
 // One Horner step loop for output quantity s on k3 tiles K0 .. K0+NT-1.
-template <int NT>
+// un (fused time-step mode, else null): this lane's base in the next state u_next; one more step
+// with coefficient 1 then gives u_next = q + L(qavg) (the corrector's volume term) in registers
+// and goes straight to HBM.  urow = doubles per (k3, k2) row of u_next.
+template <int NT, bool FUSED>
 __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const double* cf, int s, int K0, int g,
-                                            int t, int col, double d0, double d1, const double (&c4)[4]) {
+                                            int t, int col, double d0, double d1, const double (&c4)[4],
+                                            double* un, int urow) {
   const int in_x = kIn[s][0], in_y = kIn[s][1], in_z = kIn[s][2];
   const double cx = sel4(c4, kCoef[s][0]), cy = sel4(c4, kCoef[s][1]), cz = sel4(c4, kCoef[s][2]);
   const bool has_x = kCoef[s][0] != 4, has_y = kCoef[s][1] != 4, has_z = kCoef[s][2] != 4;
   const double bx0 = cx * d0, bx1 = cx * d1;  // B-fragments of c_x D^T
   const double ay0 = cy * d0, ay1 = cy * d1;  // A-fragments of c_y D
   const int own = s * PV + K0 * 64 + col;
+  constexpr int o_end = FUSED ? -1 : 0;
 #pragma unroll 1
-  for (int o = N8 - 2; o >= 0; --o) {
-    const double co = cf[o];
+  for (int o = N8 - 2; o >= o_end; --o) {
+    const double co = (!FUSED || o >= 0) ? cf[o] : 1.0;
     double tt[NT][2];
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
@@ -205,6 +210,11 @@ __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const do
     if (has_x) mma_x<NT>(tt, P + in_x * PV, K0, g, t, bx0, bx1);
     if (has_y) mma_y<NT>(tt, P + in_y * PV, K0, g, t, ay0, ay1);
     if (has_z) dfma_z<NT>(tt, P + in_z * PV, K0, col, cz);
+    if (FUSED && o < 0) {  // fused: u_next = q + L(qavg)
+#pragma unroll
+      for (int k = 0; k < NT; ++k) st_cs2(un + ((K0 + k) * 8) * urow + s * 8, tt[k][0], tt[k][1]);
+      break;
+    }
     __syncthreads();  // every warp has finished reading r
 #pragma unroll
     for (int k = 0; k < NT; ++k) sts2(P + own + k * 64, tt[k][0], tt[k][1]);
@@ -214,13 +224,15 @@ __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const do
 
 // Normal stresses on k3 tiles K0 .. K0+NT-1: a = Dx u, b = Dy v, c = Dz w (unscaled), then
 // t_sxx = lambda (a+b+c) + 2 mu a, etc. (proj/src/pde.cpp:180-190)
-template <int NT>
+template <int NT, bool FUSED>
 __device__ __forceinline__ void ck_normal(double* P, const double* Q, const double* cf, int K0, int g, int t,
-                                          int col, double d0, double d1, const double (&c4)[4]) {
+                                          int col, double d0, double d1, const double (&c4)[4], double* un,
+                                          int urow) {
   const double lam = c4[1], two_mu = 2.0 * c4[2];
+  constexpr int o_end = FUSED ? -1 : 0;
 #pragma unroll 1
-  for (int o = N8 - 2; o >= 0; --o) {
-    const double co = cf[o];
+  for (int o = N8 - 2; o >= o_end; --o) {
+    const double co = (!FUSED || o >= 0) ? cf[o] : 1.0;
     double ta[NT][2], tb[NT][2], tc[NT][2];
 #pragma unroll
     for (int k = 0; k < NT; ++k) ta[k][0] = ta[k][1] = tb[k][0] = tb[k][1] = tc[k][0] = tc[k][1] = 0.0;
@@ -240,6 +252,16 @@ __device__ __forceinline__ void ck_normal(double* P, const double* Q, const doub
         tc[k][j] = fma(co, qv[2][j], fma(two_mu, tc[k][j], sum));
       }
     }
+    if (FUSED && o < 0) {  // fused: u_next = q + L(qavg)
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        double* r = un + ((K0 + k) * 8) * urow;
+        st_cs2(r, ta[k][0], ta[k][1]);
+        st_cs2(r + 8, tb[k][0], tb[k][1]);
+        st_cs2(r + 16, tc[k][0], tc[k][1]);
+      }
+      break;
+    }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
@@ -252,6 +274,7 @@ __device__ __forceinline__ void ck_normal(double* P, const double* Q, const doub
   }
 }
 
+template <bool FUSED>
 __global__ void __maxnreg__(80)
 stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   constexpr int THREADS8 = NWARP * 32;
@@ -320,10 +343,13 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   // ---- Cauchy-Kowalewsky recursion, Horner form ------------------------------------------
   {
     const int role = kRole[warp];
+    const int urow = kp.q_stride * 8;
+    double* un = FUSED ? a.u_next + e * (long long)(PV * kp.q_stride) + g * urow + 2 * t : nullptr;
     if (role >= 0)
-      ck_quantity<8>(P, Q, kp.cf, role, 0, g, t, col, d0, d1, c4);
+      ck_quantity<8, FUSED>(P, Q, kp.cf, role, 0, g, t, col, d0, d1, c4, un, urow);
     else
-      ck_normal<4>(P, Q, kp.cf, 4 * (-role - 1), g, t, col, d0, d1, c4);
+      ck_normal<4, FUSED>(P, Q, kp.cf, 4 * (-role - 1), g, t, col, d0, d1, c4, un, urow);
+    if (FUSED) __syncthreads();  // q (the Q region) is read until here; faces stage over it
   }
 
   TM3(2);
@@ -348,9 +374,11 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
       qa[k][0] = v.x;
       qa[k][1] = v.y;
     }
-    double* qout = a.qavg + e * (long long)(PV * NV) + s * 8 + 2 * t;
+    if (!FUSED || a.qavg) {
+      double* qout = a.qavg + e * (long long)(PV * NV) + s * 8 + 2 * t;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) st_cs2(qout + ((K0 + k) * 8 + g) * NV * 8, qa[k][0], qa[k][1]);
+      for (int k = 0; k < 4; ++k) st_cs2(qout + ((K0 + k) * 8 + g) * NV * 8, qa[k][0], qa[k][1]);
+    }
     if (a.favg) {
       double* fout = a.favg + e * (long long)(3 * PV * NV) + 2 * t;
       const int nout = kOutN[s];
@@ -478,7 +506,7 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
       kp.cf[o] = c;
     }
   }
-  auto kern = stp_dmma8_kernel;
+  auto kern = a.u_next ? stp_dmma8_kernel<true> : stp_dmma8_kernel<false>;
   int smem = kSmem8;
 #ifdef ADERSTP_EXPT_TIMING
   if (const char* x = std::getenv("ADERSTP_EXPT_SMEM")) smem += std::atoi(x);  // occupancy experiments
