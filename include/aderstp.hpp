@@ -116,6 +116,28 @@ class Predictor {
     check(aderstp_predict_batch_host(plan_, n_elem, q, par, dt, t_start, qavg, favg, face_q, face_f));
   }
   void status(void* stream = nullptr) { check(aderstp_plan_status(plan_, stream)); }
+
+  // ader::corrector_step (proj/src/solver.cpp:257-311) on a periodic e^3 mesh, device buffers.
+  void correct_device(const aderstp_mesh& mesh, double* u, const double* par, const double* qavg,
+                      const double* face_q, const double* face_f, double max_wavespeed,
+                      void* stream = nullptr) const {
+    check(aderstp_correct_batch(plan_, &mesh, u, par, qavg, face_q, face_f, max_wavespeed, stream));
+  }
+  // ader::run_simulation (proj/src/solver.cpp:313-359); returns the reference's RunResult fields.
+  struct RunResult {
+    int64_t steps = 0;
+    double t_final = 0.0;
+    bool stable = true;
+  };
+  RunResult run_simulation_device(const aderstp_mesh& mesh, double* u, const double* par, double cfl,
+                                  double t_end, double max_wavespeed, void* stream = nullptr) const {
+    RunResult r;
+    const int rc = aderstp_run_simulation(plan_, &mesh, u, par, cfl, t_end, max_wavespeed, &r.steps,
+                                          &r.t_final, stream);
+    if (rc == ADERSTP_ERR_NONFINITE) r.stable = false;
+    else check(rc);
+    return r;
+  }
   aderstp_plan* handle() const { return plan_; }
 
  private:
