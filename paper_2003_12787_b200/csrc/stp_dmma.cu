@@ -8,8 +8,9 @@
 // zeros on the padding and the real nodes see exactly the N-term sums; N <= 4 needs a single
 // k-step.  z contractions: register DFMA over the N planes with D from the constant cache.
 // Roles (no redundant derivative fields): velocities (warps 0-2), shear (3, 6, 7), normal
-// stresses on two k3 halves sharing Dx u, Dy v, Dz w (4, 5).  Shared memory: p and the qavg
-// accumulator, 2 x 9 x N x 64 doubles, XOR-swizzled rows (bank-conflict free fragment loads).
+// stresses on two k3 halves sharing Dx u, Dy v, Dz w (4, 5).  The CK series in Horner form (see
+// stp_dmma8.cu).  Shared memory: r and q, 2 x 9 x N x 64 doubles, XOR-swizzled rows
+// (bank-conflict free fragment loads).
 #include <cstdint>
 
 #include "../../include/aderstp.h"
@@ -49,6 +50,7 @@ struct GeoP {
 struct ParamsP {
   double d[64];      // zero-padded D
   double phi[2][8];  // zero-padded phi(0), phi(1)
+  double cf[8];      // cf[o] = dt^(o+1)/(o+1)! (Horner coefficients, stp_splitck.cpp:45,64)
   int check, par_kind, q_stride;
 };
 
@@ -140,10 +142,11 @@ __device__ __forceinline__ void dfma_zp(double (&acc)[NT][2], const double* f, i
 }
 
 // normal stresses on planes K0 .. K0+NT-1: a = Dx u, b = Dy v, c = Dz w, then
-// t_ii = lambda (a+b+c) + 2 mu {a,b,c}_i; qavg += coeff t; t -> p (after the read barrier)
+// t_ii = lambda (a+b+c) + 2 mu {a,b,c}_i + co q_ii (Horner, see stp_dmma8.cu); t -> p after the
+// read barrier
 template <int N, int NT>
-__device__ __forceinline__ void normal_step(double* P, double* QA, int K0, int g, int t, int col, double d0,
-                                            double d1, double lam, double two_mu, double coeff, bool last) {
+__device__ __forceinline__ void normal_step(double* P, const double* Q, int K0, int g, int t, int col, double d0,
+                                            double d1, double lam, double two_mu, double co) {
   constexpr int PV = GeoP<N>::PV;
   double ta[NT][2], tb[NT][2], tc[NT][2];
 #pragma unroll
@@ -152,31 +155,25 @@ __device__ __forceinline__ void normal_step(double* P, double* QA, int K0, int g
   mma_yp<N, NT>(tb, P + 7 * PV, K0, g, t, d0, d1);
   dfma_zp<N, NT>(tc, P + 8 * PV, K0, col, 1.0);
 #pragma unroll
-  for (int k = 0; k < NT; ++k)
+  for (int k = 0; k < NT; ++k) {
+    const int off = (K0 + k) * 64 + col;
+    const double2 qa = lds2p(Q + off), qb = lds2p(Q + PV + off), qc = lds2p(Q + 2 * PV + off);
+    const double qv[3][2] = {{qa.x, qa.y}, {qb.x, qb.y}, {qc.x, qc.y}};
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const double sum = lam * (ta[k][j] + tb[k][j] + tc[k][j]);
-      ta[k][j] = fma(two_mu, ta[k][j], sum);
-      tb[k][j] = fma(two_mu, tb[k][j], sum);
-      tc[k][j] = fma(two_mu, tc[k][j], sum);
+      ta[k][j] = fma(co, qv[0][j], fma(two_mu, ta[k][j], sum));
+      tb[k][j] = fma(co, qv[1][j], fma(two_mu, tb[k][j], sum));
+      tc[k][j] = fma(co, qv[2][j], fma(two_mu, tc[k][j], sum));
     }
+  }
+  __syncthreads();  // every warp has finished reading r (single buffer)
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
     const int off = (K0 + k) * 64 + col;
-    const double2 va = lds2p(QA + off), vb = lds2p(QA + PV + off), vc = lds2p(QA + 2 * PV + off);
-    sts2p(QA + off, fma(coeff, ta[k][0], va.x), fma(coeff, ta[k][1], va.y));
-    sts2p(QA + PV + off, fma(coeff, tb[k][0], vb.x), fma(coeff, tb[k][1], vb.y));
-    sts2p(QA + 2 * PV + off, fma(coeff, tc[k][0], vc.x), fma(coeff, tc[k][1], vc.y));
-  }
-  __syncthreads();  // every warp has finished reading p (single buffer)
-  if (!last) {
-#pragma unroll
-    for (int k = 0; k < NT; ++k) {
-      const int off = (K0 + k) * 64 + col;
-      sts2p(P + off, ta[k][0], ta[k][1]);
-      sts2p(P + PV + off, tb[k][0], tb[k][1]);
-      sts2p(P + 2 * PV + off, tc[k][0], tc[k][1]);
-    }
+    sts2p(P + off, ta[k][0], ta[k][1]);
+    sts2p(P + PV + off, tb[k][0], tb[k][1]);
+    sts2p(P + 2 * PV + off, tc[k][0], tc[k][1]);
   }
 }
 
@@ -213,8 +210,8 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   using G = GeoP<N>;
   constexpr int PV = G::PV, FACE = G::FACE;
   extern __shared__ __align__(16) double smq[];
-  double* P = smq;
-  double* QA = smq + NVP * PV;
+  double* P = smq;              // Horner iterate r; qavg at the end
+  double* Q = smq + NVP * PV;   // q
   double* RAW = smq + 2 * NVP * PV;                                     // PERSIST: q of the next element
   uint64_t* mbar = reinterpret_cast<uint64_t*>(RAW + N * N * N * kp.q_stride);
   const int tid = threadIdx.x;
@@ -255,7 +252,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     c4[3] = 1.0 / rho;
   }
 
-  // ---- stage q into the padded planes (padding = 0) and QA = dt q -----------------------
+  // ---- stage q into the padded planes (padding = 0): Q = q, P = c_(n-1) q -----------------
   // (s, k3, k2 < 8, k1-pair < 4) positions, IT per thread; every load is issued before the
   // first shared store so the DRAM latencies overlap
   if (PERSIST) mbar_wait(mbar, phase);
@@ -291,8 +288,8 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
       const int s = r / N, k3 = r - s * N;
       if (kp.check && !(isfinite(v0[it]) && isfinite(v1[it]))) flags |= 1u;
       const int j = s * PV + k3 * 64 + physp(k2, 2 * kp2);
-      sts2p(P + j, v0[it], v1[it]);
-      sts2p(QA + j, dt * v0[it], dt * v1[it]);
+      sts2p(Q + j, v0[it], v1[it]);
+      sts2p(P + j, kp.cf[N - 1] * v0[it], kp.cf[N - 1] * v1[it]);
     }
   }
   __syncthreads();
@@ -308,7 +305,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   const int role = kRoleP[warp];
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];
 
-  double coeff = dt;
+  // ---- CK series in Horner form (stp_dmma8.cu): r <- c_o q + L r, o = N-2 .. 0 ----------
   if (role >= 0) {
     const int s = role;
     const int in_x = kInP[s][0], in_y = kInP[s][1], in_z = kInP[s][2];
@@ -317,41 +314,40 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     const double bx0 = cx * d0, bx1 = cx * d1, ay0 = cy * d0, ay1 = cy * d1;
     const int own = s * PV + col;
 #pragma unroll 1
-    for (int o = 1; o < N; ++o) {
+    for (int o = N - 2; o >= 0; --o) {
+      const double co = kp.cf[o];
       double tt[N][2];
 #pragma unroll
       for (int k3 = 0; k3 < N; ++k3) tt[k3][0] = tt[k3][1] = 0.0;
       if (has_x) mma_xp<N, N>(tt, P + in_x * PV, 0, g, t, bx0, bx1);
       if (has_y) mma_yp<N, N>(tt, P + in_y * PV, 0, g, t, ay0, ay1);
       if (has_z) dfma_zp<N, N>(tt, P + in_z * PV, 0, col, cz);
-      coeff *= dt / (o + 1);
 #pragma unroll
-      for (int k3 = 0; k3 < N; ++k3) {
-        const double2 v = lds2p(QA + own + k3 * 64);
-        sts2p(QA + own + k3 * 64, fma(coeff, tt[k3][0], v.x), fma(coeff, tt[k3][1], v.y));
+      for (int k3 = 0; k3 < N; ++k3) {  // + c_o q (loaded late: fewer live registers)
+        const double2 v = lds2p(Q + own + k3 * 64);
+        tt[k3][0] = fma(co, v.x, tt[k3][0]);
+        tt[k3][1] = fma(co, v.y, tt[k3][1]);
       }
       __syncthreads();
-      if (o + 1 < N) {
 #pragma unroll
-        for (int k3 = 0; k3 < N; ++k3) sts2p(P + own + k3 * 64, tt[k3][0], tt[k3][1]);
-      }
+      for (int k3 = 0; k3 < N; ++k3) sts2p(P + own + k3 * 64, tt[k3][0], tt[k3][1]);
       __syncthreads();
     }
   } else {
     const int h = -role - 1;
     const double lam = c4[1], two_mu = 2.0 * c4[2];
 #pragma unroll 1
-    for (int o = 1; o < N; ++o) {
-      coeff *= dt / (o + 1);
-      if (h == 0) normal_step<N, G::H0>(P, QA, 0, g, t, col, d0, d1, lam, two_mu, coeff, o + 1 == N);
-      else normal_step<N, G::H1>(P, QA, G::H0, g, t, col, d0, d1, lam, two_mu, coeff, o + 1 == N);
+    for (int o = N - 2; o >= 0; --o) {
+      const double co = kp.cf[o];
+      if (h == 0) normal_step<N, G::H0>(P, Q, 0, g, t, col, d0, d1, lam, two_mu, co);
+      else normal_step<N, G::H1>(P, Q, G::H0, g, t, col, d0, d1, lam, two_mu, co);
       __syncthreads();
     }
   }
 
   TM2(2);
   // ---- epilogue: 9 quantities x k3 planes over the 8 warps ------------------------------
-  double* FQ = smq;  // face staging [6][N][N][9] over the dead p buffer
+  double* FQ = Q;  // face staging [6][N][N][9] over the dead q buffer
   const bool faces = a.face_q || a.face_f;
   const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0;
   const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
@@ -364,7 +360,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
 #pragma unroll 1
     for (int u = warp; u < NVP * N; u += NWP) {
       const int s = u / N, k3 = u - s * N;
-      const double2 v = lds2p(QA + s * PV + k3 * 64 + col);
+      const double2 v = lds2p(P + s * PV + k3 * 64 + col);
       if (rowok) {
         const int base = ((k3 * N + g) * NVP + s) * N + 2 * t;
         st_pair<N>(qout + base, v.x, v.y, k1a, k1b);
@@ -385,7 +381,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
 #pragma unroll 1
     for (int u = warp; u < NVP * N; u += NWP) {
       const int s = u / N, k3 = u - s * N;
-      const double* qs = QA + s * PV;
+      const double* qs = P + s * PV;
       double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
       dmmap(x0, x1, qs[k3 * 64 + physp(g, t)], bphi0);
       if (G::KS > 1) dmmap(x0, x1, qs[k3 * 64 + physp(g, 4 + t)], bphi1);
@@ -402,7 +398,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     }
 #pragma unroll 1
     for (int s = warp; s < NVP; s += NWP) {
-      const double* qs = QA + s * PV;
+      const double* qs = P + s * PV;
       if (rowok) {
         double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0};
 #pragma unroll
@@ -426,7 +422,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     __syncthreads();
     TM2(4);
     // face_f = F_d(face_q) staged next to face_q; both leave as TMA bulk stores (UBLKCP)
-    double* FF = smq + 6 * FACE;
+    double* FF = P;  // qavg (P) is no longer read
     if (a.face_f && tid < 252) {
       const int so = tid % NVP, ab0 = tid / NVP;  // 28 in-face nodes per sweep
 #pragma unroll
@@ -479,6 +475,14 @@ cudaError_t launch_dmmap_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t
   kp.check = p.check;
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
+  {
+    double c = a.dt;  // same operation sequence as proj/src/stp_splitck.cpp:45,64
+    kp.cf[0] = c;
+    for (int o = 1; o < 8; ++o) {
+      c *= a.dt / (o + 1);
+      kp.cf[o] = c;
+    }
+  }
   // the persistent TMA-prefetch variant needs 16-byte granular element blocks of q
   const bool persist = p.dmmap_persist && ((N * N * N * p.q_stride) % 2 == 0);
   auto kern = persist ? stp_dmmap_kernel<N, true> : stp_dmmap_kernel<N, false>;

@@ -4,3 +4,4 @@ for c in n9 c4; do
   timeout 120 python bench.py --config $c --steps 10 --no-e2e --no-cpu-baseline --no-other-configs 2>&1 | tail -1 | \
     python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$c', d['value'], d['roofline']['frac'])"
 done
+python tools/expt_timing.py 2>&1 | grep bip
