@@ -261,6 +261,8 @@ def measure_timestep(S, n, e, steps, warmup):
     ev1.record(stream)
     torch.cuda.synchronize()
     res["run_simulation_step"] = ev0.elapsed_time(ev1) / max(nsteps, 1)
+    res["run_simulation_steps"] = nsteps
+    res["run_simulation_stable"] = ok
     pred.status()
     m = 9
     corr_bytes = 8 * (3 * n ** 3 * m + 24 * n * n * m + 3)  # u in/out, qavg, own + neighbour faces, par
@@ -269,6 +271,7 @@ def measure_timestep(S, n, e, steps, warmup):
             "elements_per_s": E / (res["step"] * 1e-3), "ms_per_step": res["step"],
             "predictor_ms": res["predictor"], "corrector_ms": res["corrector"],
             "run_simulation_ms_per_step": res["run_simulation_step"],
+            "run_simulation_steps": res["run_simulation_steps"], "run_simulation_stable": res["run_simulation_stable"],
             "run_simulation_elements_per_s": E / (res["run_simulation_step"] * 1e-3),
             "corrector_bytes_per_element": corr_bytes,
             "corrector_achieved_gbs": E * corr_bytes / (res["corrector"] * 1e-3) / 1e9,

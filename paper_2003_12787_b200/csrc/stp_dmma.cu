@@ -144,9 +144,11 @@ __device__ __forceinline__ void dfma_zp(double (&acc)[NT][2], const double* f, i
 // normal stresses on planes K0 .. K0+NT-1: a = Dx u, b = Dy v, c = Dz w, then
 // t_ii = lambda (a+b+c) + 2 mu {a,b,c}_i + co q_ii (Horner, see stp_dmma8.cu); t -> p after the
 // read barrier
+// un (fused time-step mode): the step with co = 1 writes u_next = q + L(qavg) to HBM instead of r
 template <int N, int NT>
 __device__ __forceinline__ void normal_step(double* P, const double* Q, int K0, int g, int t, int col, double d0,
-                                            double d1, double lam, double two_mu, double co) {
+                                            double d1, double lam, double two_mu, double co, double* un = nullptr,
+                                            int uplane = 0) {
   constexpr int PV = GeoP<N>::PV;
   double ta[NT][2], tb[NT][2], tc[NT][2];
 #pragma unroll
@@ -166,6 +168,19 @@ __device__ __forceinline__ void normal_step(double* P, const double* Q, int K0, 
       tb[k][j] = fma(co, qv[1][j], fma(two_mu, tb[k][j], sum));
       tc[k][j] = fma(co, qv[2][j], fma(two_mu, tc[k][j], sum));
     }
+  }
+  if (un) {  // fused: lane base un, uplane doubles per k3 plane of u_next
+    if (g < N) {
+      const bool ok0 = 2 * t < N, ok1 = 2 * t + 1 < N;
+#pragma unroll
+      for (int k = 0; k < NT; ++k) {
+        double* r = un + (K0 + k) * uplane;
+        st_pair<N>(r, ta[k][0], ta[k][1], ok0, ok1);
+        st_pair<N>(r + N, tb[k][0], tb[k][1], ok0, ok1);
+        st_pair<N>(r + 2 * N, tc[k][0], tc[k][1], ok0, ok1);
+      }
+    }
+    return;
   }
   __syncthreads();  // every warp has finished reading r (single buffer)
 #pragma unroll
@@ -205,7 +220,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
 
 // PERSIST: one CTA per SM slot loops over elements; element e+stride's input is prefetched
 // into a raw shared buffer by a TMA bulk copy (mbarrier-tracked) while element e computes.
-template <int N, bool PERSIST>
+template <int N, bool PERSIST, bool FUSED = false>
 __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsigned int* status) {
   using G = GeoP<N>;
   constexpr int PV = G::PV, FACE = G::FACE;
@@ -313,9 +328,10 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     const bool has_x = kCoefP[s][0] != 4, has_y = kCoefP[s][1] != 4, has_z = kCoefP[s][2] != 4;
     const double bx0 = cx * d0, bx1 = cx * d1, ay0 = cy * d0, ay1 = cy * d1;
     const int own = s * PV + col;
+    constexpr int o_end = FUSED ? -1 : 0;
 #pragma unroll 1
-    for (int o = N - 2; o >= 0; --o) {
-      const double co = kp.cf[o];
+    for (int o = N - 2; o >= o_end; --o) {
+      const double co = (!FUSED || o >= 0) ? kp.cf[o] : 1.0;
       double tt[N][2];
 #pragma unroll
       for (int k3 = 0; k3 < N; ++k3) tt[k3][0] = tt[k3][1] = 0.0;
@@ -327,6 +343,16 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
         const double2 v = lds2p(Q + own + k3 * 64);
         tt[k3][0] = fma(co, v.x, tt[k3][0]);
         tt[k3][1] = fma(co, v.y, tt[k3][1]);
+      }
+      if (FUSED && o < 0) {  // u_next = q + L(qavg): the corrector's volume term, straight to HBM
+        if (g < N) {
+          const int qs = kp.q_stride;
+          double* un = a.u_next + e * (long long)(N * N * N * qs) + (g * qs + s) * N + 2 * t;
+#pragma unroll
+          for (int k3 = 0; k3 < N; ++k3)
+            st_pair<N>(un + k3 * N * qs * N, tt[k3][0], tt[k3][1], 2 * t < N, 2 * t + 1 < N);
+        }
+        break;
       }
       __syncthreads();
 #pragma unroll
@@ -343,7 +369,14 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
       else normal_step<N, G::H1>(P, Q, G::H0, g, t, col, d0, d1, lam, two_mu, co);
       __syncthreads();
     }
+    if (FUSED) {
+      const int qs = kp.q_stride;
+      double* un = a.u_next + e * (long long)(N * N * N * qs) + g * qs * N + 2 * t;
+      if (h == 0) normal_step<N, G::H0>(P, Q, 0, g, t, col, d0, d1, lam, two_mu, 1.0, un, N * qs * N);
+      else normal_step<N, G::H1>(P, Q, G::H0, g, t, col, d0, d1, lam, two_mu, 1.0, un, N * qs * N);
+    }
   }
+  if (FUSED) __syncthreads();  // q (the Q region) is read until here; faces stage over it
 
   TM2(2);
   // ---- epilogue: 9 quantities x k3 planes over the 8 warps ------------------------------
@@ -355,7 +388,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   const bool k1a = 2 * t < N, k1b = 2 * t + 1 < N;
   // qavg / favg: units (quantity s, plane k3), 9 N of them round-robin over the 8 warps
   {
-    double* qout = a.qavg + e * (long long)(N * N * N * NVP);
+    double* qout = FUSED ? nullptr : a.qavg + e * (long long)(N * N * N * NVP);
     double* fout = a.favg ? a.favg + e * (long long)(3 * N * N * N * NVP) : nullptr;
 #pragma unroll 1
     for (int u = warp; u < NVP * N; u += NWP) {
@@ -363,7 +396,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
       const double2 v = lds2p(P + s * PV + k3 * 64 + col);
       if (rowok) {
         const int base = ((k3 * N + g) * NVP + s) * N + 2 * t;
-        st_pair<N>(qout + base, v.x, v.y, k1a, k1b);
+        if (!FUSED) st_pair<N>(qout + base, v.x, v.y, k1a, k1b);
         if (fout) {
           const int nout = kOutNP[s];
           for (int k = 0; k < nout; ++k) {
@@ -484,8 +517,9 @@ cudaError_t launch_dmmap_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t
     }
   }
   // the persistent TMA-prefetch variant needs 16-byte granular element blocks of q
-  const bool persist = p.dmmap_persist && ((N * N * N * p.q_stride) % 2 == 0);
-  auto kern = persist ? stp_dmmap_kernel<N, true> : stp_dmmap_kernel<N, false>;
+  const bool persist = !a.u_next && p.dmmap_persist && ((N * N * N * p.q_stride) % 2 == 0);
+  auto kern = a.u_next ? stp_dmmap_kernel<N, false, true>
+                       : persist ? stp_dmmap_kernel<N, true> : stp_dmmap_kernel<N, false>;
   const int smem = G::SMEM + (persist ? N * N * N * p.q_stride * 8 + 16 : 0);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err == cudaSuccess)
