@@ -99,6 +99,7 @@ cudaError_t launch_dmmap(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
 bool pass_applicable(const LaunchPlan& p);
 cudaError_t init_pass(const LaunchPlan& p);
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
+bool bip_selected(const LaunchPlan& p, const BatchArgs& a);  // launch_pass takes the bipartite kernel
 cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 
 }  // namespace aderstp

@@ -481,15 +481,21 @@ bool use_dmmap(const LaunchPlan& p, const BatchArgs& a) {
                        al16(a.u_next);
   return !p.force_generic && !p.no_dmmap && aligned && dmmap_applicable(p);
 }
+bool use_bip(const LaunchPlan& p, const BatchArgs& a) {
+  return !p.force_generic && pass_applicable(p) && bip_selected(p, a);
+}
 }  // namespace
 
-bool fused_supported(const LaunchPlan& p, const BatchArgs& a) { return use_dmma8(p, a) || use_dmmap(p, a); }
+bool fused_supported(const LaunchPlan& p, const BatchArgs& a) {
+  return use_dmma8(p, a) || use_dmmap(p, a) || use_bip(p, a);
+}
 
 cudaError_t launch_stp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   const bool aligned = al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) && al16(a.face_f);
   if (use_dmma8(p, a)) return launch_dmma8(p, a, stream);
   if (a.u_next && use_dmmap(p, a)) return launch_dmmap(p, a, stream);
+  if (a.u_next && use_bip(p, a)) return launch_pass(p, a, stream);
   if (a.u_next) return cudaErrorInvalidValue;  // the fused mode exists only where fused_supported()
   if (!p.force_generic && !p.no_dmmap && aligned && dmmap_applicable(p)) return launch_dmmap(p, a, stream);
   if (!p.force_generic && pass_applicable(p)) return launch_pass(p, a, stream);

@@ -674,7 +674,7 @@ __device__ __forceinline__ void bip_line_z(const double* src, double* const* dst
   }
 }
 
-template <int N>
+template <int N, bool FUSED = false>
 __global__ void __launch_bounds__(GeoB<N>::THREADS, GeoB<N>::MINB)
 stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   using G = GeoB<N>;
@@ -799,9 +799,123 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
 
   TMB(1);
   int vb = 6;  // slot of u (velocities occupy vb .. vb+2; the other three slots are TEMP)
+  // ---- epilogue pieces (called after the recursion; in the fused time-step mode the faces are
+  // taken from qavg before one more Horner step with coefficient 1 gives u + L(qavg)) ---------
+  auto fld = [&](int s) { return s < 6 ? s : vb + (s - 6); };
+  auto emit_qavg = [&]() {
+  if constexpr (N % 2 == 0) {  // k1 pairs: 16-byte shared loads and global stores
+    for (int i = tid; i < N3 / 2; i += G::THREADS) {
+      const int k1 = 2 * (i % (N / 2)), k32 = i / (N / 2);
+      const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+      double2 v[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) v[s] = *reinterpret_cast<const double2*>(qs + fld(s) * G::VS);
+      const long long ob = e * (long long)OUTV + k32 * NVE * N + k1;
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) __stcs(reinterpret_cast<double2*>(a.qavg + ob + s * N), v[s]);
+      if (a.favg) {
+        double* fo = a.favg + e * (long long)(3 * OUTV) + k32 * NVE * N + k1;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int s = 0; s < NVE; ++s) {
+            const double c = c4[e_coef(s, d) == 4 ? 0 : e_coef(s, d)];
+            const double2 x = v[e_in(s, d)];
+            __stcs(reinterpret_cast<double2*>(fo + d * OUTV + s * N),
+                   e_coef(s, d) == 4 ? make_double2(0.0, 0.0) : make_double2(c * x.x, c * x.y));
+          }
+      }
+    }
+  } else {
+    for (int i = tid; i < N3; i += G::THREADS) {
+      const int k1 = i % N, k32 = i / N;
+      const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+      double v[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) v[s] = qs[fld(s) * G::VS];
+      const long long ob = e * (long long)OUTV + k32 * NVE * N + k1;
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) __stcs(a.qavg + ob + s * N, v[s]);
+      if (a.favg) {
+        double* fo = a.favg + e * (long long)(3 * OUTV) + k32 * NVE * N + k1;
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+#pragma unroll
+          for (int s = 0; s < NVE; ++s)
+            __stcs(fo + d * OUTV + s * N, e_coef(s, d) == 4 ? 0.0 : c4[e_coef(s, d)] * v[e_in(s, d)]);
+      }
+    }
+  }
+  };
+  auto emit_faces = [&]() {
+  if (a.face_q || a.face_f) {
+    constexpr int FV = N * N * NVE;
+    for (int i = tid; i < 3 * N * N; i += G::THREADS) {
+      const int d = i / (N * N);
+      const int ab = i - d * N * N;
+      const int aa = ab / N, bb = ab - aa * N;
+      const int start = d == 0 ? aa * G::PL + bb * G::RS : d == 1 ? aa * G::PL + bb : aa * G::RS + bb;
+      const int stride = d == 0 ? 1 : d == 1 ? G::RS : G::PL;
+      double f0[NVE], f1[NVE];
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) {
+        const double* q0 = E + fld(s) * G::VS + start;
+        double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double x = q0[j * stride];
+          x0 = fma(kp.phi[0][j], x, x0);
+          x1 = fma(kp.phi[1][j], x, x1);
+        }
+        f0[s] = x0;
+        f1[s] = x1;
+      }
+      const long long fb = e * 6LL * FV + (2 * d) * FV + ab * NVE;
+      if (a.face_q) {
+#pragma unroll
+        for (int s = 0; s < NVE; ++s) {
+          __stcs(a.face_q + fb + s, f0[s]);
+          __stcs(a.face_q + fb + FV + s, f1[s]);
+        }
+      }
+      if (a.face_f) {
+#pragma unroll
+        for (int s = 0; s < NVE; ++s) {
+          double g0, g1;
+          if (d == 0) {
+            g0 = e_coef(s, 0) == 4 ? 0.0 : c4[e_coef(s, 0)] * f0[e_in(s, 0)];
+            g1 = e_coef(s, 0) == 4 ? 0.0 : c4[e_coef(s, 0)] * f1[e_in(s, 0)];
+          } else if (d == 1) {
+            g0 = e_coef(s, 1) == 4 ? 0.0 : c4[e_coef(s, 1)] * f0[e_in(s, 1)];
+            g1 = e_coef(s, 1) == 4 ? 0.0 : c4[e_coef(s, 1)] * f1[e_in(s, 1)];
+          } else {
+            g0 = e_coef(s, 2) == 4 ? 0.0 : c4[e_coef(s, 2)] * f0[e_in(s, 2)];
+            g1 = e_coef(s, 2) == 4 ? 0.0 : c4[e_coef(s, 2)] * f1[e_in(s, 2)];
+          }
+          __stcs(a.face_f + fb + s, g0);
+          __stcs(a.face_f + fb + FV + s, g1);
+        }
+      }
+    }
+  }
+  };
+  auto emit_state = [&]() {  // fused: u_next in q's layout from the nine fields
+    const int qs = kp.q_stride;
+    for (int i = tid; i < N3; i += G::THREADS) {
+      const int k1 = i % N, k32 = i / N;
+      const double* src = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
+      double* dst = a.u_next + e * (long long)(N3 * qs) + k32 * qs * N + k1;
+#pragma unroll
+      for (int s = 0; s < NVE; ++s) __stcs(dst + s * N, src[fld(s) * G::VS]);
+    }
+  };
 #pragma unroll 1
-  for (int o = N - 2; o >= 0; --o) {
-    const double co = kp.cf[o];
+  for (int o = N - 2; o >= (FUSED ? -1 : 0); --o) {
+    if (FUSED && o < 0) {  // faces of qavg, then the extra step overwrites the fields
+      emit_faces();
+      __syncthreads();
+    }
+    const double co = (!FUSED || o >= 0) ? kp.cf[o] : 1.0;
     const int tb = 15 - vb;  // TEMP base: 9 when vb = 6, 6 when vb = 9
     const double crho[3] = {c4[3], 0.0, 0.0};
     // phase V: velocity targets from stress sources, into TEMP
@@ -907,101 +1021,12 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
                  : "memory");
 
   TMB(2);
-  // ---- epilogue: qavg = the last iterate (fields 0..5 and vb..vb+2) -----------------------
-  auto fld = [&](int s) { return s < 6 ? s : vb + (s - 6); };
-  if constexpr (N % 2 == 0) {  // k1 pairs: 16-byte shared loads and global stores
-    for (int i = tid; i < N3 / 2; i += G::THREADS) {
-      const int k1 = 2 * (i % (N / 2)), k32 = i / (N / 2);
-      const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
-      double2 v[NVE];
-#pragma unroll
-      for (int s = 0; s < NVE; ++s) v[s] = *reinterpret_cast<const double2*>(qs + fld(s) * G::VS);
-      const long long ob = e * (long long)OUTV + k32 * NVE * N + k1;
-#pragma unroll
-      for (int s = 0; s < NVE; ++s) __stcs(reinterpret_cast<double2*>(a.qavg + ob + s * N), v[s]);
-      if (a.favg) {
-        double* fo = a.favg + e * (long long)(3 * OUTV) + k32 * NVE * N + k1;
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int s = 0; s < NVE; ++s) {
-            const double c = c4[e_coef(s, d) == 4 ? 0 : e_coef(s, d)];
-            const double2 x = v[e_in(s, d)];
-            __stcs(reinterpret_cast<double2*>(fo + d * OUTV + s * N),
-                   e_coef(s, d) == 4 ? make_double2(0.0, 0.0) : make_double2(c * x.x, c * x.y));
-          }
-      }
-    }
+  if (FUSED) {
+    emit_state();
   } else {
-    for (int i = tid; i < N3; i += G::THREADS) {
-      const int k1 = i % N, k32 = i / N;
-      const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
-      double v[NVE];
-#pragma unroll
-      for (int s = 0; s < NVE; ++s) v[s] = qs[fld(s) * G::VS];
-      const long long ob = e * (long long)OUTV + k32 * NVE * N + k1;
-#pragma unroll
-      for (int s = 0; s < NVE; ++s) __stcs(a.qavg + ob + s * N, v[s]);
-      if (a.favg) {
-        double* fo = a.favg + e * (long long)(3 * OUTV) + k32 * NVE * N + k1;
-#pragma unroll
-        for (int d = 0; d < 3; ++d)
-#pragma unroll
-          for (int s = 0; s < NVE; ++s)
-            __stcs(fo + d * OUTV + s * N, e_coef(s, d) == 4 ? 0.0 : c4[e_coef(s, d)] * v[e_in(s, d)]);
-      }
-    }
-  }
-  TMB(3);
-  if (a.face_q || a.face_f) {
-    constexpr int FV = N * N * NVE;
-    for (int i = tid; i < 3 * N * N; i += G::THREADS) {
-      const int d = i / (N * N);
-      const int ab = i - d * N * N;
-      const int aa = ab / N, bb = ab - aa * N;
-      const int start = d == 0 ? aa * G::PL + bb * G::RS : d == 1 ? aa * G::PL + bb : aa * G::RS + bb;
-      const int stride = d == 0 ? 1 : d == 1 ? G::RS : G::PL;
-      double f0[NVE], f1[NVE];
-#pragma unroll
-      for (int s = 0; s < NVE; ++s) {
-        const double* q0 = E + fld(s) * G::VS + start;
-        double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          const double x = q0[j * stride];
-          x0 = fma(kp.phi[0][j], x, x0);
-          x1 = fma(kp.phi[1][j], x, x1);
-        }
-        f0[s] = x0;
-        f1[s] = x1;
-      }
-      const long long fb = e * 6LL * FV + (2 * d) * FV + ab * NVE;
-      if (a.face_q) {
-#pragma unroll
-        for (int s = 0; s < NVE; ++s) {
-          __stcs(a.face_q + fb + s, f0[s]);
-          __stcs(a.face_q + fb + FV + s, f1[s]);
-        }
-      }
-      if (a.face_f) {
-#pragma unroll
-        for (int s = 0; s < NVE; ++s) {
-          double g0, g1;
-          if (d == 0) {
-            g0 = e_coef(s, 0) == 4 ? 0.0 : c4[e_coef(s, 0)] * f0[e_in(s, 0)];
-            g1 = e_coef(s, 0) == 4 ? 0.0 : c4[e_coef(s, 0)] * f1[e_in(s, 0)];
-          } else if (d == 1) {
-            g0 = e_coef(s, 1) == 4 ? 0.0 : c4[e_coef(s, 1)] * f0[e_in(s, 1)];
-            g1 = e_coef(s, 1) == 4 ? 0.0 : c4[e_coef(s, 1)] * f1[e_in(s, 1)];
-          } else {
-            g0 = e_coef(s, 2) == 4 ? 0.0 : c4[e_coef(s, 2)] * f0[e_in(s, 2)];
-            g1 = e_coef(s, 2) == 4 ? 0.0 : c4[e_coef(s, 2)] * f1[e_in(s, 2)];
-          }
-          __stcs(a.face_f + fb + s, g0);
-          __stcs(a.face_f + fb + FV + s, g1);
-        }
-      }
-    }
+    emit_qavg();
+    TMB(3);
+    emit_faces();
   }
 #ifdef ADERSTP_EXPT_TIMING
   __syncthreads();
@@ -1015,7 +1040,7 @@ cudaError_t launch_bip_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   using G = GeoB<N>;
   PassParams<N> kp;
   fill_pass_params(p, a, kp);
-  auto kern = stp_bip_kernel<N>;
+  auto kern = a.u_next ? stp_bip_kernel<N, true> : stp_bip_kernel<N, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err == cudaSuccess)
     err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
@@ -1050,6 +1075,12 @@ cudaError_t init_pass(const LaunchPlan& p) {
     buf[60 + h] = D[h * n + h];
   }
   return cudaMemcpyToSymbol(aderstp_kEO, buf, sizeof(buf), sizeof(double) * 80 * n);
+}
+
+bool bip_selected(const LaunchPlan& p, const BatchArgs& a) {
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  const bool vec_ok = (p.n % 2) || (al16(a.q) && al16(a.qavg) && al16(a.favg));
+  return vec_ok && (p.n == 9 || p.n == 10) && (p.pass_slots == 12 || (p.pass_slots == 0 && p.n >= 9));
 }
 
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
