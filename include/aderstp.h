@@ -176,6 +176,52 @@ int aderstp_run_simulation(const aderstp_plan* plan, const aderstp_mesh* mesh, d
                            const double* par, double cfl, double t_end, double max_wavespeed,
                            int64_t* steps, double* t_final, void* stream);
 
+/* ---- the time loop over several GPUs: z-slabs of the mesh, one per rank -------------------
+ * Rank r owns the layers [z0, z0 + nz) (elements (iz - z0) e^2 + iy e + ix of its arrays).  The
+ * corrector reads the predictor faces of the two neighbouring slabs straight from their memory
+ * (peer pointers over NVLink: aderstp_ipc_handle / aderstp_ipc_open), inside the same kernel
+ * that applies them -- there is no separate halo copy.  With one slab (nz = e) the halos are
+ * unused and everything equals aderstp_correct_batch / aderstp_run_simulation. */
+typedef struct aderstp_slab {
+  int z0;
+  int nz;
+} aderstp_slab;
+
+typedef struct aderstp_halo {
+  const double* face_q; /* the neighbouring slab's face_q / face_f (its predictor outputs)        */
+  const double* face_f;
+  const double* par;    /* its per-element material (elastic kinds: per-face smax), else NULL     */
+  int z_base;           /* its first layer                                                        */
+} aderstp_halo;
+
+int aderstp_correct_slab(const aderstp_plan* plan, const aderstp_mesh* mesh, const aderstp_slab* slab,
+                         double* u, const double* par, const double* qavg, const double* face_q,
+                         const double* face_f, const aderstp_halo* lo, const aderstp_halo* hi,
+                         double max_wavespeed, void* stream);
+
+/* Host synchronisation between the ranks, called twice per step: after the predictor (the faces
+ * of every slab are complete) and after the corrector (nobody reads them any more).  It receives
+ * this rank's flag (non-zero = non-finite state) and returns the maximum over all ranks. */
+typedef int (*aderstp_rank_sync_fn)(void* ctx, int local_flag);
+
+/* run_simulation on this rank's slab: face_q / face_f are this rank's predictor output buffers
+ * (n_local x 6 x n^2 m doubles each, shared with the neighbours), lo / hi the neighbours' (peer
+ * pointers).  max_wavespeed > 0 is the GLOBAL maximum wave speed (same dt on every rank); the
+ * elastic corrector uses the per-face max(cp) from par and the halos' par. */
+int aderstp_run_simulation_slab(const aderstp_plan* plan, const aderstp_mesh* mesh, const aderstp_slab* slab,
+                                double* u, const double* par, double* face_q, double* face_f,
+                                const aderstp_halo* lo, const aderstp_halo* hi, double cfl, double t_end,
+                                double max_wavespeed, aderstp_rank_sync_fn sync, void* ctx, int64_t* steps,
+                                double* t_final, void* stream);
+
+/* device buffers shareable with other processes (cudaMalloc'd, so their IPC handle addresses
+ * the buffer itself) and CUDA IPC handles (64 bytes) */
+int aderstp_device_alloc(size_t bytes, void** ptr);
+int aderstp_device_free(void* ptr);
+int aderstp_ipc_handle(const void* ptr, void* handle64);
+int aderstp_ipc_open(const void* handle64, void** ptr);
+int aderstp_ipc_close(void* ptr);
+
 /* ---- host helpers -------------------------------------------------------------------- */
 int aderstp_basis(int order, double* nodes, double* weights, double* d, double* face_left,
                   double* face_right);

@@ -62,15 +62,25 @@ struct BatchArgs {
 };
 
 // corrector.cu: GPU corrector step (proj/src/solver.cpp:184-311) and time-loop helpers
+// Predictor outputs of a z-slab of the mesh held elsewhere (a neighbouring rank's buffers, read
+// through peer memory over NVLink), element (iz - z_base mod e) * e^2 + iy * e + ix.
+struct HaloRef {
+  const double* face_q = nullptr;
+  const double* face_f = nullptr;
+  const double* par = nullptr;
+  int z_base = 0;
+};
 struct CorrArgs {
-  double* u;             // mesh state, the plan's q layout, element (iz*e + iy)*e + ix
+  double* u;             // mesh state of the slab, the plan's q layout, local element (iz-z0)*e^2 + iy*e + ix
   const double* par;     // per-element material (elastic)
-  const double* qavg;
+  const double* qavg;    // null: surface terms only (the fused predictor applied the volume term)
   const double* face_q;
   const double* face_f;
   int e;                 // elements per dimension (periodic)
   double inv_h;          // 1 / h
   double smax;           // scaled max wave speed, < 0: elastic per-face max(cp) / h
+  int z0 = 0, nz = 0;    // this slab: layers [z0, z0 + nz); nz = 0 means the whole mesh
+  HaloRef lo, hi;        // the slabs below / above (used for z-neighbours outside [z0, z0 + nz))
 };
 cudaError_t launch_correct(const LaunchPlan& p, const CorrArgs& a, cudaStream_t stream);
 cudaError_t launch_scale_par(const double* in, int par_kind, double s, long long n, double* out,

@@ -489,6 +489,194 @@ int aderstp_correct_batch(const aderstp_plan* p, const aderstp_mesh* mesh, doubl
   return ADERSTP_OK;
 }
 
+namespace {
+
+// The time loop of run_simulation (src/solver.cpp:313-359) on the slab [z0, z0 + nz): predictor on
+// ScaledPde(1/h), a rank sync, the corrector (z-neighbours outside the slab from lo / hi), a rank
+// sync with the stability flag.  face_q / face_f: caller buffers (n_local x 6 x n^2 m).
+int run_loop(const aderstp_plan* p, const aderstp_mesh* mesh, int z0, int nz, double* u, const double* par,
+             double* face_q, double* face_f, const aderstp::HaloRef& lo, const aderstp::HaloRef& hi, double cfl,
+             double t_end, double smax, bool per_face_smax, aderstp_rank_sync_fn sync, void* ctx,
+             int64_t* steps, double* t_final, cudaStream_t st) {
+  const bool elastic = p->lp.kind == ADERSTP_PDE_ELASTIC;
+  const int e = mesh->elements_per_dim;
+  const long long E = (long long)e * e * nz;
+  const int n = p->lp.n;
+  const double h = mesh->domain_len / e, s = 1.0 / h;
+  aderstp::LaunchPlan sp = p->lp;  // the predictor on ScaledPde(1/h)
+  if (!elastic)
+    for (int q = 0; q < aderstp::kMaxM; ++q)
+      for (int d = 0; d < 3; ++d)
+        for (int k = 0; k < aderstp::kMaxTerms; ++k) {
+          sp.tc[q][d][k] *= s;
+          sp.fc[q][d][k] *= s;
+        }
+  double *par_s = nullptr, *qavg = nullptr;
+  auto cleanup = [&]() {
+    if (par_s) cudaFree(par_s);
+    if (qavg) cudaFree(qavg);
+  };
+  cudaError_t err = cudaSuccess;
+  if (elastic) {
+    err = cudaMalloc(&par_s, sizeof(double) * 3 * (E > 0 ? E : 1));
+    if (err == cudaSuccess) err = aderstp::launch_scale_par(par, p->lp.par_kind, s, E, par_s, st);
+    sp.par_kind = ADERSTP_PAR_LAMBDA_MU_RHO;
+  }
+  aderstp::BatchArgs probe{u, elastic ? par_s : par, nullptr, nullptr, face_q, face_f, E, 1.0, 0.0};
+  probe.u_next = u;
+  const bool fused = aderstp::fused_supported(sp, probe);
+  if (err == cudaSuccess && !fused) err = cudaMalloc(&qavg, sizeof(double) * (size_t)n * n * n * p->lp.out_stride * (E > 0 ? E : 1));
+  if (err != cudaSuccess) {
+    cleanup();
+    return cuda_fail(err, "run_simulation setup");
+  }
+  const double dt0 = smax > 0.0 ? cfl * h / (3.0 * smax * (2.0 * n - 1.0)) : std::numeric_limits<double>::infinity();
+  double t = 0.0;
+  int64_t done = 0;
+  int rc = ADERSTP_OK;
+  while (t < t_end - 1e-14 * std::max(1.0, t_end)) {
+    const double dt = std::min(dt0, t_end - t);
+    aderstp::BatchArgs ba{u, elastic ? par_s : par, fused ? nullptr : qavg, nullptr, face_q, face_f, E, dt, t};
+    if (fused) ba.u_next = u;
+    err = E > 0 ? aderstp::launch_stp(sp, ba, st) : cudaSuccess;
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) {
+      rc = cuda_fail(err, "run_simulation predictor");
+      break;
+    }
+    if (sync) sync(ctx, 0);  // every slab's faces are complete
+    aderstp::CorrArgs ca{u, par, fused ? nullptr : qavg, face_q, face_f, e, s, per_face_smax ? -1.0 : smax * s};
+    ca.z0 = z0;
+    ca.nz = nz;
+    ca.lo = lo;
+    ca.hi = hi;
+    err = E > 0 ? aderstp::launch_correct(p->lp, ca, st) : cudaSuccess;
+    unsigned int flags = 0;
+    if (err == cudaSuccess) err = cudaMemcpyAsync(&flags, p->lp.d_status, sizeof flags, cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    if (err != cudaSuccess) {
+      rc = cuda_fail(err, "run_simulation corrector");
+      break;
+    }
+    if (flags) {
+      cudaMemsetAsync(p->lp.d_status, 0, sizeof flags, st);
+      cudaStreamSynchronize(st);
+    }
+    const int any = sync ? sync(ctx, flags ? (int)flags : 0) : (int)flags;  // nobody reads the faces any more
+    if (any) {
+      rc = fail((any & 2) ? ADERSTP_ERR_MATERIAL : ADERSTP_ERR_NONFINITE,
+                (any & 2) ? "elastic_pde: need rho > 0, mu >= 0, lambda + 2mu > 0"
+                          : "corrector_step: non-finite update (unstable)");
+      break;
+    }
+    t += dt;
+    ++done;
+  }
+  if (steps) *steps = done;
+  if (t_final) *t_final = t;
+  cleanup();
+  return rc;
+}
+
+aderstp::HaloRef halo_of(const aderstp_halo* h) {
+  aderstp::HaloRef r;
+  if (h) {
+    r.face_q = h->face_q;
+    r.face_f = h->face_f;
+    r.par = h->par;
+    r.z_base = h->z_base;
+  }
+  return r;
+}
+
+int validate_slab(const aderstp_mesh* mesh, const aderstp_slab* slab, const aderstp_halo* lo,
+                  const aderstp_halo* hi, bool elastic, const char* who) {
+  if (!slab) return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": null slab");
+  const int e = mesh->elements_per_dim;
+  if (slab->z0 < 0 || slab->nz < 1 || slab->z0 + slab->nz > e)
+    return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": slab outside the mesh");
+  if (slab->nz < e) {
+    if (!lo || !hi || !lo->face_q || !lo->face_f || !hi->face_q || !hi->face_f)
+      return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": a partial slab needs both halos");
+    if (elastic && (!lo->par || !hi->par))
+      return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": elastic halos need the neighbours' material");
+  }
+  return ADERSTP_OK;
+}
+
+}  // namespace
+
+int aderstp_correct_slab(const aderstp_plan* p, const aderstp_mesh* mesh, const aderstp_slab* slab, double* u,
+                         const double* par, const double* qavg, const double* face_q, const double* face_f,
+                         const aderstp_halo* lo, const aderstp_halo* hi, double max_wavespeed, void* stream) {
+  int rc = validate_mesh(p, mesh, u, par, "corrector_step");
+  if (rc == ADERSTP_OK) rc = validate_slab(mesh, slab, lo, hi, p->lp.kind == ADERSTP_PDE_ELASTIC, "corrector_step");
+  if (rc != ADERSTP_OK) return rc;
+  if (!qavg || !face_q || !face_f)
+    return fail(ADERSTP_ERR_INVALID_ARG, "corrector_step: one predictor output per element required");
+  if (p->lp.kind != ADERSTP_PDE_ELASTIC && !(max_wavespeed >= 0.0))
+    return fail(ADERSTP_ERR_INVALID_ARG, "corrector_step: max_wavespeed required for table PDEs");
+  const double inv_h = mesh->elements_per_dim / mesh->domain_len;
+  aderstp::CorrArgs a{u, par, qavg, face_q, face_f, mesh->elements_per_dim, inv_h,
+                      max_wavespeed >= 0.0 ? max_wavespeed * inv_h : -1.0};
+  a.z0 = slab->z0;
+  a.nz = slab->nz;
+  a.lo = halo_of(lo);
+  a.hi = halo_of(hi);
+  cudaError_t e = aderstp::launch_correct(p->lp, a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "correct_slab launch");
+  return ADERSTP_OK;
+}
+
+int aderstp_run_simulation_slab(const aderstp_plan* p, const aderstp_mesh* mesh, const aderstp_slab* slab,
+                                double* u, const double* par, double* face_q, double* face_f,
+                                const aderstp_halo* lo, const aderstp_halo* hi, double cfl, double t_end,
+                                double max_wavespeed, aderstp_rank_sync_fn sync, void* ctx, int64_t* steps,
+                                double* t_final, void* stream) {
+  if (steps) *steps = 0;
+  if (t_final) *t_final = 0.0;
+  int rc = validate_mesh(p, mesh, u, par, "run_simulation");
+  const bool elastic = p && p->lp.kind == ADERSTP_PDE_ELASTIC;
+  if (rc == ADERSTP_OK) rc = validate_slab(mesh, slab, lo, hi, elastic, "run_simulation");
+  if (rc != ADERSTP_OK) return rc;
+  if (!face_q || !face_f) return fail(ADERSTP_ERR_INVALID_ARG, "run_simulation: null face buffers");
+  if (!(cfl > 0.0) || !(t_end >= 0.0)) return fail(ADERSTP_ERR_INVALID_ARG, "run_simulation: bad cfl or t_end");
+  if (!(max_wavespeed > 0.0))
+    return fail(ADERSTP_ERR_INVALID_ARG, "run_simulation: the global max_wavespeed must be positive");
+  return run_loop(p, mesh, slab->z0, slab->nz, u, par, face_q, face_f, halo_of(lo), halo_of(hi), cfl, t_end,
+                  max_wavespeed, elastic, sync, ctx, steps, t_final, static_cast<cudaStream_t>(stream));
+}
+
+int aderstp_device_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return fail(ADERSTP_ERR_INVALID_ARG, "device_alloc: null pointer");
+  cudaError_t e = cudaMalloc(ptr, bytes ? bytes : 1);
+  return e == cudaSuccess ? ADERSTP_OK : cuda_fail(e, "device_alloc");
+}
+int aderstp_device_free(void* ptr) {
+  cudaError_t e = cudaFree(ptr);
+  return e == cudaSuccess ? ADERSTP_OK : cuda_fail(e, "device_free");
+}
+int aderstp_ipc_handle(const void* ptr, void* handle64) {
+  if (!ptr || !handle64) return fail(ADERSTP_ERR_INVALID_ARG, "ipc_handle: null argument");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, const_cast<void*>(ptr));
+  if (e != cudaSuccess) return cuda_fail(e, "ipc_handle");
+  static_assert(sizeof h == 64, "CUDA IPC handles are 64 bytes");
+  std::memcpy(handle64, &h, sizeof h);
+  return ADERSTP_OK;
+}
+int aderstp_ipc_open(const void* handle64, void** ptr) {
+  if (!handle64 || !ptr) return fail(ADERSTP_ERR_INVALID_ARG, "ipc_open: null argument");
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle64, sizeof h);
+  cudaError_t e = cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  return e == cudaSuccess ? ADERSTP_OK : cuda_fail(e, "ipc_open");
+}
+int aderstp_ipc_close(void* ptr) {
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  return e == cudaSuccess ? ADERSTP_OK : cuda_fail(e, "ipc_close");
+}
+
 int aderstp_run_simulation(const aderstp_plan* p, const aderstp_mesh* mesh, double* u, const double* par,
                            double cfl, double t_end, double max_wavespeed, int64_t* steps, double* t_final,
                            void* stream) {
@@ -503,90 +691,27 @@ int aderstp_run_simulation(const aderstp_plan* p, const aderstp_mesh* mesh, doub
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int e = mesh->elements_per_dim;
   const long long E = (long long)e * e * e;
-  const int n = p->lp.n, m = p->lp.m;
-  const double h = mesh->domain_len / e, s = 1.0 / h;
-
-  // the predictor on ScaledPde(1/h): table terms x s, elastic material (s lambda, s mu, rho / s)
-  aderstp::LaunchPlan sp = p->lp;
-  if (!elastic)
-    for (int q = 0; q < aderstp::kMaxM; ++q)
-      for (int d = 0; d < 3; ++d)
-        for (int k = 0; k < aderstp::kMaxTerms; ++k) {
-          sp.tc[q][d][k] *= s;
-          sp.fc[q][d][k] *= s;
-        }
-  double *par_s = nullptr, *qavg = nullptr, *faces = nullptr;
+  const size_t face = 6 * (size_t)p->lp.n * p->lp.n * p->lp.m;
+  double* faces = nullptr;
   unsigned long long* d_cp = nullptr;
-  auto cleanup = [&]() {
-    if (par_s) cudaFree(par_s);
-    if (qavg) cudaFree(qavg);
-    if (faces) cudaFree(faces);
-    if (d_cp) cudaFree(d_cp);
-  };
-  const size_t n3 = (size_t)n * n * n, face = 6 * (size_t)n * n * m;
-  cudaError_t err = cudaMalloc(&qavg, sizeof(double) * n3 * p->lp.out_stride * E);
-  if (err == cudaSuccess) err = cudaMalloc(&faces, sizeof(double) * 2 * face * E);
   double smax = max_wavespeed;
-  if (err == cudaSuccess && elastic) {
-    err = cudaMalloc(&par_s, sizeof(double) * 3 * E);
-    if (err == cudaSuccess) err = aderstp::launch_scale_par(par, p->lp.par_kind, s, E, par_s, st);
-    sp.par_kind = ADERSTP_PAR_LAMBDA_MU_RHO;
-    if (err == cudaSuccess && !(smax >= 0.0)) {
-      unsigned long long bits = 0;
-      err = cudaMalloc(&d_cp, sizeof bits);
-      if (err == cudaSuccess) err = aderstp::launch_max_cp(par, p->lp.par_kind, E, d_cp, st);
-      if (err == cudaSuccess) err = cudaMemcpyAsync(&bits, d_cp, sizeof bits, cudaMemcpyDeviceToHost, st);
-      if (err == cudaSuccess) err = cudaStreamSynchronize(st);
-      double v;
-      std::memcpy(&v, &bits, sizeof v);
-      smax = v;
-    }
-  }
-  if (err != cudaSuccess) {
-    cleanup();
-    return cuda_fail(err, "run_simulation setup");
-  }
-  // stable_dt (src/solver.cpp:170-174)
-  const double dt0 = smax > 0.0 ? cfl * h / (3.0 * smax * (2.0 * n - 1.0)) : std::numeric_limits<double>::infinity();
-  double* face_q = faces;
-  double* face_f = faces + face * E;
-  double t = 0.0;
-  int64_t done = 0;
-  rc = ADERSTP_OK;
-  // fused step where the predictor supports it: the predictor writes u + L(qavg) in place (one more
-  // Horner step with coefficient 1, the corrector's volume term) and the corrector adds only the
-  // surface terms; elsewhere qavg goes through HBM to the full corrector
-  aderstp::BatchArgs probe{u, elastic ? par_s : par, nullptr, nullptr, face_q, face_f, E, 1.0, 0.0};
-  probe.u_next = u;
-  const bool fused = aderstp::fused_supported(sp, probe);
-  while (t < t_end - 1e-14 * std::max(1.0, t_end)) {
-    const double dt = std::min(dt0, t_end - t);
-    aderstp::BatchArgs ba{u, elastic ? par_s : par, fused ? nullptr : qavg, nullptr, face_q, face_f, E, dt, t};
-    if (fused) ba.u_next = u;
-    err = aderstp::launch_stp(sp, ba, st);
-    aderstp::CorrArgs ca{u, par, fused ? nullptr : qavg, face_q, face_f, e, s,
-                         (elastic && max_wavespeed < 0.0) ? -1.0 : smax * s};
-    if (err == cudaSuccess) err = aderstp::launch_correct(p->lp, ca, st);
-    unsigned int flags = 0;
-    if (err == cudaSuccess) err = cudaMemcpyAsync(&flags, p->lp.d_status, sizeof flags, cudaMemcpyDeviceToHost, st);
+  cudaError_t err = cudaMalloc(&faces, sizeof(double) * 2 * face * E);
+  if (err == cudaSuccess && elastic && !(smax >= 0.0)) {  // the global max cp (stable_dt)
+    unsigned long long bits = 0;
+    err = cudaMalloc(&d_cp, sizeof bits);
+    if (err == cudaSuccess) err = aderstp::launch_max_cp(par, p->lp.par_kind, E, d_cp, st);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(&bits, d_cp, sizeof bits, cudaMemcpyDeviceToHost, st);
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
-    if (err != cudaSuccess) {
-      rc = cuda_fail(err, "run_simulation step");
-      break;
-    }
-    if (flags) {
-      cudaMemsetAsync(p->lp.d_status, 0, sizeof flags, st);
-      cudaStreamSynchronize(st);
-      rc = fail((flags & 2u) ? ADERSTP_ERR_MATERIAL : ADERSTP_ERR_NONFINITE,
-                (flags & 2u) ? "elastic_pde: need rho > 0, mu >= 0, lambda + 2mu > 0"
-                             : "corrector_step: non-finite update (unstable)");
-      break;
-    }
-    t += dt;
-    ++done;
+    std::memcpy(&smax, &bits, sizeof smax);
   }
-  if (steps) *steps = done;
-  if (t_final) *t_final = t;
-  cleanup();
+  if (err == cudaSuccess) {
+    const aderstp::HaloRef none;
+    rc = run_loop(p, mesh, 0, e, u, par, faces, faces + face * E, none, none, cfl, t_end, smax,
+                  elastic && max_wavespeed < 0.0, nullptr, nullptr, steps, t_final, st);
+  } else {
+    rc = cuda_fail(err, "run_simulation setup");
+  }
+  if (faces) cudaFree(faces);
+  if (d_cp) cudaFree(d_cp);
   return rc;
 }

@@ -71,24 +71,17 @@ __device__ __forceinline__ Material material(const double* pr, int par_kind) {
   return mt;
 }
 
-__device__ __forceinline__ long long wrap_index(int ix, int iy, int iz, int e) {  // Mesh::cell_index
-  ix = (ix % e + e) % e;
-  iy = (iy % e + e) % e;
-  iz = (iz % e + e) % e;
-  return ((long long)iz * e + iy) * e + ix;
-}
-
 constexpr int kCorrThreads = 512;
 
 // VOL = false: the volume term was already applied by the fused predictor (BatchArgs::u_next),
 // only the surface fluctuations remain.
 template <int N, bool ELASTIC, bool VOL>
-__global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, double* __restrict__ u,
-                                                      const double* __restrict__ par,
-                                                      const double* __restrict__ qavg,
-                                                      const double* __restrict__ face_q,
-                                                      const double* __restrict__ face_f,
-                                                      unsigned int* status) {
+__global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, CorrArgs ca, unsigned int* status) {
+  double* __restrict__ u = ca.u;
+  const double* __restrict__ par = ca.par;
+  const double* __restrict__ qavg = ca.qavg;
+  const double* __restrict__ face_q = ca.face_q;
+  const double* __restrict__ face_f = ca.face_f;
   constexpr int N2 = N * N, N3 = N * N * N;
   const int m = ELASTIC ? NVC : kp.m;
   extern __shared__ __align__(16) double smc[];
@@ -98,9 +91,27 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, do
   __shared__ double SC[2][N];      // sign * phi_side[j] / w_j
   __shared__ double SMAX[6];       // per face
   const int e = kp.e;
-  const long long c = blockIdx.x;
-  const int ix = (int)(c % e), iy = (int)((c / e) % e), iz = (int)(c / ((long long)e * e));
+  const long long c = blockIdx.x;  // element of this slab
+  const int ix = (int)(c % e), iy = (int)((c / e) % e), iz = ca.z0 + (int)(c / ((long long)e * e));
+  const int nz = ca.nz > 0 ? ca.nz : e;
   const int tid = threadIdx.x;
+  // the neighbour across face (d, step): local, or in the slab below / above (peer memory)
+  struct Nb {
+    const double* fq;
+    const double* ff;
+    const double* pr;
+    long long idx;
+  };
+  auto neighbour = [&](int d, int step) -> Nb {
+    const int ixn = ((ix + (d == 0 ? step : 0)) % e + e) % e;
+    const int iyn = ((iy + (d == 1 ? step : 0)) % e + e) % e;
+    const int izn = ((iz + (d == 2 ? step : 0)) % e + e) % e;
+    if (izn >= ca.z0 && izn < ca.z0 + nz)
+      return {face_q, face_f, par, ((long long)(izn - ca.z0) * e + iyn) * e + ixn};
+    const HaloRef& hr = step < 0 ? ca.lo : ca.hi;
+    const int lz = ((izn - hr.z_base) % e + e) % e;
+    return {hr.face_q, hr.face_f, hr.par, ((long long)lz * e + iyn) * e + ixn};
+  };
 
   Material mine;
   if (ELASTIC) {
@@ -117,9 +128,8 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, do
     const int d = tid >> 1, step = (tid & 1) ? 1 : -1;
     double smax = kp.smax;
     if (ELASTIC && smax < 0.0) {
-      const long long nb =
-          wrap_index(ix + (d == 0 ? step : 0), iy + (d == 1 ? step : 0), iz + (d == 2 ? step : 0), e);
-      smax = fmax(material(par + 3 * c, kp.par_kind).cp, material(par + 3 * nb, kp.par_kind).cp) * kp.inv_h;
+      const Nb nb = neighbour(d, step);
+      smax = fmax(material(par + 3 * c, kp.par_kind).cp, material(nb.pr + 3 * nb.idx, kp.par_kind).cp) * kp.inv_h;
     }
     SMAX[tid] = smax;
   }
@@ -150,10 +160,9 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, do
     for (int i = tid; i < 6 * FV; i += blockDim.x) {
       const int f = i / FV, r = i - f * FV;
       const int d = f >> 1, side = f & 1, step = side ? 1 : -1;
-      const long long nb =
-          wrap_index(ix + (d == 0 ? step : 0), iy + (d == 1 ? step : 0), iz + (d == 2 ? step : 0), e);
-      const double* tq = face_q + nb * 6LL * FV;
-      const double* tf = face_f + nb * 6LL * FV;
+      const Nb nb = neighbour(d, step);
+      const double* tq = nb.fq + nb.idx * 6LL * FV;
+      const double* tf = nb.ff + nb.idx * 6LL * FV;
       double q_plus, q_minus, f_plus, f_minus;
       if (side == 1) {
         q_plus = tq[(2 * d) * FV + r];
@@ -300,8 +309,8 @@ cudaError_t launch_correct_n(const LaunchPlan& p, const CorrArgs& a, cudaStream_
                       : (vol ? correct_kernel<N, false, true> : correct_kernel<N, false, false>);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
-  const long long cells = (long long)a.e * a.e * a.e;
-  kern<<<(unsigned)cells, kCorrThreads, smem, stream>>>(kp, a.u, a.par, a.qavg, a.face_q, a.face_f, p.d_status);
+  const long long cells = (long long)a.e * a.e * (a.nz > 0 ? a.nz : a.e);
+  kern<<<(unsigned)cells, kCorrThreads, smem, stream>>>(kp, a, p.d_status);
   return cudaGetLastError();
 }
 

@@ -69,6 +69,18 @@ class _Mesh(ctypes.Structure):
     _fields_ = [("elements_per_dim", ctypes.c_int), ("domain_len", ctypes.c_double)]
 
 
+class _Slab(ctypes.Structure):
+    _fields_ = [("z0", ctypes.c_int), ("nz", ctypes.c_int)]
+
+
+class _Halo(ctypes.Structure):
+    _fields_ = [("face_q", ctypes.c_void_p), ("face_f", ctypes.c_void_p), ("par", ctypes.c_void_p),
+                ("z_base", ctypes.c_int)]
+
+
+_SyncFn = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int)
+
+
 def _load():
     if not os.path.exists(library_path):
         raise ImportError(
@@ -91,6 +103,17 @@ def _load():
     L.aderstp_correct_batch.argtypes = [_vp, ctypes.POINTER(_Mesh), _vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp]
     L.aderstp_run_simulation.argtypes = [_vp, ctypes.POINTER(_Mesh), _vp, _vp, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, ctypes.POINTER(_i64), _dp, _vp]
+    L.aderstp_correct_slab.argtypes = [_vp, ctypes.POINTER(_Mesh), ctypes.POINTER(_Slab), _vp, _vp, _vp, _vp, _vp,
+                                       ctypes.POINTER(_Halo), ctypes.POINTER(_Halo), ctypes.c_double, _vp]
+    L.aderstp_run_simulation_slab.argtypes = [_vp, ctypes.POINTER(_Mesh), ctypes.POINTER(_Slab), _vp, _vp, _vp, _vp,
+                                              ctypes.POINTER(_Halo), ctypes.POINTER(_Halo), ctypes.c_double,
+                                              ctypes.c_double, ctypes.c_double, _SyncFn, _vp,
+                                              ctypes.POINTER(_i64), _dp, _vp]
+    L.aderstp_device_alloc.argtypes = [ctypes.c_size_t, ctypes.POINTER(_vp)]
+    L.aderstp_device_free.argtypes = [_vp]
+    L.aderstp_ipc_handle.argtypes = [_vp, ctypes.c_char_p]
+    L.aderstp_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(_vp)]
+    L.aderstp_ipc_close.argtypes = [_vp]
     L.aderstp_basis.argtypes = [ctypes.c_int, _dp, _dp, _dp, _dp, _dp]
     L.aderstp_flop_count.restype = ctypes.c_double
     L.aderstp_flop_count.argtypes = [ctypes.c_int, ctypes.c_int]
@@ -389,6 +412,47 @@ class Plan:
             _check(rc)
         return rc == ADERSTP_OK, steps.value, t_final.value
 
+    # ---- the time loop on a z-slab of the mesh (one rank of a multi-GPU run) -----------------
+    @staticmethod
+    def _halo(h):
+        """h = (face_q, face_f, par, z_base): device pointers (ints) or tensors."""
+        if h is None:
+            return None
+        ptr = lambda t: None if t is None else (t if isinstance(t, int) else t.data_ptr())  # noqa: E731
+        return _Halo(ptr(h[0]), ptr(h[1]), ptr(h[2]), int(h[3]))
+
+    def correct_slab(self, u, elements_per_dim: int, slab, out: PredictorOutput, lo=None, hi=None, par=None,
+                     domain_len: float = 1.0, max_wavespeed: float | None = None, stream=None):
+        """corrector_step on the layers [z0, z0 + nz) (slab = (z0, nz)); z-neighbours outside the
+        slab come from the halos lo / hi = (face_q, face_f, par, z_base) of the adjacent slabs."""
+        mesh, sl = _Mesh(elements_per_dim, domain_len), _Slab(*slab)
+        hl, hh = self._halo(lo), self._halo(hi)
+        ptr = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        _check(lib.aderstp_correct_slab(self._h, ctypes.byref(mesh), ctypes.byref(sl), ptr(u), ptr(par),
+                                        ptr(out.qavg), ptr(out.face_q), ptr(out.face_f),
+                                        ctypes.byref(hl) if hl else None, ctypes.byref(hh) if hh else None,
+                                        self._smax(max_wavespeed), _stream_handle(stream)))
+
+    def run_simulation_slab(self, u, elements_per_dim: int, slab, face_q, face_f, t_end: float,
+                            max_wavespeed: float, lo=None, hi=None, par=None, cfl: float = 0.35,
+                            domain_len: float = 1.0, sync=None, stream=None):
+        """aderstp_run_simulation_slab: this rank's slab (z0, nz); face_q / face_f its predictor
+        output buffers (tensors or device pointers) shared with the neighbours; sync(flag) -> max
+        over ranks (shard.make_rank_sync()).  Returns (stable, steps, t_final)."""
+        mesh, sl = _Mesh(elements_per_dim, domain_len), _Slab(*slab)
+        hl, hh = self._halo(lo), self._halo(hi)
+        cb = _SyncFn(lambda ctx, flag: int(sync(int(flag)))) if sync is not None else _SyncFn(0)
+        steps, t_final = _i64(0), ctypes.c_double(0.0)
+        vp = lambda t: None if t is None else ctypes.c_void_p(t if isinstance(t, int) else t.data_ptr())  # noqa: E731
+        rc = lib.aderstp_run_simulation_slab(self._h, ctypes.byref(mesh), ctypes.byref(sl), vp(u), vp(par), vp(face_q),
+                                             vp(face_f), ctypes.byref(hl) if hl else None,
+                                             ctypes.byref(hh) if hh else None, cfl, t_end, float(max_wavespeed),
+                                             cb, None, ctypes.byref(steps), ctypes.byref(t_final),
+                                             _stream_handle(stream))
+        if rc not in (ADERSTP_OK, ADERSTP_ERR_NONFINITE):
+            _check(rc)
+        return rc == ADERSTP_OK, steps.value, t_final.value
+
     def status(self, stream=None):
         """Synchronise and raise on flagged inputs (validate_stp's non-finite / material checks)."""
         _check(lib.aderstp_plan_status(self._h, _stream_handle(stream)))
@@ -454,3 +518,30 @@ def convert_layout(order, quantities, n_elem, src_layout, src_stride, src, dst_l
                                       ctypes.c_void_p(src.data_ptr()), dst_layout, dst_stride,
                                       ctypes.c_void_p(dst.data_ptr()), _stream_handle(stream)))
     return dst
+
+
+# ---- shareable device buffers and CUDA IPC (multi-GPU time loop) --------------------------------
+def device_alloc(nbytes: int) -> int:
+    p = _vp()
+    _check(lib.aderstp_device_alloc(nbytes, ctypes.byref(p)))
+    return p.value
+
+
+def device_free(ptr: int):
+    _check(lib.aderstp_device_free(ctypes.c_void_p(ptr)))
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    _check(lib.aderstp_ipc_handle(ctypes.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    p = _vp()
+    _check(lib.aderstp_ipc_open(handle, ctypes.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int):
+    _check(lib.aderstp_ipc_close(ctypes.c_void_p(ptr)))

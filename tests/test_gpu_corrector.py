@@ -250,3 +250,73 @@ def test_corrector_rejects_point_sources(S):
     u = torch.zeros(8, plan.q_size, dtype=torch.float64, device="cuda")
     with pytest.raises(S.StpError):
         plan.run_simulation(u, 2, 0.1, max_wavespeed=0.0)
+
+
+# ---- the slab decomposition of the multi-GPU time loop (one slab per thread on one GPU) --------
+class _ThreadSync:
+    """sync(flag) -> max over the slab threads; doubles as the barrier (host side only: no kernel
+    waits on another slab)."""
+
+    def __init__(self, parties):
+        import threading
+        self.flags = [0] * parties
+        self.barrier = threading.Barrier(parties)
+        self.local = threading.local()
+
+    def bind(self, idx):
+        def sync(flag):
+            self.flags[idx] = int(flag)
+            self.barrier.wait()
+            out = max(self.flags)
+            self.barrier.wait()
+            return out
+        return sync
+
+
+@pytest.mark.parametrize("n,e,slabs", [(4, 6, 2), (4, 6, 3), (8, 4, 2), (10, 3, 3)])
+def test_slab_decomposition_matches_single_gpu(S, n, e, slabs):
+    """aderstp_run_simulation_slab on `slabs` z-slabs, each corrector reading its neighbours'
+    faces through halo pointers, reproduces the single-GPU run_simulation."""
+    import threading
+    from paper_2003_12787_b200.shard import slab_partition
+    E = e ** 3
+    q, par = S.generate(0, 99 + n, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
+    p = par.cpu().numpy()
+    mu = p[:, 0] * p[:, 2] * p[:, 2]
+    lam = p[:, 0] * p[:, 1] * p[:, 1] - 2.0 * mu
+    cp_max = float(np.sqrt((lam + 2.0 * mu) / p[:, 0]).max())
+    dt = 0.35 * (1.0 / e) / (3.0 * cp_max * (2 * n - 1))
+    t_end = 3.5 * dt
+    u_ref = q.clone()
+    ok, steps_ref, _ = plan.run_simulation(u_ref, e, t_end, par=par, cfl=0.35)
+    assert ok and steps_ref == 4
+    parts = [slab_partition(e, slabs, r) for r in range(slabs)]
+    us, pars, fqs, ffs = [], [], [], []
+    for z0, nz in parts:
+        a, b = z0 * e * e, (z0 + nz) * e * e
+        us.append(q[a:b].clone())
+        pars.append(par[a:b].contiguous())
+        fqs.append(torch.empty(b - a, 6, plan.face_size, dtype=torch.float64, device="cuda"))
+        ffs.append(torch.empty_like(fqs[-1]))
+    halo = lambda r: (fqs[r], ffs[r], pars[r], parts[r][0])  # noqa: E731
+    sync = _ThreadSync(slabs)
+    results = [None] * slabs
+    torch.cuda.synchronize()
+
+    def work(r):
+        stream = torch.cuda.Stream()
+        results[r] = plan.run_simulation_slab(us[r], e, parts[r], fqs[r], ffs[r], t_end, cp_max,
+                                              lo=halo((r - 1) % slabs), hi=halo((r + 1) % slabs), par=pars[r],
+                                              cfl=0.35, sync=sync.bind(r), stream=stream)
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(slabs)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    torch.cuda.synchronize()
+    assert all(r is not None and r[0] and r[1] == steps_ref for r in results), results
+    got = torch.cat(us).cpu().numpy()
+    worst = O.per_element_rel_diff(u_ref.cpu().numpy(), got)
+    assert worst <= 1e-12, worst

@@ -83,3 +83,39 @@ def test_two_rank_gloo_matches_single_process():
     want = float(out.qavg.sum() + out.face_f.sum())
     assert abs(checksum - want) <= 1e-12 * max(1.0, abs(want))
     assert slowest == 2.0
+
+
+def _slab_worker(rank, world, port, out):
+    import torch.distributed as dist
+    from paper_2003_12787_b200.shard import make_rank_sync, slab_neighbours, slab_partition
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        sync = make_rank_sync()
+        # the stability flag is the max over ranks: rank 1 reports non-finite in round 2
+        flags = [sync(0), sync(3 if rank == 1 else 0), sync(0)]
+        out.put((rank, slab_partition(7, world, rank), slab_neighbours(rank, world), flags))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_partition_and_rank_sync_gloo():
+    """The multi-GPU time loop's host logic (paper_2003_12787_b200/timeloop.py): z-slabs cover
+    the mesh exactly once, periodic neighbours, and the per-step rank sync is a max over ranks."""
+    import multiprocessing as mp
+    from paper_2003_12787_b200.shard import slab_partition
+    world = 2
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_slab_worker, args=(r, world, port, out)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = sorted(out.get(timeout=120) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert res[0][1] == (0, 4) and res[1][1] == (4, 3)
+    assert res[0][2] == (1, 1) and res[1][2] == (0, 0)
+    assert res[0][3] == [0, 3, 0] and res[1][3] == [0, 3, 0]
+    layers = [slab_partition(10, 4, r) for r in range(4)]
+    assert [z for z0, nz in layers for z in range(z0, z0 + nz)] == list(range(10))
