@@ -160,6 +160,11 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     lp.force_generic = (env && env[0] == '1') ? 1 : 0;
     const char* nd = std::getenv("ADERSTP_NO_DMMA8");
     lp.no_dmma8 = (nd && nd[0] == '1') ? 1 : 0;
+    // L2 prefetch distance of the tensor-core kernels: one wave of SMs ahead (measured: C3 +5 %)
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const char* pf = std::getenv("ADERSTP_PREFETCH");
+    lp.dmma8_prefetch = pf ? std::atoi(pf) : sms;
     const char* pe = std::getenv("ADERSTP_PERSIST");
     lp.dmmap_persist = (pe && pe[0] == '1') ? 1 : 0;
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");

@@ -52,7 +52,16 @@ struct ParamsP {
   double phi[2][8];  // zero-padded phi(0), phi(1)
   double cf[8];      // cf[o] = dt^(o+1)/(o+1)! (Horner coefficients, stp_splitck.cpp:45,64)
   int check, par_kind, q_stride;
+  int prefetch;      // L2 prefetch distance in elements (0: off)
 };
+
+// L2 prefetch of [ptr, ptr + bytes) rounded out to 16-byte bounds (cp.async.bulk.prefetch.L2)
+__device__ __forceinline__ void prefetch_l2(const void* ptr, unsigned long long bytes) {
+  const unsigned long long a0 = reinterpret_cast<unsigned long long>(ptr) & ~15ull;
+  const unsigned long long a1 = (reinterpret_cast<unsigned long long>(ptr) + bytes + 15ull) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+}
+
 
 __constant__ int kRoleP[NWP] = {6, 7, 8, 4, -1, -2, 3, 5};
 __constant__ int kInP[NVP][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
@@ -247,6 +256,8 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
 #pragma unroll 1
   for (long long e = blockIdx.x; e < a.n_elem; e += stride) {
   TM2(0);
+  if (!PERSIST && kp.prefetch && tid == 0 && e + kp.prefetch < a.n_elem)
+    prefetch_l2(a.q + (e + kp.prefetch) * (long long)(N * N * N * kp.q_stride), 8ull * N * N * N * kp.q_stride);
   double c4[4];
   {
     const double p0 = a.par[3 * e], p1 = a.par[3 * e + 1], p2 = a.par[3 * e + 2];
@@ -508,6 +519,7 @@ cudaError_t launch_dmmap_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t
   kp.check = p.check;
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
+  kp.prefetch = p.dmma8_prefetch;
   {
     double c = a.dt;  // same operation sequence as proj/src/stp_splitck.cpp:45,64
     kp.cf[0] = c;

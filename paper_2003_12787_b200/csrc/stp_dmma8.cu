@@ -65,6 +65,7 @@ struct Params8 {
   int check;
   int par_kind;
   int q_stride;
+  int prefetch;  // element distance of the L2 prefetch (0: off)
 };
 
 // role of each warp: a single output quantity (0..8), or -1 / -2 for the normal-stress warps on
@@ -288,6 +289,17 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   const int col = phys(g, 2 * t);  // + k3*64: this lane's node pair within a quantity plane
   unsigned int flags = 0;
   TM3(0);
+  // L2 prefetch of the q of element e + prefetch (one wave of SMs ahead: CTAs start in order),
+  // issued first thing, so that CTA stages from L2 instead of HBM (cp.async.bulk.prefetch.L2)
+  if (kp.prefetch && tid == 0) {
+    const long long nx = e + kp.prefetch;
+    if (nx < a.n_elem) {
+      const unsigned bytes = PV * kp.q_stride * 8;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.q + nx * (long long)(PV * kp.q_stride)),
+                   "r"(bytes)
+                   : "memory");
+    }
+  }
 
   // ---- material (proj/src/pde.cpp:171-178) -------------------------------------------
   double c4[4];
@@ -498,6 +510,7 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   kp.check = p.check;
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
+  kp.prefetch = p.dmma8_prefetch;
   {
     double c = a.dt;  // same operation sequence as proj/src/stp_splitck.cpp:45,64
     kp.cf[0] = c;

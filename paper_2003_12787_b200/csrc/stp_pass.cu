@@ -211,7 +211,16 @@ struct PassParams {
   double phi[2][N];
   double cf[N];  // cf[o] = dt^(o+1)/(o+1)! (Horner coefficients, stp_splitck.cpp:45,64)
   int check, par_kind, q_stride;
+  int prefetch;  // L2 prefetch distance in elements (0: off)
 };
+
+// L2 prefetch of [ptr, ptr + bytes) rounded out to 16-byte bounds (cp.async.bulk.prefetch.L2)
+__device__ __forceinline__ void prefetch_l2(const void* ptr, unsigned long long bytes) {
+  const unsigned long long a0 = reinterpret_cast<unsigned long long>(ptr) & ~15ull;
+  const unsigned long long a1 = (reinterpret_cast<unsigned long long>(ptr) + bytes + 15ull) & ~15ull;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a0), "r"((unsigned)(a1 - a0)) : "memory");
+}
+
 
 template <int N>
 void fill_pass_params(const LaunchPlan& p, const BatchArgs& a, PassParams<N>& kp) {
@@ -228,6 +237,7 @@ void fill_pass_params(const LaunchPlan& p, const BatchArgs& a, PassParams<N>& kp
   kp.check = p.check;
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
+  kp.prefetch = p.dmma8_prefetch;
 }
 
 // Node-wise epilogue helpers: the elastic flux F_d(q)_s = coef(s,d) q[in(s,d)] with
@@ -696,6 +706,8 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   const int xline = N == 9 ? kXPerm9[line < 81 ? line : 0] : line;  // x passes: permuted line
   const int lax = xline / N, lbx = xline - lax * N;
 
+  if (kp.prefetch && tid == 0 && e + kp.prefetch < a.n_elem)
+    prefetch_l2(a.q + (e + kp.prefetch) * (long long)(N3 * kp.q_stride), 8ull * N3 * kp.q_stride);
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&tmem_base_s)),
