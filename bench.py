@@ -141,6 +141,15 @@ def dist_setup():
     return world, rank, local
 
 
+def load_ncu_field(cfg_name, key):
+    """A field of the committed ncu summary (profiles/ncu_summary.json) for this config."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get(cfg_name, {}).get(key)
+    except Exception:
+        return None
+
+
 def load_traffic(cfg_name, elements_per_launch):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the STP kernel, from the
     committed ncu --set full capture (profiles/ncu_summary.json, measured per element and scaled
@@ -314,7 +323,7 @@ def measure_e2e(S, plan, cfg, world, rank, dt, steps):
                 api="aderstp_predict_batch_host (pinned host buffers, copies pipelined on 3 streams)")
 
 
-def cpu_reference_run(cfg, sample, reps=3, threads=None):
+def cpu_reference_run(cfg, sample, reps=3, threads=None, single_core=False):
     """The reference's own CPU path (oracle/_ref) on `sample` elements: best of reps, faster of
     splitck / splitck_aosoa.  Falls back to our C port when _ref is absent."""
     import oracle as O
@@ -342,9 +351,16 @@ def cpu_reference_run(cfg, sample, reps=3, threads=None):
             orc.stp(n, 9, q, dt, par=lmr, threads=threads)
             best = min(best, time.perf_counter() - t0)
         variant_used, lib = "oracle/stp_oracle.c", "libstp_oracle.so"
-    return dict(value=sample / best, unit=UNIT, cores=threads, kind=kind,
-                sample=f"{sample} elements of {cfg['desc'].split(':')[0]}, best of {reps} reps, "
-                       f"variant {variant_used} ({lib}), {threads} threads, predict loop only")
+    out = dict(value=sample / best, unit=UNIT, cores=threads, kind=kind,
+               sample=f"{sample} elements of {cfg['desc'].split(':')[0]}, best of {reps} reps, "
+                      f"variant {variant_used} ({lib}), {threads} threads, predict loop only")
+    if single_core and O.reference_available() and threads > 1:  # also report 1 core
+        one = max(64, sample // threads)
+        r1 = min(ref.stp(n, 9, q[:one], dt, par=lmr[:one], variant=variant_used, threads=1).seconds
+                 for _ in range(reps))
+        out["single_core_value"] = one / r1
+        out["single_core_sample"] = f"{one} elements, 1 thread, variant {variant_used}"
+    return out
 
 
 def run_reference_arm(args):
@@ -417,8 +433,13 @@ def main():
     total = cfg["elems"] if cfg.get("strong") else world * cfg["elems"]
     value = total / (ms * 1e-3)
     per_gpu = value / world
-    roofline = roofline_of(S, n, per_gpu, res["elements_per_launch"],
-                           load_traffic("c3" if args.config == "c5" else args.config, res["elements_per_launch"]))
+    ncu_cfg = "c3" if args.config == "c5" else args.config
+    roofline = roofline_of(S, n, per_gpu, res["elements_per_launch"], load_traffic(ncu_cfg, res["elements_per_launch"]))
+    # physical pipe utilisation of the same kernel (ncu, profiles/ncu_summary.json): the elastic
+    # kernels do ~2/3 of the algorithmic FLOPs (sparse flux), so this is the truth beside `frac`
+    roofline["ncu_fp64_pipe_pct"] = load_ncu_field(ncu_cfg, "fp64_pipe_pct")
+    roofline["ncu_dmma_pipe_pct"] = load_ncu_field(ncu_cfg, "dmma_pipe_pct")
+    roofline["ncu_lsu_wavefront_pct"] = load_ncu_field(ncu_cfg, "lsu_wavefront_pct")
 
     e2e = None
     if not args.no_e2e:
@@ -442,7 +463,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_run(cfg, 16384 if n <= 8 else 4096)
+        cpu = cpu_reference_run(cfg, 16384 if n <= 8 else 4096, single_core=True)
 
     if rank == 0:
         sh = res["shard"]
