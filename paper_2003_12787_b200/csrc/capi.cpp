@@ -165,12 +165,10 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const char* pf = std::getenv("ADERSTP_PREFETCH");
     lp.dmma8_prefetch = pf ? std::atoi(pf) : sms;
-    const char* pe = std::getenv("ADERSTP_PERSIST");
-    lp.dmmap_persist = (pe && pe[0] == '1') ? 1 : 0;
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");
     lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
     const char* ps = std::getenv("ADERSTP_PASS_SLOTS");
-    lp.pass_slots = !ps ? 0 : (ps[0] == '6') ? 6 : (ps[0] == '8') ? 8 : (ps[0] == '1' && ps[1] == '2') ? 12 : 0;
+    lp.pass_slots = !ps ? 0 : (ps[0] == '6') ? 6 : (ps[0] == '1' && ps[1] == '2') ? 12 : 0;
   }
   aderstp::make_host_basis(n, &lp.basis);
 

@@ -201,62 +201,24 @@ __device__ __forceinline__ void normal_step(double* P, const double* Q, int K0, 
   }
 }
 
-// mbarrier / bulk-copy helpers (TMA 1-D bulk copies, SASS UBLKCP)
-__device__ __forceinline__ void mbar_init(uint64_t* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)) : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-}
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          (unsigned)__cvta_generic_to_shared(dst)),
-      "l"(src), "r"(bytes), "r"(b)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
-  unsigned done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(b), "r"(phase)
-        : "memory");
-  }
-}
-
-// PERSIST: one CTA per SM slot loops over elements; element e+stride's input is prefetched
-// into a raw shared buffer by a TMA bulk copy (mbarrier-tracked) while element e computes.
-template <int N, bool PERSIST, bool FUSED = false>
+// FUSED: the time-loop mode (BatchArgs::u_next), see stp_dmma8.cu.
+template <int N, bool FUSED = false>
 __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsigned int* status) {
   using G = GeoP<N>;
   constexpr int PV = G::PV, FACE = G::FACE;
   extern __shared__ __align__(16) double smq[];
   double* P = smq;              // Horner iterate r; qavg at the end
   double* Q = smq + NVP * PV;   // q
-  double* RAW = smq + 2 * NVP * PV;                                     // PERSIST: q of the next element
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(RAW + N * N * N * kp.q_stride);
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
   const int col = physp(g, 2 * t);
   unsigned int flags = 0;
   const double dt = a.dt;
-  const long long stride = PERSIST ? gridDim.x : a.n_elem;
-  const unsigned raw_bytes = N * N * N * kp.q_stride * 8;
-  unsigned phase = 0;
-  if (PERSIST && tid == 0) {
-    mbar_init(mbar);
-    if (blockIdx.x < a.n_elem) bulk_load(RAW, a.q + (long long)blockIdx.x * (N * N * N * kp.q_stride), raw_bytes, mbar);
-  }
-  if (PERSIST) __syncthreads();
-
-#pragma unroll 1
-  for (long long e = blockIdx.x; e < a.n_elem; e += stride) {
+  {
+  const long long e = blockIdx.x;
   TM2(0);
-  if (!PERSIST && kp.prefetch && tid == 0 && e + kp.prefetch < a.n_elem)
+  if (kp.prefetch && tid == 0 && e + kp.prefetch < a.n_elem)
     prefetch_l2(a.q + (e + kp.prefetch) * (long long)(N * N * N * kp.q_stride), 8ull * N * N * N * kp.q_stride);
   double c4[4];
   {
@@ -281,10 +243,9 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   // ---- stage q into the padded planes (padding = 0): Q = q, P = c_(n-1) q -----------------
   // (s, k3, k2 < 8, k1-pair < 4) positions, IT per thread; every load is issued before the
   // first shared store so the DRAM latencies overlap
-  if (PERSIST) mbar_wait(mbar, phase);
   {
     const int qs = kp.q_stride;
-    const double* qe = PERSIST ? RAW : a.q + e * (long long)(N * N * N * qs);
+    const double* qe = a.q + e * (long long)(N * N * N * qs);
     constexpr int PAIRS = NVP * N * 32;
     constexpr int IT = (PAIRS + THREADSP - 1) / THREADSP;
     double v0[IT], v1[IT];
@@ -297,13 +258,8 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
       v0[it] = v1[it] = 0.0;
       if (i < PAIRS && k2 < N) {
         const double* src = qe + ((k3 * N + k2) * qs + s) * N;
-        if (PERSIST) {
-          if (k1 < N) v0[it] = src[k1];
-          if (k1 + 1 < N) v1[it] = src[k1 + 1];
-        } else {
-          if (k1 < N) v0[it] = __ldcs(src + k1);
-          if (k1 + 1 < N) v1[it] = __ldcs(src + k1 + 1);
-        }
+        if (k1 < N) v0[it] = __ldcs(src + k1);
+        if (k1 + 1 < N) v1[it] = __ldcs(src + k1 + 1);
       }
     }
 #pragma unroll
@@ -319,14 +275,6 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     }
   }
   __syncthreads();
-  if (PERSIST) {  // RAW has been consumed: prefetch the next element of this CTA
-    phase ^= 1;
-    if (tid == 0 && e + stride < a.n_elem) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      bulk_load(RAW, a.q + (e + stride) * (long long)(N * N * N * kp.q_stride), raw_bytes, mbar);
-    }
-  }
-
   TM2(1);
   const int role = kRoleP[warp];
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];
@@ -499,7 +447,6 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
     }
   }
-  __syncthreads();  // the next element overwrites p / qavg (thread 0 has waited for the bulk reads)
   }
   if (kp.check && flags) atomicOr(status, flags);
   TM2(5);
@@ -528,27 +475,15 @@ cudaError_t launch_dmmap_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t
       kp.cf[o] = c;
     }
   }
-  // the persistent TMA-prefetch variant needs 16-byte granular element blocks of q
-  const bool persist = !a.u_next && p.dmmap_persist && ((N * N * N * p.q_stride) % 2 == 0);
-  auto kern = a.u_next ? stp_dmmap_kernel<N, false, true>
-                       : persist ? stp_dmmap_kernel<N, true> : stp_dmmap_kernel<N, false>;
-  const int smem = G::SMEM + (persist ? N * N * N * p.q_stride * 8 + 16 : 0);
+  auto kern = a.u_next ? stp_dmmap_kernel<N, true> : stp_dmmap_kernel<N, false>;
+  const int smem = G::SMEM;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err == cudaSuccess)
     err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (err != cudaSuccess) return err;
   if (a.n_elem == 0) return cudaSuccess;
   if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
-  long long grid = a.n_elem;
-  if (persist) {
-    int per_sm = 0, dev = 0, sms = 0;
-    err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, THREADSP, smem);
-    if (err == cudaSuccess) err = cudaGetDevice(&dev);
-    if (err == cudaSuccess) err = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (err != cudaSuccess) return err;
-    const long long slots = (long long)(per_sm > 0 ? per_sm : 1) * sms;
-    if (grid > slots) grid = slots;
-  }
+  const long long grid = a.n_elem;
   kern<<<(unsigned)grid, THREADSP, smem, stream>>>(kp, a, p.d_status);
   return cudaGetLastError();
 }

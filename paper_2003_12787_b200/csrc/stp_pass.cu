@@ -57,15 +57,6 @@ __constant__ PassSlot kPass[3][6] = {
     {{6, 3, {0, 1, 2}, {0, 1, 1}}, {7, 1, {3}, {2}}, {8, 1, {4}, {2}}, {0, 1, {6}, {3}}, {3, 1, {7}, {3}}, {4, 1, {8}, {3}}},
     {{7, 3, {0, 1, 2}, {1, 0, 1}}, {6, 1, {3}, {2}}, {8, 1, {5}, {2}}, {3, 1, {6}, {3}}, {1, 1, {7}, {3}}, {5, 1, {8}, {3}}},
     {{8, 3, {0, 1, 2}, {1, 1, 0}}, {6, 1, {4}, {2}}, {7, 1, {5}, {2}}, {4, 1, {6}, {3}}, {5, 1, {7}, {3}}, {2, 1, {8}, {3}}}};
-// target-balanced variant: 8 single-target tasks per line and pass (the three normal-stress
-// targets each recompute the derivative of their common source; +1/3 fp64, no divergence)
-struct PassTask {
-  int8_t src, tgt, coef;
-};
-__constant__ PassTask kPass8[3][8] = {
-    {{6, 0, 0}, {6, 1, 1}, {6, 2, 1}, {7, 3, 2}, {8, 4, 2}, {0, 6, 3}, {3, 7, 3}, {4, 8, 3}},
-    {{7, 0, 1}, {7, 1, 0}, {7, 2, 1}, {6, 3, 2}, {8, 5, 2}, {3, 6, 3}, {1, 7, 3}, {5, 8, 3}},
-    {{8, 0, 1}, {8, 1, 1}, {8, 2, 0}, {6, 4, 2}, {7, 5, 2}, {4, 6, 3}, {5, 7, 3}, {2, 8, 3}}};
 // flux table for favg / face_f: F_d(q)_s = coef(s,d) q[in(s,d)], coef 4 = 0
 __constant__ int8_t kInE[NVE][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
                                     {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
@@ -80,7 +71,7 @@ struct Geo {
   static constexpr int VS = N * PL;                    // one quantity
   static constexpr int ES = NVE * VS;                  // one tensor
   static constexpr int LINES = N * N;
-  static constexpr int SLOTS = SL;                     // tasks per line and pass (6 or 8)
+  static constexpr int SLOTS = SL;                     // tasks per line and pass
   static constexpr int TASKS = SL * LINES;             // per element per pass
   static constexpr int EPB = N <= 2 ? 16 : N == 3 ? 8 : N <= 4 ? 4 : N <= 6 ? 2 : 1;
   static constexpr int THREADS = ((TASKS * EPB + 31) / 32) * 32;
@@ -160,26 +151,6 @@ template <int N, int D, int SL>
 __device__ __forceinline__ void line_pass(const double* P, double* T, int slot, int la, int lb,
                                           const double (&c4)[4]) {
   using G = Geo<N, SL>;
-  if (SL == 8) {
-    constexpr int ST8 = D == 0 ? 1 : D == 1 ? G::RS : G::PL;
-    const int start8 = D == 0 ? la * G::PL + lb * G::RS : D == 1 ? la * G::PL + lb : la * G::RS + lb;
-    const PassTask& pt = kPass8[D][slot];
-    double p8[N], o8[N];
-    const double* src8 = P + pt.src * G::VS + start8;
-#pragma unroll
-    for (int l = 0; l < N; ++l) p8[l] = src8[l * ST8];
-    eo_apply<N>(p8, o8);
-    const double c = pick4(c4, pt.coef);
-    double* dst = T + pt.tgt * G::VS + start8;
-    if (D == 0 || (D == 1 && pt.tgt == 5)) {
-#pragma unroll
-      for (int l = 0; l < N; ++l) dst[l * ST8] = c * o8[l];
-    } else {
-#pragma unroll
-      for (int l = 0; l < N; ++l) dst[l * ST8] = fma(c, o8[l], dst[l * ST8]);
-    }
-    return;
-  }
   constexpr int ST = D == 0 ? 1 : D == 1 ? G::RS : G::PL;
   const int start = D == 0 ? la * G::PL + lb * G::RS : D == 1 ? la * G::PL + lb : la * G::RS + lb;
   const PassSlot& ps = kPass[D][slot];
@@ -1096,7 +1067,7 @@ bool bip_selected(const LaunchPlan& p, const BatchArgs& a) {
 }
 
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
-  // bipartite + TMEM kernel: the default for nDof 9 and 10 (ADERSTP_PASS_SLOTS=6/8 select the
+  // bipartite + TMEM kernel: the default for nDof 9 and 10 (ADERSTP_PASS_SLOTS=6 selects the
   // older line-pass kernel)
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   const bool vec_ok = (p.n % 2) || (al16(a.q) && al16(a.qavg) && al16(a.favg));  // 16-byte accesses
@@ -1106,9 +1077,8 @@ cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t st
       case 10: return launch_bip_n<10>(p, a, stream);
     }
   }
-  const bool eight = p.pass_slots == 8;
 #define ADERSTP_PASS_CASE(NN) \
-  case NN: return eight ? launch_pass_n<NN, 8>(p, a, stream) : launch_pass_n<NN, 6>(p, a, stream);
+  case NN: return launch_pass_n<NN, 6>(p, a, stream);
   switch (p.n) {
     ADERSTP_PASS_CASE(2)
     ADERSTP_PASS_CASE(3)

@@ -76,18 +76,28 @@ def test_order8_kernels_parity(stp, oracle, monkeypatch, force_generic, q_stride
     assert max(worst.values()) <= TOL, worst
 
 
-@pytest.mark.parametrize("n", [2, 3, 5, 8, 9])
+@pytest.mark.parametrize("n", [2, 3, 5, 6, 8, 9, 10])
 def test_kernel_variants_agree(stp, oracle, monkeypatch, n):
-    """Every kernel family (DMMA nDof 8, line-pass, generic table) against the oracle."""
+    """Every kernel family against the oracle: the default dispatch (dmmap nDof 4-7, dmma8 nDof 8,
+    bip nDof 9-10, line-pass nDof 2-3), the line-pass kernel at every order (NO_DMMA8 / NO_DMMAP /
+    PASS_SLOTS=6), the bipartite kernel forced, the generic table kernel, and no L2 prefetch."""
     S = stp
     E = 19
     q, par = S.generate(0, 5 + n, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
     par_h = par.cpu().numpy()
     dt = O.cfl_dt(n, par_h[:, 1].max())
     ref = oracle.stp(n, 9, oracle.from_aosoa(n, 9, 9, q.cpu().numpy()), dt, par=oracle.material_lmr(par_h))
-    for env in ({"ADERSTP_NO_DMMA8": "1"}, {"ADERSTP_FORCE_GENERIC": "1"}):
-        for k in ("ADERSTP_NO_DMMA8", "ADERSTP_FORCE_GENERIC"):
-            monkeypatch.setenv(k, env.get(k, "0"))
+    keys = ("ADERSTP_NO_DMMA8", "ADERSTP_NO_DMMAP", "ADERSTP_PASS_SLOTS", "ADERSTP_FORCE_GENERIC", "ADERSTP_PREFETCH")
+    variants = [{}, {"ADERSTP_NO_DMMA8": "1", "ADERSTP_NO_DMMAP": "1", "ADERSTP_PASS_SLOTS": "6"},
+                {"ADERSTP_FORCE_GENERIC": "1"}, {"ADERSTP_PREFETCH": "0"}]
+    if n in (9, 10):
+        variants.append({"ADERSTP_PASS_SLOTS": "12"})
+    for env in variants:
+        for k in keys:
+            if k in env:
+                monkeypatch.setenv(k, env[k])
+            else:
+                monkeypatch.delenv(k, raising=False)
         plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
         out = plan.predict(q, dt, par=par)
         plan.status()
