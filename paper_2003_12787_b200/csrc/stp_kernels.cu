@@ -542,11 +542,57 @@ __global__ void convert_kernel(int n, int m, long long total, int src_layout, in
   }
 }
 
+// The same conversion by (k3, k2) rows: a row is n x src_stride doubles in one layout and
+// n x dst_stride in the other, both contiguous, so a block stages ROWS rows in shared memory with
+// coalesced loads and writes them back transposed with coalesced stores.
+constexpr int kConvRows = 16;
+__global__ void __launch_bounds__(256) convert_rows_kernel(int n, int m, long long rows, int src_layout, int src_stride,
+                                                          const double* __restrict__ src, int dst_layout,
+                                                          int dst_stride, double* __restrict__ dst) {
+  extern __shared__ double tile[];  // kConvRows x n x src_stride
+  const int srow = n * src_stride, drow = n * dst_stride;
+  for (long long r0 = (long long)blockIdx.x * kConvRows; r0 < rows; r0 += (long long)gridDim.x * kConvRows) {
+    const int nr = (int)(rows - r0 < kConvRows ? rows - r0 : kConvRows);
+    const double* s0 = src + r0 * srow;
+    for (int i = threadIdx.x; i < nr * srow; i += blockDim.x) tile[i] = s0[i];
+    __syncthreads();
+    double* d0 = dst + r0 * drow;
+    for (int i = threadIdx.x; i < nr * drow; i += blockDim.x) {
+      const int r = i / drow, j = i - r * drow;
+      int s, k1;
+      if (dst_layout == ADERSTP_LAYOUT_AOSOA) {
+        s = j / n;
+        k1 = j - s * n;
+      } else {
+        k1 = j / dst_stride;
+        s = j - k1 * dst_stride;
+      }
+      double v = 0.0;
+      if (s < m) v = tile[r * srow + (src_layout == ADERSTP_LAYOUT_AOSOA ? s * n + k1 : k1 * src_stride + s)];
+      d0[i] = v;
+    }
+    __syncthreads();
+  }
+}
+
 cudaError_t launch_convert(int n, int m, long long n_elem, int src_layout, int src_stride,
                            const double* src, int dst_layout, int dst_stride, double* dst,
                            cudaStream_t stream) {
   const long long total = n_elem * n * n * n * (long long)dst_stride;
   if (total == 0) return cudaSuccess;
+  if (src_layout != dst_layout) {  // AoS <-> AoSoA: row transposes through shared memory
+    const long long rows = n_elem * n * n;
+    long long blocks = (rows + kConvRows - 1) / kConvRows;
+    if (blocks > 148LL * 32) blocks = 148LL * 32;
+    const size_t smem = sizeof(double) * kConvRows * n * src_stride;
+    cudaError_t err = cudaSuccess;
+    if (smem > 48 * 1024)
+      err = cudaFuncSetAttribute(convert_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (err != cudaSuccess) return err;
+    convert_rows_kernel<<<(unsigned)blocks, 256, smem, stream>>>(n, m, rows, src_layout, src_stride, src, dst_layout,
+                                                                 dst_stride, dst);
+    return cudaGetLastError();
+  }
   const int threads = 256;
   long long blocks = (total + threads - 1) / threads;
   if (blocks > 148LL * 64) blocks = 148LL * 64;

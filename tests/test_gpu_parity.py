@@ -309,3 +309,56 @@ def test_dense_volume_operator_taylor_series(stp, oracle):
     out = plan.predict(torch.from_numpy(oracle.to_aosoa(n, 9, 9, qc[None])).cuda(), dt)
     got = oracle.from_aosoa(n, 9, 9, out.qavg.cpu().numpy())[0]
     assert O.rel_diff(want, got) < 1e-11
+
+
+@pytest.mark.parametrize("n", [3, 6, 8, 10])
+def test_aos_staged_path_matches_generic_and_oracle(stp, oracle, monkeypatch, n):
+    """The reference layout (AoS, m_pad 16) runs through device transposes and the tuned kernel;
+    the generic kernel (ADERSTP_FORCE_GENERIC) on the same AoS buffers and the oracle agree."""
+    S = stp
+    E = 11
+    q, par = S.generate(1, 77 + n, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
+    aos = torch.empty(E, n ** 3 * 16, dtype=torch.float64, device="cuda")
+    S.convert_layout(n, 9, E, S.LAYOUT_AOSOA, 9, q, S.LAYOUT_AOS, 16, aos)
+    par_h = par.cpu().numpy()
+    dt = O.cfl_dt(n, par_h[:, 1].max())
+    ref = oracle.stp(n, 9, oracle.from_aosoa(n, 9, 9, q.cpu().numpy()), dt, par=oracle.material_lmr(par_h))
+    for generic in ("0", "1"):
+        monkeypatch.setenv("ADERSTP_FORCE_GENERIC", generic)
+        plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOS, q_stride=16, out_stride=16, par_kind=S.PAR_RHO_CP_CS)
+        out = plan.predict(aos, dt, par=par)
+        plan.status()
+        worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOS, 16)
+        assert max(worst.values()) <= TOL, (generic, worst)
+        qa = out.qavg.cpu().numpy().reshape(E, n ** 3, 16)
+        assert not np.any(qa[:, :, 9:])
+
+
+def test_aos_plan_alone_in_a_fresh_process(stp):
+    """An AoS plan must upload the device constants of the kernels its staged path uses even
+    when no native-layout plan was ever created in the process."""
+    import subprocess
+    import sys
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle as O, paper_2003_12787_b200 as S
+orc = O.Oracle()
+worst = 0.0
+for n in (4, 8, 10):
+    E = 5
+    q, par = S.generate(0, 3 + n, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
+    qc = orc.from_aosoa(n, 9, 9, q.cpu().numpy())
+    aos = np.zeros((E, n ** 3, 16)); aos[:, :, :9] = qc.reshape(E, n ** 3, 9)
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOS, q_stride=16, out_stride=16, par_kind=S.PAR_RHO_CP_CS)
+    dt = O.cfl_dt(n, float(par[:, 1].max()))
+    out = plan.predict(torch.from_numpy(aos.reshape(E, -1)).cuda(), dt, par=par)
+    plan.status()
+    ref = orc.stp(n, 9, qc, dt, par=orc.material_lmr(par.cpu().numpy()))
+    got = out.qavg.cpu().numpy().reshape(E, n ** 3, 16)[:, :, :9].reshape(E, -1)
+    worst = max(worst, O.per_element_rel_diff(ref.qavg, got))
+print(worst)
+""" % _os.path.dirname(_os.path.dirname(_os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert float(r.stdout.strip().splitlines()[-1]) <= TOL
