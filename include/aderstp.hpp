@@ -17,6 +17,7 @@
 #ifndef ADERSTP_HPP
 #define ADERSTP_HPP
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <stdexcept>
@@ -143,6 +144,32 @@ class Predictor {
  private:
   aderstp_plan* plan_ = nullptr;
 };
+
+// Drop-in batch call over the reference's own containers: `cells` is a sequence of ElementTensor-
+// like objects (data() / size(), the AoS m_pad layout of the plan) and `outs` of PredictorOutput-
+// like objects (qavg, favg[3] tensors and face_q[6], face_f[6] vectors,
+// proj/include/ader/predictor.hpp:22-29).  One call replaces the per-element
+// predict(...) + extrapolate_faces(...) loop of run_simulation (proj/src/solver.cpp:334-345);
+// par: per-element material (elastic) or nullptr.
+template <class Cells, class Outs>
+void predict_elements(Predictor& gpu, const Cells& cells, const double* par, double dt, double t_start, Outs& outs) {
+  const size_t E = cells.size();
+  if (E == 0) return;
+  if (outs.size() != E) throw Error(ADERSTP_ERR_INVALID_ARG, "aderstp: one PredictorOutput per element required");
+  const size_t vol = cells[0].size(), face = outs[0].face_q[0].size();
+  std::vector<double> q(E * vol), qavg(E * vol), favg(3 * E * vol), fq(6 * E * face), ff(6 * E * face);
+  for (size_t e = 0; e < E; ++e) std::copy(cells[e].data(), cells[e].data() + vol, q.data() + e * vol);
+  gpu.predict(static_cast<int64_t>(E), q.data(), par, dt, t_start, qavg.data(), favg.data(), fq.data(), ff.data());
+  for (size_t e = 0; e < E; ++e) {
+    std::copy(qavg.data() + e * vol, qavg.data() + (e + 1) * vol, outs[e].qavg.data());
+    for (int d = 0; d < 3; ++d)
+      std::copy(favg.data() + (3 * e + d) * vol, favg.data() + (3 * e + d + 1) * vol, outs[e].favg[d].data());
+    for (int f = 0; f < 6; ++f) {
+      std::copy(fq.data() + (6 * e + f) * face, fq.data() + (6 * e + f + 1) * face, outs[e].face_q[f].data());
+      std::copy(ff.data() + (6 * e + f) * face, ff.data() + (6 * e + f + 1) * face, outs[e].face_f[f].data());
+    }
+  }
+}
 
 }  // namespace aderstp
 

@@ -115,6 +115,46 @@ int main() {
       worst = std::max(worst, run_case("paper demo (probed)", 6, 6, 9, gpu,
                                        [&](int) { return ader::paper_demo_pde(); }, {}, 0.01, 0.0));
     }
+    // aderstp::predict_elements straight on the reference's containers (ElementTensor in,
+    // PredictorOutput out), as run_simulation would call it
+    {
+      const int n = 8, E = 11;
+      const ader::LayoutSpec sp = ader::LayoutSpec::aos(n, 9, 8);
+      const ader::BasisOperators ops = ader::make_basis(n);
+      ader::SolverConfig cfg;
+      cfg.order = n;
+      ader::ScratchArena arena(ader::Variant::splitck, cfg);
+      std::vector<ader::ElementTensor> cells;
+      std::vector<ader::PredictorOutput> outs, ref;
+      std::vector<double> par;
+      ader::SplitMix64 rng(99);
+      for (int e = 0; e < E; ++e) {
+        cells.emplace_back(sp);
+        for (int k3 = 0; k3 < n; ++k3)
+          for (int k2 = 0; k2 < n; ++k2)
+            for (int k1 = 0; k1 < n; ++k1)
+              for (int s = 0; s < 9; ++s) cells.back().at(k3, k2, k1, s) = rng.next_symmetric();
+        par.insert(par.end(), {2.0 + 0.02 * e, 1.0, 1.2});
+        outs.emplace_back(sp);
+        ref.emplace_back(sp);
+        auto pde = ader::elastic_pde(par[3 * e], par[3 * e + 1], par[3 * e + 2]);
+        ader::predict(ader::Variant::splitck, cells.back(), *pde, 1e-3, ops, arena, ref.back(), 0.0);
+        ader::extrapolate_faces(ref.back(), ops);
+      }
+      aderstp::Predictor gpu(aderstp::elastic_config(n));
+      aderstp::predict_elements(gpu, cells, par.data(), 1e-3, 0.0, outs);
+      double w = 0.0;
+      for (int e = 0; e < E; ++e) {
+        w = std::max(w, rel_diff(ref[e].qavg.data(), outs[e].qavg.data(), sp.size()));
+        for (int d = 0; d < 3; ++d) w = std::max(w, rel_diff(ref[e].favg[d].data(), outs[e].favg[d].data(), sp.size()));
+        for (int f = 0; f < 6; ++f) {
+          w = std::max(w, rel_diff(ref[e].face_q[f].data(), outs[e].face_q[f].data(), outs[e].face_q[f].size()));
+          w = std::max(w, rel_diff(ref[e].face_f[f].data(), outs[e].face_f[f].data(), outs[e].face_f[f].size()));
+        }
+      }
+      std::printf("%-28s n=%d E=%d worst rel_diff %.3e\n", "predict_elements (containers)", n, E, w);
+      worst = std::max(worst, w);
+    }
     // the reference's validate_stp rejects non-finite input: so does the adapter
     {
       aderstp::Predictor gpu(aderstp::elastic_config(4));
