@@ -86,8 +86,11 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, Co
   const int m = ELASTIC ? NVC : kp.m;
   extern __shared__ __align__(16) double smc[];
   double* QA = smc;           // qavg [s][k3][k2][k1]
-  double* DL = smc + (VOL ? m * N3 : 0);  // fhat - f_self  [f][a][b][s]
-  __shared__ double Ds[N * N];     // D (per-thread row indices: shared, not the constant bank)
+  // quantity planes of QA padded by 8 doubles (different source fields of one warp's rows fall
+  // on different bank halves); rows of D padded to N + 1 (per-lane rows k1: conflict free)
+  constexpr int QP = N3 + 8, DR = N + 1;
+  double* DL = smc + (VOL ? m * QP : 0);  // fhat - f_self  [f][a][b][s]
+  __shared__ double Ds[N * DR];     // D (per-thread row indices: shared, not the constant bank)
   __shared__ double SC[2][N];      // sign * phi_side[j] / w_j
   __shared__ double SMAX[6];       // per face
   const int e = kp.e;
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, Co
 #pragma unroll
     for (int i = 0; i < 4; ++i) mine.c4[i] *= kp.inv_h;  // ScaledPde: flux x 1/h
   }
-  for (int i = tid; i < N * N; i += blockDim.x) Ds[i] = kp.d[i];
+  for (int i = tid; i < N * N; i += blockDim.x) Ds[(i / N) * DR + i % N] = kp.d[i];
   if (tid < 2 * N) {
     const int side = tid / N, j = tid - side * N;
     SC[side][j] = (side == 0 ? -1.0 : 1.0) * kp.phi[side][j] * kp.inv_w[j];
@@ -149,7 +152,7 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, Co
         s = j % os;
         node = j / os;
       }
-      if (s < m) QA[s * N3 + node] = qa[j];
+      if (s < m) QA[s * QP + node] = qa[j];
     }
   }
   // ---- face fluctuations (solver.cpp:218-226) --------------------------------------------
@@ -213,19 +216,19 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, Co
         const int cf = kCoefC[s][d];
         if (cf == 4) continue;
         const double cc = cf == 0 ? mine.c4[0] : cf == 1 ? mine.c4[1] : cf == 2 ? mine.c4[2] : mine.c4[3];
-        const double* src = QA + kInC[s][d] * N3 + base;
+        const double* src = QA + kInC[s][d] * QP + base;
         double acc = 0.0;
 #pragma unroll
-        for (int l = 0; l < N; ++l) acc = fma(Ds[kd * N + l], cc * src[l * stride], acc);
+        for (int l = 0; l < N; ++l) acc = fma(Ds[kd * DR + l], cc * src[l * stride], acc);
         vol += acc;
       } else {
         for (int k = 0; k < kp.n_terms; ++k) {
           const double cc = kp.tc[s][d][k] * kp.inv_h;
           if (cc == 0.0) continue;
-          const double* src = QA + kp.tr[s][d][k] * N3 + base;
+          const double* src = QA + kp.tr[s][d][k] * QP + base;
           double acc = 0.0;
 #pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(Ds[kd * N + l], cc * src[l * stride], acc);
+          for (int l = 0; l < N; ++l) acc = fma(Ds[kd * DR + l], cc * src[l * stride], acc);
           vol += acc;
         }
       }
@@ -304,7 +307,7 @@ cudaError_t launch_correct_n(const LaunchPlan& p, const CorrArgs& a, cudaStream_
   kp.smax = a.smax;
   const bool elastic = p.kind == ADERSTP_PDE_ELASTIC;
   const bool vol = a.qavg != nullptr;
-  const size_t smem = sizeof(double) * (size_t)p.m * ((vol ? N * N * N : 0) + 6 * N * N);
+  const size_t smem = sizeof(double) * (size_t)p.m * ((vol ? N * N * N + 8 : 0) + 6 * N * N);
   auto kern = elastic ? (vol ? correct_kernel<N, true, true> : correct_kernel<N, true, false>)
                       : (vol ? correct_kernel<N, false, true> : correct_kernel<N, false, false>);
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
