@@ -41,6 +41,7 @@ struct LaunchPlan {
   int force_generic = 0;             // env ADERSTP_FORCE_GENERIC=1: skip specialised kernels
   int no_dmma8 = 0;                  // env ADERSTP_NO_DMMA8=1: nDof 8 on the line-pass kernel
   int dmma8_prefetch = 0;            // L2 prefetch distance (elements) of q; env ADERSTP_PREFETCH, 0 = off
+  int aos_chunk = 0;                 // env ADERSTP_AOS_CHUNK: elements per chunk of the AoS staged path (tests)
   int pass_slots = 0;                // env ADERSTP_PASS_SLOTS: 6 = line-pass kernel, 12 = bipartite, 0 auto
   int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel
 };

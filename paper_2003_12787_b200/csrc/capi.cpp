@@ -183,6 +183,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     lp.dmma8_prefetch = pf ? std::atoi(pf) : sms;
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");
     lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
+    const char* ac = std::getenv("ADERSTP_AOS_CHUNK");
+    lp.aos_chunk = ac ? std::atoi(ac) : 0;
     const char* ps = std::getenv("ADERSTP_PASS_SLOTS");
     lp.pass_slots = !ps ? 0 : (ps[0] == '6') ? 6 : (ps[0] == '1' && ps[1] == '2') ? 12 : 0;
   }
@@ -330,7 +332,8 @@ cudaError_t predict_aos_staged(const aderstp_plan* plan, const aderstp::BatchArg
   const int n = lp.n;
   const size_t t9 = (size_t)n * n * n * 9;  // one AoSoA tensor (doubles)
   const size_t per = t9 * (a.favg ? 5 : 2);  // q, qavg (+ favg[3])
-  const long long chunk = std::max<long long>(1, std::min<long long>(a.n_elem, (8ll << 30) / (long long)(per * 8)));
+  long long chunk = std::max<long long>(1, std::min<long long>(a.n_elem, (8ll << 30) / (long long)(per * 8)));
+  if (lp.aos_chunk > 0) chunk = std::min<long long>(chunk, lp.aos_chunk);  // tests: force several chunks
   double* buf = nullptr;
   cudaError_t err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&buf), sizeof(double) * per * chunk, plan->pool, st);
   if (err != cudaSuccess) return err;

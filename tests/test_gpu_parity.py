@@ -323,8 +323,9 @@ def test_aos_staged_path_matches_generic_and_oracle(stp, oracle, monkeypatch, n)
     par_h = par.cpu().numpy()
     dt = O.cfl_dt(n, par_h[:, 1].max())
     ref = oracle.stp(n, 9, oracle.from_aosoa(n, 9, 9, q.cpu().numpy()), dt, par=oracle.material_lmr(par_h))
-    for generic in ("0", "1"):
+    for generic, chunk in (("0", "0"), ("0", "4"), ("1", "0")):  # "4": three chunks, the last ragged
         monkeypatch.setenv("ADERSTP_FORCE_GENERIC", generic)
+        monkeypatch.setenv("ADERSTP_AOS_CHUNK", chunk)
         plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOS, q_stride=16, out_stride=16, par_kind=S.PAR_RHO_CP_CS)
         out = plan.predict(aos, dt, par=par)
         plan.status()
