@@ -291,13 +291,13 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   TM3(0);
   // L2 prefetch of the q of element e + prefetch (one wave of SMs ahead: CTAs start in order),
   // issued first thing, so that CTA stages from L2 instead of HBM (cp.async.bulk.prefetch.L2)
-  if (kp.prefetch && tid == 0) {
+  // Only the 9 used quantity slots of each (k3, k2) row are fetched when q_stride > 9 (C3: 12),
+  // one 576-byte row per thread of the first two warps.
+  if (kp.prefetch && tid < 64) {
     const long long nx = e + kp.prefetch;
     if (nx < a.n_elem) {
-      const unsigned bytes = PV * kp.q_stride * 8;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.q + nx * (long long)(PV * kp.q_stride)),
-                   "r"(bytes)
-                   : "memory");
+      const double* row = a.q + nx * (long long)(PV * kp.q_stride) + tid * kp.q_stride * 8;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(row), "r"(NV * 8 * 8) : "memory");
     }
   }
 

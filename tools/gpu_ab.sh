@@ -1,7 +1,8 @@
-# A/B of an environment switch on the same box
+# A/B device throughput of two library builds (ADERSTP_LIB) on the same box
 exec > gpurun_out/ab.log 2>&1
-for rep in 1 2; do for v in 0 1; do for c in ${CONFIGS:-c2}; do
-  if [ $v = 1 ]; then export ADERSTP_COOP_FACES=1; else unset ADERSTP_COOP_FACES; fi
-  python bench.py --config $c --steps 10 --no-e2e --no-cpu-baseline --no-other-configs 2>&1 | tail -1 | \
-    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('v=$v $c', d['value'], d['roofline']['frac'])"
+for rep in 1 2; do
+for lib in tools/libaderstp_old.so paper_2003_12787_b200/libaderstp.so; do
+for c in ${CONFIGS:-c3}; do
+  ADERSTP_LIB=$PWD/$lib python bench.py --config $c --steps 20 --no-e2e --no-cpu-baseline --no-other-configs 2>&1 | tail -1 | \
+    python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$lib'.split('/')[-1], '$c', d['value'], d['roofline']['frac'])"
 done; done; done
