@@ -84,6 +84,8 @@ class Oracle:
         lib.orc_stp_batch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp, _dp,
                                       ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp, _dp, _dp,
                                       _dp, ctypes.c_int]
+        lib.orc_corrector_step.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int,
+                                           _dp, _dp, ctypes.c_double, _dp, _dp, _dp, _dp]
         lib.orc_canonical_to_aosoa.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp]
         lib.orc_aosoa_to_canonical.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp]
         self.lib = lib
@@ -123,6 +125,20 @@ class Oracle:
         if rc != 0:
             raise ValueError("oracle: invalid arguments (validate_stp semantics)")
         return Outputs(qavg, favg, fq, ff)
+
+    def corrector_step(self, n, m, e, domain_len, u, qavg, face_q, face_f, max_wavespeed, par=None,
+                       pde_kind=PDE_ELASTIC, args=None):
+        """orc_corrector_step (restates proj/src/solver.cpp:184-311); returns (u, finite)."""
+        u = np.ascontiguousarray(u, dtype=np.float64).copy()
+        par_a = None if par is None else np.ascontiguousarray(par, dtype=np.float64).reshape(3)
+        args_a = np.zeros(8) if args is None else np.ascontiguousarray(args, dtype=np.float64)
+        rc = self.lib.orc_corrector_step(n, m, e, domain_len, pde_kind, _ptr(par_a), _ptr(args_a), max_wavespeed,
+                                         _ptr(u), _ptr(np.ascontiguousarray(qavg, dtype=np.float64)),
+                                         _ptr(np.ascontiguousarray(face_q, dtype=np.float64)),
+                                         _ptr(np.ascontiguousarray(face_f, dtype=np.float64)))
+        if rc == -1:
+            raise ValueError("oracle: invalid corrector arguments")
+        return u, rc == 0
 
     def to_aosoa(self, n, m, qs, q):
         q = np.ascontiguousarray(q, dtype=np.float64)

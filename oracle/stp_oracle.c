@@ -417,6 +417,97 @@ int orc_stp_batch(int n, int m, long n_elem, const double* q, const double* par,
   return bad ? -1 : 0;
 }
 
+/* ------------------------------------------------------------ corrector ----- */
+
+int orc_corrector_step(int n, int m, int e, double domain_len, int pde_kind, const double* par3,
+                       const double* args, double max_wavespeed, double* u, const double* qavg,
+                       const double* face_q, const double* face_f) {
+  if (n < 1 || n > ORC_MAX_ORDER || m < 1 || m > ORC_MAX_Q || e < 1 || !(domain_len > 0.0)) return -1;
+  if (pde_kind == ORC_PDE_ELASTIC_SOURCE || pde_kind == ORC_PDE_SOURCE_ONLY) return -1;
+  if (pde_kind == ORC_PDE_ELASTIC && (m != 9 || !par3)) return -1;
+  orc_basis b;
+  b.n = n;
+  orc_make_basis(n, b.nodes, b.w, b.d, b.fl, b.fr);
+  orc_pde p;
+  memset(&p, 0, sizeof p);
+  p.kind = pde_kind;
+  p.m = m;
+  if (pde_kind == ORC_PDE_ELASTIC) {
+    p.lam = par3[0];
+    p.mu = par3[1];
+    p.inv_rho = 1.0 / par3[2];
+  }
+  if (pde_kind == ORC_PDE_ADVECTION || pde_kind == ORC_PDE_NCP_ADVECTION)
+    for (int i = 0; i < 3; ++i) p.v[i] = args[i];
+  const double h = domain_len / e, gs = 1.0 / h, smax = gs * max_wavespeed; /* ScaledPde (solver.cpp:111-156) */
+  const long nn = (long)n * n * n, vol = nn * m, face = (long)n * n * m;
+  const long cells = (long)e * e * e;
+  double* fw = (double*)malloc(sizeof(double) * vol);
+  double* gw = (double*)malloc(sizeof(double) * vol);
+  double* vv = (double*)malloc(sizeof(double) * vol);
+  double* fh = (double*)malloc(sizeof(double) * face);
+  double tmp[ORC_MAX_Q];
+  int bad = 0;
+  for (long c = 0; c < cells; ++c) {
+    const int ix = (int)(c % e), iy = (int)((c / e) % e), iz = (int)(c / ((long)e * e));
+    const double* qa = qavg + c * vol;
+    double* uc = u + c * vol;
+    /* volume: sum_d D_d F_d(qavg) + B_d (D_d qavg), flux and ncp scaled by 1/h */
+    memset(vv, 0, sizeof(double) * vol);
+    for (int d = 0; d < 3; ++d) {
+      for (long k = 0; k < nn; ++k) {
+        pde_flux(&p, qa + k * m, d, fw + k * m);
+        for (int s = 0; s < m; ++s) fw[k * m + s] *= gs;
+      }
+      derive(d, n, m, b.d, fw, vv, 1);
+      derive(d, n, m, b.d, qa, gw, 0);
+      for (long k = 0; k < nn; ++k) {
+        pde_ncp(&p, gw + k * m, d, tmp);
+        for (int s = 0; s < m; ++s) vv[k * m + s] += gs * tmp[s];
+      }
+    }
+    for (long i = 0; i < vol; ++i) uc[i] += vv[i];
+    /* surface (solver.cpp:211-250): plus side = the neighbour in +d */
+    for (int d = 0; d < 3; ++d)
+      for (int side = 0; side < 2; ++side) {
+        const int step = side == 0 ? -1 : 1;
+        const int nx = ((ix + (d == 0 ? step : 0)) % e + e) % e;
+        const int ny = ((iy + (d == 1 ? step : 0)) % e + e) % e;
+        const int nz = ((iz + (d == 2 ? step : 0)) % e + e) % e;
+        const long nb = ((long)nz * e + ny) * e + nx;
+        const double* mq = face_q + c * 6 * face;
+        const double* mf = face_f + c * 6 * face;
+        const double* tq = face_q + nb * 6 * face;
+        const double* tf = face_f + nb * 6 * face;
+        const double* q_plus = side == 1 ? tq + (2 * d) * face : mq + (2 * d) * face;
+        const double* q_minus = side == 1 ? mq + (2 * d + 1) * face : tq + (2 * d + 1) * face;
+        const double* f_plus = side == 1 ? tf + (2 * d) * face : mf + (2 * d) * face;
+        const double* f_minus = side == 1 ? mf + (2 * d + 1) * face : tf + (2 * d + 1) * face;
+        for (long i = 0; i < face; ++i)
+          fh[i] = 0.5 * (f_plus[i] + f_minus[i]) - 0.5 * smax * (q_minus[i] - q_plus[i]);
+        const double* fs = mf + (2 * d + side) * face;
+        const double* coeff = side == 0 ? b.fl : b.fr;
+        const double sign = side == 0 ? -1.0 : 1.0;
+        for (int a = 0; a < n; ++a)
+          for (int bb = 0; bb < n; ++bb)
+            for (int j = 0; j < n; ++j) {
+              const double scale = sign * coeff[j] * (1.0 / b.w[j]);
+              const long node = d == 0 ? ((long)a * n + bb) * n + j : d == 1 ? ((long)a * n + j) * n + bb
+                                                                            : ((long)j * n + a) * n + bb;
+              for (int s = 0; s < m; ++s)
+                uc[node * m + s] += scale * (fh[((long)a * n + bb) * m + s] - fs[((long)a * n + bb) * m + s]);
+            }
+      }
+    for (long i = 0; i < vol; ++i)
+      if (!isfinite(uc[i])) bad = 1;
+  }
+  free(fw);
+  free(gw);
+  free(vv);
+  free(fh);
+  return bad ? -2 : 0;
+}
+
 /* -------------------------------------------------------------- layouts ----- */
 
 void orc_canonical_to_aosoa(int n, int m, int qs, long n_elem, const double* src, double* dst) {

@@ -59,6 +59,17 @@ int orc_stp_batch(int n, int m, long n_elem, const double* q, const double* par,
                   const double* args, int pde_kind, double dt, double t_start, double* qavg,
                   double* favg, double* face_q, double* face_f, int n_threads);
 
+/* One corrector step (proj/src/solver.cpp:257-311, correct_cell :184-253) on a periodic e^3
+ * mesh of element size h = domain_len / e with ONE material / PDE for all elements (like the
+ * reference): u += V(qavg) on the 1/h-scaled PDE (apply_volume_once,
+ * predictor_common.cpp:243-259) + the Rusanov surface fluctuations lifted through the inverse
+ * mass; smax = max_wavespeed / h.  u, qavg canonical; faces [c][f][a][b][s].  Point sources are
+ * not supported (as in the GPU corrector).  Returns 0, -1 on bad arguments, -2 when the update
+ * is not finite ("corrector_step: non-finite update"). */
+int orc_corrector_step(int n, int m, int e, double domain_len, int pde_kind, const double* par3,
+                       const double* args, double max_wavespeed, double* u, const double* qavg,
+                       const double* face_q, const double* face_f);
+
 /* Canonical <-> native AoSoA ([k3][k2][s<q_stride][k1]) per element. */
 void orc_canonical_to_aosoa(int n, int m, int q_stride, long n_elem, const double* src,
                             double* dst);

@@ -226,3 +226,26 @@ def test_oracle_matches_live_reference(oracle, reference):
 
 def test_golden_files_present():
     assert len(glob.glob(os.path.join(GOLDEN, "elastic_n*.npz"))) == 9
+
+
+@pytest.mark.parametrize("kind,m,n,args,par", [
+    (O.PDE_ELASTIC, 9, 3, None, [2.0, 1.0, 1.3]),
+    (O.PDE_ELASTIC, 9, 5, None, [1.5, 0.7, 2.0]),
+    (O.PDE_ADVECTION, 2, 4, [1.0, 0.5, 0.25], None),
+    (O.PDE_NCP_ADVECTION, 3, 3, [0.3, -1.0, 0.5], None),
+    (O.PDE_DEMO, 6, 2, None, None),
+])
+def test_corrector_restatement_matches_reference(oracle, reference, kind, m, n, args, par):
+    """orc_corrector_step pinned against the reference's own corrector_step (solver.cpp:257-311)."""
+    e, L = 3, 2.0
+    E = e ** 3
+    rng = np.random.default_rng(n + m)
+    u0 = rng.standard_normal((E, n ** 3 * m))
+    qavg = rng.standard_normal((E, n ** 3 * m))
+    fq = rng.standard_normal((E, 6, n * n * m))
+    ff = rng.standard_normal((E, 6, n * n * m))
+    smax = reference.max_wavespeed(kind, m, par=par, args=args)
+    ref_u, ok = reference.corrector_step(n, m, e, L, u0, qavg, fq, ff, 0.01, par=par, pde_kind=kind, args=args)
+    got, ok2 = oracle.corrector_step(n, m, e, L, u0, qavg, fq, ff, smax, par=par, pde_kind=kind, args=args)
+    assert ok and ok2
+    assert O.per_element_rel_diff(ref_u - u0, got - u0) <= 1e-13
