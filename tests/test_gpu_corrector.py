@@ -320,3 +320,23 @@ def test_slab_decomposition_matches_single_gpu(S, n, e, slabs):
     got = torch.cat(us).cpu().numpy()
     worst = O.per_element_rel_diff(u_ref.cpu().numpy(), got)
     assert worst <= 1e-12, worst
+
+
+def test_long_run_matches_reference(S, oracle, reference):
+    """100 full time steps (elastic nDof 5 on a 3^3 mesh, smooth data): the GPU time loop stays
+    on the reference's trajectory (no drift beyond rounding)."""
+    n, m, e = 5, 9, 3
+    pde, kind, _, args, par = pde_cases(S)["elastic"]
+    init = lambda x, y, z, t, s: np.sin(2 * np.pi * (x + 2 * y) + s) * np.cos(2 * np.pi * z)  # noqa: E731
+    q0 = set_initial(S, n, e, m, init)
+    smax = reference.max_wavespeed(kind, m, par=par)
+    dt = 0.35 * (1.0 / e) / (3.0 * smax * (2 * n - 1))
+    t_end = 100 * dt
+    ref_u, stable, steps, _ = reference.run_simulation(n, m, e, 1.0, q0, 0.35, t_end, par=par, pde_kind=kind)
+    assert stable and steps == 100
+    plan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA)
+    u = to_dev(oracle, n, m, q0)
+    ok, our_steps, _ = plan.run_simulation(u, e, t_end)
+    assert ok and our_steps == steps
+    worst = O.per_element_rel_diff(ref_u, from_dev(oracle, n, m, u))
+    assert worst <= 1e-10, worst
