@@ -198,6 +198,18 @@ def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
         step()
     plan.status()
     torch.cuda.synchronize()
+    # one step (all its launches) captured once in a CUDA graph and replayed: the small configs
+    # (C1: a 10 us kernel) are otherwise bound by the host-side launch path, not the GPU
+    run, graphed = step, False
+    try:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        graph.replay()
+        torch.cuda.synchronize()
+        run, graphed = graph.replay, True
+    except Exception:  # noqa: BLE001 (fall back to direct launches)
+        torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     sampler = ClockSampler(torch.cuda.current_device()) if want_clocks else None
     barrier()
@@ -206,7 +218,7 @@ def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
         sampler.__enter__()
     ev0.record(stream)
     for _ in range(steps):
-        step()
+        run()
     ev1.record(stream)
     torch.cuda.synchronize()
     if sampler:
@@ -218,7 +230,7 @@ def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
     res = dict(ms=max_over_ranks(ms, device="cuda"), dt=dt,
                checksum=sum_over_ranks(checksum, device="cuda"),
                clocks=sampler.summary() if sampler else None, plan=plan, shard=sh,
-               launches_per_step=len(ranges), elements_per_launch=chunk)
+               launches_per_step=len(ranges), elements_per_launch=chunk, cuda_graph=graphed)
     del q, par, out
     return res
 
@@ -454,7 +466,7 @@ def main():
             r = measure_device(S, c, 1, 0, max(5, args.steps // 4), 3, want_clocks=False)
             pg = c["elems"] / (r["ms"] * 1e-3)
             rf = roofline_of(S, c["n"], pg, c["elems"], load_traffic(name, c["elems"]))
-            others[name] = {"workload": c["desc"], "elements_per_s": pg, "ms_per_step": r["ms"],
+            others[name] = {"workload": c["desc"], "elements_per_s": pg, "ms_per_step": r["ms"], "cuda_graph": r["cuda_graph"],
                             "fp64_gflops": pg * rf["flop_per_element"] / 1e9,
                             "achieved_gbs": pg * rf["byte_per_element"] / 1e9,
                             "roofline_elements_per_s": rf["roofline_elements_per_s"],
@@ -476,7 +488,7 @@ def main():
                 "config": {"workload": cfg["desc"], "order": n - 1, "n_dof": n, "elements_per_gpu": E,
                            "global_elements": total,
                            "parallelism": f"element shards x{world} (no hot-path collective)",
-                           "launches_per_step": res["launches_per_step"],
+                           "launches_per_step": res["launches_per_step"], "cuda_graph": res["cuda_graph"],
                            "layout": f"AoSoA [e][k3][k2][s<{cfg['q_stride']}][k1] in, [e][k3][k2][9][k1] out",
                            "dt": res["dt"], "cfl": 0.5,
                            "l2": "no flush needed: inputs %.1f GB and outputs %.1f GB per step >> 126 MB L2" % (
