@@ -113,4 +113,18 @@ cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t st
 bool bip_selected(const LaunchPlan& p, const BatchArgs& a);  // launch_pass takes the bipartite kernel
 cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 
+// Elastic flux tables for the tuned kernels' epilogues (proj/src/pde.cpp:180-218):
+// F_d(q)_s = c[coef(s,d)] q[in(s,d)] with c = (lambda + 2 mu, lambda, mu, 1/rho) and coef 4 = an
+// exact zero entry.  constexpr, so with compile-time (s, d) every index folds to a constant.
+__host__ __device__ constexpr int e_in(int s, int d) {
+  constexpr int t[9][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
+                           {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
+  return t[s][d];
+}
+__host__ __device__ constexpr int e_coef(int s, int d) {
+  constexpr int t[9][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
+                           {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
+  return t[s][d];
+}
+
 }  // namespace aderstp

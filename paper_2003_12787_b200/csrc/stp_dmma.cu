@@ -12,6 +12,7 @@
 // stp_dmma8.cu).  Shared memory: r and q, 2 x 9 x N x 64 doubles, XOR-swizzled rows
 // (bank-conflict free fragment loads).
 #include <cstdint>
+#include <type_traits>
 
 #include "../../include/aderstp.h"
 #include "aderstp_internal.h"
@@ -345,47 +346,57 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   const double bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
   const bool rowok = g < N;
   const bool k1a = 2 * t < N, k1b = 2 * t + 1 < N;
-  // qavg / favg: units (quantity s, plane k3), 9 N of them round-robin over the 8 warps
+  // qavg / favg: warp w emits the k3 planes w, w + 8, ...; the plane's 9 quantities are read
+  // once and every output row (9 qavg, 27 favg = F_d(qavg)) is stored with compile-time indices
   {
     double* qout = FUSED ? nullptr : a.qavg + e * (long long)(N * N * N * NVP);
     double* fout = a.favg ? a.favg + e * (long long)(3 * N * N * N * NVP) : nullptr;
 #pragma unroll 1
-    for (int u = warp; u < NVP * N; u += NWP) {
-      const int s = u / N, k3 = u - s * N;
-      const double2 v = lds2p(P + s * PV + k3 * 64 + col);
+    for (int k3 = warp; k3 < N; k3 += NWP) {
+      double2 v[NVP];
+#pragma unroll
+      for (int s = 0; s < NVP; ++s) v[s] = lds2p(P + s * PV + k3 * 64 + col);
       if (rowok) {
-        const int base = ((k3 * N + g) * NVP + s) * N + 2 * t;
-        if (!FUSED) st_pair<N>(qout + base, v.x, v.y, k1a, k1b);
+        const int base = (k3 * N + g) * NVP * N + 2 * t;
+        if (!FUSED) {
+#pragma unroll
+          for (int s = 0; s < NVP; ++s) st_pair<N>(qout + base + s * N, v[s].x, v[s].y, k1a, k1b);
+        }
         if (fout) {
-          const int nout = kOutNP[s];
-          for (int k = 0; k < nout; ++k) {
-            const int so = kOutP[s][k][0], d = kOutP[s][k][1];
-            const double c = selp(c4, kOutP[s][k][2]);
-            const int fb = d * (N * N * N * NVP) + ((k3 * N + g) * NVP + so) * N + 2 * t;
-            st_pair<N>(fout + fb, c * v.x, c * v.y, k1a, k1b);
-          }
+#pragma unroll
+          for (int d = 0; d < 3; ++d)
+#pragma unroll
+            for (int so = 0; so < NVP; ++so) {
+              const int ci = e_coef(so, d), si = e_in(so, d);
+              const double c = ci == 4 ? 0.0 : c4[ci & 3];
+              st_pair<N>(fout + d * (N * N * N * NVP) + base + so * N, ci == 4 ? 0.0 : c * v[si].x,
+                         ci == 4 ? 0.0 : c * v[si].y, k1a, k1b);
+            }
         }
       }
     }
   }
   TM2(3);
   if (faces) {
+    // x and y faces of plane k3 (DMMA against phi), every quantity of the plane per warp
 #pragma unroll 1
-    for (int u = warp; u < NVP * N; u += NWP) {
-      const int s = u / N, k3 = u - s * N;
-      const double* qs = P + s * PV;
-      double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
-      dmmap(x0, x1, qs[k3 * 64 + physp(g, t)], bphi0);
-      if (G::KS > 1) dmmap(x0, x1, qs[k3 * 64 + physp(g, 4 + t)], bphi1);
-      dmmap(y0, y1, bphi0, qs[k3 * 64 + physp(t, g)]);
-      if (G::KS > 1) dmmap(y0, y1, bphi1, qs[k3 * 64 + physp(4 + t, g)]);
-      if (t == 0 && g < N) {
-        FQ[0 * FACE + (k3 * N + g) * NVP + s] = x0;
-        FQ[1 * FACE + (k3 * N + g) * NVP + s] = x1;
-      }
-      if (g < 2) {
-        if (k1a) FQ[(2 + g) * FACE + (k3 * N + 2 * t) * NVP + s] = y0;
-        if (k1b) FQ[(2 + g) * FACE + (k3 * N + 2 * t + 1) * NVP + s] = y1;
+    for (int k3 = warp; k3 < N; k3 += NWP) {
+#pragma unroll
+      for (int s = 0; s < NVP; ++s) {
+        const double* qs = P + s * PV + k3 * 64;
+        double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
+        dmmap(x0, x1, qs[physp(g, t)], bphi0);
+        if (G::KS > 1) dmmap(x0, x1, qs[physp(g, 4 + t)], bphi1);
+        dmmap(y0, y1, bphi0, qs[physp(t, g)]);
+        if (G::KS > 1) dmmap(y0, y1, bphi1, qs[physp(4 + t, g)]);
+        if (t == 0 && g < N) {
+          FQ[0 * FACE + (k3 * N + g) * NVP + s] = x0;
+          FQ[1 * FACE + (k3 * N + g) * NVP + s] = x1;
+        }
+        if (g < 2) {
+          if (k1a) FQ[(2 + g) * FACE + (k3 * N + 2 * t) * NVP + s] = y0;
+          if (k1b) FQ[(2 + g) * FACE + (k3 * N + 2 * t + 1) * NVP + s] = y1;
+        }
       }
     }
 #pragma unroll 1
@@ -413,20 +424,29 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     }
     __syncthreads();
     TM2(4);
-    // face_f = F_d(face_q) staged next to face_q; both leave as TMA bulk stores (UBLKCP)
+    // face_f = F_d(face_q) staged next to face_q; both leave as TMA bulk stores (UBLKCP).
+    // Thread = (face f, in-face node ab): 9 loads, 9 stores, compile-time flux per direction.
     double* FF = P;  // qavg (P) is no longer read
-    if (a.face_f && tid < 252) {
-      const int so = tid % NVP, ab0 = tid / NVP;  // 28 in-face nodes per sweep
+    if (a.face_f) {
+#pragma unroll 1
+      for (int i = tid; i < 6 * N * N; i += THREADSP) {
+        const int f = i / (N * N), d = f >> 1;
+        const double* src = FQ + f * FACE + (i - f * N * N) * NVP;
+        double* dst = FF + f * FACE + (i - f * N * N) * NVP;
+        double v[NVP];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double c = selp(c4, kCoefP[so][d]);
-        const int src = kInP[so][d];
+        for (int s = 0; s < NVP; ++s) v[s] = src[s];
+        auto emit = [&](auto dd) {
+          constexpr int D = decltype(dd)::value;
 #pragma unroll
-        for (int sd = 0; sd < 2; ++sd)
-          for (int ab = ab0; ab < N * N; ab += 28) {
-            const int base = (2 * d + sd) * FACE + ab * NVP;
-            FF[base + so] = c * FQ[base + src];
+          for (int so = 0; so < NVP; ++so) {
+            const int ci = e_coef(so, D);
+            dst[so] = ci == 4 ? 0.0 : c4[ci & 3] * v[e_in(so, D)];
           }
+        };
+        if (d == 0) emit(std::integral_constant<int, 0>{});
+        else if (d == 1) emit(std::integral_constant<int, 1>{});
+        else emit(std::integral_constant<int, 2>{});
       }
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

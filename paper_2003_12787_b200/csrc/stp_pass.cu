@@ -211,18 +211,6 @@ void fill_pass_params(const LaunchPlan& p, const BatchArgs& a, PassParams<N>& kp
   kp.prefetch = p.dmma8_prefetch;
 }
 
-// Node-wise epilogue helpers: the elastic flux F_d(q)_s = coef(s,d) q[in(s,d)] with
-// compile-time (s, d), so every index below folds to a constant.
-__host__ __device__ constexpr int e_in(int s, int d) {
-  constexpr int t[9][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
-                           {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
-  return t[s][d];
-}
-__host__ __device__ constexpr int e_coef(int s, int d) {
-  constexpr int t[9][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
-                           {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
-  return t[s][d];
-}
 
 template <int N, int SL>
 __global__ void __launch_bounds__(Geo<N, SL>::THREADS, Geo<N, SL>::MINB)
