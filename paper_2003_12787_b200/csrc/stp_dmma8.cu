@@ -25,6 +25,7 @@
 // DFMA (z normal) from qavg, staged in the reference's [f][a][b][s] order and leave as TMA bulk
 // stores, face_f = F_d(face_q).
 #include <cstdint>
+#include <type_traits>
 #include <cstdlib>
 
 #include "../../include/aderstp.h"
@@ -446,24 +447,28 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     __syncthreads();  // FQ complete; qavg (P) no longer read, so face_f is staged over it
     TM3(3);
     double* FF = P;
-    // face_f[f][ab][so] = coef(so, d) face_q[f][ab][in(so, d)]: thread tid owns quantity
-    // so = tid % 9 for in-face nodes ab = tid / 9 + 28 i (252 active threads)
-    if (a.face_f && tid < 252) {
-      const int so = tid % NV, ab0 = tid / NV;
+    // face_f[f][ab][so] = coef(so, d) face_q[f][ab][in(so, d)]: thread = (face f, node ab), 9 loads
+    // and 9 stores with the compile-time flux of direction d = f / 2
+    if (a.face_f) {
+#pragma unroll 1
+      for (int i = tid; i < 6 * 64; i += THREADS8) {
+        const int f = i >> 6, d = f >> 1;
+        const double* src = FQ + f * FACE + (i & 63) * NV;
+        double* dst = FF + f * FACE + (i & 63) * NV;
+        double w[NV];
 #pragma unroll
-      for (int d = 0; d < 3; ++d) {
-        const double c = sel4(c4, kCoef[so][d]);
-        const int src = kIn[so][d];
+        for (int s = 0; s < NV; ++s) w[s] = src[s];
+        auto emit = [&](auto dd) {
+          constexpr int D = decltype(dd)::value;
 #pragma unroll
-        for (int sd = 0; sd < 2; ++sd)
-#pragma unroll
-          for (int i = 0; i < 3; ++i) {
-            const int ab = ab0 + 28 * i;
-            if (ab < 64) {
-              const int base = (2 * d + sd) * FACE + ab * NV;
-              FF[base + so] = c * FQ[base + src];
-            }
+          for (int so = 0; so < NV; ++so) {
+            const int ci = e_coef(so, D);
+            dst[so] = ci == 4 ? 0.0 : c4[ci & 3] * w[e_in(so, D)];
           }
+        };
+        if (d == 0) emit(std::integral_constant<int, 0>{});
+        else if (d == 1) emit(std::integral_constant<int, 1>{});
+        else emit(std::integral_constant<int, 2>{});
       }
     }
     // face_q / face_f leave as two TMA bulk stores (cp.async.bulk, SASS UBLKCP)
