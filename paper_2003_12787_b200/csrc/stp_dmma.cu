@@ -16,6 +16,7 @@
 
 #include "../../include/aderstp.h"
 #include "aderstp_internal.h"
+#include "tmem.cuh"
 
 // zero-padded 8 x 8 D per order (row k = node, col l), uploaded at plan creation
 extern "C" {
@@ -46,6 +47,9 @@ struct GeoP {
   static constexpr int SMEM = 2 * NVP * PV * 8;      // p + qavg accumulator
   static constexpr int KS = N > 4 ? 2 : 1;           // k-steps of 4
   static constexpr int H0 = (N + 1) / 2, H1 = N / 2; // normal-stress k3 halves
+  // TMEM columns for q: 4N (lower warps) + max(12 H0, 4N) (upper warps), power of two >= 32
+  static constexpr int TC = 4 * N + (12 * H0 > 4 * N ? 12 * H0 : 4 * N);
+  static constexpr int TCOLS = TC <= 32 ? 32 : TC <= 64 ? 64 : 128;
 };
 
 struct ParamsP {
@@ -151,32 +155,33 @@ __device__ __forceinline__ void dfma_zp(double (&acc)[NT][2], const double* f, i
   }
 }
 
-// normal stresses on planes K0 .. K0+NT-1: a = Dx u, b = Dy v, c = Dz w, then
-// t_ii = lambda (a+b+c) + 2 mu {a,b,c}_i + co q_ii (Horner, see stp_dmma8.cu); t -> p after the
-// read barrier
-// un (fused time-step mode): the step with co = 1 writes u_next = q + L(qavg) to HBM instead of r
+// normal stresses on planes K0 .. K0+NT-1 from the iterate R: a = Dx u, b = Dy v, c = Dz w, then
+// t_ii = lambda (a+b+c) + 2 mu {a,b,c}_i + co q_ii (Horner, see stp_dmma8.cu; q_ii from TMEM,
+// 12 columns per plane at tq) -> W, the other buffer of the ping-pong pair.
+// un (fused time-step mode): the step with co = 1 writes u_next = q + L(qavg) to HBM instead
 template <int N, int NT>
-__device__ __forceinline__ void normal_step(double* P, const double* Q, int K0, int g, int t, int col, double d0,
-                                            double d1, double lam, double two_mu, double co, double* un = nullptr,
-                                            int uplane = 0) {
+__device__ __forceinline__ void normal_step(const double* R, double* W, uint32_t tq, int K0, int g, int t, int col,
+                                            double d0, double d1, double lam, double two_mu, double co,
+                                            double* un = nullptr, int uplane = 0) {
   constexpr int PV = GeoP<N>::PV;
   double ta[NT][2], tb[NT][2], tc[NT][2];
 #pragma unroll
   for (int k = 0; k < NT; ++k) ta[k][0] = ta[k][1] = tb[k][0] = tb[k][1] = tc[k][0] = tc[k][1] = 0.0;
-  mma_xp<N, NT>(ta, P + 6 * PV, K0, g, t, d0, d1);
-  mma_yp<N, NT>(tb, P + 7 * PV, K0, g, t, d0, d1);
-  dfma_zp<N, NT>(tc, P + 8 * PV, K0, col, 1.0);
+  mma_xp<N, NT>(ta, R + 6 * PV, K0, g, t, d0, d1);
+  mma_yp<N, NT>(tb, R + 7 * PV, K0, g, t, d0, d1);
+  dfma_zp<N, NT>(tc, R + 8 * PV, K0, col, 1.0);
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
-    const int off = (K0 + k) * 64 + col;
-    const double2 qa = lds2p(Q + off), qb = lds2p(Q + PV + off), qc = lds2p(Q + 2 * PV + off);
-    const double qv[3][2] = {{qa.x, qa.y}, {qb.x, qb.y}, {qc.x, qc.y}};
+    uint32_t r[12];
+    tm_ld8(tq + 12 * k, r);
+    tm_ld4(tq + 12 * k + 8, r + 8);
+    tm_wait_ld();
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const double sum = lam * (ta[k][j] + tb[k][j] + tc[k][j]);
-      ta[k][j] = fma(co, qv[0][j], fma(two_mu, ta[k][j], sum));
-      tb[k][j] = fma(co, qv[1][j], fma(two_mu, tb[k][j], sum));
-      tc[k][j] = fma(co, qv[2][j], fma(two_mu, tc[k][j], sum));
+      ta[k][j] = fma(co, tm_double(r, j), fma(two_mu, ta[k][j], sum));
+      tb[k][j] = fma(co, tm_double(r, 2 + j), fma(two_mu, tb[k][j], sum));
+      tc[k][j] = fma(co, tm_double(r, 4 + j), fma(two_mu, tc[k][j], sum));
     }
   }
   if (un) {  // fused: lane base un, uplane doubles per k3 plane of u_next
@@ -192,13 +197,12 @@ __device__ __forceinline__ void normal_step(double* P, const double* Q, int K0, 
     }
     return;
   }
-  __syncthreads();  // every warp has finished reading r (single buffer)
 #pragma unroll
   for (int k = 0; k < NT; ++k) {
     const int off = (K0 + k) * 64 + col;
-    sts2p(P + off, ta[k][0], ta[k][1]);
-    sts2p(P + PV + off, tb[k][0], tb[k][1]);
-    sts2p(P + 2 * PV + off, tc[k][0], tc[k][1]);
+    sts2p(W + off, ta[k][0], ta[k][1]);
+    sts2p(W + PV + off, tb[k][0], tb[k][1]);
+    sts2p(W + 2 * PV + off, tc[k][0], tc[k][1]);
   }
 }
 
@@ -208,8 +212,9 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   using G = GeoP<N>;
   constexpr int PV = G::PV, FACE = G::FACE;
   extern __shared__ __align__(16) double smq[];
-  double* P = smq;              // Horner iterate r; qavg at the end
-  double* Q = smq + NVP * PV;   // q
+  __shared__ uint32_t tmem_base_s;
+  double* P = smq;              // staging: c_(N-1) q; then the Horner ping-pong pair (P, Q)
+  double* Q = smq + NVP * PV;   // staging: q (moved to TMEM before the first step)
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -221,6 +226,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   TM2(0);
   if (kp.prefetch && tid == 0 && e + kp.prefetch < a.n_elem)
     prefetch_l2(a.q + (e + kp.prefetch) * (long long)(N * N * N * kp.q_stride), 8ull * N * N * N * kp.q_stride);
+  if (warp == 0) tm_alloc<G::TCOLS>(&tmem_base_s);
   double c4[4];
   {
     const double p0 = a.par[3 * e], p1 = a.par[3 * e + 1], p2 = a.par[3 * e + 2];
@@ -280,7 +286,46 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   const int role = kRoleP[warp];
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];
 
+  // ---- q -> tensor memory (thread-private columns), then P / Q become a ping-pong pair ----
+  // role warps keep their quantity's N node pairs (4N columns), the normal-stress warps the
+  // three normal stresses of their k3 half (12 columns per plane); warps w and w + 4 share a
+  // TMEM lane quarter, so the upper four warps start at column 4N.
+  tm_fence_after();
+  const uint32_t tq = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp < 4 ? 0 : 4 * N);
+  {
+    if (role >= 0) {
+#pragma unroll
+      for (int k3 = 0; k3 < N; ++k3) {
+        const double2 v = lds2p(Q + role * PV + k3 * 64 + col);
+        uint32_t r[4];
+        tm_split(v.x, r, 0);
+        tm_split(v.y, r, 1);
+        tm_st4(tq + 4 * k3, r);
+      }
+    } else {
+      const int h = -role - 1, K0 = h ? G::H0 : 0, NT = h ? G::H1 : G::H0;
+#pragma unroll
+      for (int k = 0; k < G::H0; ++k) {
+        if (k >= NT) break;
+        uint32_t r[12];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double2 v = lds2p(Q + j * PV + (K0 + k) * 64 + col);
+          tm_split(v.x, r, 2 * j);
+          tm_split(v.y, r, 2 * j + 1);
+        }
+        tm_st8(tq + 12 * k, r);
+        tm_st4(tq + 12 * k + 8, r + 8);
+      }
+    }
+    tm_wait_st();
+    __syncthreads();  // every q is in TMEM: the Q buffer takes the first Horner iterate
+  }
+
   // ---- CK series in Horner form (stp_dmma8.cu): r <- c_o q + L r, o = N-2 .. 0 ----------
+  // step i reads B[i % 2] and writes B[(i + 1) % 2]: B0 = P (c_(N-1) q), B1 = Q; one barrier
+  // per step.  The Horner term c_o q (TMEM) initialises the accumulators.
+  double* B[2] = {P, Q};
   if (role >= 0) {
     const int s = role;
     const int in_x = kInP[s][0], in_y = kInP[s][1], in_z = kInP[s][2];
@@ -290,20 +335,33 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     const int own = s * PV + col;
     constexpr int o_end = FUSED ? -1 : 0;
 #pragma unroll 1
-    for (int o = N - 2; o >= o_end; --o) {
+    for (int o = N - 2, i = 0; o >= o_end; --o, ++i) {
       const double co = (!FUSED || o >= 0) ? kp.cf[o] : 1.0;
+      const double* R = B[i & 1];
       double tt[N][2];
+      {  // two halves of the planes per TMEM round trip
+        constexpr int HA = (N + 1) / 2;
+        uint32_t r[4 * HA];
 #pragma unroll
-      for (int k3 = 0; k3 < N; ++k3) tt[k3][0] = tt[k3][1] = 0.0;
-      if (has_x) mma_xp<N, N>(tt, P + in_x * PV, 0, g, t, bx0, bx1);
-      if (has_y) mma_yp<N, N>(tt, P + in_y * PV, 0, g, t, ay0, ay1);
-      if (has_z) dfma_zp<N, N>(tt, P + in_z * PV, 0, col, cz);
+        for (int k3 = 0; k3 < HA; ++k3) tm_ld4(tq + 4 * k3, r + 4 * k3);
+        tm_wait_ld();
 #pragma unroll
-      for (int k3 = 0; k3 < N; ++k3) {  // + c_o q (loaded late: fewer live registers)
-        const double2 v = lds2p(Q + own + k3 * 64);
-        tt[k3][0] = fma(co, v.x, tt[k3][0]);
-        tt[k3][1] = fma(co, v.y, tt[k3][1]);
+        for (int k3 = 0; k3 < HA; ++k3) {
+          tt[k3][0] = co * tm_double(r + 4 * k3, 0);
+          tt[k3][1] = co * tm_double(r + 4 * k3, 1);
+        }
+#pragma unroll
+        for (int k3 = HA; k3 < N; ++k3) tm_ld4(tq + 4 * k3, r + 4 * (k3 - HA));
+        tm_wait_ld();
+#pragma unroll
+        for (int k3 = HA; k3 < N; ++k3) {
+          tt[k3][0] = co * tm_double(r + 4 * (k3 - HA), 0);
+          tt[k3][1] = co * tm_double(r + 4 * (k3 - HA), 1);
+        }
       }
+      if (has_x) mma_xp<N, N>(tt, R + in_x * PV, 0, g, t, bx0, bx1);
+      if (has_y) mma_yp<N, N>(tt, R + in_y * PV, 0, g, t, ay0, ay1);
+      if (has_z) dfma_zp<N, N>(tt, R + in_z * PV, 0, col, cz);
       if (FUSED && o < 0) {  // u_next = q + L(qavg): the corrector's volume term, straight to HBM
         if (g < N) {
           const int qs = kp.q_stride;
@@ -314,29 +372,38 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
         }
         break;
       }
-      __syncthreads();
+      double* W = B[(i + 1) & 1];
 #pragma unroll
-      for (int k3 = 0; k3 < N; ++k3) sts2p(P + own + k3 * 64, tt[k3][0], tt[k3][1]);
+      for (int k3 = 0; k3 < N; ++k3) sts2p(W + own + k3 * 64, tt[k3][0], tt[k3][1]);
       __syncthreads();
     }
   } else {
     const int h = -role - 1;
     const double lam = c4[1], two_mu = 2.0 * c4[2];
 #pragma unroll 1
-    for (int o = N - 2; o >= 0; --o) {
+    for (int o = N - 2, i = 0; o >= 0; --o, ++i) {
       const double co = kp.cf[o];
-      if (h == 0) normal_step<N, G::H0>(P, Q, 0, g, t, col, d0, d1, lam, two_mu, co);
-      else normal_step<N, G::H1>(P, Q, G::H0, g, t, col, d0, d1, lam, two_mu, co);
+      if (h == 0) normal_step<N, G::H0>(B[i & 1], B[(i + 1) & 1], tq, 0, g, t, col, d0, d1, lam, two_mu, co);
+      else normal_step<N, G::H1>(B[i & 1], B[(i + 1) & 1], tq, G::H0, g, t, col, d0, d1, lam, two_mu, co);
       __syncthreads();
     }
     if (FUSED) {
       const int qs = kp.q_stride;
       double* un = a.u_next + e * (long long)(N * N * N * qs) + g * qs * N + 2 * t;
-      if (h == 0) normal_step<N, G::H0>(P, Q, 0, g, t, col, d0, d1, lam, two_mu, 1.0, un, N * qs * N);
-      else normal_step<N, G::H1>(P, Q, G::H0, g, t, col, d0, d1, lam, two_mu, 1.0, un, N * qs * N);
+      const double* R = B[(N - 1) & 1];
+      if (h == 0) normal_step<N, G::H0>(R, nullptr, tq, 0, g, t, col, d0, d1, lam, two_mu, 1.0, un, N * qs * N);
+      else normal_step<N, G::H1>(R, nullptr, tq, G::H0, g, t, col, d0, d1, lam, two_mu, 1.0, un, N * qs * N);
     }
   }
-  if (FUSED) __syncthreads();  // q (the Q region) is read until here; faces stage over it
+  // every TMEM read has completed (tcgen05.wait::ld); the allocating warp frees the columns
+  tm_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tm_fence_after();
+    tm_dealloc<G::TCOLS>(tmem_base_s);
+  }
+  P = B[(N - 1) & 1];  // qavg: the last Horner iterate
+  Q = B[N & 1];        // free: the face staging buffer
 
   TM2(2);
   // ---- epilogue: 9 quantities x k3 planes over the 8 warps ------------------------------
