@@ -323,9 +323,8 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   }
 
   // ---- CK series in Horner form (stp_dmma8.cu): r <- c_o q + L r, o = N-2 .. 0 ----------
-  // step i reads B[i % 2] and writes B[(i + 1) % 2]: B0 = P (c_(N-1) q), B1 = Q; one barrier
+  // step i reads buffer i % 2 and writes (i + 1) % 2: 0 = P (c_(N-1) q), 1 = Q; one barrier
   // per step.  The Horner term c_o q (TMEM) initialises the accumulators.
-  double* B[2] = {P, Q};
   if (role >= 0) {
     const int s = role;
     const int in_x = kInP[s][0], in_y = kInP[s][1], in_z = kInP[s][2];
@@ -337,7 +336,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
 #pragma unroll 1
     for (int o = N - 2, i = 0; o >= o_end; --o, ++i) {
       const double co = (!FUSED || o >= 0) ? kp.cf[o] : 1.0;
-      const double* R = B[i & 1];
+      const double* R = smq + (i & 1) * (NVP * PV);
       double tt[N][2];
       {  // two halves of the planes per TMEM round trip
         constexpr int HA = (N + 1) / 2;
@@ -372,7 +371,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
         }
         break;
       }
-      double* W = B[(i + 1) & 1];
+      double* W = smq + ((i + 1) & 1) * (NVP * PV);
 #pragma unroll
       for (int k3 = 0; k3 < N; ++k3) sts2p(W + own + k3 * 64, tt[k3][0], tt[k3][1]);
       __syncthreads();
@@ -383,14 +382,14 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
 #pragma unroll 1
     for (int o = N - 2, i = 0; o >= 0; --o, ++i) {
       const double co = kp.cf[o];
-      if (h == 0) normal_step<N, G::H0>(B[i & 1], B[(i + 1) & 1], tq, 0, g, t, col, d0, d1, lam, two_mu, co);
-      else normal_step<N, G::H1>(B[i & 1], B[(i + 1) & 1], tq, G::H0, g, t, col, d0, d1, lam, two_mu, co);
+      if (h == 0) normal_step<N, G::H0>(smq + (i & 1) * (NVP * PV), smq + ((i + 1) & 1) * (NVP * PV), tq, 0, g, t, col, d0, d1, lam, two_mu, co);
+      else normal_step<N, G::H1>(smq + (i & 1) * (NVP * PV), smq + ((i + 1) & 1) * (NVP * PV), tq, G::H0, g, t, col, d0, d1, lam, two_mu, co);
       __syncthreads();
     }
     if (FUSED) {
       const int qs = kp.q_stride;
       double* un = a.u_next + e * (long long)(N * N * N * qs) + g * qs * N + 2 * t;
-      const double* R = B[(N - 1) & 1];
+      const double* R = smq + ((N - 1) & 1) * (NVP * PV);
       if (h == 0) normal_step<N, G::H0>(R, nullptr, tq, 0, g, t, col, d0, d1, lam, two_mu, 1.0, un, N * qs * N);
       else normal_step<N, G::H1>(R, nullptr, tq, G::H0, g, t, col, d0, d1, lam, two_mu, 1.0, un, N * qs * N);
     }
@@ -402,8 +401,8 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     tm_fence_after();
     tm_dealloc<G::TCOLS>(tmem_base_s);
   }
-  P = B[(N - 1) & 1];  // qavg: the last Horner iterate
-  Q = B[N & 1];        // free: the face staging buffer
+  P = smq + ((N - 1) & 1) * (NVP * PV);  // qavg: the last Horner iterate
+  Q = smq + (N & 1) * (NVP * PV);        // free: the face staging buffer
 
   TM2(2);
   // ---- epilogue: 9 quantities x k3 planes over the 8 warps ------------------------------
