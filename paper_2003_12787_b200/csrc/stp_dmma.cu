@@ -99,6 +99,7 @@ __device__ __forceinline__ double selp(const double c[4], int i) {
 }
 __device__ __forceinline__ double2 lds2p(const double* p) { return *reinterpret_cast<const double2*>(p); }
 __device__ __forceinline__ void sts2p(double* p, double a, double b) {
+  __builtin_assume(__isShared(p));
   *reinterpret_cast<double2*>(p) = make_double2(a, b);
 }
 
