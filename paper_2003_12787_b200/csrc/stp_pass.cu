@@ -551,6 +551,12 @@ __device__ __forceinline__ void tm_store_q(uint32_t ta, int k, const double (&q)
 // annealing the bank model (tools/bank_model.py), cuts the x-pass wavefronts by 11 %.
 __constant__ uint8_t kXPerm9[81] = {12, 60, 27, 70, 79, 55, 73, 67, 34, 80, 8, 61, 54, 56, 78, 63, 71, 42, 0, 10, 19, 1, 28, 43, 72, 30, 5, 77, 68, 41, 62, 31, 3, 65, 37, 59, 22, 13, 11, 47, 64, 6, 25, 51, 74, 40, 4, 15, 76, 52, 46, 21, 48, 49, 18, 69, 17, 32, 39, 20, 50, 66, 75, 23, 45, 26, 58, 14, 38, 9, 57, 33, 24, 2, 36, 29, 53, 7, 35, 16, 44};
 
+// nDof 10, passes x: the 16-byte x-line accesses of a quarter-warp hit bank group
+// (la PL + lb RS) / 2 mod 8 = 5 (la + lb) mod 8; this permutation (annealed with the same bank model,
+// started from a periodic residue sequence) spreads every quarter-warp over distinct groups:
+// modelled x-pass wavefronts 1400 -> 980 per CK step (ideal 890).
+__constant__ uint8_t kXPerm10[100] = {62, 9, 99, 61, 93, 18, 95, 3, 17, 76, 20, 87, 83, 22, 42, 90, 82, 67, 71, 16, 13, 89, 77, 92, 79, 5, 91, 70, 68, 98, 66, 12, 50, 64, 97, 7, 72, 57, 6, 56, 96, 94, 55, 88, 48, 45, 59, 47, 53, 49, 11, 52, 4, 65, 51, 10, 80, 32, 19, 43, 84, 36, 24, 21, 34, 41, 2, 35, 31, 27, 33, 74, 44, 14, 46, 25, 39, 29, 86, 1, 26, 23, 37, 78, 38, 54, 15, 75, 8, 73, 85, 69, 30, 63, 60, 40, 0, 28, 58, 81};
+
 // phase-V pass D, slot j: stress source -> velocity target (coefficient 1/rho)
 __constant__ int8_t kBipV[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
 // phase-S pass D: slot 0 source (u, v, w)[D] -> sxx, syy, szz with (coef idx); slots 1, 2 shear
@@ -662,7 +668,7 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   const bool active = slot < 3;
   const int sl = active ? slot : 0;
   const int la = line / N, lb = line - la * N;
-  const int xline = N == 9 ? kXPerm9[line < 81 ? line : 0] : line;  // x passes: permuted line
+  const int xline = N == 9 ? kXPerm9[line < 81 ? line : 0] : N == 10 ? kXPerm10[line < 100 ? line : 0] : line;  // x passes
   const int lax = xline / N, lbx = xline - lax * N;
 
   if (kp.prefetch && tid == 0 && e + kp.prefetch < a.n_elem)
