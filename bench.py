@@ -134,8 +134,15 @@ def dist_setup():
     world, rank, local = env_world()
     if world > 1:
         import torch.distributed as dist
+        # ADERSTP_BENCH_BACKEND=gloo validates the multi-rank flow on a box with fewer GPUs than
+        # ranks (ranks then share devices; never a timing run).  Default: NCCL, one GPU per rank.
+        backend = os.environ.get("ADERSTP_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     return world, rank, local
