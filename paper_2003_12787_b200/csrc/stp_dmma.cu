@@ -489,9 +489,18 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
         }
       }
     }
+    // face_q is complete and leaves at once (TMA bulk store, UBLKCP), overlapping the face_f pass
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
+    if (tid == 0 && a.face_q) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                       a.face_q + e * (long long)(6 * FACE)),
+                   "r"((unsigned)__cvta_generic_to_shared(FQ)), "r"((unsigned)(6 * FACE * 8))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
     TM2(4);
-    // face_f = F_d(face_q) staged next to face_q; both leave as TMA bulk stores (UBLKCP).
+    // face_f = F_d(face_q) staged over qavg; it leaves as a second bulk store.
     // Thread = (face f, in-face node ab): 9 loads, 9 stores, compile-time flux per direction.
     double* FF = P;  // qavg (P) is no longer read
     if (a.face_f) {
@@ -520,11 +529,6 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     __syncthreads();
     if (tid == 0) {
       const unsigned bytes = 6 * FACE * 8;
-      if (a.face_q)
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
-                         a.face_q + e * (long long)(6 * FACE)),
-                     "r"((unsigned)__cvta_generic_to_shared(FQ)), "r"(bytes)
-                     : "memory");
       if (a.face_f)
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
                          a.face_f + e * (long long)(6 * FACE)),

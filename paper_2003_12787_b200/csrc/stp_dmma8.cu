@@ -444,7 +444,17 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     }
   }
   if (faces) {
-    __syncthreads();  // FQ complete; qavg (P) no longer read, so face_f is staged over it
+    // FQ complete; qavg (P) is no longer read, so face_f is staged over it.  face_q leaves at once
+    // (TMA bulk store, SASS UBLKCP) and its copy overlaps the face_f pass below.
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && a.face_q) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                       a.face_q + e * (long long)(6 * FACE)),
+                   "r"((unsigned)__cvta_generic_to_shared(FQ)), "r"((unsigned)(6 * FACE * 8))
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
     TM3(3);
     double* FF = P;
     // face_f[f][ab][so] = coef(so, d) face_q[f][ab][in(so, d)]: thread = (face f, node ab), 9 loads
@@ -471,16 +481,14 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
         else emit(std::integral_constant<int, 2>{});
       }
     }
-    // face_q / face_f leave as two TMA bulk stores (cp.async.bulk, SASS UBLKCP)
+    TM3(4);
+    // face_f leaves as a second TMA bulk store; thread 0 then waits until both copies have read
+    // the shared memory (the CTA's shared memory must outlive them)
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
+    TM3(5);
     if (tid == 0) {
       const unsigned bytes = 6 * FACE * 8;
-      if (a.face_q)
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
-                         a.face_q + e * (long long)(6 * FACE)),
-                     "r"((unsigned)__cvta_generic_to_shared(FQ)), "r"(bytes)
-                     : "memory");
       if (a.face_f)
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
                          a.face_f + e * (long long)(6 * FACE)),
@@ -491,7 +499,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     }
   }
   if (kp.check && flags) atomicOr(status, flags);
-  TM3(4);
+  TM3(6);
 }
 
 }  // namespace
