@@ -250,6 +250,120 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, Co
   if (flags) atomicOr(status, flags);
 }
 
+// Surface-only corrector of the fused time step (elastic, AoSoA state with quantity stride QS,
+// even N): the volume term was applied by the fused predictor, so per element only the six face
+// fluctuations fhat - f_self (solver.cpp:218-226) and their lifting onto every node
+// (solver.cpp:228-249) remain.  HBM-bound (u read + written, every face array read by its owner
+// and its neighbour): the neighbour face blocks are resolved once per CTA, the fluctuations are
+// formed from 16-byte loads, and the state is updated as k1 pairs with compile-time indexing.
+constexpr int kSurfThreads = 256;
+// V entries per thread and step: 2 (16-byte pairs) for even N, 1 for odd N
+template <int V>
+struct VecT;
+template <>
+struct VecT<1> {
+  using T = double;
+  __device__ static double& at(T& v, int) { return v; }
+};
+template <>
+struct VecT<2> {
+  using T = double2;
+  __device__ static double& at(T& v, int i) { return i ? v.y : v.x; }
+};
+
+template <int N, int QS>
+__global__ void __launch_bounds__(kSurfThreads) surface_kernel(CorrParams kp, CorrArgs ca, unsigned int* status) {
+  constexpr int V = N % 2 == 0 ? 2 : 1;
+  using VT = typename VecT<V>::T;
+  constexpr int N2 = N * N, N3 = N * N * N, FV = N2 * NVC;
+  extern __shared__ __align__(16) double sms[];
+  double* DL = sms;  // fhat - f_self  [f][a][b][s]
+  __shared__ double SC[2][N];
+  __shared__ double SMAX[6];
+  __shared__ const double* NBQ[6];
+  __shared__ const double* NBF[6];
+  const int e = kp.e;
+  const long long c = blockIdx.x;
+  const int ix = (int)(c % e), iy = (int)((c / e) % e), iz = ca.z0 + (int)(c / ((long long)e * e));
+  const int nz = ca.nz > 0 ? ca.nz : e;
+  const int tid = threadIdx.x;
+  if (tid < 6) {
+    const int d = tid >> 1, step = (tid & 1) ? 1 : -1;
+    const int ixn = ((ix + (d == 0 ? step : 0)) % e + e) % e;
+    const int iyn = ((iy + (d == 1 ? step : 0)) % e + e) % e;
+    const int izn = ((iz + (d == 2 ? step : 0)) % e + e) % e;
+    const double *fq, *ff, *pr;
+    long long idx;
+    if (izn >= ca.z0 && izn < ca.z0 + nz) {
+      fq = ca.face_q; ff = ca.face_f; pr = ca.par;
+      idx = ((long long)(izn - ca.z0) * e + iyn) * e + ixn;
+    } else {
+      const HaloRef& hr = step < 0 ? ca.lo : ca.hi;
+      fq = hr.face_q; ff = hr.face_f; pr = hr.par;
+      idx = ((long long)(((izn - hr.z_base) % e + e) % e) * e + iyn) * e + ixn;
+    }
+    NBQ[tid] = fq + idx * 6LL * FV;
+    NBF[tid] = ff + idx * 6LL * FV;
+    double smax = kp.smax;
+    if (smax < 0.0)
+      smax = fmax(material(ca.par + 3 * c, kp.par_kind).cp, material(pr + 3 * idx, kp.par_kind).cp) * kp.inv_h;
+    SMAX[tid] = smax;
+  }
+  if (tid < 2 * N) {
+    const int side = tid / N, j = tid - side * N;
+    SC[side][j] = (side == 0 ? -1.0 : 1.0) * kp.phi[side][j] * kp.inv_w[j];
+  }
+  __syncthreads();
+  {  // fluctuations, V face entries per thread and step (V divides FV)
+    const double* mq = ca.face_q + c * 6LL * FV;
+    const double* mf = ca.face_f + c * 6LL * FV;
+    for (int i = V * tid; i < 6 * FV; i += V * kSurfThreads) {
+      const int f = i / FV, r = i - f * FV;
+      VT qo = *reinterpret_cast<const VT*>(mq + i), fo = *reinterpret_cast<const VT*>(mf + i);
+      VT qn = *reinterpret_cast<const VT*>(NBQ[f] + (f ^ 1) * FV + r);
+      VT fn = *reinterpret_cast<const VT*>(NBF[f] + (f ^ 1) * FV + r);
+      const double sm = SMAX[f];
+      VT dl;
+#pragma unroll
+      for (int k = 0; k < V; ++k) {
+        const double a_o = VecT<V>::at(qo, k), a_n = VecT<V>::at(qn, k);
+        const double b_o = VecT<V>::at(fo, k), b_n = VecT<V>::at(fn, k);
+        // + side: the element is the minus state; - side: the plus state (solver.cpp:218-226)
+        VecT<V>::at(dl, k) = (f & 1) ? (0.5 * (b_n + b_o) - 0.5 * sm * (a_o - a_n)) - b_o
+                                     : (0.5 * (b_o + b_n) - 0.5 * sm * (a_n - a_o)) - b_o;
+      }
+      *reinterpret_cast<VT*>(DL + i) = dl;
+    }
+  }
+  __syncthreads();
+  unsigned int flags = 0;
+  double* ue = ca.u + c * (long long)(N3 * QS);
+  for (int jv = tid; jv < N3 * QS / V; jv += kSurfThreads) {
+    const int k1 = V * (jv % (N / V)), r = jv / (N / V);
+    const int s = r % QS, k32 = r / QS, k2 = k32 % N, k3 = k32 / N;
+    if (s >= NVC) continue;
+    VT v = *reinterpret_cast<const VT*>(ue + V * jv);
+    // x faces: the in-face node (k3, k2) is shared by the k1 run, the lifting differs; y faces
+    // (k3, k1) and z faces (k2, k1): per-node fluctuations, shared lifting
+    const double dxm = DL[(k3 * N + k2) * NVC + s], dxp = DL[(N2 + k3 * N + k2) * NVC + s];
+    const int iy0 = (2 * N2 + k3 * N + k1) * NVC + s, iz0 = (4 * N2 + k2 * N + k1) * NVC + s;
+#pragma unroll
+    for (int k = 0; k < V; ++k) {
+      double x = VecT<V>::at(v, k);
+      x += SC[0][k1 + k] * dxm;
+      x += SC[1][k1 + k] * dxp;
+      x += SC[0][k2] * DL[iy0 + k * NVC];
+      x += SC[1][k2] * DL[iy0 + N2 * NVC + k * NVC];
+      x += SC[0][k3] * DL[iz0 + k * NVC];
+      x += SC[1][k3] * DL[iz0 + N2 * NVC + k * NVC];
+      if (!isfinite(x)) flags |= 1u;
+      VecT<V>::at(v, k) = x;
+    }
+    *reinterpret_cast<VT*>(ue + V * jv) = v;
+  }
+  if (flags) atomicOr(status, flags);
+}
+
 // (lambda, mu, rho) scaled like ScaledPde(1/h): every flux coefficient x s  ->  (s lambda, s mu, rho / s)
 __global__ void scale_par_kernel(const double* __restrict__ in, int par_kind, double s, long long n,
                                  double* __restrict__ out) {
@@ -307,6 +421,17 @@ cudaError_t launch_correct_n(const LaunchPlan& p, const CorrArgs& a, cudaStream_
   kp.smax = a.smax;
   const bool elastic = p.kind == ADERSTP_PDE_ELASTIC;
   const bool vol = a.qavg != nullptr;
+  {
+    if (elastic && !vol && p.layout == ADERSTP_LAYOUT_AOSOA && p.q_stride == NVC && p.m == NVC) {
+      const size_t ssm = sizeof(double) * 6 * N * N * NVC;
+      cudaError_t err = cudaFuncSetAttribute(surface_kernel<N, NVC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+      if (err != cudaSuccess) return err;
+      const long long cells = (long long)a.e * a.e * (a.nz > 0 ? a.nz : a.e);
+      if (cells == 0) return cudaSuccess;
+      surface_kernel<N, NVC><<<(unsigned)cells, kSurfThreads, ssm, stream>>>(kp, a, p.d_status);
+      return cudaGetLastError();
+    }
+  }
   const size_t smem = sizeof(double) * (size_t)p.m * ((vol ? N * N * N + 8 : 0) + 6 * N * N);
   auto kern = elastic ? (vol ? correct_kernel<N, true, true> : correct_kernel<N, true, false>)
                       : (vol ? correct_kernel<N, false, true> : correct_kernel<N, false, false>);

@@ -130,8 +130,9 @@ def test_corrector_elastic_per_face_wavespeed(S, oracle):
 
 
 # ---- the time loop ---------------------------------------------------------------------------
-@pytest.mark.parametrize("case,n,e", [("elastic", 4, 2), ("elastic", 6, 2), ("elastic", 8, 2), ("elastic", 9, 2),
-                                      ("elastic", 10, 2), ("advection", 5, 3), ("demo", 3, 2)])
+@pytest.mark.parametrize("case,n,e", [("elastic", 4, 2), ("elastic", 5, 2), ("elastic", 6, 2), ("elastic", 7, 2),
+                                      ("elastic", 8, 2), ("elastic", 9, 2), ("elastic", 10, 2), ("elastic", 8, 3),
+                                      ("advection", 5, 3), ("demo", 3, 2)])
 def test_run_simulation_matches_reference(S, oracle, reference, case, n, e):
     pde, kind, m, args, par = pde_cases(S)[case]
     init = lambda x, y, z, t, s: np.sin(2 * np.pi * x + s) + 0.3 * np.cos(2 * np.pi * (y - z) + 0.2 * s)  # noqa: E731
@@ -273,7 +274,7 @@ class _ThreadSync:
         return sync
 
 
-@pytest.mark.parametrize("n,e,slabs", [(4, 6, 2), (4, 6, 3), (8, 4, 2), (10, 3, 3)])
+@pytest.mark.parametrize("n,e,slabs", [(4, 6, 2), (4, 6, 3), (5, 4, 2), (8, 4, 2), (9, 3, 3), (10, 3, 3)])
 def test_slab_decomposition_matches_single_gpu(S, n, e, slabs):
     """aderstp_run_simulation_slab on `slabs` z-slabs, each corrector reading its neighbours'
     faces through halo pointers, reproduces the single-GPU run_simulation."""
