@@ -270,10 +270,12 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   if (aos_staged(lp)) {
     kl.layout = ADERSTP_LAYOUT_AOSOA;
     kl.q_stride = kl.out_stride = 9;
-    if (e == cudaSuccess) e = cudaMemPoolCreate(&p->pool, &pool_props_of(p->device));
-    const uint64_t keep = UINT64_MAX;
-    if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, (void*)&keep);
   }
+  // plan-owned stream-ordered pool (AoS staging, time-loop faces): keeps its memory between
+  // calls, returned when the plan is destroyed
+  if (e == cudaSuccess) e = cudaMemPoolCreate(&p->pool, &pool_props_of(p->device));
+  const uint64_t keep = UINT64_MAX;
+  if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, (void*)&keep);
   if (e == cudaSuccess && aderstp::dmma8_applicable(kl)) e = aderstp::init_dmma8(kl);
   if (e == cudaSuccess && aderstp::pass_applicable(kl)) e = aderstp::init_pass(kl);
   if (e == cudaSuccess && aderstp::dmmap_applicable(kl)) e = aderstp::init_dmmap(kl);
@@ -594,19 +596,21 @@ int run_loop(const aderstp_plan* p, const aderstp_mesh* mesh, int z0, int nz, do
         }
   double *par_s = nullptr, *qavg = nullptr;
   auto cleanup = [&]() {
-    if (par_s) cudaFree(par_s);
-    if (qavg) cudaFree(qavg);
+    if (par_s) cudaFreeAsync(par_s, st);
+    if (qavg) cudaFreeAsync(qavg, st);
   };
   cudaError_t err = cudaSuccess;
   if (elastic) {
-    err = cudaMalloc(&par_s, sizeof(double) * 3 * (E > 0 ? E : 1));
+    err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&par_s), sizeof(double) * 3 * (E > 0 ? E : 1), p->pool, st);
     if (err == cudaSuccess) err = aderstp::launch_scale_par(par, p->lp.par_kind, s, E, par_s, st);
     sp.par_kind = ADERSTP_PAR_LAMBDA_MU_RHO;
   }
   aderstp::BatchArgs probe{u, elastic ? par_s : par, nullptr, nullptr, face_q, face_f, E, 1.0, 0.0};
   probe.u_next = u;
   const bool fused = aderstp::fused_supported(sp, probe);
-  if (err == cudaSuccess && !fused) err = cudaMalloc(&qavg, sizeof(double) * (size_t)n * n * n * p->lp.out_stride * (E > 0 ? E : 1));
+  if (err == cudaSuccess && !fused)
+    err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&qavg), sizeof(double) * (size_t)n * n * n * p->lp.out_stride * (E > 0 ? E : 1),
+                                  p->pool, st);
   if (err != cudaSuccess) {
     cleanup();
     return cuda_fail(err, "run_simulation setup");
@@ -620,7 +624,9 @@ int run_loop(const aderstp_plan* p, const aderstp_mesh* mesh, int z0, int nz, do
     aderstp::BatchArgs ba{u, elastic ? par_s : par, fused ? nullptr : qavg, nullptr, face_q, face_f, E, dt, t};
     if (fused) ba.u_next = u;
     err = E > 0 ? aderstp::launch_stp(sp, ba, st) : cudaSuccess;
-    if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+    // other slabs read this slab's faces: the rank sync needs them complete (one GPU: the
+    // corrector below is stream-ordered after the predictor, no host round trip)
+    if (err == cudaSuccess && sync) err = cudaStreamSynchronize(st);
     if (err != cudaSuccess) {
       rc = cuda_fail(err, "run_simulation predictor");
       break;
@@ -776,10 +782,12 @@ int aderstp_run_simulation(const aderstp_plan* p, const aderstp_mesh* mesh, doub
   double* faces = nullptr;
   unsigned long long* d_cp = nullptr;
   double smax = max_wavespeed;
-  cudaError_t err = cudaMalloc(&faces, sizeof(double) * 2 * face * E);
+  // scratch from the plan's pool (kept between calls: no re-mapping of the face buffers per call)
+  cudaError_t err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&faces), sizeof(double) * 2 * face * (E > 0 ? E : 1),
+                                            p->pool, st);
   if (err == cudaSuccess && elastic && !(smax >= 0.0)) {  // the global max cp (stable_dt)
     unsigned long long bits = 0;
-    err = cudaMalloc(&d_cp, sizeof bits);
+    err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&d_cp), sizeof bits, p->pool, st);
     if (err == cudaSuccess) err = aderstp::launch_max_cp(par, p->lp.par_kind, E, d_cp, st);
     if (err == cudaSuccess) err = cudaMemcpyAsync(&bits, d_cp, sizeof bits, cudaMemcpyDeviceToHost, st);
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
@@ -792,7 +800,8 @@ int aderstp_run_simulation(const aderstp_plan* p, const aderstp_mesh* mesh, doub
   } else {
     rc = cuda_fail(err, "run_simulation setup");
   }
-  if (faces) cudaFree(faces);
-  if (d_cp) cudaFree(d_cp);
+  if (faces) cudaFreeAsync(faces, st);
+  if (d_cp) cudaFreeAsync(d_cp, st);
+  cudaStreamSynchronize(st);  // the call is synchronous, like the reference's
   return rc;
 }

@@ -271,13 +271,23 @@ struct VecT<2> {
   __device__ static double& at(T& v, int i) { return i ? v.y : v.x; }
 };
 
-template <int N, int QS>
-__global__ void __launch_bounds__(kSurfThreads) surface_kernel(CorrParams kp, CorrArgs ca, unsigned int* status) {
+// VOL: also the volume term V(qavg) (the public corrector_step, solver.cpp:257-311): qavg is
+// staged in shared memory and the state is walked quantity-major, so that the quantity (and with
+// it the flux table entries) is uniform across a warp.
+template <int N, bool VOL>
+constexpr int surf_threads() { return VOL && N >= 9 ? 512 : kSurfThreads; }  // 1 CTA/SM at N >= 9
+
+template <int N, int QS, bool VOL>
+__global__ void __launch_bounds__(surf_threads<N, VOL>()) surface_kernel(CorrParams kp, CorrArgs ca, unsigned int* status) {
+  constexpr int NT = surf_threads<N, VOL>();
   constexpr int V = N % 2 == 0 ? 2 : 1;
   using VT = typename VecT<V>::T;
   constexpr int N2 = N * N, N3 = N * N * N, FV = N2 * NVC;
+  constexpr int QP = N3 + 8, DR = N + 1;  // padded quantity planes of qavg, padded rows of D
   extern __shared__ __align__(16) double sms[];
-  double* DL = sms;  // fhat - f_self  [f][a][b][s]
+  double* DL = sms;            // fhat - f_self  [f][a][b][s]
+  double* QA = sms + 6 * FV;   // VOL: qavg [s][k3][k2][k1]
+  __shared__ double Ds[VOL ? N * DR : 1];
   __shared__ double SC[2][N];
   __shared__ double SMAX[6];
   __shared__ const double* NBQ[6];
@@ -313,11 +323,23 @@ __global__ void __launch_bounds__(kSurfThreads) surface_kernel(CorrParams kp, Co
     const int side = tid / N, j = tid - side * N;
     SC[side][j] = (side == 0 ? -1.0 : 1.0) * kp.phi[side][j] * kp.inv_w[j];
   }
+  Material mine;
+  if (VOL) {
+    mine = material(ca.par + 3 * c, kp.par_kind);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mine.c4[i] *= kp.inv_h;  // ScaledPde: flux x 1/h
+    for (int i = tid; i < N2; i += NT) Ds[(i / N) * DR + i % N] = kp.d[i];
+    const double* qa = ca.qavg + c * (long long)(N3 * NVC);
+    for (int iv = tid; iv < N3 * NVC / V; iv += NT) {  // [k3][k2][s][k1] -> [s][k3][k2][k1]
+      const int k1 = V * (iv % (N / V)), r = iv / (N / V), sq = r % NVC, k32 = r / NVC;
+      *reinterpret_cast<VT*>(QA + sq * QP + k32 * N + k1) = *reinterpret_cast<const VT*>(qa + V * iv);
+    }
+  }
   __syncthreads();
   {  // fluctuations, V face entries per thread and step (V divides FV)
     const double* mq = ca.face_q + c * 6LL * FV;
     const double* mf = ca.face_f + c * 6LL * FV;
-    for (int i = V * tid; i < 6 * FV; i += V * kSurfThreads) {
+    for (int i = V * tid; i < 6 * FV; i += V * NT) {
       const int f = i / FV, r = i - f * FV;
       VT qo = *reinterpret_cast<const VT*>(mq + i), fo = *reinterpret_cast<const VT*>(mf + i);
       VT qn = *reinterpret_cast<const VT*>(NBQ[f] + (f ^ 1) * FV + r);
@@ -337,12 +359,64 @@ __global__ void __launch_bounds__(kSurfThreads) surface_kernel(CorrParams kp, Co
   }
   __syncthreads();
   unsigned int flags = 0;
-  double* ue = ca.u + c * (long long)(N3 * QS);
-  for (int jv = tid; jv < N3 * QS / V; jv += kSurfThreads) {
-    const int k1 = V * (jv % (N / V)), r = jv / (N / V);
-    const int s = r % QS, k32 = r / QS, k2 = k32 % N, k3 = k32 / N;
-    if (s >= NVC) continue;
-    VT v = *reinterpret_cast<const VT*>(ue + V * jv);
+  const int qs = QS ? QS : kp.q_stride;  // QS = 0: run-time quantity stride of the state
+  double* ue = ca.u + c * (long long)(N3 * qs);
+  for (int jv = tid; jv < N3 * NVC / V; jv += NT) {
+    // VOL: quantity-major walk (s = jv / (N^3 / V) uniform over runs of N^3 / V threads, so the
+    // flux table lookups are warp-uniform); surface only: the state's own order (contiguous)
+    int s, k1, k32;
+    if (VOL) {
+      s = jv / (N3 / V);
+      const int rem = jv - s * (N3 / V);
+      k1 = V * (rem % (N / V));
+      k32 = rem / (N / V);
+    } else {
+      k1 = V * (jv % (N / V));
+      const int r = jv / (N / V);
+      s = r % NVC;
+      k32 = r / NVC;
+    }
+    const int k2 = k32 % N, k3 = k32 / N;
+    double* up = ue + (k32 * qs + s) * N + k1;
+    VT v = *reinterpret_cast<const VT*>(up);
+    if (VOL) {  // apply_volume_once (predictor_common.cpp:243-259) on the scaled elastic flux
+      double vol[V];
+#pragma unroll
+      for (int k = 0; k < V; ++k) vol[k] = 0.0;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int cf = kCoefC[s][d];
+        if (cf == 4) continue;
+        const double cc = cf == 0 ? mine.c4[0] : cf == 1 ? mine.c4[1] : cf == 2 ? mine.c4[2] : mine.c4[3];
+        const double* src = QA + kInC[s][d] * QP;
+        double acc[V];
+#pragma unroll
+        for (int k = 0; k < V; ++k) acc[k] = 0.0;
+        if (d == 0) {  // x: the row (k3, k2) is shared by the k1 run
+          const double* row = src + k32 * N;
+#pragma unroll
+          for (int l = 0; l < N; ++l) {
+            const double x = cc * row[l];
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc[k] = fma(Ds[(k1 + k) * DR + l], x, acc[k]);
+          }
+        } else {       // y (stride N, D row k2) and z (stride N^2, D row k3): k1 runs are contiguous
+          const int kd = d == 1 ? k2 : k3, stride = d == 1 ? N : N2;
+          const double* col = src + k3 * N2 + k2 * N + k1 - kd * stride;
+#pragma unroll
+          for (int l = 0; l < N; ++l) {
+            VT x = *reinterpret_cast<const VT*>(col + l * stride);
+            const double dl = Ds[kd * DR + l];
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc[k] = fma(dl, cc * VecT<V>::at(x, k), acc[k]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < V; ++k) vol[k] += acc[k];
+      }
+#pragma unroll
+      for (int k = 0; k < V; ++k) VecT<V>::at(v, k) += vol[k];
+    }
     // x faces: the in-face node (k3, k2) is shared by the k1 run, the lifting differs; y faces
     // (k3, k1) and z faces (k2, k1): per-node fluctuations, shared lifting
     const double dxm = DL[(k3 * N + k2) * NVC + s], dxp = DL[(N2 + k3 * N + k2) * NVC + s];
@@ -359,7 +433,7 @@ __global__ void __launch_bounds__(kSurfThreads) surface_kernel(CorrParams kp, Co
       if (!isfinite(x)) flags |= 1u;
       VecT<V>::at(v, k) = x;
     }
-    *reinterpret_cast<VT*>(ue + V * jv) = v;
+    *reinterpret_cast<VT*>(up) = v;
   }
   if (flags) atomicOr(status, flags);
 }
@@ -421,16 +495,17 @@ cudaError_t launch_correct_n(const LaunchPlan& p, const CorrArgs& a, cudaStream_
   kp.smax = a.smax;
   const bool elastic = p.kind == ADERSTP_PDE_ELASTIC;
   const bool vol = a.qavg != nullptr;
-  {
-    if (elastic && !vol && p.layout == ADERSTP_LAYOUT_AOSOA && p.q_stride == NVC && p.m == NVC) {
-      const size_t ssm = sizeof(double) * 6 * N * N * NVC;
-      cudaError_t err = cudaFuncSetAttribute(surface_kernel<N, NVC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
-      if (err != cudaSuccess) return err;
-      const long long cells = (long long)a.e * a.e * (a.nz > 0 ? a.nz : a.e);
-      if (cells == 0) return cudaSuccess;
-      surface_kernel<N, NVC><<<(unsigned)cells, kSurfThreads, ssm, stream>>>(kp, a, p.d_status);
-      return cudaGetLastError();
-    }
+  if (elastic && p.layout == ADERSTP_LAYOUT_AOSOA && p.m == NVC && (!vol || p.out_stride == NVC)) {
+    // tuned elastic path (any q stride; qavg in the compact AoSoA output layout)
+    const size_t ssm = sizeof(double) * (6 * N * N * NVC + (vol ? NVC * (N * N * N + 8) : 0));
+    auto sk = vol ? surface_kernel<N, 0, true> : surface_kernel<N, 0, false>;
+    if (p.q_stride == NVC) sk = vol ? surface_kernel<N, NVC, true> : surface_kernel<N, NVC, false>;
+    cudaError_t err = cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
+    if (err != cudaSuccess) return err;
+    const long long cells = (long long)a.e * a.e * (a.nz > 0 ? a.nz : a.e);
+    if (cells == 0) return cudaSuccess;
+    sk<<<(unsigned)cells, vol ? surf_threads<N, true>() : surf_threads<N, false>(), ssm, stream>>>(kp, a, p.d_status);
+    return cudaGetLastError();
   }
   const size_t smem = sizeof(double) * (size_t)p.m * ((vol ? N * N * N + 8 : 0) + 6 * N * N);
   auto kern = elastic ? (vol ? correct_kernel<N, true, true> : correct_kernel<N, true, false>)
