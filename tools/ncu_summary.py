@@ -41,7 +41,11 @@ def main(rep, chunk=50):
     src = ncu_csv(rep, "--page", "source", "--print-source", "sass")
     h = src[1]
     isrc, iss = h.index("Source"), h.index("Warp Stall Sampling (All Samples)")
-    data = src[2:]
+    data = []
+    for r in src[2:]:  # the first kernel of the report (a second one starts with its own header)
+        if len(r) <= iss or not r[iss].strip().isdigit():
+            break
+        data.append(r)
     tot = sum(int(r[iss]) for r in data) or 1
     for i in range(0, len(data), chunk):
         part = data[i:i + chunk]
