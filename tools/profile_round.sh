@@ -15,6 +15,6 @@ for cfg in c3 c2 c4 n9; do
       python tools/profile_stp.py --config $cfg --elems $E > $OUT/ncu_$cfg.log 2>&1 || true
 done
 python tools/profile_corrector.py > $OUT/plain_corr.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:correct_kernel -c 2 -o $OUT/full_corr \
+ncu --set full --clock-control none --import-source on -k regex:"correct_kernel|surface_kernel" -c 2 -o $OUT/full_corr \
     python tools/profile_corrector.py > $OUT/ncu_corr.log 2>&1 || true
 ls -la $OUT
