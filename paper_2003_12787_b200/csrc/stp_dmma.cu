@@ -32,6 +32,10 @@ int aderstp_dbg_clock2_copy(long long* host, int count) {
 #endif
 }
 
+#ifndef DMMAP_MAXN
+#define DMMAP_MAXN 7
+#endif
+
 namespace aderstp {
 
 namespace {
@@ -51,6 +55,9 @@ struct GeoP {
   static constexpr int TC = 4 * N + (12 * H0 > 4 * N ? 12 * H0 : 4 * N);
   static constexpr int TCOLS = TC <= 32 ? 32 : TC <= 64 ? 64 : 128;
 };
+
+template <int N>
+constexpr int role_planes() { return N > 3 * GeoP<N>::H0 ? N : 3 * GeoP<N>::H0; }
 
 struct ParamsP {
   double d[64];      // zero-padded D
@@ -214,8 +221,8 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   constexpr int PV = G::PV, FACE = G::FACE;
   extern __shared__ __align__(16) double smq[];
   __shared__ uint32_t tmem_base_s;
-  double* P = smq;              // staging: c_(N-1) q; then the Horner ping-pong pair (P, Q)
-  double* Q = smq + NVP * PV;   // staging: q (moved to TMEM before the first step)
+  double* P = smq;              // c_(N-1) q (staging), then the Horner ping-pong pair (P, Q)
+  double* Q = smq + NVP * PV;   // the other buffer of the Horner ping-pong pair
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -248,59 +255,57 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     c4[3] = 1.0 / rho;
   }
 
-  // ---- stage q into the padded planes (padding = 0): Q = q, P = c_(n-1) q -----------------
-  // (s, k3, k2 < 8, k1-pair < 4) positions, IT per thread; every load is issued before the
-  // first shared store so the DRAM latencies overlap
-  {
-    const int qs = kp.q_stride;
-    const double* qe = a.q + e * (long long)(N * N * N * qs);
-    constexpr int PAIRS = NVP * N * 32;
-    constexpr int IT = (PAIRS + THREADSP - 1) / THREADSP;
-    double v0[IT], v1[IT];
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int i = tid + it * THREADSP;
-      const int kp2 = i & 3, k2 = (i >> 2) & 7, r = i >> 5;  // r = s * N + k3
-      const int s = r / N, k3 = r - s * N;
-      const int k1 = 2 * kp2;
-      v0[it] = v1[it] = 0.0;
-      if (i < PAIRS && k2 < N) {
-        const double* src = qe + ((k3 * N + k2) * qs + s) * N;
-        if (k1 < N) v0[it] = __ldcs(src + k1);
-        if (k1 + 1 < N) v1[it] = __ldcs(src + k1 + 1);
-      }
-    }
-#pragma unroll
-    for (int it = 0; it < IT; ++it) {
-      const int i = tid + it * THREADSP;
-      if (i >= PAIRS) continue;
-      const int kp2 = i & 3, k2 = (i >> 2) & 7, r = i >> 5;
-      const int s = r / N, k3 = r - s * N;
-      if (kp.check && !(isfinite(v0[it]) && isfinite(v1[it]))) flags |= 1u;
-      const int j = s * PV + k3 * 64 + physp(k2, 2 * kp2);
-      sts2p(Q + j, v0[it], v1[it]);
-      sts2p(P + j, kp.cf[N - 1] * v0[it], kp.cf[N - 1] * v1[it]);
-    }
-  }
-  __syncthreads();
-  TM2(1);
   const int role = kRoleP[warp];
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];
 
-  // ---- q -> tensor memory (thread-private columns), then P / Q become a ping-pong pair ----
-  // role warps keep their quantity's N node pairs (4N columns), the normal-stress warps the
-  // three normal stresses of their k3 half (12 columns per plane); warps w and w + 4 share a
-  // TMEM lane quarter, so the upper four warps start at column 4N.
+  // ---- stage q straight into tensor memory and the first Horner iterate ---------------------
+  // Every warp loads exactly the (quantity, k3) planes it keeps in TMEM -- role warps their
+  // quantity on all N planes, the normal-stress warps sxx, syy, szz on their k3 half -- as the
+  // node pair (k2 = g, k1 = 2t, 2t+1) of lane (g, t), i.e. in the C-fragment layout of the CK
+  // step.  q goes register -> TMEM (thread-private columns: warps w and w + 4 share a lane
+  // quarter, the upper four start at column 4N) and c_(N-1) q -> P, padding lanes writing the
+  // zero padding; q never passes through shared memory.  Every global load is issued before the
+  // barrier that publishes the TMEM base address, so the DRAM/L2 latency overlaps it.
+  const bool ok0 = g < N && 2 * t < N, ok1 = g < N && 2 * t + 1 < N;
+  const double* qe = a.q + e * (long long)(N * N * N * kp.q_stride);
+  auto ldq = [&](int sq, int k3, double& v0, double& v1) {
+    const double* src = qe + ((k3 * N + g) * kp.q_stride + sq) * N + 2 * t;
+    if (N % 2 == 0) {  // 16-byte aligned pair (q_stride * N even)
+      double2 v = ok0 ? __ldcs(reinterpret_cast<const double2*>(src)) : make_double2(0.0, 0.0);
+      v0 = v.x;
+      v1 = v.y;
+    } else {
+      v0 = ok0 ? __ldcs(src) : 0.0;
+      v1 = ok1 ? __ldcs(src + 1) : 0.0;
+    }
+  };
+  constexpr int NQ = role_planes<N>();  // planes staged per warp: max(N, 3 H0)
+  double qv[NQ][2];
+  if (role >= 0) {
+#pragma unroll
+    for (int k3 = 0; k3 < N; ++k3) ldq(role, k3, qv[k3][0], qv[k3][1]);
+  } else {
+    const int h = -role - 1, K0 = h ? G::H0 : 0, NT = h ? G::H1 : G::H0;
+#pragma unroll
+    for (int k = 0; k < G::H0; ++k)
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (k < NT) ldq(j, K0 + k, qv[3 * k + j][0], qv[3 * k + j][1]);
+  }
+  tm_fence_before();
+  __syncthreads();  // the TMEM base address (warp 0's tcgen05.alloc) is visible
   tm_fence_after();
   const uint32_t tq = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp < 4 ? 0 : 4 * N);
   {
+    const double c0 = kp.cf[N - 1];
     if (role >= 0) {
 #pragma unroll
       for (int k3 = 0; k3 < N; ++k3) {
-        const double2 v = lds2p(Q + role * PV + k3 * 64 + col);
+        if (kp.check && !(isfinite(qv[k3][0]) && isfinite(qv[k3][1]))) flags |= 1u;
+        sts2p(P + role * PV + k3 * 64 + col, c0 * qv[k3][0], c0 * qv[k3][1]);
         uint32_t r[4];
-        tm_split(v.x, r, 0);
-        tm_split(v.y, r, 1);
+        tm_split(qv[k3][0], r, 0);
+        tm_split(qv[k3][1], r, 1);
         tm_st4(tq + 4 * k3, r);
       }
     } else {
@@ -311,17 +316,20 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
         uint32_t r[12];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-          const double2 v = lds2p(Q + j * PV + (K0 + k) * 64 + col);
-          tm_split(v.x, r, 2 * j);
-          tm_split(v.y, r, 2 * j + 1);
+          const double v0 = qv[3 * k + j][0], v1 = qv[3 * k + j][1];
+          if (kp.check && !(isfinite(v0) && isfinite(v1))) flags |= 1u;
+          sts2p(P + j * PV + (K0 + k) * 64 + col, c0 * v0, c0 * v1);
+          tm_split(v0, r, 2 * j);
+          tm_split(v1, r, 2 * j + 1);
         }
         tm_st8(tq + 12 * k, r);
         tm_st4(tq + 12 * k + 8, r + 8);
       }
     }
     tm_wait_st();
-    __syncthreads();  // every q is in TMEM: the Q buffer takes the first Horner iterate
+    __syncthreads();  // P = c_(N-1) q complete; Q takes the first Horner iterate
   }
+  TM2(1);
 
   // ---- CK series in Horner form (stp_dmma8.cu): r <- c_o q + L r, o = N-2 .. 0 ----------
   // step i reads buffer i % 2 and writes (i + 1) % 2: 0 = P (c_(N-1) q), 1 = Q; one barrier
@@ -582,7 +590,7 @@ cudaError_t launch_dmmap_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t
 }  // namespace
 
 bool dmmap_applicable(const LaunchPlan& p) {
-  return p.n >= 4 && p.n <= 7 && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
+  return p.n >= 4 && p.n <= DMMAP_MAXN && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
          p.layout == ADERSTP_LAYOUT_AOSOA && p.out_stride == 9 && p.q_stride >= 9 && p.q_stride <= 64;
 }
 
@@ -599,6 +607,9 @@ cudaError_t launch_dmmap(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
     case 5: return launch_dmmap_n<5>(p, a, stream);
     case 6: return launch_dmmap_n<6>(p, a, stream);
     case 7: return launch_dmmap_n<7>(p, a, stream);
+#if DMMAP_MAXN >= 8
+    case 8: return launch_dmmap_n<8>(p, a, stream);
+#endif
   }
   return cudaErrorInvalidValue;
 }
