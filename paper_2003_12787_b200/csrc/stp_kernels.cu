@@ -575,6 +575,67 @@ __global__ void __launch_bounds__(256) convert_rows_kernel(int n, int m, long lo
   }
 }
 
+// Fast path of the conversion for the drop-in pair: the reference's AoS rows [k1][s < 16] (m = 9,
+// padding slots 9..15) <-> compact AoSoA rows [s < 9][k1], even n.  16-byte loads and stores,
+// compile-time indexing, the AoS padding slots neither read (AoS -> AoSoA: 80 of the 128 bytes of
+// a node) nor staged (AoSoA -> AoS: written as zeros); the tile rows are padded (stride n + 1 per
+// quantity) so that both sides of the transpose are bank-conflict free.
+template <int N, bool TO_AOSOA>
+__global__ void __launch_bounds__(256) convert_rows16_kernel(long long rows, const double* __restrict__ src,
+                                                             double* __restrict__ dst) {
+  constexpr int R = kConvRows, M = 9, TS = N + 1, TROW = M * TS;  // tile: [r][s][k1 (+1 pad)]
+  constexpr int AROW = N * 16, CROW = N * M;                        // AoS / AoSoA row lengths
+  __shared__ double tile[R * TROW];
+  for (long long r0 = (long long)blockIdx.x * R; r0 < rows; r0 += (long long)gridDim.x * R) {
+    const int nr = (int)(rows - r0 < R ? rows - r0 : R);
+    if (TO_AOSOA) {
+      // AoS source: per node k1 the pairs (s, s + 1), s = 0, 2, 4, 6, 8 (slot 9 is padding)
+      const double* s0 = src + r0 * AROW;
+      for (int i = threadIdx.x; i < nr * N * 5; i += blockDim.x) {
+        const int r = i / (N * 5), j = i - r * (N * 5), k1 = j / 5, sp = 2 * (j - k1 * 5);
+        const double2 v = *reinterpret_cast<const double2*>(s0 + r * AROW + k1 * 16 + sp);
+        tile[r * TROW + sp * TS + k1] = v.x;
+        if (sp + 1 < M) tile[r * TROW + (sp + 1) * TS + k1] = v.y;
+      }
+      __syncthreads();
+      double* d0 = dst + r0 * CROW;
+      for (int i = threadIdx.x; i < nr * CROW / 2; i += blockDim.x) {
+        const int r = i / (CROW / 2), j = 2 * (i - r * (CROW / 2)), sq = j / N, k1 = j - sq * N;
+        const double* t = tile + r * TROW + sq * TS + k1;
+        *reinterpret_cast<double2*>(d0 + r * CROW + j) = make_double2(t[0], t[1]);
+      }
+    } else {
+      const double* s0 = src + r0 * CROW;
+      for (int i = threadIdx.x; i < nr * CROW / 2; i += blockDim.x) {
+        const int r = i / (CROW / 2), j = 2 * (i - r * (CROW / 2)), sq = j / N, k1 = j - sq * N;
+        const double2 v = *reinterpret_cast<const double2*>(s0 + r * CROW + j);
+        tile[r * TROW + sq * TS + k1] = v.x;
+        tile[r * TROW + sq * TS + k1 + 1] = v.y;
+      }
+      __syncthreads();
+      double* d0 = dst + r0 * AROW;
+      for (int i = threadIdx.x; i < nr * AROW / 2; i += blockDim.x) {
+        const int r = i / (AROW / 2), j = i - r * (AROW / 2), k1 = j >> 3, sp = 2 * (j & 7);
+        const double* t = tile + r * TROW + k1;
+        const double a = sp < M ? t[sp * TS] : 0.0, b = sp + 1 < M ? t[(sp + 1) * TS] : 0.0;
+        *reinterpret_cast<double2*>(d0 + r * AROW + 16 * k1 + sp) = make_double2(a, b);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int N>
+cudaError_t launch_convert16(bool to_aosoa, long long rows, const double* src, double* dst, cudaStream_t stream) {
+  long long blocks = (rows + kConvRows - 1) / kConvRows;
+  if (blocks > 148LL * 16) blocks = 148LL * 16;
+  if (to_aosoa)
+    convert_rows16_kernel<N, true><<<(unsigned)blocks, 256, 0, stream>>>(rows, src, dst);
+  else
+    convert_rows16_kernel<N, false><<<(unsigned)blocks, 256, 0, stream>>>(rows, src, dst);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_convert(int n, int m, long long n_elem, int src_layout, int src_stride,
                            const double* src, int dst_layout, int dst_stride, double* dst,
                            cudaStream_t stream) {
@@ -582,6 +643,20 @@ cudaError_t launch_convert(int n, int m, long long n_elem, int src_layout, int s
   if (total == 0) return cudaSuccess;
   if (src_layout != dst_layout) {  // AoS <-> AoSoA: row transposes through shared memory
     const long long rows = n_elem * n * n;
+    const bool al16 = ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+    const bool pair16 = m == 9 && al16 && n % 2 == 0 &&
+                        ((src_layout == ADERSTP_LAYOUT_AOS && src_stride == 16 && dst_stride == 9) ||
+                         (dst_layout == ADERSTP_LAYOUT_AOS && dst_stride == 16 && src_stride == 9));
+    if (pair16) {
+      const bool to_aosoa = dst_layout == ADERSTP_LAYOUT_AOSOA;
+      switch (n) {
+        case 2: return launch_convert16<2>(to_aosoa, rows, src, dst, stream);
+        case 4: return launch_convert16<4>(to_aosoa, rows, src, dst, stream);
+        case 6: return launch_convert16<6>(to_aosoa, rows, src, dst, stream);
+        case 8: return launch_convert16<8>(to_aosoa, rows, src, dst, stream);
+        case 10: return launch_convert16<10>(to_aosoa, rows, src, dst, stream);
+      }
+    }
     long long blocks = (rows + kConvRows - 1) / kConvRows;
     if (blocks > 148LL * 32) blocks = 148LL * 32;
     const size_t smem = sizeof(double) * kConvRows * n * src_stride;
