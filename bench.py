@@ -242,6 +242,38 @@ def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
     return res
 
 
+def measure_reference_layout(S, cfg, steps, warmup):
+    """The drop-in boundary on the reference's own element layout: C3's workload (nDof 8,
+    131,072 elements, per-element material) held as ElementTensor AoS rows (quantity padded to
+    m_pad = 16, proj/src/layout.cpp:9-21) in and PredictorOutput AoS rows out.  Device-resident,
+    CUDA events; the plan transposes to/from the tuned kernel's AoSoA on the device."""
+    import torch
+    n, E = cfg["n"], cfg["elems"]
+    q9, par = S.generate(cfg["dist"], SEED, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
+    q = torch.empty(E, n ** 3 * 16, dtype=torch.float64, device="cuda")
+    S.convert_layout(n, 9, E, S.LAYOUT_AOSOA, 9, q9, S.LAYOUT_AOS, 16, q)
+    del q9
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOS, q_stride=16, out_stride=16, par_kind=S.PAR_RHO_CP_CS)
+    out = plan.alloc_output(E)
+    dt = S.stable_dt(n, float(par[:, 1].max()), cfl=0.5)
+    for _ in range(warmup):
+        plan.predict(q, dt, par=par, out=out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        plan.predict(q, dt, par=par, out=out)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    plan.status()
+    ms = ev0.elapsed_time(ev1) / steps
+    del q, out
+    return {"workload": "C3 on the reference layout: ElementTensor AoS (m_pad 16) in, PredictorOutput AoS out",
+            "elements_per_s": E / (ms * 1e-3), "ms_per_step": ms,
+            "path": "device AoS->AoSoA transpose, stp_dmma8, AoSoA->AoS transposes (qavg, favg)"}
+
+
 def measure_timestep(S, n, e, steps, warmup):
     """One full time step of the GPU solver on an e^3 periodic mesh: the
     predictor on the 1/h-scaled PDE without favg (the corrector never reads it, solver.cpp:184-253)
@@ -479,6 +511,7 @@ def main():
                             "roofline_elements_per_s": rf["roofline_elements_per_s"],
                             "frac_of_roofline": pg / rf["roofline_elements_per_s"], "bound": rf["bound"]}
         others["timestep_n8"] = measure_timestep(S, 8, 50, max(5, args.steps // 4), 3)
+        others["c3_reference_layout"] = measure_reference_layout(S, CONFIGS["c3"], max(5, args.steps // 4), 3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
