@@ -43,6 +43,7 @@ struct LaunchPlan {
   int dmma8_prefetch = 0;            // L2 prefetch distance (elements) of q; env ADERSTP_PREFETCH, 0 = off
   int aos_chunk = 0;                 // env ADERSTP_AOS_CHUNK: elements per chunk of the AoS staged path (tests)
   int pass_slots = 0;                // env ADERSTP_PASS_SLOTS: 6 = line-pass kernel, 12 = bipartite, 0 auto
+  int aos_staged = 0;                // env ADERSTP_AOS_STAGED=1: reference layout through the transposes
   int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel
 };
 
@@ -101,6 +102,7 @@ cudaError_t launch_generate(int dist, uint64_t seed, int n, long long e0, long l
 bool kernel_available(int n);
 // stp_dmma8.cu: nDof = 8 elastic kernel on the fp64 tensor cores
 bool dmma8_applicable(const LaunchPlan& p);
+bool dmma8_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
 cudaError_t init_dmma8(const LaunchPlan& p);  // once per device, at plan creation
 // stp_dmma.cu: nDof 4..7 on zero-padded 8x8 DMMA tiles
 bool dmmap_applicable(const LaunchPlan& p);

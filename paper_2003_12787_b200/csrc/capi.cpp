@@ -181,6 +181,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const char* pf = std::getenv("ADERSTP_PREFETCH");
     lp.dmma8_prefetch = pf ? std::atoi(pf) : sms;
+    const char* as = std::getenv("ADERSTP_AOS_STAGED");
+    lp.aos_staged = (as && as[0] == '1') ? 1 : 0;
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");
     lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
     const char* ac = std::getenv("ADERSTP_AOS_CHUNK");
@@ -364,6 +366,14 @@ cudaError_t predict_aos_staged(const aderstp_plan* plan, const aderstp::BatchArg
 
 }  // namespace
 
+// the device-side dispatch of one batch: the reference layout straight into the nDof 8 kernel,
+// through the device transposes for the other orders, every other case to launch_stp
+cudaError_t predict_device(const aderstp_plan* p, const aderstp::BatchArgs& a, cudaStream_t st) {
+  if (aderstp::dmma8_aos_applicable(p->lp, a)) return aderstp::launch_dmma8(p->lp, a, st);
+  if (aos_staged(p->lp) && p->pool) return predict_aos_staged(p, a, st);
+  return aderstp::launch_stp(p->lp, a, st);
+}
+
 int aderstp_predict_batch(const aderstp_plan* p, int64_t n_elem, const double* q,
                           const double* par, double dt, double t_start, double* qavg,
                           double* favg, double* face_q, double* face_f, void* stream) {
@@ -372,7 +382,7 @@ int aderstp_predict_batch(const aderstp_plan* p, int64_t n_elem, const double* q
   if (n_elem == 0) return ADERSTP_OK;
   aderstp::BatchArgs a{q, par, qavg, favg, face_q, face_f, (long long)n_elem, dt, t_start};
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  cudaError_t e = (aos_staged(p->lp) && p->pool) ? predict_aos_staged(p, a, st) : aderstp::launch_stp(p->lp, a, st);
+  cudaError_t e = predict_device(p, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "predict_batch launch");
   return ADERSTP_OK;
 }
@@ -475,7 +485,7 @@ int aderstp_predict_batch_host(aderstp_plan* p, int64_t n_elem, const double* q,
     if (e == cudaSuccess) {
       aderstp::BatchArgs a{dq, elastic ? dpar : nullptr, dqa, favg ? dfa : nullptr,
                            face_q ? dfq : nullptr, face_f ? dff : nullptr, (long long)cnt, dt, t_start};
-      e = aderstp::launch_stp(p->lp, a, st);
+      e = predict_device(p, a, st);
     }
     if (e == cudaSuccess)
       e = cudaMemcpyAsync(qavg + done * c.qavg, dqa, sizeof(double) * c.qavg * cnt, cudaMemcpyDeviceToHost, st);

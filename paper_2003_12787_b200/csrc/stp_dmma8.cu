@@ -188,7 +188,7 @@ __device__ __forceinline__ void dfma_z(double (&acc)[NT][2], const double* f, in
 // un (fused time-step mode, else null): this lane's base in the next state u_next; one more step
 // with coefficient 1 then gives u_next = q + L(qavg) (the corrector's volume term) in registers
 // and goes straight to HBM.  urow = doubles per (k3, k2) row of u_next.
-template <int NT, bool FUSED>
+template <int NT, bool FUSED, int PS>
 __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const double* cf, int s, int K0, int g,
                                             int t, int col, double d0, double d1, const double (&c4)[4],
                                             double* un, int urow) {
@@ -197,7 +197,7 @@ __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const do
   const bool has_x = kCoef[s][0] != 4, has_y = kCoef[s][1] != 4, has_z = kCoef[s][2] != 4;
   const double bx0 = cx * d0, bx1 = cx * d1;  // B-fragments of c_x D^T
   const double ay0 = cy * d0, ay1 = cy * d1;  // A-fragments of c_y D
-  const int own = s * PV + K0 * 64 + col;
+  const int own = s * PS + K0 * 64 + col;
   constexpr int o_end = FUSED ? -1 : 0;
 #pragma unroll 1
   for (int o = N8 - 2; o >= o_end; --o) {
@@ -209,9 +209,9 @@ __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const do
       tt[k][0] = co * v.x;
       tt[k][1] = co * v.y;
     }
-    if (has_x) mma_x<NT>(tt, P + in_x * PV, K0, g, t, bx0, bx1);
-    if (has_y) mma_y<NT>(tt, P + in_y * PV, K0, g, t, ay0, ay1);
-    if (has_z) dfma_z<NT>(tt, P + in_z * PV, K0, col, cz);
+    if (has_x) mma_x<NT>(tt, P + in_x * PS, K0, g, t, bx0, bx1);
+    if (has_y) mma_y<NT>(tt, P + in_y * PS, K0, g, t, ay0, ay1);
+    if (has_z) dfma_z<NT>(tt, P + in_z * PS, K0, col, cz);
     if (FUSED && o < 0) {  // fused: u_next = q + L(qavg)
 #pragma unroll
       for (int k = 0; k < NT; ++k) st_cs2(un + ((K0 + k) * 8) * urow + s * 8, tt[k][0], tt[k][1]);
@@ -226,7 +226,7 @@ __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const do
 
 // Normal stresses on k3 tiles K0 .. K0+NT-1: a = Dx u, b = Dy v, c = Dz w (unscaled), then
 // t_sxx = lambda (a+b+c) + 2 mu a, etc. (proj/src/pde.cpp:180-190)
-template <int NT, bool FUSED>
+template <int NT, bool FUSED, int PS>
 __device__ __forceinline__ void ck_normal(double* P, const double* Q, const double* cf, int K0, int g, int t,
                                           int col, double d0, double d1, const double (&c4)[4], double* un,
                                           int urow) {
@@ -238,13 +238,13 @@ __device__ __forceinline__ void ck_normal(double* P, const double* Q, const doub
     double ta[NT][2], tb[NT][2], tc[NT][2];
 #pragma unroll
     for (int k = 0; k < NT; ++k) ta[k][0] = ta[k][1] = tb[k][0] = tb[k][1] = tc[k][0] = tc[k][1] = 0.0;
-    mma_x<NT>(ta, P + 6 * PV, K0, g, t, d0, d1);
-    mma_y<NT>(tb, P + 7 * PV, K0, g, t, d0, d1);
-    dfma_z<NT>(tc, P + 8 * PV, K0, col, 1.0);
+    mma_x<NT>(ta, P + 6 * PS, K0, g, t, d0, d1);
+    mma_y<NT>(tb, P + 7 * PS, K0, g, t, d0, d1);
+    dfma_z<NT>(tc, P + 8 * PS, K0, col, 1.0);
 #pragma unroll
     for (int k = 0; k < NT; ++k) {
       const int off = (K0 + k) * 64 + col;
-      const double2 qa = lds2(Q + off), qb = lds2(Q + PV + off), qc = lds2(Q + 2 * PV + off);
+      const double2 qa = lds2(Q + off), qb = lds2(Q + PS + off), qc = lds2(Q + 2 * PS + off);
       const double qv[3][2] = {{qa.x, qa.y}, {qb.x, qb.y}, {qc.x, qc.y}};
 #pragma unroll
       for (int j = 0; j < 2; ++j) {
@@ -269,20 +269,31 @@ __device__ __forceinline__ void ck_normal(double* P, const double* Q, const doub
     for (int k = 0; k < NT; ++k) {
       const int off = (K0 + k) * 64 + col;
       sts2(P + off, ta[k][0], ta[k][1]);
-      sts2(P + PV + off, tb[k][0], tb[k][1]);
-      sts2(P + 2 * PV + off, tc[k][0], tc[k][1]);
+      sts2(P + PS + off, tb[k][0], tb[k][1]);
+      sts2(P + 2 * PS + off, tc[k][0], tc[k][1]);
     }
     __syncthreads();
   }
 }
 
-template <bool FUSED>
+// AOS: the reference's own layout, ElementTensor rows [k3][k2][k1][s < 16] in and PredictorOutput
+// rows out (proj/src/layout.cpp:9-21, padding slots 9..15 written as zeros), no transposes: the
+// quantity planes are staged from the node rows, and qavg / favg leave as whole 128-byte node rows
+// (4 nodes per warp instruction) from the planes after the recursion.  Shared-memory planes are
+// then 514 doubles apart, so that the 5 slot pairs of a node stored by neighbouring lanes fall on
+// different banks (a uniform shift per plane: the fragment and column accesses stay conflict free).
+template <bool AOS>
+constexpr int plane_stride() { return AOS ? PV + 2 : PV; }
+
+template <bool FUSED, bool AOS = false>
 __global__ void __maxnreg__(80)
 stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
+  static_assert(!(FUSED && AOS), "the time loop runs on AoSoA");
   constexpr int THREADS8 = NWARP * 32;
+  constexpr int PS = plane_stride<AOS>();
   extern __shared__ __align__(16) double sm8[];
   double* P = sm8;            // Horner iterate r   [9][8][8][8] swizzled; qavg at the end
-  double* Q = sm8 + NV * PV;  // q (constant during the recursion)
+  double* Q = sm8 + NV * PS;  // q (constant during the recursion)
   const long long e = blockIdx.x;
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -298,7 +309,9 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     const long long nx = e + kp.prefetch;
     if (nx < a.n_elem) {
       const double* row = a.q + nx * (long long)(PV * kp.q_stride) + tid * kp.q_stride * 8;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(row), "r"(NV * 8 * 8) : "memory");
+      // AOS: the (k3, k2) row is 8 whole node rows (the used slots are not contiguous)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(row), "r"(AOS ? 8 * 16 * 8 : NV * 8 * 8)
+                   : "memory");
     }
   }
 
@@ -326,7 +339,28 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   // ---- stage q: AoSoA [k3][k2][s < QS][k1] -> Q = q and P = c_(n-1) q ------------------
   // 64 rows (k3,k2) x 9 quantities x 4 k1-pairs = 2304 pairs = 9 per thread; every load is
   // issued before the first shared store so their latencies overlap.
-  {
+  if constexpr (AOS) {  // node rows [k3][k2][k1][s < 16]: 512 nodes x 5 slot pairs (slot 9 unused)
+    const double* qe = a.q + e * (long long)(PV * 16);
+    constexpr int IT = 512 * 5 / THREADS8;
+    double2 v[IT];
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int i = tid + it * THREADS8, node = i / 5, sp = 2 * (i - node * 5);
+      v[it] = ld_nc2(qe + node * 16 + sp);
+    }
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      const int i = tid + it * THREADS8, node = i / 5, sp = 2 * (i - node * 5);
+      if (kp.check && !(isfinite(v[it].x) && (sp == 8 || isfinite(v[it].y)))) flags |= 1u;
+      const int j = sp * PS + (node >> 6) * 64 + phys((node >> 3) & 7, node & 7);
+      Q[j] = v[it].x;
+      P[j] = kp.cf[N8 - 1] * v[it].x;
+      if (sp < 8) {
+        Q[j + PS] = v[it].y;
+        P[j + PS] = kp.cf[N8 - 1] * v[it].y;
+      }
+    }
+  } else {
     const double* qe = a.q + e * (long long)(PV * kp.q_stride);
     constexpr int IT = (2304 + THREADS8 - 1) / THREADS8;
     double2 v[IT];
@@ -342,7 +376,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
       if (2304 % THREADS8 != 0 && i >= 2304) break;
       const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
       if (kp.check && !(isfinite(v[it].x) && isfinite(v[it].y))) flags |= 1u;
-      const int j = si * PV + (k32 >> 3) * 64 + phys(k32 & 7, 2 * (i & 3));
+      const int j = si * PS + (k32 >> 3) * 64 + phys(k32 & 7, 2 * (i & 3));
       sts2(Q + j, v[it].x, v[it].y);
       sts2(P + j, kp.cf[N8 - 1] * v[it].x, kp.cf[N8 - 1] * v[it].y);
     }
@@ -359,9 +393,9 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     const int urow = kp.q_stride * 8;
     double* un = FUSED ? a.u_next + e * (long long)(PV * kp.q_stride) + g * urow + 2 * t : nullptr;
     if (role >= 0)
-      ck_quantity<8, FUSED>(P, Q, kp.cf, role, 0, g, t, col, d0, d1, c4, un, urow);
+      ck_quantity<8, FUSED, PS>(P, Q, kp.cf, role, 0, g, t, col, d0, d1, c4, un, urow);
     else
-      ck_normal<4, FUSED>(P, Q, kp.cf, 4 * (-role - 1), g, t, col, d0, d1, c4, un, urow);
+      ck_normal<4, FUSED, PS>(P, Q, kp.cf, 4 * (-role - 1), g, t, col, d0, d1, c4, un, urow);
     if (FUSED) __syncthreads();  // q (the Q region) is read until here; faces stage over it
   }
 
@@ -379,7 +413,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     const int unit = kUnits[warp][ku];
     if (unit < 0) break;
     const int s = unit >> 1, h = unit & 1, K0 = 4 * h;
-    const double* qs = P + s * PV;
+    const double* qs = P + s * PS;
     double qa[4][2];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -387,12 +421,12 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
       qa[k][0] = v.x;
       qa[k][1] = v.y;
     }
-    if (!FUSED || a.qavg) {
+    if (!AOS && (!FUSED || a.qavg)) {
       double* qout = a.qavg + e * (long long)(PV * NV) + s * 8 + 2 * t;
 #pragma unroll
       for (int k = 0; k < 4; ++k) st_cs2(qout + ((K0 + k) * 8 + g) * NV * 8, qa[k][0], qa[k][1]);
     }
-    if (a.favg) {
+    if (!AOS && a.favg) {
       double* fout = a.favg + e * (long long)(3 * PV * NV) + 2 * t;
       const int nout = kOutN[s];
 #pragma unroll 1
@@ -440,6 +474,39 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
           FQ[4 * FACE + (g * 8 + 2 * t + j) * NV + s] = z0[j];
           FQ[5 * FACE + (g * 8 + 2 * t + j) * NV + s] = z1[j];
         }
+      }
+    }
+  }
+  if constexpr (AOS) {
+    // qavg and favg as whole node rows [node][s < 16]: lane = (node ns of 4, slot pair c), so a
+    // warp instruction writes 4 x 128 contiguous bytes; the flux table entries of the lane's two
+    // slots are fixed per lane (F_d(q)_so = coef(so, d) q[in(so, d)], proj/src/pde.cpp:180-218)
+    const int ns = lane >> 3, c2 = 2 * (lane & 7);
+    int src[3][2];
+    double cfo[3][2];
+    bool val[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int so = c2 + j;
+      val[j] = so < NV;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ci = val[j] ? kCoef[so][d] : 4;
+        src[d][j] = val[j] ? kIn[so][d] : 0;
+        cfo[d][j] = ci == 4 ? 0.0 : sel4(c4, ci);
+      }
+    }
+    double* qo = a.qavg + e * (long long)(PV * 16);
+    double* fo = a.favg ? a.favg + e * (long long)(3 * PV * 16) : nullptr;
+#pragma unroll 1
+    for (int nb = 4 * warp + ns; nb < PV; nb += 4 * NWARP) {
+      const int pos = (nb >> 6) * 64 + phys((nb >> 3) & 7, nb & 7);
+      st_cs2(qo + nb * 16 + c2, val[0] ? P[c2 * PS + pos] : 0.0, val[1] ? P[(c2 + 1) * PS + pos] : 0.0);
+      if (fo) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          st_cs2(fo + d * (PV * 16) + nb * 16 + c2, cfo[d][0] != 0.0 ? cfo[d][0] * P[src[d][0] * PS + pos] : 0.0,
+                 cfo[d][1] != 0.0 ? cfo[d][1] * P[src[d][1] * PS + pos] : 0.0);
       }
     }
   }
@@ -509,6 +576,15 @@ bool dmma8_applicable(const LaunchPlan& p) {
          p.out_stride == 9 && p.q_stride >= 9 && p.q_stride <= 64;
 }
 
+// the reference's own layout straight into the kernel: ElementTensor AoS rows with the quantity
+// padded to 16 (proj/src/layout.cpp:9-21) in and out, 16-byte aligned buffers
+bool dmma8_aos_applicable(const LaunchPlan& p, const BatchArgs& a) {
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  return p.n == 8 && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 && p.layout == ADERSTP_LAYOUT_AOS &&
+         p.q_stride == 16 && p.out_stride == 16 && !p.force_generic && !p.no_dmma8 && !p.aos_staged &&
+         !a.u_next && al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) && al16(a.face_f);
+}
+
 cudaError_t init_dmma8(const LaunchPlan& p) {
   return cudaMemcpyToSymbol(aderstp_kD8, p.basis.d, sizeof(double) * 64);
 }
@@ -532,8 +608,9 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
       kp.cf[o] = c;
     }
   }
-  auto kern = a.u_next ? stp_dmma8_kernel<true> : stp_dmma8_kernel<false>;
-  int smem = kSmem8;
+  const bool aos = p.layout == ADERSTP_LAYOUT_AOS;  // dmma8_aos_applicable
+  auto kern = a.u_next ? stp_dmma8_kernel<true> : aos ? stp_dmma8_kernel<false, true> : stp_dmma8_kernel<false>;
+  int smem = aos ? 2 * NV * plane_stride<true>() * 8 : kSmem8;
 #ifdef ADERSTP_EXPT_TIMING
   if (const char* x = std::getenv("ADERSTP_EXPT_SMEM")) smem += std::atoi(x);  // occupancy experiments
 #endif

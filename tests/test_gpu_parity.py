@@ -313,8 +313,9 @@ def test_dense_volume_operator_taylor_series(stp, oracle):
 
 @pytest.mark.parametrize("n", [3, 6, 8, 10])
 def test_aos_staged_path_matches_generic_and_oracle(stp, oracle, monkeypatch, n):
-    """The reference layout (AoS, m_pad 16) runs through device transposes and the tuned kernel;
-    the generic kernel (ADERSTP_FORCE_GENERIC) on the same AoS buffers and the oracle agree."""
+    """The reference layout (AoS, m_pad 16) runs straight through stp_dmma8 (nDof 8) or through
+    device transposes and the tuned kernel; the generic kernel (ADERSTP_FORCE_GENERIC) on the same
+    AoS buffers and the oracle agree."""
     S = stp
     E = 11
     q, par = S.generate(1, 77 + n, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
@@ -323,16 +324,23 @@ def test_aos_staged_path_matches_generic_and_oracle(stp, oracle, monkeypatch, n)
     par_h = par.cpu().numpy()
     dt = O.cfl_dt(n, par_h[:, 1].max())
     ref = oracle.stp(n, 9, oracle.from_aosoa(n, 9, 9, q.cpu().numpy()), dt, par=oracle.material_lmr(par_h))
-    for generic, chunk in (("0", "0"), ("0", "4"), ("1", "0")):  # "4": three chunks, the last ragged
+    # default (nDof 8: straight into stp_dmma8), the transposes (one chunk, three chunks with the
+    # last ragged), the generic kernel on the AoS buffers
+    for generic, chunk, staged in (("0", "0", "0"), ("0", "0", "1"), ("0", "4", "1"), ("1", "0", "0")):
         monkeypatch.setenv("ADERSTP_FORCE_GENERIC", generic)
         monkeypatch.setenv("ADERSTP_AOS_CHUNK", chunk)
+        monkeypatch.setenv("ADERSTP_AOS_STAGED", staged)
         plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOS, q_stride=16, out_stride=16, par_kind=S.PAR_RHO_CP_CS)
         out = plan.predict(aos, dt, par=par)
         plan.status()
         worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOS, 16)
-        assert max(worst.values()) <= TOL, (generic, worst)
+        assert max(worst.values()) <= TOL, (generic, staged, worst)
         qa = out.qavg.cpu().numpy().reshape(E, n ** 3, 16)
         assert not np.any(qa[:, :, 9:])
+        if generic == "0" and chunk == "0":  # the host-buffer path takes the same device route
+            host = plan.predict_host(aos.cpu().numpy(), dt, par=par_h)
+            assert np.array_equal(host.qavg, out.qavg.cpu().numpy())
+            assert np.array_equal(host.face_f, out.face_f.cpu().numpy())
 
 
 def test_aos_plan_alone_in_a_fresh_process(stp):
