@@ -80,15 +80,6 @@ __constant__ int kInP[NVP][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8,
                                  {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
 __constant__ int kCoefP[NVP][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
                                    {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
-__constant__ int kOutNP[NVP] = {1, 1, 1, 3, 3, 3, 5, 5, 5};
-__constant__ int kOutP[NVP][5][3] = {
-    {{6, 0, 3}}, {{7, 1, 3}}, {{8, 2, 3}},
-    {{6, 1, 3}, {7, 0, 3}, {3, 2, 4}},
-    {{6, 2, 3}, {8, 0, 3}, {4, 1, 4}},
-    {{7, 2, 3}, {8, 1, 3}, {5, 0, 4}},
-    {{0, 0, 0}, {1, 0, 1}, {2, 0, 1}, {3, 1, 2}, {4, 2, 2}},
-    {{0, 1, 1}, {1, 1, 0}, {2, 1, 1}, {3, 0, 2}, {5, 2, 2}},
-    {{0, 2, 1}, {1, 2, 1}, {2, 2, 0}, {4, 0, 2}, {5, 1, 2}}};
 
 __device__ __forceinline__ double ldcp(const double* p) {
   double v;
@@ -228,7 +219,6 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   const int g = lane >> 2, t = lane & 3;
   const int col = physp(g, 2 * t);
   unsigned int flags = 0;
-  const double dt = a.dt;
   {
   const long long e = blockIdx.x;
   TM2(0);

@@ -57,25 +57,17 @@ __constant__ PassSlot kPass[3][6] = {
     {{6, 3, {0, 1, 2}, {0, 1, 1}}, {7, 1, {3}, {2}}, {8, 1, {4}, {2}}, {0, 1, {6}, {3}}, {3, 1, {7}, {3}}, {4, 1, {8}, {3}}},
     {{7, 3, {0, 1, 2}, {1, 0, 1}}, {6, 1, {3}, {2}}, {8, 1, {5}, {2}}, {3, 1, {6}, {3}}, {1, 1, {7}, {3}}, {5, 1, {8}, {3}}},
     {{8, 3, {0, 1, 2}, {1, 1, 0}}, {6, 1, {4}, {2}}, {7, 1, {5}, {2}}, {4, 1, {6}, {3}}, {5, 1, {7}, {3}}, {2, 1, {8}, {3}}}};
-// flux table for favg / face_f: F_d(q)_s = coef(s,d) q[in(s,d)], coef 4 = 0
-__constant__ int8_t kInE[NVE][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
-                                    {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
-__constant__ int8_t kCoefE[NVE][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
-                                      {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
 
 template <int N, int SL = 6>
 struct Geo {
-  static constexpr int H = N / 2;
   static constexpr int RS = (N % 2 == 0) ? N + 1 : N;  // odd row stride: conflict-free lines
   static constexpr int PL = N * RS;                    // k3 plane
   static constexpr int VS = N * PL;                    // one quantity
   static constexpr int ES = NVE * VS;                  // one tensor
   static constexpr int LINES = N * N;
-  static constexpr int SLOTS = SL;                     // tasks per line and pass
   static constexpr int TASKS = SL * LINES;             // per element per pass
   static constexpr int EPB = N <= 2 ? 16 : N == 3 ? 8 : N <= 4 ? 4 : N <= 6 ? 2 : 1;
   static constexpr int THREADS = ((TASKS * EPB + 31) / 32) * 32;
-  static constexpr int OUTV = NVE * N * N * N;         // qavg values per element
   static constexpr int QPT = (ES * EPB + THREADS - 1) / THREADS;  // qavg values per thread
   static constexpr int FQV = 6 * N * N * NVE;                        // face staging
   static constexpr int EB = ES + (ES > FQV ? ES : FQV);             // per-element doubles
@@ -600,22 +592,22 @@ __device__ __forceinline__ void bip_line(const double* src, double* const* dst, 
         }
       }
     }
-    return;
-  }
+  } else {
 #pragma unroll
-  for (int l = 0; l < N; ++l) p[l] = src[l * ST];
-  eo_apply<N>(p, out);
+    for (int l = 0; l < N; ++l) p[l] = src[l * ST];
+    eo_apply<N>(p, out);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) {
-    if (k < nt) {
-      double* d = dst[k];
-      const double c = cf[k];
-      if (write) {
+    for (int k = 0; k < 3; ++k) {
+      if (k < nt) {
+        double* d = dst[k];
+        const double c = cf[k];
+        if (write) {
 #pragma unroll
-        for (int l = 0; l < N; ++l) d[l * ST] = c * out[l];
-      } else {
+          for (int l = 0; l < N; ++l) d[l * ST] = c * out[l];
+        } else {
 #pragma unroll
-        for (int l = 0; l < N; ++l) d[l * ST] = fma(c, out[l], d[l * ST]);
+          for (int l = 0; l < N; ++l) d[l * ST] = fma(c, out[l], d[l * ST]);
+        }
       }
     }
   }
