@@ -371,3 +371,44 @@ print(worst)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stderr[-2000:]
     assert float(r.stdout.strip().splitlines()[-1]) <= TOL
+
+
+@pytest.mark.parametrize("n", [6, 8, 10])
+def test_reference_layout_checks_and_edges(stp, oracle, n):
+    """The reference (AoS, m_pad 16) layout on the tuned paths: non-finite DOFs flagged (slot 8
+    of a node is the tail of a 16-byte pair), padding slots never read (NaN there is harmless),
+    empty batch, and an unaligned batch (staged through the generic transposes) agreeing with the
+    aligned one."""
+    S = stp
+    E = 6
+    q, par = S.generate(0, 5 + n, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
+    aos = torch.empty(E, n ** 3 * 16, dtype=torch.float64, device="cuda")
+    S.convert_layout(n, 9, E, S.LAYOUT_AOSOA, 9, q, S.LAYOUT_AOS, 16, aos)
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOS, q_stride=16, out_stride=16, par_kind=S.PAR_RHO_CP_CS,
+                  check_inputs=True)
+    dt = O.cfl_dt(n, float(par[:, 1].max()))
+    assert plan.predict(aos[:0], dt, par=par[:0]).qavg.shape[0] == 0
+    ref = plan.predict(aos, dt, par=par)
+    plan.status()
+    padded = aos.clone().view(E, n ** 3, 16)
+    padded[:, :, 9:] = float("nan")  # ElementTensor padding lanes are never read
+    out = plan.predict(padded.view(E, -1), dt, par=par)
+    plan.status()
+    assert torch.equal(out.qavg, ref.qavg) and torch.equal(out.face_f, ref.face_f)
+    for slot in (0, 8):
+        bad = aos.clone().view(E, n ** 3, 16)
+        bad[E - 1, n ** 3 - 1, slot] = float("inf")
+        plan.predict(bad.view(E, -1), dt, par=par)
+        with pytest.raises(S.StpError) as e:
+            plan.status()
+        assert e.value.code == S.ADERSTP_ERR_NONFINITE
+    # an 8-byte offset batch cannot take the 16-byte paths: generic transposes, same results
+    buf = torch.empty(E * n ** 3 * 16 + 1, dtype=torch.float64, device="cuda")
+    buf[1:].copy_(aos.view(-1))
+    qoff = buf[1:].view(E, -1)
+    o2 = S.PredictorOutput(*(torch.empty(t.numel() + 1, dtype=torch.float64, device="cuda")[1:].view(t.shape)
+                             for t in (ref.qavg, ref.favg, ref.face_q, ref.face_f)))
+    plan.predict(qoff, dt, par=par, out=o2)
+    plan.status()
+    for a, b in ((o2.qavg, ref.qavg), (o2.favg, ref.favg), (o2.face_q, ref.face_q), (o2.face_f, ref.face_f)):
+        assert O.per_element_rel_diff(b.cpu().numpy().reshape(E, -1), a.cpu().numpy().reshape(E, -1)) <= TOL
