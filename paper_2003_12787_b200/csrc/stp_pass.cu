@@ -641,9 +641,13 @@ __device__ __forceinline__ void bip_line_z(const double* src, double* const* dst
   }
 }
 
-template <int N, bool FUSED = false>
+// AOS: the reference's ElementTensor / PredictorOutput node rows [k3][k2][k1][s < 16] in and out
+// (proj/src/layout.cpp:9-21): q is staged node-wise from the rows, qavg / favg leave as whole
+// 128-byte node rows (4 nodes per warp instruction, padding slots as zeros).
+template <int N, bool FUSED = false, bool AOS = false>
 __global__ void __launch_bounds__(GeoB<N>::THREADS, GeoB<N>::MINB)
 stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
+  static_assert(!(FUSED && AOS), "the time loop runs on AoSoA");
   using G = GeoB<N>;
   extern __shared__ __align__(16) double smb[];
   __shared__ uint32_t tmem_base_s;
@@ -694,7 +698,24 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   }
 
   // ---- stage q -> field slots 0..8 (node-wise, coalesced AoSoA loads; k1 pairs for even N) --
-  {
+  if constexpr (AOS) {  // node rows: slots 0..8 as four 16-byte pairs and one scalar
+    for (int i = tid; i < N3; i += G::THREADS) {
+      const double* src = a.q + e * (long long)(N3 * 16) + i * 16;
+      double* dst = E + (i / (N * N)) * G::PL + ((i / N) % N) * G::RS + i % N;
+      double2 v[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) v[j] = __ldcs(reinterpret_cast<const double2*>(src + 2 * j));
+      const double v8 = __ldcs(src + 8);
+      if (kp.check && !isfinite(v8)) flags |= 1u;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (kp.check && !(isfinite(v[j].x) && isfinite(v[j].y))) flags |= 1u;
+        dst[(2 * j) * G::VS] = v[j].x;
+        dst[(2 * j + 1) * G::VS] = v[j].y;
+      }
+      dst[8 * G::VS] = v8;
+    }
+  } else {
     const int qs = kp.q_stride;
     constexpr int V = N % 2 == 0 ? 2 : 1;  // nodes per task
     for (int i = tid; i < N3 / V; i += G::THREADS) {
@@ -772,7 +793,38 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   // taken from qavg before one more Horner step with coefficient 1 gives u + L(qavg)) ---------
   auto fld = [&](int s) { return s < 6 ? s : vb + (s - 6); };
   auto emit_qavg = [&]() {
-  if constexpr (N % 2 == 0) {  // k1 pairs: 16-byte shared loads and global stores
+  if constexpr (AOS) {
+    // lane = (node ns of 4, slot pair c2): 4 x 128 contiguous bytes per warp instruction; the
+    // flux table entries of the lane's two slots are fixed per lane
+    const int lane = tid & 31, ns = lane >> 3, c2 = 2 * (lane & 7);
+    int srcf[3][2], fl[2];
+    double cfo[3][2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int so = c2 + j;
+      fl[j] = so < NVE ? fld(so) : -1;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ci = so < NVE ? e_coef(so, d) : 4;
+        srcf[d][j] = so < NVE ? fld(e_in(so, d)) : 0;
+        cfo[d][j] = ci == 4 ? 0.0 : pick4(c4, ci);
+      }
+    }
+    double* qo = a.qavg + e * (long long)(N3 * 16);
+    double* fo = a.favg ? a.favg + e * (long long)(3 * N3 * 16) : nullptr;
+    for (int nb = 4 * warp + ns; nb < N3; nb += 4 * G::NW) {
+      const int pos = (nb / (N * N)) * G::PL + ((nb / N) % N) * G::RS + nb % N;
+      __stcs(reinterpret_cast<double2*>(qo + nb * 16 + c2),
+             make_double2(fl[0] >= 0 ? E[fl[0] * G::VS + pos] : 0.0, fl[1] >= 0 ? E[fl[1] * G::VS + pos] : 0.0));
+      if (fo) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          __stcs(reinterpret_cast<double2*>(fo + d * (N3 * 16) + nb * 16 + c2),
+                 make_double2(cfo[d][0] != 0.0 ? cfo[d][0] * E[srcf[d][0] * G::VS + pos] : 0.0,
+                              cfo[d][1] != 0.0 ? cfo[d][1] * E[srcf[d][1] * G::VS + pos] : 0.0));
+      }
+    }
+  } else if constexpr (N % 2 == 0) {  // k1 pairs: 16-byte shared loads and global stores
     for (int i = tid; i < N3 / 2; i += G::THREADS) {
       const int k1 = 2 * (i % (N / 2)), k32 = i / (N / 2);
       const double* qs = E + (k32 / N) * G::PL + (k32 % N) * G::RS + k1;
@@ -1009,7 +1061,8 @@ cudaError_t launch_bip_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   using G = GeoB<N>;
   PassParams<N> kp;
   fill_pass_params(p, a, kp);
-  auto kern = a.u_next ? stp_bip_kernel<N, true> : stp_bip_kernel<N, false>;
+  auto kern = a.u_next ? stp_bip_kernel<N, true> : p.layout == ADERSTP_LAYOUT_AOS ? stp_bip_kernel<N, false, true>
+                                                                                  : stp_bip_kernel<N, false>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM);
   if (err == cudaSuccess)
     err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
@@ -1046,10 +1099,26 @@ cudaError_t init_pass(const LaunchPlan& p) {
   return cudaMemcpyToSymbol(aderstp_kEO, buf, sizeof(buf), sizeof(double) * 80 * n);
 }
 
+// the reference's own layout straight into the bipartite kernel (nDof 9, 10)
+bool bip_aos_applicable(const LaunchPlan& p, const BatchArgs& a) {
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  return (p.n == 9 || p.n == 10) && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
+         p.layout == ADERSTP_LAYOUT_AOS && p.q_stride == 16 && p.out_stride == 16 && !p.force_generic &&
+         !p.aos_staged && p.pass_slots == 0 && !a.u_next && al16(a.q) && al16(a.qavg) && al16(a.favg);
+}
+
 bool bip_selected(const LaunchPlan& p, const BatchArgs& a) {
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   const bool vec_ok = (p.n % 2) || (al16(a.q) && al16(a.qavg) && al16(a.favg));
   return vec_ok && (p.n == 9 || p.n == 10) && (p.pass_slots == 12 || (p.pass_slots == 0 && p.n >= 9));
+}
+
+cudaError_t launch_bip(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
+  switch (p.n) {
+    case 9: return launch_bip_n<9>(p, a, stream);
+    case 10: return launch_bip_n<10>(p, a, stream);
+  }
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {

@@ -311,9 +311,9 @@ def test_dense_volume_operator_taylor_series(stp, oracle):
     assert O.rel_diff(want, got) < 1e-11
 
 
-@pytest.mark.parametrize("n", [3, 6, 8, 10])
+@pytest.mark.parametrize("n", [3, 6, 8, 9, 10])
 def test_aos_staged_path_matches_generic_and_oracle(stp, oracle, monkeypatch, n):
-    """The reference layout (AoS, m_pad 16) runs straight through stp_dmma8 (nDof 8) or through
+    """The reference layout (AoS, m_pad 16) runs straight through stp_dmma8 / stp_bip (nDof 8-10) or through
     device transposes and the tuned kernel; the generic kernel (ADERSTP_FORCE_GENERIC) on the same
     AoS buffers and the oracle agree."""
     S = stp
@@ -373,7 +373,7 @@ print(worst)
     assert float(r.stdout.strip().splitlines()[-1]) <= TOL
 
 
-@pytest.mark.parametrize("n", [6, 8, 10])
+@pytest.mark.parametrize("n", [6, 8, 9, 10])
 def test_reference_layout_checks_and_edges(stp, oracle, n):
     """The reference (AoS, m_pad 16) layout on the tuned paths: non-finite DOFs flagged (slot 8
     of a node is the tail of a 16-byte pair), padding slots never read (NaN there is harmless),

@@ -4,7 +4,7 @@ python - <<'PY'
 import sys, torch
 sys.path.insert(0, '.')
 import paper_2003_12787_b200 as S
-for n, E in ((8, 32768), (6, 32768), (10, 8192)):
+for n, E in ((8, 32768), (6, 32768), (10, 8192), (9, 8192)):
     q, par = S.generate(0, 1, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
     qa = torch.empty(E, n ** 3 * 16, dtype=torch.float64, device='cuda')
     S.convert_layout(n, 9, E, S.LAYOUT_AOSOA, 9, q, S.LAYOUT_AOS, 16, qa)
