@@ -104,6 +104,7 @@ bool kernel_available(int n);
 bool dmma8_applicable(const LaunchPlan& p);
 bool dmma8_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
 bool bip_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
+bool dmmap_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
 cudaError_t launch_bip(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 cudaError_t init_dmma8(const LaunchPlan& p);  // once per device, at plan creation
 // stp_dmma.cu: nDof 4..7 on zero-padded 8x8 DMMA tiles

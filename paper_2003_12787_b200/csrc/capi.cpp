@@ -371,6 +371,7 @@ cudaError_t predict_aos_staged(const aderstp_plan* plan, const aderstp::BatchArg
 cudaError_t predict_device(const aderstp_plan* p, const aderstp::BatchArgs& a, cudaStream_t st) {
   if (aderstp::dmma8_aos_applicable(p->lp, a)) return aderstp::launch_dmma8(p->lp, a, st);
   if (aderstp::bip_aos_applicable(p->lp, a)) return aderstp::launch_bip(p->lp, a, st);
+  if (aderstp::dmmap_aos_applicable(p->lp, a)) return aderstp::launch_dmmap(p->lp, a, st);
   if (aos_staged(p->lp) && p->pool) return predict_aos_staged(p, a, st);
   return aderstp::launch_stp(p->lp, a, st);
 }

@@ -206,8 +206,12 @@ __device__ __forceinline__ void normal_step(const double* R, double* W, uint32_t
 }
 
 // FUSED: the time-loop mode (BatchArgs::u_next), see stp_dmma8.cu.
-template <int N, bool FUSED = false>
+// AOS: the reference's ElementTensor / PredictorOutput node rows [k3][k2][k1][s < 16] in and out
+// (proj/src/layout.cpp:9-21): the node rows are first staged into the Q planes (real nodes only;
+// the padding of Q is never read), qavg / favg leave as whole 128-byte node rows.
+template <int N, bool FUSED = false, bool AOS = false>
 __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, BatchArgs a, unsigned int* status) {
+  static_assert(!(FUSED && AOS), "the time loop runs on AoSoA");
   using G = GeoP<N>;
   constexpr int PV = G::PV, FACE = G::FACE;
   extern __shared__ __align__(16) double smq[];
@@ -258,7 +262,24 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   // barrier that publishes the TMEM base address, so the DRAM/L2 latency overlaps it.
   const bool ok0 = g < N && 2 * t < N, ok1 = g < N && 2 * t + 1 < N;
   const double* qe = a.q + e * (long long)(N * N * N * kp.q_stride);
+  if constexpr (AOS) {  // node rows -> Q planes (5 slot pairs per node; slot 9 is padding)
+    const double* qn = a.q + e * (long long)(N * N * N * 16);
+    for (int i = tid; i < N * N * N * 5; i += THREADSP) {
+      const int node = i / 5, sp = 2 * (i - node * 5), k1 = node % N, k32 = node / N;
+      const double2 v = __ldcs(reinterpret_cast<const double2*>(qn + node * 16 + sp));
+      const int j = sp * PV + (k32 / N) * 64 + physp(k32 % N, k1);
+      Q[j] = v.x;
+      if (sp < 8) Q[j + PV] = v.y;
+    }
+    __syncthreads();
+  }
   auto ldq = [&](int sq, int k3, double& v0, double& v1) {
+    if constexpr (AOS) {  // from the staged planes (C-fragment positions, padding lanes: 0)
+      const double* src = Q + sq * PV + k3 * 64 + col;
+      v0 = ok0 ? src[0] : 0.0;
+      v1 = ok1 ? src[1] : 0.0;
+      return;
+    }
     const double* src = qe + ((k3 * N + g) * kp.q_stride + sq) * N + 2 * t;
     if (N % 2 == 0) {  // 16-byte aligned pair (q_stride * N even)
       double2 v = ok0 ? __ldcs(reinterpret_cast<const double2*>(src)) : make_double2(0.0, 0.0);
@@ -413,7 +434,40 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   const bool k1a = 2 * t < N, k1b = 2 * t + 1 < N;
   // qavg / favg: warp w emits the k3 planes w, w + 8, ...; the plane's 9 quantities are read
   // once and every output row (9 qavg, 27 favg = F_d(qavg)) is stored with compile-time indices
-  {
+  if constexpr (AOS) {
+    // node rows: lane = (node ns of 4, slot pair c2), 4 x 128 contiguous bytes per instruction
+    const int ns = lane >> 3, c2 = 2 * (lane & 7);
+    int srcq[3][2];
+    double cfo[3][2];
+    bool val[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int so = c2 + j;
+      val[j] = so < NVP;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        const int ci = val[j] ? e_coef(so, d) : 4;
+        srcq[d][j] = val[j] ? e_in(so, d) : 0;
+        cfo[d][j] = ci == 4 ? 0.0 : selp(c4, ci);
+      }
+    }
+    constexpr int N3 = N * N * N;
+    double* qo = a.qavg + e * (long long)(N3 * 16);
+    double* fo = a.favg ? a.favg + e * (long long)(3 * N3 * 16) : nullptr;
+#pragma unroll 1
+    for (int nb = 4 * warp + ns; nb < N3; nb += 4 * NWP) {
+      const int k32 = nb / N, pos = (k32 / N) * 64 + physp(k32 % N, nb % N);
+      __stcs(reinterpret_cast<double2*>(qo + nb * 16 + c2),
+             make_double2(val[0] ? P[c2 * PV + pos] : 0.0, val[1] ? P[(c2 + 1) * PV + pos] : 0.0));
+      if (fo) {
+#pragma unroll
+        for (int d = 0; d < 3; ++d)
+          __stcs(reinterpret_cast<double2*>(fo + d * (N3 * 16) + nb * 16 + c2),
+                 make_double2(cfo[d][0] != 0.0 ? cfo[d][0] * P[srcq[d][0] * PV + pos] : 0.0,
+                              cfo[d][1] != 0.0 ? cfo[d][1] * P[srcq[d][1] * PV + pos] : 0.0));
+      }
+    }
+  } else {
     double* qout = FUSED ? nullptr : a.qavg + e * (long long)(N * N * N * NVP);
     double* fout = a.favg ? a.favg + e * (long long)(3 * N * N * N * NVP) : nullptr;
 #pragma unroll 1
@@ -564,7 +618,8 @@ cudaError_t launch_dmmap_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t
       kp.cf[o] = c;
     }
   }
-  auto kern = a.u_next ? stp_dmmap_kernel<N, true> : stp_dmmap_kernel<N, false>;
+  auto kern = a.u_next ? stp_dmmap_kernel<N, true> : p.layout == ADERSTP_LAYOUT_AOS ? stp_dmmap_kernel<N, false, true>
+                                                                                    : stp_dmmap_kernel<N, false>;
   const int smem = G::SMEM;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err == cudaSuccess)
@@ -582,6 +637,15 @@ cudaError_t launch_dmmap_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t
 bool dmmap_applicable(const LaunchPlan& p) {
   return p.n >= 4 && p.n <= DMMAP_MAXN && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
          p.layout == ADERSTP_LAYOUT_AOSOA && p.out_stride == 9 && p.q_stride >= 9 && p.q_stride <= 64;
+}
+
+// the reference's own layout straight into the padded-DMMA kernel (nDof 4..7)
+bool dmmap_aos_applicable(const LaunchPlan& p, const BatchArgs& a) {
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  return p.n >= 4 && p.n <= DMMAP_MAXN && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
+         p.layout == ADERSTP_LAYOUT_AOS && p.q_stride == 16 && p.out_stride == 16 && !p.force_generic &&
+         !p.no_dmmap && !p.aos_staged && !a.u_next && al16(a.q) && al16(a.qavg) && al16(a.favg) &&
+         al16(a.face_q) && al16(a.face_f);
 }
 
 cudaError_t init_dmmap(const LaunchPlan& p) {
