@@ -101,9 +101,14 @@ constexpr int max_threads() {
   return ELASTIC ? elastic_epb<N>() * 9 * N * N : 1024;
 }
 
-template <int N, bool ELASTIC>
-__global__ void __launch_bounds__(max_threads<N, ELASTIC>()) stp_kernel(KParams<N> kp, BatchArgs a,
-                                                                       int epb, unsigned int* status) {
+// MT: the block-size bound the kernel is compiled for (registers per thread = 64 K / MT).  The
+// table kernel exists twice per order: MT = 1024 (any m) and MT = 9 N^2 rounded up to a warp
+// (m <= 9: one element of the elastic size per block, up to 112 registers, no spills).
+template <int N>
+constexpr int table_small_threads() { return ((9 * N * N + 31) / 32) * 32; }
+
+template <int N, bool ELASTIC, int MT = max_threads<N, ELASTIC>()>
+__global__ void __launch_bounds__(MT) stp_kernel(KParams<N> kp, BatchArgs a, int epb, unsigned int* status) {
   extern __shared__ double smem[];
   constexpr int RS = row_stride<N>();
   constexpr int DS = N + 1;  // padded row stride of D in shared memory
@@ -127,9 +132,14 @@ __global__ void __launch_bounds__(max_threads<N, ELASTIC>()) stp_kernel(KParams<
   unsigned int flags = 0;
 
   // ---- per-thread terms for output quantity s ----------------------------------------
+  // Terms of output quantity s: elastic -- the one term per (s, d) in registers; table PDEs in
+  // the small-block variant (MT < 900) read theirs from the parameter bank at the point of use
+  // (s is warp-uniform for N >= 6), which keeps 36 registers free; otherwise in registers.
   constexpr int K = ELASTIC ? 1 : kMaxTerms;
-  int in[3][K];
-  double cf[3][K];
+  constexpr bool TP = !ELASTIC && MT < 900;
+  constexpr int KR = TP ? 1 : K;
+  int in[3][KR];
+  double cf[3][KR];
   double dt = a.dt;
   if (live) {
     if (ELASTIC) {
@@ -140,11 +150,11 @@ __global__ void __launch_bounds__(max_threads<N, ELASTIC>()) stp_kernel(KParams<
         in[d][0] = kElasticIn[s][d];
         cf[d][0] = pick(c4, kElasticCoef[s][d]);
       }
-    } else {
+    } else if (!TP) {
 #pragma unroll
       for (int d = 0; d < 3; ++d)
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
+        for (int k = 0; k < KR; ++k) {
           in[d][k] = kp.tr[s][d][k];
           cf[d][k] = kp.tc[s][d][k];
         }
@@ -153,11 +163,13 @@ __global__ void __launch_bounds__(max_threads<N, ELASTIC>()) stp_kernel(KParams<
 #pragma unroll
     for (int d = 0; d < 3; ++d)
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
+      for (int k = 0; k < KR; ++k) {
         in[d][k] = 0;
         cf[d][k] = 0.0;
       }
   }
+  auto term_in = [&](int d, int k) -> int { return TP ? kp.tr[s][d][k] : in[d][TP ? 0 : k]; };
+  auto term_cf = [&](int d, int k) -> double { return TP ? kp.tc[s][d][k] : cf[d][TP ? 0 : k]; };
 
   // ---- stage q (coalesced flat loop over this element's input region) ----------------
   if (el < epb && e < a.n_elem) {
@@ -204,8 +216,8 @@ __global__ void __launch_bounds__(max_threads<N, ELASTIC>()) stp_kernel(KParams<
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (!ELASTIC && k >= kp.n_terms) break;
-        const double* px = P + sidx<N>(in[0][k], 0, k2, 0);
-        const double c = cf[0][k];
+        const double* px = P + sidx<N>(term_in(0, k), 0, k2, 0);
+        const double c = term_cf(0, k);
 #pragma unroll
         for (int l = 0; l < N; ++l) {
           const double cd = c * Ds[k1 * DS + l];
@@ -217,8 +229,8 @@ __global__ void __launch_bounds__(max_threads<N, ELASTIC>()) stp_kernel(KParams<
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (!ELASTIC && k >= kp.n_terms) break;
-        const double* py = P + sidx<N>(in[1][k], 0, 0, k1);
-        const double c = cf[1][k];
+        const double* py = P + sidx<N>(term_in(1, k), 0, 0, k1);
+        const double c = term_cf(1, k);
 #pragma unroll
         for (int l = 0; l < N; ++l) {
           const double cd = c * Ds[k2 * DS + l];
@@ -230,11 +242,11 @@ __global__ void __launch_bounds__(max_threads<N, ELASTIC>()) stp_kernel(KParams<
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         if (!ELASTIC && k >= kp.n_terms) break;
-        const double* pz = P + sidx<N>(in[2][k], 0, k2, k1);
+        const double* pz = P + sidx<N>(term_in(2, k), 0, k2, k1);
         double colv[N];
 #pragma unroll
         for (int l = 0; l < N; ++l) colv[l] = pz[l * N * RS];
-        const double c = cf[2][k];
+        const double c = term_cf(2, k);
 #pragma unroll
         for (int k3 = 0; k3 < N; ++k3) {
           double acc = 0.0;
@@ -430,12 +442,14 @@ cudaError_t launch_order(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   fill_params<N>(p, a, kp);
   const int m = p.m;
   const int tpe = m * N * N;
-  int epb = ELASTIC ? elastic_epb<N>() : 1024 / tpe;
+  constexpr int SMALL = table_small_threads<N>();
+  const bool small = !ELASTIC && tpe <= SMALL;
+  int epb = ELASTIC ? elastic_epb<N>() : (small ? SMALL : 1024) / tpe;
   if (epb < 1) return cudaErrorInvalidConfiguration;
   if (epb > 8) epb = 8;
   const size_t smem =
       sizeof(double) * (N * (N + 1) + (N * (N + 1)) % 2 + (size_t)epb * elem_smem_doubles<N>(m));
-  auto kern = stp_kernel<N, ELASTIC>;
+  auto kern = small ? stp_kernel<N, ELASTIC, (ELASTIC ? max_threads<N, ELASTIC>() : SMALL)> : stp_kernel<N, ELASTIC>;
   cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   const long long blocks = (a.n_elem + epb - 1) / epb;
