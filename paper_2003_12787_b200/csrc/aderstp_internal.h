@@ -61,6 +61,9 @@ struct BatchArgs {
   // corrector's volume term (solver.cpp:199-207) applied by one more Horner step; qavg may then be
   // null.  Only kernels with fused_supported() honour it.
   double* u_next = nullptr;
+  // volume mode (with u_next, stp_dmma8 only): the corrector's volume term alone, u_next = q +
+  // L(vol_r) with vol_r = qavg (compact AoSoA); no faces, no Horner recursion
+  const double* vol_r = nullptr;
 };
 
 // corrector.cu: GPU corrector step (proj/src/solver.cpp:184-311) and time-loop helpers

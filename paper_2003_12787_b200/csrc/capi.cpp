@@ -579,7 +579,31 @@ int aderstp_correct_batch(const aderstp_plan* p, const aderstp_mesh* mesh, doubl
   const double inv_h = mesh->elements_per_dim / mesh->domain_len;
   aderstp::CorrArgs a{u, par, qavg, face_q, face_f, mesh->elements_per_dim, inv_h,
                       max_wavespeed >= 0.0 ? max_wavespeed * inv_h : -1.0};
-  cudaError_t e = aderstp::launch_correct(p->lp, a, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const long long E = (long long)mesh->elements_per_dim * mesh->elements_per_dim * mesh->elements_per_dim;
+  // elastic nDof 8: the volume term on the tensor cores -- stp_dmma8's last Horner step with the
+  // iterate started from qavg on the 1/h-scaled material, u <- u + V(qavg) in place -- then the
+  // surface-only corrector
+  aderstp::BatchArgs vb{u, nullptr, nullptr, nullptr, nullptr, nullptr, E, 1.0, 0.0};
+  vb.u_next = u;
+  vb.vol_r = qavg;
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  if (E > 0 && aderstp::dmma8_applicable(p->lp) && !p->lp.force_generic && !p->lp.no_dmma8 && al16(u) &&
+      al16(qavg)) {
+    double* par_s = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&par_s), sizeof(double) * 3 * E, p->pool, st);
+    if (e == cudaSuccess) e = aderstp::launch_scale_par(par, p->lp.par_kind, inv_h, E, par_s, st);
+    aderstp::LaunchPlan sp = p->lp;
+    sp.par_kind = ADERSTP_PAR_LAMBDA_MU_RHO;
+    vb.par = par_s;
+    if (e == cudaSuccess) e = aderstp::launch_dmma8(sp, vb, st);
+    if (par_s) cudaFreeAsync(par_s, st);
+    a.qavg = nullptr;  // the volume term is applied
+    if (e == cudaSuccess) e = aderstp::launch_correct(p->lp, a, st);
+    if (e != cudaSuccess) return cuda_fail(e, "correct_batch launch");
+    return ADERSTP_OK;
+  }
+  cudaError_t e = aderstp::launch_correct(p->lp, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "correct_batch launch");
   return ADERSTP_OK;
 }

@@ -67,6 +67,10 @@ struct Params8 {
   int par_kind;
   int q_stride;
   int prefetch;  // element distance of the L2 prefetch (0: off)
+  // volume mode (the corrector's volume term, solver.cpp:199-207): the iterate starts from r_src
+  // (qavg, compact AoSoA) instead of c_(n-1) q and only the coefficient-1 step runs (o_start = -1)
+  const double* r_src;
+  int o_start;
 };
 
 // role of each warp: a single output quantity (0..8), or -1 / -2 for the normal-stress warps on
@@ -191,7 +195,7 @@ __device__ __forceinline__ void dfma_z(double (&acc)[NT][2], const double* f, in
 template <int NT, bool FUSED, int PS>
 __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const double* cf, int s, int K0, int g,
                                             int t, int col, double d0, double d1, const double (&c4)[4],
-                                            double* un, int urow) {
+                                            double* un, int urow, int o_start) {
   const int in_x = kIn[s][0], in_y = kIn[s][1], in_z = kIn[s][2];
   const double cx = sel4(c4, kCoef[s][0]), cy = sel4(c4, kCoef[s][1]), cz = sel4(c4, kCoef[s][2]);
   const bool has_x = kCoef[s][0] != 4, has_y = kCoef[s][1] != 4, has_z = kCoef[s][2] != 4;
@@ -200,7 +204,7 @@ __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const do
   const int own = s * PS + K0 * 64 + col;
   constexpr int o_end = FUSED ? -1 : 0;
 #pragma unroll 1
-  for (int o = N8 - 2; o >= o_end; --o) {
+  for (int o = o_start; o >= o_end; --o) {
     const double co = (!FUSED || o >= 0) ? cf[o] : 1.0;
     double tt[NT][2];
 #pragma unroll
@@ -229,11 +233,11 @@ __device__ __forceinline__ void ck_quantity(double* P, const double* Q, const do
 template <int NT, bool FUSED, int PS>
 __device__ __forceinline__ void ck_normal(double* P, const double* Q, const double* cf, int K0, int g, int t,
                                           int col, double d0, double d1, const double (&c4)[4], double* un,
-                                          int urow) {
+                                          int urow, int o_start) {
   const double lam = c4[1], two_mu = 2.0 * c4[2];
   constexpr int o_end = FUSED ? -1 : 0;
 #pragma unroll 1
-  for (int o = N8 - 2; o >= o_end; --o) {
+  for (int o = o_start; o >= o_end; --o) {
     const double co = (!FUSED || o >= 0) ? cf[o] : 1.0;
     double ta[NT][2], tb[NT][2], tc[NT][2];
 #pragma unroll
@@ -285,10 +289,11 @@ __device__ __forceinline__ void ck_normal(double* P, const double* Q, const doub
 template <bool AOS>
 constexpr int plane_stride() { return AOS ? PV + 2 : PV; }
 
-template <bool FUSED, bool AOS = false>
+template <bool FUSED, bool AOS = false, bool VOLM = false>
 __global__ void __maxnreg__(80)
 stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   static_assert(!(FUSED && AOS), "the time loop runs on AoSoA");
+  static_assert(!VOLM || FUSED, "the volume mode writes u_next");
   constexpr int THREADS8 = NWARP * 32;
   constexpr int PS = plane_stride<AOS>();
   extern __shared__ __align__(16) double sm8[];
@@ -370,6 +375,16 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
       const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
       if (2304 % THREADS8 == 0 || i < 2304) v[it] = ld_nc2(qe + (k32 * kp.q_stride + si) * 8 + 2 * (i & 3));
     }
+    double2 w[VOLM ? IT : 1];  // volume mode: the iterate qavg, compact AoSoA (stride 9)
+    if (VOLM) {
+      const double* re = kp.r_src + e * (long long)(PV * NV);
+#pragma unroll
+      for (int it = 0; it < (VOLM ? IT : 1); ++it) {
+        const int i = tid + it * THREADS8;
+        const int r9 = i >> 2, k32 = r9 / NV, si = r9 - k32 * NV;
+        if (2304 % THREADS8 == 0 || i < 2304) w[it] = ld_nc2(re + (k32 * NV + si) * 8 + 2 * (i & 3));
+      }
+    }
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       const int i = tid + it * THREADS8;
@@ -378,7 +393,10 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
       if (kp.check && !(isfinite(v[it].x) && isfinite(v[it].y))) flags |= 1u;
       const int j = si * PS + (k32 >> 3) * 64 + phys(k32 & 7, 2 * (i & 3));
       sts2(Q + j, v[it].x, v[it].y);
-      sts2(P + j, kp.cf[N8 - 1] * v[it].x, kp.cf[N8 - 1] * v[it].y);
+      if (VOLM)
+        sts2(P + j, w[VOLM ? it : 0].x, w[VOLM ? it : 0].y);
+      else
+        sts2(P + j, kp.cf[N8 - 1] * v[it].x, kp.cf[N8 - 1] * v[it].y);
     }
   }
   __syncthreads();
@@ -393,9 +411,9 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     const int urow = kp.q_stride * 8;
     double* un = FUSED ? a.u_next + e * (long long)(PV * kp.q_stride) + g * urow + 2 * t : nullptr;
     if (role >= 0)
-      ck_quantity<8, FUSED, PS>(P, Q, kp.cf, role, 0, g, t, col, d0, d1, c4, un, urow);
+      ck_quantity<8, FUSED, PS>(P, Q, kp.cf, role, 0, g, t, col, d0, d1, c4, un, urow, VOLM ? -1 : N8 - 2);
     else
-      ck_normal<4, FUSED, PS>(P, Q, kp.cf, 4 * (-role - 1), g, t, col, d0, d1, c4, un, urow);
+      ck_normal<4, FUSED, PS>(P, Q, kp.cf, 4 * (-role - 1), g, t, col, d0, d1, c4, un, urow, VOLM ? -1 : N8 - 2);
     if (FUSED) __syncthreads();  // q (the Q region) is read until here; faces stage over it
   }
 
@@ -600,6 +618,8 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   kp.par_kind = p.par_kind;
   kp.q_stride = p.q_stride;
   kp.prefetch = p.dmma8_prefetch;
+  kp.r_src = a.vol_r;
+  kp.o_start = a.vol_r ? -1 : N8 - 2;
   {
     double c = a.dt;  // same operation sequence as proj/src/stp_splitck.cpp:45,64
     kp.cf[0] = c;
@@ -609,7 +629,10 @@ cudaError_t launch_dmma8(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
     }
   }
   const bool aos = p.layout == ADERSTP_LAYOUT_AOS;  // dmma8_aos_applicable
-  auto kern = a.u_next ? stp_dmma8_kernel<true> : aos ? stp_dmma8_kernel<false, true> : stp_dmma8_kernel<false>;
+  auto kern = a.vol_r    ? stp_dmma8_kernel<true, false, true>
+              : a.u_next ? stp_dmma8_kernel<true>
+              : aos      ? stp_dmma8_kernel<false, true>
+                         : stp_dmma8_kernel<false>;
   int smem = aos ? 2 * NV * plane_stride<true>() * 8 : kSmem8;
 #ifdef ADERSTP_EXPT_TIMING
   if (const char* x = std::getenv("ADERSTP_EXPT_SMEM")) smem += std::atoi(x);  // occupancy experiments
