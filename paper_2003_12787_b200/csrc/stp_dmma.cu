@@ -56,9 +56,6 @@ struct GeoP {
   static constexpr int TCOLS = TC <= 32 ? 32 : TC <= 64 ? 64 : 128;
 };
 
-template <int N>
-constexpr int role_planes() { return N > 3 * GeoP<N>::H0 ? N : 3 * GeoP<N>::H0; }
-
 struct ParamsP {
   double d[64];      // zero-padded D
   double phi[2][8];  // zero-padded phi(0), phi(1)
@@ -258,8 +255,7 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   // node pair (k2 = g, k1 = 2t, 2t+1) of lane (g, t), i.e. in the C-fragment layout of the CK
   // step.  q goes register -> TMEM (thread-private columns: warps w and w + 4 share a lane
   // quarter, the upper four start at column 4N) and c_(N-1) q -> P, padding lanes writing the
-  // zero padding; q never passes through shared memory.  Every global load is issued before the
-  // barrier that publishes the TMEM base address, so the DRAM/L2 latency overlaps it.
+  // zero padding; q never passes through shared memory.
   const bool ok0 = g < N && 2 * t < N, ok1 = g < N && 2 * t + 1 < N;
   const double* qe = a.q + e * (long long)(N * N * N * kp.q_stride);
   if constexpr (AOS) {  // node rows -> Q planes (5 slot pairs per node; slot 9 is padding)
@@ -290,33 +286,22 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
       v1 = ok1 ? __ldcs(src + 1) : 0.0;
     }
   };
-  constexpr int NQ = role_planes<N>();  // planes staged per warp: max(N, 3 H0)
-  double qv[NQ][2];
-  if (role >= 0) {
-#pragma unroll
-    for (int k3 = 0; k3 < N; ++k3) ldq(role, k3, qv[k3][0], qv[k3][1]);
-  } else {
-    const int h = -role - 1, K0 = h ? G::H0 : 0, NT = h ? G::H1 : G::H0;
-#pragma unroll
-    for (int k = 0; k < G::H0; ++k)
-#pragma unroll
-      for (int j = 0; j < 3; ++j)
-        if (k < NT) ldq(j, K0 + k, qv[3 * k + j][0], qv[3 * k + j][1]);
-  }
   tm_fence_before();
   __syncthreads();  // the TMEM base address (warp 0's tcgen05.alloc) is visible
   tm_fence_after();
   const uint32_t tq = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)(warp < 4 ? 0 : 4 * N);
-  {
+  {  // each plane: load, check, c_(n-1) q -> P, q -> TMEM (the compiler batches the loads ahead)
     const double c0 = kp.cf[N - 1];
     if (role >= 0) {
 #pragma unroll
       for (int k3 = 0; k3 < N; ++k3) {
-        if (kp.check && !(isfinite(qv[k3][0]) && isfinite(qv[k3][1]))) flags |= 1u;
-        sts2p(P + role * PV + k3 * 64 + col, c0 * qv[k3][0], c0 * qv[k3][1]);
+        double v0, v1;
+        ldq(role, k3, v0, v1);
+        if (kp.check && !(isfinite(v0) && isfinite(v1))) flags |= 1u;
+        sts2p(P + role * PV + k3 * 64 + col, c0 * v0, c0 * v1);
         uint32_t r[4];
-        tm_split(qv[k3][0], r, 0);
-        tm_split(qv[k3][1], r, 1);
+        tm_split(v0, r, 0);
+        tm_split(v1, r, 1);
         tm_st4(tq + 4 * k3, r);
       }
     } else {
@@ -327,7 +312,8 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
         uint32_t r[12];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
-          const double v0 = qv[3 * k + j][0], v1 = qv[3 * k + j][1];
+          double v0, v1;
+          ldq(j, K0 + k, v0, v1);
           if (kp.check && !(isfinite(v0) && isfinite(v1))) flags |= 1u;
           sts2p(P + j * PV + (K0 + k) * 64 + col, c0 * v0, c0 * v1);
           tm_split(v0, r, 2 * j);
