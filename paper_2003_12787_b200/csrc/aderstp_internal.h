@@ -106,6 +106,8 @@ bool kernel_available(int n);
 // stp_dmma8.cu: nDof = 8 elastic kernel on the fp64 tensor cores
 bool dmma8_applicable(const LaunchPlan& p);
 bool dmma8_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
+bool dmma8_table_applicable(const LaunchPlan& p, const BatchArgs& a);
+cudaError_t launch_dmma8_table(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 bool bip_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
 bool dmmap_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
 cudaError_t launch_bip(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);

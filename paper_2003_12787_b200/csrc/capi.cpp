@@ -278,7 +278,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   if (e == cudaSuccess) e = cudaMemPoolCreate(&p->pool, &pool_props_of(p->device));
   const uint64_t keep = UINT64_MAX;
   if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, (void*)&keep);
-  if (e == cudaSuccess && aderstp::dmma8_applicable(kl)) e = aderstp::init_dmma8(kl);
+  // D of nDof 8 in the constant bank: the elastic and the table-PDE tensor-core kernels
+  if (e == cudaSuccess && kl.n == 8) e = aderstp::init_dmma8(kl);
   if (e == cudaSuccess && aderstp::pass_applicable(kl)) e = aderstp::init_pass(kl);
   if (e == cudaSuccess && aderstp::dmmap_applicable(kl)) e = aderstp::init_dmmap(kl);
   if (e != cudaSuccess) {

@@ -587,6 +587,185 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   TM3(6);
 }
 
+// ---- table PDEs (any constant-coefficient LinearPde given as term tables, m <= 8) -----------
+// The user-PDE path on the tensor cores: warp s owns output quantity s (m <= 8 warps), and a CK step
+// is  t_s = c_o q_s + sum_d sum_k tc[s][d][k] D_d r_{tr[s][d][k]}  (build_terms folds the ncp
+// matrices in: D_d (A_d + B_d) p, proj/src/stp_splitck.cpp:53-61 for constant coefficients) --
+// every term one more pair of DMMAs (x, y) or register DFMAs (z) into the same accumulators, the
+// coefficient folded into the D fragments.  favg_d = A_d qavg and face_f = A_d face_q from the
+// favg tables (fr, fc); faces and bulk stores as in the elastic kernel.
+constexpr int GM = 8;  // quantities of the table kernel
+struct ParamsG {
+  double d[64];
+  double phi[2][8];
+  double cf[8];
+  double tc[GM][3][kMaxTerms];
+  double fc[GM][3][kMaxTerms];
+  signed char tr[GM][3][kMaxTerms];
+  signed char fr[GM][3][kMaxTerms];
+  int m, n_terms, q_stride, check;
+};
+
+__global__ void __launch_bounds__(NWARP * 32) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, unsigned int* status) {
+  constexpr int THREADS8 = NWARP * 32;
+  extern __shared__ __align__(16) double smg[];
+  const int m = kp.m, nt = kp.n_terms;
+  double* P = smg;           // iterate r [m][8][8][8] swizzled; qavg at the end
+  double* Q = smg + m * PV;  // q
+  const long long e = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int col = phys(g, 2 * t);
+  unsigned int flags = 0;
+  // ---- stage q: AoSoA [k3][k2][s < q_stride][k1] -> Q = q, P = c_(n-1) q -------------------
+  {
+    const double* qe = a.q + e * (long long)(PV * kp.q_stride);
+    const int pairs = 64 * m * 4;
+    for (int i = tid; i < pairs; i += THREADS8) {
+      const int r = i >> 2, k32 = r / m, si = r - k32 * m;
+      const double2 v = ld_nc2(qe + (k32 * kp.q_stride + si) * 8 + 2 * (i & 3));
+      if (kp.check && !(isfinite(v.x) && isfinite(v.y))) flags |= 1u;
+      const int j = si * PV + (k32 >> 3) * 64 + phys(k32 & 7, 2 * (i & 3));
+      sts2(Q + j, v.x, v.y);
+      sts2(P + j, kp.cf[N8 - 1] * v.x, kp.cf[N8 - 1] * v.y);
+    }
+  }
+  __syncthreads();
+  const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];
+  const int s = warp;
+  const bool own = s < m;
+  double tt[8][2];
+  // ---- Horner form of the CK series (see ck_quantity) ----------------------------------------
+#pragma unroll 1
+  for (int o = N8 - 2; o >= 0; --o) {
+    if (own) {
+      const double co = kp.cf[o];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const double2 v = lds2(Q + s * PV + k * 64 + col);
+        tt[k][0] = co * v.x;
+        tt[k][1] = co * v.y;
+      }
+#pragma unroll 1
+      for (int k = 0; k < nt; ++k) {
+        const double cx = kp.tc[s][0][k], cy = kp.tc[s][1][k], cz = kp.tc[s][2][k];
+        if (cx != 0.0) mma_x<8>(tt, P + kp.tr[s][0][k] * PV, 0, g, t, cx * d0, cx * d1);
+        if (cy != 0.0) mma_y<8>(tt, P + kp.tr[s][1][k] * PV, 0, g, t, cy * d0, cy * d1);
+        if (cz != 0.0) dfma_z<8>(tt, P + kp.tr[s][2][k] * PV, 0, col, cz);
+      }
+    }
+    __syncthreads();  // every warp has finished reading r
+    if (own) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sts2(P + s * PV + k * 64 + col, tt[k][0], tt[k][1]);
+    }
+    __syncthreads();  // new r (qavg after the last step) complete
+  }
+  // ---- epilogue: qavg and favg of quantity s, x/y/z faces --------------------------------------
+  double* FQ = Q;  // face_q staging [6][8][8][m] (q is dead)
+  constexpr int FA = 64;  // in-face nodes
+  const int FACE = FA * m;
+  const bool faces = a.face_q || a.face_f;
+  if (own) {
+    double* qout = a.qavg + e * (long long)(PV * m) + s * 8 + 2 * t;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) st_cs2(qout + (k * 8 + g) * m * 8, tt[k][0], tt[k][1]);
+    if (a.favg) {
+      double* fout = a.favg + e * (long long)(3 * PV * m) + s * 8 + 2 * t;
+#pragma unroll 1
+      for (int d = 0; d < 3; ++d) {
+        double f[8][2];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k][0] = f[k][1] = 0.0;
+#pragma unroll 1
+        for (int kt = 0; kt < nt; ++kt) {
+          const double c = kp.fc[s][d][kt];
+          if (c == 0.0) continue;
+          const double* src = P + kp.fr[s][d][kt] * PV + col;
+#pragma unroll
+          for (int k = 0; k < 8; ++k) {
+            const double2 v = lds2(src + k * 64);
+            f[k][0] = fma(c, v.x, f[k][0]);
+            f[k][1] = fma(c, v.y, f[k][1]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) st_cs2(fout + d * (PV * m) + (k * 8 + g) * m * 8, f[k][0], f[k][1]);
+      }
+    }
+    if (faces) {
+      const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0, bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
+      const double* qs = P + s * PV;
+      double xf[8][2], yf[8][2];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) xf[k][0] = xf[k][1] = yf[k][0] = yf[k][1] = 0.0;
+      mma_x<8>(xf, qs, 0, g, t, bphi0, bphi1);
+      mma_y<8>(yf, qs, 0, g, t, bphi0, bphi1);
+#pragma unroll
+      for (int k3 = 0; k3 < 8; ++k3) {
+        if (t == 0) {
+          FQ[0 * FACE + (k3 * 8 + g) * m + s] = xf[k3][0];
+          FQ[1 * FACE + (k3 * 8 + g) * m + s] = xf[k3][1];
+        }
+        if (g < 2) {
+          FQ[(2 + g) * FACE + (k3 * 8 + 2 * t) * m + s] = yf[k3][0];
+          FQ[(2 + g) * FACE + (k3 * 8 + 2 * t + 1) * m + s] = yf[k3][1];
+        }
+      }
+      double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0};
+#pragma unroll
+      for (int k3 = 0; k3 < 8; ++k3)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          z0[j] = fma(kp.phi[0][k3], tt[k3][j], z0[j]);
+          z1[j] = fma(kp.phi[1][k3], tt[k3][j], z1[j]);
+        }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        FQ[4 * FACE + (g * 8 + 2 * t + j) * m + s] = z0[j];
+        FQ[5 * FACE + (g * 8 + 2 * t + j) * m + s] = z1[j];
+      }
+    }
+  }
+  if (faces) {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+    __syncthreads();  // FQ complete; qavg (P) no longer read
+    const unsigned bytes = 6u * FACE * 8u;
+    if (tid == 0 && a.face_q) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                       a.face_q + e * (long long)(6 * FACE)),
+                   "r"((unsigned)__cvta_generic_to_shared(FQ)), "r"(bytes)
+                   : "memory");
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    }
+    double* FF = P;
+    if (a.face_f) {  // face_f[f][ab][so] = sum_k fc[so][d][k] face_q[f][ab][fr[so][d][k]], d = f / 2
+      for (int i = tid; i < 6 * FA * m; i += THREADS8) {
+        const int fa = i / m, so = i - fa * m, f = fa / FA, d = f >> 1;
+        const double* src = FQ + fa * m;
+        double v = 0.0;
+        for (int kt = 0; kt < nt; ++kt) {
+          const double c = kp.fc[so][d][kt];
+          if (c != 0.0) v = fma(c, src[kp.fr[so][d][kt]], v);
+        }
+        FF[i] = v;
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();
+      if (tid == 0)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
+                         a.face_f + e * (long long)(6 * FACE)),
+                     "r"((unsigned)__cvta_generic_to_shared(FF)), "r"(bytes)
+                     : "memory");
+    }
+    if (tid == 0) {
+      asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    }
+  }
+  if (kp.check && flags) atomicOr(status, flags);
+}
+
 }  // namespace
 
 bool dmma8_applicable(const LaunchPlan& p) {
@@ -601,6 +780,55 @@ bool dmma8_aos_applicable(const LaunchPlan& p, const BatchArgs& a) {
   return p.n == 8 && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 && p.layout == ADERSTP_LAYOUT_AOS &&
          p.q_stride == 16 && p.out_stride == 16 && !p.force_generic && !p.no_dmma8 && !p.aos_staged &&
          !a.u_next && al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) && al16(a.face_f);
+}
+
+// table PDEs at nDof 8 on the tensor cores: m <= 8, compact AoSoA outputs, no point source
+bool dmma8_table_applicable(const LaunchPlan& p, const BatchArgs& a) {
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  return p.n == 8 && p.kind != ADERSTP_PDE_ELASTIC && p.kind != ADERSTP_PDE_ELASTIC_SOURCE && p.src_comp < 0 &&
+         p.m >= 1 && p.m <= GM && p.layout == ADERSTP_LAYOUT_AOSOA && p.out_stride == p.m && p.q_stride >= p.m &&
+         p.q_stride <= 64 && p.n_terms <= kMaxTerms && !p.force_generic && !p.no_dmma8 && !a.u_next &&
+         al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) && al16(a.face_f);
+}
+
+cudaError_t launch_dmma8_table(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
+  ParamsG kp;
+  for (int i = 0; i < 64; ++i) kp.d[i] = p.basis.d[i];
+  for (int j = 0; j < 8; ++j) {
+    kp.phi[0][j] = p.basis.face_left[j];
+    kp.phi[1][j] = p.basis.face_right[j];
+  }
+  {
+    double c = a.dt;  // same operation sequence as proj/src/stp_splitck.cpp:45,64
+    kp.cf[0] = c;
+    for (int o = 1; o < N8; ++o) {
+      c *= a.dt / (o + 1);
+      kp.cf[o] = c;
+    }
+  }
+  for (int s = 0; s < GM; ++s)
+    for (int d = 0; d < 3; ++d)
+      for (int k = 0; k < kMaxTerms; ++k) {
+        const bool in = s < p.m && k < p.n_terms;
+        kp.tr[s][d][k] = in ? p.tr[s][d][k] : 0;
+        kp.tc[s][d][k] = in ? p.tc[s][d][k] : 0.0;
+        kp.fr[s][d][k] = in ? p.fr[s][d][k] : 0;
+        kp.fc[s][d][k] = in ? p.fc[s][d][k] : 0.0;
+      }
+  kp.m = p.m;
+  kp.n_terms = p.n_terms;
+  kp.q_stride = p.q_stride;
+  kp.check = p.check;
+  const int smem = 2 * p.m * PV * 8;
+  cudaError_t err = cudaFuncSetAttribute(stp_dmma8_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(stp_dmma8_table_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               cudaSharedmemCarveoutMaxShared);
+  if (err != cudaSuccess) return err;
+  if (a.n_elem == 0) return cudaSuccess;
+  if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
+  stp_dmma8_table_kernel<<<(unsigned)a.n_elem, NWARP * 32, smem, stream>>>(kp, a, p.d_status);
+  return cudaGetLastError();
 }
 
 cudaError_t init_dmma8(const LaunchPlan& p) {

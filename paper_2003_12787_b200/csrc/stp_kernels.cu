@@ -508,6 +508,7 @@ cudaError_t launch_stp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t str
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   const bool aligned = al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) && al16(a.face_f);
   if (use_dmma8(p, a)) return launch_dmma8(p, a, stream);
+  if (dmma8_table_applicable(p, a)) return launch_dmma8_table(p, a, stream);
   if (a.u_next && use_dmmap(p, a)) return launch_dmmap(p, a, stream);
   if (a.u_next && use_bip(p, a)) return launch_pass(p, a, stream);
   if (a.u_next) return cudaErrorInvalidValue;  // the fused mode exists only where fused_supported()

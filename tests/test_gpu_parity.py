@@ -4,6 +4,8 @@ Tolerance: the reference's rel_diff metric (proj/src/checks.cpp:27-34), per elem
 output array, <= 1e-12 (BASELINE.json north_star).  Inputs are generated on the device and copied
 back, so both sides see bit-identical data.
 """
+import zlib as _zlib
+
 import numpy as np
 import pytest
 
@@ -412,3 +414,46 @@ def test_reference_layout_checks_and_edges(stp, oracle, n):
     plan.status()
     for a, b in ((o2.qavg, ref.qavg), (o2.favg, ref.favg), (o2.face_q, ref.face_q), (o2.face_f, ref.face_f)):
         assert O.per_element_rel_diff(b.cpu().numpy().reshape(E, -1), a.cpu().numpy().reshape(E, -1)) <= TOL
+
+
+@pytest.mark.parametrize("case", ["advection_m3", "ncp_advection_m2", "demo_m6", "probed_m5", "probed_m8"])
+def test_table_pdes_on_tensor_cores_nDof8(stp, oracle, monkeypatch, case):
+    """Table PDEs (the user-LinearPde path) at nDof 8 run on stp_dmma8_table; the reference's
+    PDEs against the oracle, random probed systems (flux + ncp matrices, up to 4 nonzeros per
+    (row, dim)) against the generic table kernel on the same inputs."""
+    S = stp
+    n, E = 8, 7
+    rng = np.random.default_rng(_zlib.crc32(case.encode()))
+    if case == "advection_m3":
+        m, pde, kind, args = 3, S.advection_pde((1.0, 0.5, 0.25), 3), O.PDE_ADVECTION, [1.0, 0.5, 0.25]
+    elif case == "ncp_advection_m2":
+        m, pde, kind, args = 2, S.ncp_advection_pde((1.0, 0.5, 0.25), 2), O.PDE_NCP_ADVECTION, [1.0, 0.5, 0.25]
+    elif case == "demo_m6":
+        m, pde, kind, args = 6, S.paper_demo_pde(), O.PDE_DEMO, []
+    else:
+        m = int(case[-1])
+        A, B = [], []
+        for _ in range(3):
+            a, b = np.zeros((m, m)), np.zeros((m, m))
+            for r in range(m):  # two flux and one ncp nonzero per row
+                a[r, rng.choice(m, 2, replace=False)] = rng.uniform(-1, 1, 2)
+                b[r, rng.integers(m)] = rng.uniform(-0.5, 0.5)
+            A.append(a)
+            B.append(b)
+        pde, kind, args = S.linear_pde(A, B), None, None
+    qn = rng.uniform(-1, 1, (E, n ** 3 * m))
+    q = torch.from_numpy(oracle.to_aosoa(n, m, m, qn)).cuda()
+    dt = 2e-3
+    plan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=m, out_stride=m)
+    out = plan.predict(q, dt)
+    plan.status()
+    if kind is not None:
+        ref = oracle.stp(n, m, qn, dt, pde_kind=kind, args=args)
+        worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, m, m=m)
+        assert max(worst.values()) <= TOL, worst
+    monkeypatch.setenv("ADERSTP_FORCE_GENERIC", "1")
+    gplan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=m, out_stride=m)
+    gen = gplan.predict(q, dt)
+    gplan.status()
+    for x, y in ((out.qavg, gen.qavg), (out.favg, gen.favg), (out.face_q, gen.face_q), (out.face_f, gen.face_f)):
+        assert O.per_element_rel_diff(y.cpu().numpy().reshape(E, -1), x.cpu().numpy().reshape(E, -1)) <= TOL

@@ -42,3 +42,22 @@ for n, E in ((4, 32768), (6, 16384), (8, 8192), (9, 4096), (10, 4096)):
     e1.record()
     torch.cuda.synchronize()
     print(lib, "linear-elastic", n, "%.3f M elem/s" % (E / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e6))
+
+for name, pde, m in (("advection-m8", S.advection_pde((1.0, 0.5, 0.25), 8), 8), ("demo-m6", S.paper_demo_pde(), 6)):
+    n, E = 8, 16384
+    q = torch.randn(E, n ** 3 * m, dtype=torch.float64, device="cuda")
+    for generic in ("0", "1"):
+        os.environ["ADERSTP_FORCE_GENERIC"] = generic
+        plan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=m, out_stride=m)
+        out = plan.alloc_output(E)
+        for _ in range(3):
+            plan.predict(q, 1e-3, out=out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            plan.predict(q, 1e-3, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        print(lib, name, n, "generic" if generic == "1" else "default", "%.3f M elem/s" % (E / (e0.elapsed_time(e1) / 10 * 1e-3) / 1e6))
+    os.environ["ADERSTP_FORCE_GENERIC"] = "0"
