@@ -606,7 +606,7 @@ struct ParamsG {
   int m, n_terms, q_stride, check;
 };
 
-__global__ void __launch_bounds__(NWARP * 32) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, unsigned int* status) {
+__global__ void __maxnreg__(80) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, unsigned int* status) {
   constexpr int THREADS8 = NWARP * 32;
   extern __shared__ __align__(16) double smg[];
   const int m = kp.m, nt = kp.n_terms;
