@@ -31,8 +31,11 @@ int cuda_fail(cudaError_t e, const char* what) {
 
 constexpr int kHostStreams = 3;
 
+// the reference layout through device transposes to a tuned AoSoA kernel: the elastic PDE, and
+// table PDEs with m <= 8 at nDof 8 (stp_dmma8_table)
 bool aos_staged(const aderstp::LaunchPlan& lp) {
-  return lp.kind == ADERSTP_PDE_ELASTIC && lp.src_comp < 0 && lp.layout == ADERSTP_LAYOUT_AOS && !lp.force_generic;
+  const bool tuned = lp.kind == ADERSTP_PDE_ELASTIC || (lp.kind != ADERSTP_PDE_ELASTIC_SOURCE && lp.n == 8 && lp.m <= 8);
+  return tuned && lp.src_comp < 0 && lp.layout == ADERSTP_LAYOUT_AOS && !lp.force_generic;
 }
 
 cudaMemPoolProps& pool_props_of(int device) {
@@ -271,7 +274,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   aderstp::LaunchPlan kl = lp;
   if (aos_staged(lp)) {
     kl.layout = ADERSTP_LAYOUT_AOSOA;
-    kl.q_stride = kl.out_stride = 9;
+    kl.q_stride = kl.out_stride = lp.m;
   }
   // plan-owned stream-ordered pool (AoS staging, time-loop faces): keeps its memory between
   // calls, returned when the plan is destroyed
@@ -332,10 +335,10 @@ cudaError_t predict_aos_staged(const aderstp_plan* plan, const aderstp::BatchArg
   const aderstp::LaunchPlan& lp = plan->lp;
   aderstp::LaunchPlan sp = lp;
   sp.layout = ADERSTP_LAYOUT_AOSOA;
-  sp.q_stride = 9;
-  sp.out_stride = 9;
-  const int n = lp.n;
-  const size_t t9 = (size_t)n * n * n * 9;  // one AoSoA tensor (doubles)
+  const int n = lp.n, m = lp.m;  // compact AoSoA staging: quantity stride m
+  sp.q_stride = m;
+  sp.out_stride = m;
+  const size_t t9 = (size_t)n * n * n * m;  // one AoSoA tensor (doubles)
   const size_t per = t9 * (a.favg ? 5 : 2);  // q, qavg (+ favg[3])
   long long chunk = std::max<long long>(1, std::min<long long>(a.n_elem, (8ll << 30) / (long long)(per * 8)));
   if (lp.aos_chunk > 0) chunk = std::min<long long>(chunk, lp.aos_chunk);  // tests: force several chunks
@@ -349,16 +352,16 @@ cudaError_t predict_aos_staged(const aderstp_plan* plan, const aderstp::BatchArg
   const size_t qin = (size_t)n * n * n * lp.q_stride, qout = (size_t)n * n * n * lp.out_stride;
   for (long long e0 = 0; e0 < a.n_elem && err == cudaSuccess; e0 += chunk) {
     const long long c = std::min(chunk, a.n_elem - e0);
-    err = aderstp::launch_convert(n, 9, c, ADERSTP_LAYOUT_AOS, lp.q_stride, a.q + e0 * qin, ADERSTP_LAYOUT_AOSOA, 9,
+    err = aderstp::launch_convert(n, m, c, ADERSTP_LAYOUT_AOS, lp.q_stride, a.q + e0 * qin, ADERSTP_LAYOUT_AOSOA, m,
                                   sq, st);
-    aderstp::BatchArgs b{sq, a.par + 3 * e0, sqa, sfa, a.face_q ? a.face_q + e0 * face : nullptr,
+    aderstp::BatchArgs b{sq, a.par ? a.par + 3 * e0 : nullptr, sqa, sfa, a.face_q ? a.face_q + e0 * face : nullptr,
                          a.face_f ? a.face_f + e0 * face : nullptr, c, a.dt, a.t_start};
     if (err == cudaSuccess) err = aderstp::launch_stp(sp, b, st);
     if (err == cudaSuccess)
-      err = aderstp::launch_convert(n, 9, c, ADERSTP_LAYOUT_AOSOA, 9, sqa, ADERSTP_LAYOUT_AOS, lp.out_stride,
+      err = aderstp::launch_convert(n, m, c, ADERSTP_LAYOUT_AOSOA, m, sqa, ADERSTP_LAYOUT_AOS, lp.out_stride,
                                     a.qavg + e0 * qout, st);
     if (sfa && err == cudaSuccess)  // favg[e][d][...]: three consecutive tensors per element in both layouts
-      err = aderstp::launch_convert(n, 9, 3 * c, ADERSTP_LAYOUT_AOSOA, 9, sfa, ADERSTP_LAYOUT_AOS, lp.out_stride,
+      err = aderstp::launch_convert(n, m, 3 * c, ADERSTP_LAYOUT_AOSOA, m, sfa, ADERSTP_LAYOUT_AOS, lp.out_stride,
                                     a.favg + e0 * 3 * qout, st);
   }
   cudaFreeAsync(buf, st);

@@ -457,3 +457,24 @@ def test_table_pdes_on_tensor_cores_nDof8(stp, oracle, monkeypatch, case):
     gplan.status()
     for x, y in ((out.qavg, gen.qavg), (out.favg, gen.favg), (out.face_q, gen.face_q), (out.face_f, gen.face_f)):
         assert O.per_element_rel_diff(y.cpu().numpy().reshape(E, -1), x.cpu().numpy().reshape(E, -1)) <= TOL
+
+
+@pytest.mark.parametrize("case", ["advection_m3", "demo_m6"])
+def test_table_pdes_reference_layout_nDof8(stp, oracle, case):
+    """The reference layout (AoS, m_pad = 8 for m <= 8, layout.cpp:9-21) of a table PDE at nDof 8
+    goes through the device transposes to stp_dmma8_table; it agrees with the oracle."""
+    S = stp
+    n, E = 8, 5
+    m, pde, kind, args = ((3, S.advection_pde((1.0, 0.5, 0.25), 3), O.PDE_ADVECTION, [1.0, 0.5, 0.25])
+                          if case == "advection_m3" else (6, S.paper_demo_pde(), O.PDE_DEMO, []))
+    rng = np.random.default_rng(_zlib.crc32(case.encode()) + 1)
+    qn = rng.uniform(-1, 1, (E, n ** 3 * m))
+    aos = np.zeros((E, n ** 3, 8))
+    aos[:, :, :m] = qn.reshape(E, n ** 3, m)
+    plan = S.Plan(n, pde, layout=S.LAYOUT_AOS, q_stride=8, out_stride=8)
+    out = plan.predict(torch.from_numpy(aos.reshape(E, -1)).cuda(), 2e-3)
+    plan.status()
+    ref = oracle.stp(n, m, qn, 2e-3, pde_kind=kind, args=args)
+    worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOS, 8, m=m)
+    assert max(worst.values()) <= TOL, worst
+    assert not np.any(out.qavg.cpu().numpy().reshape(E, n ** 3, 8)[:, :, m:])
