@@ -274,6 +274,34 @@ def measure_reference_layout(S, cfg, steps, warmup):
             "path": "stp_dmma8<AOS>: planes staged from the node rows, qavg/favg written as node rows"}
 
 
+def measure_table_pde(S, steps, warmup):
+    """The user-LinearPde path on the tensor cores: the reference's advection system with m = 8
+    quantities (proj/src/pde.cpp:61-85) at nDof 8, 65,536 elements, device-resident."""
+    import torch
+    n, m, E = 8, 8, 65536
+    pde = S.advection_pde((1.0, 0.5, 0.25), m)
+    g = torch.Generator(device="cuda").manual_seed(SEED)
+    q = torch.rand(E, n ** 3 * m, dtype=torch.float64, device="cuda", generator=g) * 2.0 - 1.0
+    plan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=m, out_stride=m)
+    out = plan.alloc_output(E)
+    dt = 0.5 / (3.0 * 1.0 * (2 * n - 1))
+    for _ in range(warmup):
+        plan.predict(q, dt, out=out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        plan.predict(q, dt, out=out)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    plan.status()
+    ms = ev0.elapsed_time(ev1) / steps
+    del q, out
+    return {"workload": "advection PDE, m = 8 quantities, nDof 8, 65,536 elements, Q~U[-1,1] (user LinearPde path)",
+            "elements_per_s": E / (ms * 1e-3), "ms_per_step": ms, "kernel": "stp_dmma8_table"}
+
+
 def measure_timestep(S, n, e, steps, warmup):
     """One full time step of the GPU solver on an e^3 periodic mesh: the
     predictor on the 1/h-scaled PDE without favg (the corrector never reads it, solver.cpp:184-253)
@@ -512,6 +540,7 @@ def main():
                             "frac_of_roofline": pg / rf["roofline_elements_per_s"], "bound": rf["bound"]}
         others["timestep_n8"] = measure_timestep(S, 8, 50, max(5, args.steps // 4), 3)
         others["c3_reference_layout"] = measure_reference_layout(S, CONFIGS["c3"], max(5, args.steps // 4), 3)
+        others["table_pde_advection_m8_n8"] = measure_table_pde(S, max(5, args.steps // 4), 3)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
