@@ -594,7 +594,7 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
 // every term one more pair of DMMAs (x, y) or register DFMAs (z) into the same accumulators, the
 // coefficient folded into the D fragments.  favg_d = A_d qavg and face_f = A_d face_q from the
 // favg tables (fr, fc); faces and bulk stores as in the elastic kernel.
-constexpr int GM = 8;  // quantities of the table kernel
+constexpr int GM = 9;  // quantities of the table kernel (the 9th is split over the warps by plane)
 struct ParamsG {
   double d[64];
   double phi[2][8];
@@ -633,8 +633,9 @@ __global__ void __maxnreg__(80) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, 
   __syncthreads();
   const double d0 = kp.d[g * 8 + t], d1 = kp.d[g * 8 + 4 + t];
   const int s = warp;
-  const bool own = s < m;
+  const bool own = s < m && s < 8;
   double tt[8][2];
+  double t8[1][2];  // m = 9: plane k3 = warp of quantity 8
   // ---- Horner form of the CK series (see ck_quantity) ----------------------------------------
 #pragma unroll 1
   for (int o = N8 - 2; o >= 0; --o) {
@@ -654,11 +655,25 @@ __global__ void __maxnreg__(80) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, 
         if (cz != 0.0) dfma_z<8>(tt, P + kp.tr[s][2][k] * PV, 0, col, cz);
       }
     }
+    if (m == GM) {  // quantity 8: warp w takes plane k3 = w
+      const double co = kp.cf[o];
+      const double2 v = lds2(Q + 8 * PV + warp * 64 + col);
+      t8[0][0] = co * v.x;
+      t8[0][1] = co * v.y;
+#pragma unroll 1
+      for (int k = 0; k < nt; ++k) {
+        const double cx = kp.tc[8][0][k], cy = kp.tc[8][1][k], cz = kp.tc[8][2][k];
+        if (cx != 0.0) mma_x<1>(t8, P + kp.tr[8][0][k] * PV, warp, g, t, cx * d0, cx * d1);
+        if (cy != 0.0) mma_y<1>(t8, P + kp.tr[8][1][k] * PV, warp, g, t, cy * d0, cy * d1);
+        if (cz != 0.0) dfma_z<1>(t8, P + kp.tr[8][2][k] * PV, warp, col, cz);
+      }
+    }
     __syncthreads();  // every warp has finished reading r
     if (own) {
 #pragma unroll
       for (int k = 0; k < 8; ++k) sts2(P + s * PV + k * 64 + col, tt[k][0], tt[k][1]);
     }
+    if (m == GM) sts2(P + 8 * PV + warp * 64 + col, t8[0][0], t8[0][1]);
     __syncthreads();  // new r (qavg after the last step) complete
   }
   // ---- epilogue: qavg and favg of quantity s, x/y/z faces --------------------------------------
@@ -724,6 +739,57 @@ __global__ void __maxnreg__(80) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, 
       for (int j = 0; j < 2; ++j) {
         FQ[4 * FACE + (g * 8 + 2 * t + j) * m + s] = z0[j];
         FQ[5 * FACE + (g * 8 + 2 * t + j) * m + s] = z1[j];
+      }
+    }
+  }
+  if (m == GM) {  // quantity 8, plane k3 = warp: qavg, favg, x / y faces; warp 0 also the z faces
+    const int k3 = warp;
+    double* qout = a.qavg + e * (long long)(PV * m) + 8 * 8 + 2 * t;
+    st_cs2(qout + (k3 * 8 + g) * m * 8, t8[0][0], t8[0][1]);
+    if (a.favg) {
+      double* fout = a.favg + e * (long long)(3 * PV * m) + 8 * 8 + 2 * t;
+#pragma unroll 1
+      for (int d = 0; d < 3; ++d) {
+        double f0 = 0.0, f1 = 0.0;
+#pragma unroll 1
+        for (int kt = 0; kt < nt; ++kt) {
+          const double c = kp.fc[8][d][kt];
+          if (c == 0.0) continue;
+          const double2 v = lds2(P + kp.fr[8][d][kt] * PV + k3 * 64 + col);
+          f0 = fma(c, v.x, f0);
+          f1 = fma(c, v.y, f1);
+        }
+        st_cs2(fout + d * (PV * m) + (k3 * 8 + g) * m * 8, f0, f1);
+      }
+    }
+    if (faces) {
+      const double bphi0 = (g < 2) ? kp.phi[g][t] : 0.0, bphi1 = (g < 2) ? kp.phi[g][4 + t] : 0.0;
+      double xf[1][2] = {{0.0, 0.0}}, yf[1][2] = {{0.0, 0.0}};
+      mma_x<1>(xf, P + 8 * PV, k3, g, t, bphi0, bphi1);
+      mma_y<1>(yf, P + 8 * PV, k3, g, t, bphi0, bphi1);
+      if (t == 0) {
+        FQ[0 * FACE + (k3 * 8 + g) * m + 8] = xf[0][0];
+        FQ[1 * FACE + (k3 * 8 + g) * m + 8] = xf[0][1];
+      }
+      if (g < 2) {
+        FQ[(2 + g) * FACE + (k3 * 8 + 2 * t) * m + 8] = yf[0][0];
+        FQ[(2 + g) * FACE + (k3 * 8 + 2 * t + 1) * m + 8] = yf[0][1];
+      }
+      if (warp == 0) {
+        double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const double2 v = lds2(P + 8 * PV + kk * 64 + col);
+          z0[0] = fma(kp.phi[0][kk], v.x, z0[0]);
+          z0[1] = fma(kp.phi[0][kk], v.y, z0[1]);
+          z1[0] = fma(kp.phi[1][kk], v.x, z1[0]);
+          z1[1] = fma(kp.phi[1][kk], v.y, z1[1]);
+        }
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          FQ[4 * FACE + (g * 8 + 2 * t + j) * m + 8] = z0[j];
+          FQ[5 * FACE + (g * 8 + 2 * t + j) * m + 8] = z1[j];
+        }
       }
     }
   }

@@ -416,7 +416,7 @@ def test_reference_layout_checks_and_edges(stp, oracle, n):
         assert O.per_element_rel_diff(b.cpu().numpy().reshape(E, -1), a.cpu().numpy().reshape(E, -1)) <= TOL
 
 
-@pytest.mark.parametrize("case", ["advection_m3", "ncp_advection_m2", "demo_m6", "probed_m5", "probed_m8"])
+@pytest.mark.parametrize("case", ["advection_m3", "ncp_advection_m2", "demo_m6", "probed_m5", "probed_m8", "probed_m9"])
 def test_table_pdes_on_tensor_cores_nDof8(stp, oracle, monkeypatch, case):
     """Table PDEs (the user-LinearPde path) at nDof 8 run on stp_dmma8_table; the reference's
     PDEs against the oracle, random probed systems (flux + ncp matrices, up to 4 nonzeros per
