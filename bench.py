@@ -29,9 +29,31 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the host cores this process may use, read before any OpenMP runtime binds the main thread
+try:
+    HOST_CORES = len(os.sched_getaffinity(0))
+except AttributeError:
+    HOST_CORES = os.cpu_count() or 1
 
-from paper_2003_12787_b200.shard import (barrier, chunks, env_world, max_over_ranks,  # noqa: E402
-                                         strong_shard, sum_over_ranks, weak_shard)
+
+
+def _load_shard_module():
+    """paper_2003_12787_b200/shard.py loaded as a standalone module: importing it through the
+    package would run the package __init__, which maps libaderstp.so -- and the reference arm's
+    process must never load our library (it times the unmodified reference only)."""
+    import importlib.util
+    path = os.path.join(ROOT, "paper_2003_12787_b200", "shard.py")
+    spec = importlib.util.spec_from_file_location("_aderstp_bench_shard", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod
+    spec.loader.exec_module(mod)
+    return mod
+
+
+_shard = _load_shard_module()
+barrier, chunks, env_world = _shard.barrier, _shard.chunks, _shard.env_world
+max_over_ranks, sum_over_ranks = _shard.max_over_ranks, _shard.sum_over_ranks
+strong_shard, weak_shard = _shard.strong_shard, _shard.weak_shard
 
 METRIC = "linear STP elements/s & fp64 GFLOP/s (% of roofline) vs order N, 1–8 B200"
 UNIT = "elements/s"
@@ -60,13 +82,52 @@ CONFIGS = {
                  desc="C5: elastic STP order N=5 (nDof 6), 1,048,576 elements split over the GPUs"),
 }
 SEED = 20031278
-REFERENCE_SAMPLE = {"c1": 64, "c2": 8192, "c3": 4096, "c4": 1024, "n9": 2048, "c5": 4096, "c5n6": 8192}
+# dt of every config: stable_dt (proj/src/solver.cpp:170-174) at CFL 0.5 for the material's largest
+# P-wave speed (cp ~ U[4,6] per element, so cp <= 6).  A fixed bound instead of the sampled maximum
+# keeps dt identical across both bench arms, every GPU count and every sample size.
+CFL, CP_BOUND = 0.5, 6.0
+# elements timed per step by the CPU reference (C1/C2 the full set, C3-C5 a
+# fixed 16,384-element subset -- elements 0..16,383 of the same seeded workload)
+REFERENCE_SAMPLE = {"c1": 64, "c2": 32768, "c3": 16384, "c4": 16384, "n9": 16384, "c5": 16384, "c5n6": 16384}
+REFERENCE_REPS = 3
+
+
+def config_dt(n):
+    return CFL / (3.0 * CP_BOUND * (2.0 * n - 1.0))
+
+
+def config_of(name, world):
+    """The workload description both arms print (identical keys and values for one --config and
+    --gpus); what a run did beyond the workload (launches, graphs, samples) goes elsewhere."""
+    cfg = CONFIGS[name]
+    n = cfg["n"]
+    total = cfg["elems"] if cfg.get("strong") else world * cfg["elems"]
+    return {"workload": cfg["desc"], "name": name, "order": n - 1, "n_dof": n, "quantities": 9,
+            "global_elements": total, "elements_per_gpu": total // world if cfg.get("strong") else cfg["elems"],
+            "layout": f"AoSoA [e][k3][k2][s<{cfg['q_stride']}][k1] in, [e][k3][k2][9][k1] out",
+            "input_distribution": ["U[-1,1]", "N(0,1)", "3 random-phase sinusoids"][cfg["dist"]],
+            "material": "per element rho~U[2,3], cp~U[4,6], cs~U[2,3.5]",
+            "dt": config_dt(n), "cfl": CFL, "seed": SEED,
+            "parallelism": f"element shards x{world} (no hot-path collective)",
+            "l2": "no flush needed: inputs %.2f GB and outputs %.2f GB per GPU step vs 126 MB L2" % (
+                (total // world if cfg.get("strong") else cfg["elems"]) * n ** 3 * cfg["q_stride"] * 8 / 1e9,
+                (total // world if cfg.get("strong") else cfg["elems"]) * (4 * n ** 3 * 9 + 12 * n * n * 9) * 8 / 1e9)}
 
 
 def fp64_peak():
-    """Measured fp64 peak on this pool's B200 (tools/fp64_peaks.cu, profiles/fp64_peaks_r01.txt):
-    DMMA 37.1 TFLOP/s, DFMA 34.1 TFLOP/s at 1965 MHz.  MEASURED_PEAKS.json has no fp64 entry."""
-    return 37.1e12
+    """fp64 pipe peak of this pool's B200, measured (MEASURED_PEAKS.json has no fp64 entry):
+    profiles/fp64_peaks_r02.json, written by tools/fp64_peaks.py -- DMMA m8n8k4 f64 sustained over
+    seconds with the SM clock and throttle reasons sampled beside it (DFMA alone is lower; the
+    larger of the two pipes is the denominator).  Returns (FLOP/s, source description)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peaks_r02.json")) as f:
+            d = json.load(f)
+        tf = max(d["dmma_sustained_tflops"], d["dfma_sustained_tflops"])
+        ck = d["dmma_sustained_clocks"]
+        return tf * 1e12, (f"measured sustained DMMA fp64 {tf} TFLOP/s at SM {ck['sm_mhz_median']} MHz "
+                           f"(reasons {ck['reasons'] or 'none'}), profiles/fp64_peaks_r02.json")
+    except (OSError, KeyError, ValueError):
+        return 37.1e12, "measured DMMA fp64 37.1 TFLOP/s, profiles/fp64_peaks_r01.txt (no clock record)"
 
 
 def hbm_peak():
@@ -188,8 +249,7 @@ def measure_device(S, cfg, world, rank, steps, warmup, want_clocks=True):
     grid = round(cfg["elems"] ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
     q, par = S.generate(cfg["dist"], SEED, n, sh.start, sh.count, grid=grid, layout=S.LAYOUT_AOSOA,
                         q_stride=cfg["q_stride"])
-    cp_max = max_over_ranks(float(par[:, 1].max().item()) if sh.count else 0.0, device="cuda")
-    dt = S.stable_dt(n, cp_max, cfl=0.5)
+    dt = config_dt(n)
     plan = make_plan(S, cfg)
     chunk = max(1, min(cfg.get("chunk", sh.count), sh.count))
     out = plan.alloc_output(chunk)
@@ -255,7 +315,7 @@ def measure_reference_layout(S, cfg, steps, warmup):
     del q9
     plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOS, q_stride=16, out_stride=16, par_kind=S.PAR_RHO_CP_CS)
     out = plan.alloc_output(E)
-    dt = S.stable_dt(n, float(par[:, 1].max()), cfl=0.5)
+    dt = config_dt(n)
     for _ in range(warmup):
         plan.predict(q, dt, par=par, out=out)
     torch.cuda.synchronize()
@@ -402,66 +462,156 @@ def measure_e2e(S, plan, cfg, world, rank, dt, steps):
                 api="aderstp_predict_batch_host (pinned host buffers, copies pipelined on 3 streams)")
 
 
-def cpu_reference_run(cfg, sample, reps=3, threads=None, single_core=False):
-    """The reference's own CPU path (oracle/_ref) on `sample` elements: best of reps, faster of
-    splitck / splitck_aosoa.  Falls back to our C port when _ref is absent."""
-    import oracle as O
-    n = cfg["n"]
-    orc = O.Oracle()
-    grid = round(cfg["elems"] ** (1.0 / 3.0)) if cfg["dist"] == 2 else 1
-    q, par = orc.generate(cfg["dist"], SEED, n, 0, sample, grid=grid)
-    lmr = orc.material_lmr(par)
-    dt = O.cfl_dt(n, 6.0)
-    threads = threads or (os.cpu_count() or 1)
-    best, variant_used = math.inf, None
-    if O.reference_available():
-        ref = O.Reference()
-        kind = "reference"
-        for variant in ("splitck", "aosoa"):
-            for _ in range(reps):
-                r = ref.stp(n, 9, q, dt, par=lmr, variant=variant, threads=threads)
-                if r.seconds < best:
-                    best, variant_used = r.seconds, variant
-        lib = os.path.basename(ref.path)
-    else:
-        kind = "port"
-        for _ in range(reps):
-            t0 = time.perf_counter()
-            orc.stp(n, 9, q, dt, par=lmr, threads=threads)
-            best = min(best, time.perf_counter() - t0)
-        variant_used, lib = "oracle/stp_oracle.c", "libstp_oracle.so"
-    out = dict(value=sample / best, unit=UNIT, cores=threads, kind=kind,
-               sample=f"{sample} elements of {cfg['desc'].split(':')[0]}, best of {reps} reps, "
-                      f"variant {variant_used} ({lib}), {threads} threads, predict loop only")
-    if single_core and O.reference_available() and threads > 1:  # SURVEY.md 8(d): also report 1 core
-        one = max(64, sample // threads)
-        r1 = min(ref.stp(n, 9, q[:one], dt, par=lmr[:one], variant=variant_used, threads=1).seconds
-                 for _ in range(reps))
+def host_cpu_info():
+    """CPU model and the cores this process may run on (the reference's OpenMP threads are pinned
+    one per core: OMP_PROC_BIND=close, OMP_PLACES=cores, set before libgomp initialises)."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"cpu_model": model, "cores_available": HOST_CORES, "os_cpu_count": os.cpu_count(),
+            "pinning": "OMP_PROC_BIND=%s OMP_PLACES=%s" % (os.environ.get("OMP_PROC_BIND"),
+                                                           os.environ.get("OMP_PLACES"))}
+
+
+def repo_libraries_mapped():
+    """Shared objects from this repository mapped into this process (/proc/self/maps): the
+    reference arm must show only oracle/_ref, never paper_2003_12787_b200/libaderstp.so."""
+    libs = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for ln in f:
+                p = ln.split()[-1] if ln.strip() else ""
+                if p.endswith(".so") and os.path.realpath(p).startswith(os.path.realpath(ROOT)):
+                    libs.add(os.path.relpath(os.path.realpath(p), os.path.realpath(ROOT)))
+    except OSError:
+        pass
+    return sorted(libs)
+
+
+def _pin_openmp():
+    # must run before oracle/_ref (and its libgomp) is loaded into this process
+    os.environ.setdefault("OMP_PROC_BIND", "close")
+    os.environ.setdefault("OMP_PLACES", "cores")
+
+
+class CpuReference:
+    """The reference's own CPU STP (oracle/_ref: the unmodified sources compiled by
+    oracle/Makefile), driven like its production caller -- an OpenMP loop over elements, one
+    ScratchArena per thread, predict(splitck | splitck_aosoa) + extrapolate_faces, one
+    elastic_pde per element (proj/src/solver.cpp:334-345) -- on elements 0..sample-1 of the
+    config's seeded workload with the config's dt.  Falls back to the C restatement (kind "port")
+    only where oracle/_ref was not built."""
+
+    def __init__(self, name, sample=None, threads=None):
+        _pin_openmp()
+        import oracle as O
+        self.O, self.name, self.cfg = O, name, CONFIGS[name]
+        n = self.cfg["n"]
+        self.sample = sample or REFERENCE_SAMPLE[name]
+        orc = O.Oracle()
+        grid = round(self.cfg["elems"] ** (1.0 / 3.0)) if self.cfg["dist"] == 2 else 1
+        self.q, par = orc.generate(self.cfg["dist"], SEED, n, 0, self.sample, grid=grid)
+        self.lmr = orc.material_lmr(par)
+        self.dt = config_dt(n)
+        self.threads = threads or host_cpu_info()["cores_available"]
+        self.ref = O.Reference() if O.reference_available() else None
+        self.orc = orc
+        self.kind = "reference" if self.ref else "port"
+        self.variant = None
+
+    def run_once(self, variant, threads=None, count=None):
+        """Seconds of one predict loop over the sample (or its first `count` elements)."""
+        n, t = self.cfg["n"], threads or self.threads
+        q, lmr = (self.q, self.lmr) if count is None else (self.q[:count], self.lmr[:count])
+        if self.ref is not None:
+            return self.ref.stp(n, 9, q, self.dt, par=lmr, variant=variant, threads=t).seconds
+        t0 = time.perf_counter()
+        self.orc.stp(n, 9, q, self.dt, par=lmr, threads=t)
+        return time.perf_counter() - t0
+
+    def pick_variant(self):
+        """The faster of splitck / splitck_aosoa on this host (one timed pass each)."""
+        if self.ref is None:
+            self.variant = "oracle/stp_oracle.c"
+        elif self.variant is None:
+            self.variant = min(("splitck", "aosoa"), key=lambda v: self.run_once(v))
+        return self.variant
+
+    def best_of(self, reps=REFERENCE_REPS):
+        v = self.pick_variant()
+        return min(self.run_once(v) for _ in range(reps))
+
+    def describe(self, value, reps):
+        lib = os.path.basename(self.ref.path) if self.ref else "oracle/libstp_oracle.so"
+        info = host_cpu_info()
+        return dict(value=value, unit=UNIT, cores=self.threads, kind=self.kind,
+                    sample=f"elements 0..{self.sample - 1} of {self.cfg['desc'].split(':')[0]} "
+                           f"({self.sample} of {self.cfg['elems']} elements; same seed, material and dt), "
+                           f"best of {reps} reps, variant {self.variant} ({lib}), {self.threads} threads, "
+                           "predict + extrapolate_faces loop",
+                    cpu_model=info["cpu_model"], pinning=info["pinning"],
+                    extrapolation="elements/s of the sample = elements/s of the full workload "
+                                  "(elements are independent)")
+
+
+def cpu_reference_run(name, reps=REFERENCE_REPS, single_core=False):
+    """cpu_baseline of our arm: the same measurement as the reference arm, once, in a child
+    process (our process has torch's OpenMP runtime loaded, so the reference's threads could not
+    be pinned here)."""
+    import subprocess
+    env = dict(os.environ, OMP_PROC_BIND="close", OMP_PLACES="cores")
+    env.pop("WORLD_SIZE", None)
+    cmd = [sys.executable, os.path.abspath(__file__), "--impl", "reference", "--config", name, "--cpu-baseline-only"]
+    if single_core:
+        cmd.append("--single-core")
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True)
+    if r.returncode != 0:
+        return {"value": None, "unit": UNIT, "error": r.stderr.strip()[-500:]}
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def _cpu_reference_measure(name, reps=REFERENCE_REPS, single_core=False):
+    cr = CpuReference(name)
+    best = cr.best_of(reps)
+    out = cr.describe(cr.sample / best, reps)
+    if single_core and cr.ref is not None and cr.threads > 1:  # SURVEY.md 8(d): also report 1 core
+        one = max(64, cr.sample // cr.threads)
+        r1 = min(cr.run_once(cr.variant, threads=1, count=one) for _ in range(reps))
         out["single_core_value"] = one / r1
-        out["single_core_sample"] = f"{one} elements, 1 thread, variant {variant_used}"
+        out["single_core_sample"] = f"{one} elements, 1 thread, variant {cr.variant}"
     return out
 
 
-def run_reference_arm(args):
-    world, rank, _ = env_world()
+def run_reference_arm(args, world, rank):
+    """--impl reference: rank 0 alone times the reference CPU STP on the same config; every
+    timed step is the best of REFERENCE_REPS passes over the fixed sample."""
     if rank != 0:
         return 0
-    cfg = CONFIGS[args.config]
-    sample = REFERENCE_SAMPLE[args.config]
-    values, info = [], None
+    cr = CpuReference(args.config)
+    cr.pick_variant()
+    values = []
     for i in range(args.warmup + args.steps):
-        info = cpu_reference_run(cfg, sample, reps=1)
+        best = cr.best_of()
         if i >= args.warmup:
-            values.append(info["value"])
+            values.append(cr.sample / best)
     value = statistics.median(values)
-    info["value"] = value
+    info = cr.describe(value, REFERENCE_REPS)
+    info["steps_values"] = values
+    cfg = CONFIGS[args.config]
     line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sample / value * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": cr.sample / value * 1e3,
             "higher_is_better": True, "scaling": "strong" if cfg.get("strong") else "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded SplitMix64, same generator as our arm)",
-            "config": {"workload": cfg["desc"], "n_dof": cfg["n"], "order": cfg["n"] - 1,
-                       "elements_per_step": sample},
+            "data": "synthetic (seeded SplitMix64, same generator, seed, material and dt as our arm)",
+            "config": config_of(args.config, world),
+            "reference_sample_elements": cr.sample,
+            "repo_libraries_mapped": repo_libraries_mapped(),
             "cpu_baseline": info,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -470,7 +620,7 @@ def run_reference_arm(args):
 
 def roofline_of(S, n, per_gpu, elements_per_launch, traffic):
     flop_e, byte_e = S.flop_count(n, 9), S.byte_count(n, 9, True)
-    fp64 = fp64_peak()
+    fp64, fp64_src = fp64_peak()
     hbm, hbm_src = hbm_peak()
     tf = per_gpu * flop_e / 1e12
     gbs = per_gpu * byte_e / 1e9
@@ -480,10 +630,59 @@ def roofline_of(S, n, per_gpu, elements_per_launch, traffic):
     if fp64 / flop_e < hbm / byte_e:
         return dict({"bound": "fp64", "achieved": tf, "peak": fp64 / 1e12, "unit": "TFLOP/s",
                      "frac": tf / (fp64 / 1e12),
-                     "peak_source": "measured DMMA fp64 peak, profiles/fp64_peaks_r01.txt",
+                     "peak_source": fp64_src,
                      "hbm_achieved_gbs": gbs, "hbm_frac": gbs / (hbm / 1e9)}, **common)
     return dict({"bound": "hbm", "achieved": gbs, "peak": hbm / 1e9, "unit": "GB/s", "frac": gbs / (hbm / 1e9),
                  "peak_source": hbm_src, "fp64_achieved_tflops": tf, "fp64_frac": tf / (fp64 / 1e12)}, **common)
+
+
+def self_launch(args):
+    """`bench.py --gpus N` outside torchrun: relaunch this command as N ranks (one process per
+    GPU) under torch.distributed.run on 127.0.0.1, exactly as the driver does, and pass the
+    rank-0 line through."""
+    import socket
+    import subprocess
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, ADERSTP_BENCH_SELF_LAUNCHED="1", OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
+def dry_run(args, world, rank):
+    """--dry-run: the multi-rank flow without kernels (CPU, gloo): shards, the post-timing
+    reductions and the rank-0 line.  Validates the launcher; never a measurement."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    cfg = CONFIGS[args.config]
+    sh = shard_of(cfg, world, rank)
+    starts = sum_over_ranks(float(sh.start))
+    counts = sum_over_ranks(float(sh.count))
+    c5 = {name: sum_over_ranks(float(shard_of(CONFIGS[name], world, rank).count)) for name in ("c5", "c5n6")}
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world, "dry_run": True,
+                          "config": config_of(args.config, world), "shard_elements_total": counts,
+                          "shard_starts_sum": starts, "c5_elements_total": c5}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_scaling_leg(S, name, world, rank, steps, warmup):
+    """BASELINE configs[4]: 1,048,576 elements split evenly over the GPUs (strong scaling);
+    per-GPU and whole-box elements/s, device-resident, max over ranks."""
+    c = CONFIGS[name]
+    r = measure_device(S, c, world, rank, steps, warmup, want_clocks=False)
+    whole = c["elems"] / (r["ms"] * 1e-3)
+    rf = roofline_of(S, c["n"], whole / world, r["elements_per_launch"], None)
+    return {"workload": c["desc"], "n_dof": c["n"], "global_elements": c["elems"], "n_gpus": world,
+            "elements_per_gpu": r["shard"].count, "launches_per_gpu_step": r["launches_per_step"],
+            "elements_per_launch": r["elements_per_launch"], "ms_per_step": r["ms"],
+            "elements_per_s": whole, "elements_per_s_per_gpu": whole / world,
+            "frac_of_roofline_per_gpu": rf["frac"], "bound": rf["bound"], "checksum": r["checksum"]}
 
 
 def main():
@@ -497,10 +696,25 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-other-configs", action="store_true")
+    ap.add_argument("--no-scaling", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="multi-rank plumbing only (CPU, gloo)")
+    ap.add_argument("--cpu-baseline-only", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--single-core", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    world, rank, _ = env_world()
+    if args.impl == "reference" and args.cpu_baseline_only:
+        print(json.dumps(_cpu_reference_measure(args.config, single_core=args.single_core)), flush=True)
+        return 0
     if args.impl == "reference":
-        return run_reference_arm(args)
+        # rank 0 alone times the host CPU; without torchrun there is nothing to launch
+        return run_reference_arm(args, max(world, args.gpus), rank)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return self_launch(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        return dry_run(args, world, rank)
 
     import paper_2003_12787_b200 as S
 
@@ -524,6 +738,13 @@ def main():
     if not args.no_e2e:
         e2e = measure_e2e(S, res["plan"], cfg, world, rank, res["dt"], args.e2e_steps)
 
+    # BASELINE configs[4] (C5) at every GPU count: nDof 8 and nDof 6, 1,048,576 elements split
+    scaling = {}
+    if not args.no_scaling:
+        for name in ("c5", "c5n6"):
+            if name != args.config:
+                scaling[name] = measure_scaling_leg(S, name, world, rank, max(5, args.steps // 4), 3)
+
     others = {}
     if not args.no_other_configs and world == 1:
         for name in ("c1", "c2", "c4", "n9"):
@@ -543,30 +764,25 @@ def main():
         others["table_pde_advection_m8_n8"] = measure_table_pde(S, max(5, args.steps // 4), 3)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_reference_run(cfg, 16384 if n <= 8 else 4096, single_core=True)
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_reference_run(args.config, single_core=(world == 1))
 
     if rank == 0:
-        sh = res["shard"]
-        E = sh.count
+        E = res["shard"].count
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong" if cfg.get("strong") else "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic (seeded SplitMix64 stream, generated on device; per-element rho~U[2,3], "
                         "cp~U[4,6], cs~U[2,3.5])",
-                "config": {"workload": cfg["desc"], "order": n - 1, "n_dof": n, "elements_per_gpu": E,
-                           "global_elements": total,
-                           "parallelism": f"element shards x{world} (no hot-path collective)",
-                           "launches_per_step": res["launches_per_step"], "cuda_graph": res["cuda_graph"],
-                           "layout": f"AoSoA [e][k3][k2][s<{cfg['q_stride']}][k1] in, [e][k3][k2][9][k1] out",
-                           "dt": res["dt"], "cfl": 0.5,
-                           "l2": "no flush needed: inputs %.1f GB and outputs %.1f GB per step >> 126 MB L2" % (
-                               E * n ** 3 * cfg["q_stride"] * 8 / 1e9,
-                               E * (4 * n ** 3 * 9 + 12 * n * n * 9) * 8 / 1e9)},
+                "config": config_of(args.config, world),
+                "run": {"elements_this_rank0": E, "launches_per_step": res["launches_per_step"],
+                        "cuda_graph": res["cuda_graph"], "elements_per_launch": res["elements_per_launch"]},
                 "fp64_gflops_per_gpu": per_gpu * roofline["flop_per_element"] / 1e9,
+                "elements_per_s_per_gpu": per_gpu,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": args.steps * res["launches_per_step"],
-                "clocks": res["clocks"], "checksum": res["checksum"], "other_configs": others}
+                "clocks": res["clocks"], "checksum": res["checksum"],
+                "c5_strong_scaling": scaling, "other_configs": others}
         print(json.dumps(line), flush=True)
     import torch.distributed as dist
     if dist.is_available() and dist.is_initialized():

@@ -179,6 +179,8 @@ class Reference:
         lib.ref_stp_batch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp,
                                       _dp, ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp, _dp,
                                       _dp, _dp, ctypes.c_int, _dp]
+        lib.ref_stp_batch_matrix.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp, _dp,
+                                             ctypes.c_double, _dp, _dp, _dp, _dp, ctypes.c_int, _dp]
         lib.ref_last_error.restype = ctypes.c_char_p
         lib.ref_make_basis.argtypes = [ctypes.c_int] + [_dp] * 5
         lib.ref_splitmix64.argtypes = [ctypes.c_uint64, ctypes.c_long, ctypes.POINTER(ctypes.c_uint64)]
@@ -233,6 +235,21 @@ class Reference:
             raise ValueError(self.lib.ref_last_error().decode())
         return Outputs(qavg, favg, fq, ff, secs.value)
 
+
+    def stp_matrix(self, n, m, q, dt, A, B=None, variant="splitck", threads=None) -> Outputs:
+        """The reference predict() + extrapolate_faces for a user LinearPde given by its
+        matrices A_d (F_d(q) = A_d q) and B_d (ncp), via the shim's MatrixPde."""
+        q = np.ascontiguousarray(q, dtype=np.float64).reshape(-1, n ** 3 * m)
+        a = np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.float64) for x in A]))
+        b = None if B is None else np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.float64) for x in B]))
+        qavg, favg, fq, ff = _alloc(n, m, q.shape[0])
+        secs = ctypes.c_double(0.0)
+        rc = self.lib.ref_stp_batch_matrix(VARIANTS[variant], n, m, q.shape[0], _ptr(q), _ptr(a), _ptr(b), dt,
+                                           _ptr(qavg), _ptr(favg), _ptr(fq), _ptr(ff),
+                                           threads or (os.cpu_count() or 1), ctypes.byref(secs))
+        if rc != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
+        return Outputs(qavg, favg, fq, ff, secs.value)
 
     # ---- corrector / time loop (proj/src/solver.cpp); mesh state canonical [c][k3][k2][k1][s] ----
     def corrector_step(self, n, m, e, domain_len, u, qavg, face_q, face_f, dt, par=None,

@@ -66,18 +66,32 @@ std::unique_ptr<ader::LinearPde> make_pde(int kind, int m, const double* par, co
 
 bool per_element_par(int kind) { return kind == kElastic || kind == kElasticSource; }
 
-}  // namespace
+// A user LinearPde defined by its coefficient matrices (see ref_stp_batch_matrix).
+class MatrixPde final : public ader::LinearPde {
+public:
+  MatrixPde(int m, const double* A, const double* B)
+      : ader::LinearPde(m, 0), a_(A, A + 3 * m * m), b_(B ? std::vector<double>(B, B + 3 * m * m)
+                                                          : std::vector<double>(3 * m * m, 0.0)) {}
+  void flux(const double* q, int dim, double* f) const override { apply(a_, q, dim, f); }
+  void ncp(const double* grad, int dim, double* out) const override { apply(b_, grad, dim, out); }
+  double max_wavespeed() const override { return 1.0; }
 
-extern "C" {
+private:
+  void apply(const std::vector<double>& mat, const double* x, int dim, double* y) const {
+    const double* a = mat.data() + static_cast<std::size_t>(dim) * m_ * m_;
+    for (int r = 0; r < m_; ++r) {
+      double s = 0.0;
+      for (int j = 0; j < m_; ++j) s += a[r * m_ + j] * x[j];
+      y[r] = s;
+    }
+  }
+  std::vector<double> a_, b_;
+};
 
-const char* ref_last_error(void) { return g_err.c_str(); }
-
-// Batched reference predictor. variant: 0 generic, 1 log, 2 splitck, 3 splitck_aosoa
-// (proj/include/ader/config.hpp:11).  Returns 0 on success, -1 if the reference threw
-// (message in ref_last_error).  *seconds receives the wall time of the predict loop alone.
-int ref_stp_batch(int variant, int n, int m, long n_elem, const double* q, const double* par,
-                  const double* args, int pde_kind, double dt, double t_start, double* qavg,
-                  double* favg, double* face_q, double* face_f, int n_threads, double* seconds) {
+int stp_batch(int variant, int n, int m, long n_elem, const double* q, const double* par,
+              const double* args, int pde_kind, std::shared_ptr<ader::LinearPde> given, double dt,
+              double t_start, double* qavg, double* favg, double* face_q, double* face_f,
+              int n_threads, double* seconds) {
   try {
     const ader::Variant v = static_cast<ader::Variant>(variant);
     ader::SolverConfig cfg;
@@ -90,8 +104,8 @@ int ref_stp_batch(int variant, int n, int m, long n_elem, const double* q, const
     const long vol = nn * m, face = static_cast<long>(n) * n * m;
     if (n_threads <= 0) n_threads = omp_get_max_threads();
 
-    std::shared_ptr<ader::LinearPde> shared;
-    if (!per_element_par(pde_kind)) shared = make_pde(pde_kind, m, nullptr, args);
+    std::shared_ptr<ader::LinearPde> shared = given;
+    if (!shared && !per_element_par(pde_kind)) shared = make_pde(pde_kind, m, nullptr, args);
     if (shared && shared->quantities() != m) throw std::invalid_argument("ref_shim: m mismatch");
 
     std::vector<std::string> errors(n_threads);
@@ -143,6 +157,39 @@ int ref_stp_batch(int variant, int n, int m, long n_elem, const double* q, const
         return -1;
       }
     return 0;
+  } catch (const std::exception& ex) {
+    g_err = ex.what();
+    return -1;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// Batched reference predictor. variant: 0 generic, 1 log, 2 splitck, 3 splitck_aosoa
+// (proj/include/ader/config.hpp:11).  Returns 0 on success, -1 if the reference threw
+// (message in ref_last_error).  *seconds receives the wall time of the predict loop alone.
+int ref_stp_batch(int variant, int n, int m, long n_elem, const double* q, const double* par,
+                  const double* args, int pde_kind, double dt, double t_start, double* qavg,
+                  double* favg, double* face_q, double* face_f, int n_threads, double* seconds) {
+  return stp_batch(variant, n, m, n_elem, q, par, args, pde_kind, nullptr, dt, t_start, qavg, favg,
+                   face_q, face_f, n_threads, seconds);
+}
+
+// The same batch for an arbitrary constant-coefficient system given as matrices: A[d] (m x m,
+// row-major, F_d(q) = A_d q) and B[d] (ncp, B_d grad; may be null), wrapped in MatrixPde -- a
+// user LinearPde subclass (proj/include/ader/pde.hpp:21-46) of the kind the reference's own
+// tests probe (proj/tests/test_pde.cpp:14-24).
+int ref_stp_batch_matrix(int variant, int n, int m, long n_elem, const double* q, const double* A,
+                         const double* B, double dt, double* qavg, double* favg, double* face_q,
+                         double* face_f, int n_threads, double* seconds) {
+  try {
+    auto pde = std::make_shared<MatrixPde>(m, A, B);
+    return stp_batch(variant, n, m, n_elem, q, nullptr, nullptr, -1, pde, dt, 0.0, qavg, favg,
+                     face_q, face_f, n_threads, seconds);
   } catch (const std::exception& ex) {
     g_err = ex.what();
     return -1;

@@ -29,3 +29,41 @@ def test_reference_arm_other_ranks_exit_quietly():
     r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
                         "--steps", "1"], capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert r.returncode == 0 and r.stdout.strip() == ""
+
+
+def test_reference_arm_is_clean_and_same_config():
+    """The reference process never maps our library, and both arms print the same `config`."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "c1",
+                        "--steps", "1", "--warmup", "3"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert not any("libaderstp" in p for p in d["repo_libraries_mapped"]), d["repo_libraries_mapped"]
+    assert d["cpu_baseline"]["pinning"] == "OMP_PROC_BIND=close OMP_PLACES=cores"
+    assert d["cpu_baseline"]["cpu_model"]
+    sys.path.insert(0, ROOT)
+    import bench
+    assert d["config"] == bench.config_of("c1", 1)
+    assert d["reference_sample_elements"] == 64
+
+
+def test_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun relaunches itself as two ranks (gloo dry run on CPU:
+    shards, reductions and the rank-0 line; no kernels)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"]
+    assert d["shard_elements_total"] == 2 * 131072 and d["shard_starts_sum"] == 131072
+    assert d["c5_elements_total"] == {"c5": 1048576, "c5n6": 1048576}
+    assert d["config"]["global_elements"] == 262144
+
+
+def test_gpus_flag_must_match_world():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dry-run"],
+                       capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
+    assert r.returncode != 0 and "WORLD_SIZE" in r.stderr

@@ -419,8 +419,9 @@ def test_reference_layout_checks_and_edges(stp, oracle, n):
 @pytest.mark.parametrize("case", ["advection_m3", "ncp_advection_m2", "demo_m6", "probed_m5", "probed_m8", "probed_m9"])
 def test_table_pdes_on_tensor_cores_nDof8(stp, oracle, monkeypatch, case):
     """Table PDEs (the user-LinearPde path) at nDof 8 run on stp_dmma8_table; the reference's
-    PDEs against the oracle, random probed systems (flux + ncp matrices, up to 4 nonzeros per
-    (row, dim)) against the generic table kernel on the same inputs."""
+    PDEs against the oracle, random probed systems (flux + ncp matrices) against the unmodified
+    reference's predict() on a MatrixPde with the same matrices; all against the generic table
+    kernel on the same inputs."""
     S = stp
     n, E = 8, 7
     rng = np.random.default_rng(_zlib.crc32(case.encode()))
@@ -449,8 +450,12 @@ def test_table_pdes_on_tensor_cores_nDof8(stp, oracle, monkeypatch, case):
     plan.status()
     if kind is not None:
         ref = oracle.stp(n, m, qn, dt, pde_kind=kind, args=args)
-        worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, m, m=m)
-        assert max(worst.values()) <= TOL, worst
+    else:  # the reference itself on a user LinearPde defined by the same matrices (MatrixPde)
+        if not O.reference_available():
+            pytest.skip("oracle/_ref not built")
+        ref = O.Reference().stp_matrix(n, m, qn, dt, A, B)
+    worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, m, m=m)
+    assert max(worst.values()) <= TOL, worst
     monkeypatch.setenv("ADERSTP_FORCE_GENERIC", "1")
     gplan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=m, out_stride=m)
     gen = gplan.predict(q, dt)

@@ -249,3 +249,43 @@ def test_corrector_restatement_matches_reference(oracle, reference, kind, m, n, 
     got, ok2 = oracle.corrector_step(n, m, e, L, u0, qavg, fq, ff, smax, par=par, pde_kind=kind, args=args)
     assert ok and ok2
     assert O.per_element_rel_diff(ref_u - u0, got - u0) <= 1e-13
+
+
+def _demo_matrices():
+    """The paper demo system (proj/include/ader/pde.hpp:68-73) as matrices: x-flux rows
+    F0 = -(Q0+Q3+Q4), F1 = -(Q1+Q3+Q5), F2 = -(Q2+Q4+Q5), y/z by the rotation (0 1 2)(3 4 5)."""
+    rot = [0, 1, 2, 3, 4, 5]
+    A = []
+    for _ in range(3):
+        a = np.zeros((6, 6))
+        for r, cols in ((0, (0, 3, 4)), (1, (1, 3, 5)), (2, (2, 4, 5))):
+            for c in cols:
+                a[rot[r], rot[c]] = -1.0
+        A.append(a)
+        rot = [rot[1], rot[2], rot[0], rot[4], rot[5], rot[3]]
+    return A
+
+
+def test_matrix_pde_shim_matches_builtin_pdes(oracle, reference):
+    """The shim's MatrixPde (a user LinearPde defined by A_d, B_d) reproduces the reference's own
+    advection / ncp-advection / demo systems given as their probed matrices: this pins the
+    matrix-PDE oracle used for the GPU's arbitrary probed systems."""
+    v = [1.0, 0.5, 0.25]
+    rng = np.random.default_rng(7)
+    n = 4
+    for kind, m, A, B, args in (
+            (O.PDE_ADVECTION, 3, [-v[d] * np.eye(3) for d in range(3)], None, v),
+            (O.PDE_NCP_ADVECTION, 2, [np.zeros((2, 2))] * 3, [-v[d] * np.eye(2) for d in range(3)], v)):
+        q = rng.uniform(-1, 1, (3, n ** 3 * m))
+        want = reference.stp(n, m, q, 2e-3, pde_kind=kind, args=args, threads=2)
+        got = reference.stp_matrix(n, m, q, 2e-3, A, B, threads=2)
+        for name in ("qavg", "favg", "face_q", "face_f"):
+            assert O.per_element_rel_diff(getattr(want, name), getattr(got, name)) <= 1e-14, (kind, name)
+    q = rng.uniform(-1, 1, (3, n ** 3 * 6))
+    want = reference.stp(n, 6, q, 2e-3, pde_kind=O.PDE_DEMO, threads=2)
+    got = reference.stp_matrix(n, 6, q, 2e-3, _demo_matrices(), threads=2)
+    for name in ("qavg", "favg", "face_q", "face_f"):
+        assert O.per_element_rel_diff(getattr(want, name), getattr(got, name)) <= 1e-14, name
+    # and the C restatement agrees with the matrix form of the demo system
+    c = oracle.stp(n, 6, q, 2e-3, pde_kind=O.PDE_DEMO)
+    assert O.per_element_rel_diff(c.face_f, got.face_f) <= TOL
