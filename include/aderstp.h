@@ -118,9 +118,10 @@ int aderstp_predict_batch(const aderstp_plan* plan, int64_t n_elem, const double
                           double* favg, double* face_q, double* face_f, void* stream);
 
 /* Host buffers (pinned or pageable).  Synchronous: splits the batch into chunks and overlaps
- * host->device copies, the kernel and device->host copies on two streams, using device
- * scratch owned by the plan (allocated on first use, aderstp_plan_reserve_host_path to size
- * it up front).  Returns the input-check status directly. */
+ * host->device copies, the kernel and device->host copies on three streams (chunk i on
+ * stream i mod 3), using device scratch owned by the plan (allocated on first use, or up front
+ * by aderstp_plan_reserve_host_path -- the only allocation this call can make).  Returns the
+ * input-check status directly. */
 int aderstp_predict_batch_host(aderstp_plan* plan, int64_t n_elem, const double* q,
                                const double* par, double dt, double t_start, double* qavg,
                                double* favg, double* face_q, double* face_f);

@@ -30,6 +30,8 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 constexpr int kHostStreams = 3;
+// per-call device scratch of the AoS staged path, and the plan pool's release threshold
+constexpr long long kStageBytes = 512ll << 20;
 
 // the reference layout through device transposes to a tuned AoSoA kernel: the elastic PDE, and
 // table PDEs with m <= 8 at nDof 8 (stp_dmma8_table)
@@ -56,8 +58,8 @@ struct aderstp_plan {
   int64_t chunk = 0;
   double* buf[kHostStreams] = {nullptr, nullptr, nullptr};
   cudaStream_t streams[kHostStreams] = {nullptr, nullptr, nullptr};
-  // stream-ordered scratch of the AoS staged path: a plan-owned pool that keeps its memory
-  // between calls (release threshold = max), so repeated calls do not re-map it
+  // stream-ordered scratch (AoS staging, time-loop buffers): a plan-owned pool that keeps up to
+  // kStageBytes between calls, so repeated calls do not re-map it
   cudaMemPool_t pool = nullptr;
 };
 
@@ -279,7 +281,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   // plan-owned stream-ordered pool (AoS staging, time-loop faces): keeps its memory between
   // calls, returned when the plan is destroyed
   if (e == cudaSuccess) e = cudaMemPoolCreate(&p->pool, &pool_props_of(p->device));
-  const uint64_t keep = UINT64_MAX;
+  const uint64_t keep = (uint64_t)kStageBytes;
   if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, (void*)&keep);
   // D of nDof 8 in the constant bank: the elastic and the table-PDE tensor-core kernels
   if (e == cudaSuccess && kl.n == 8) e = aderstp::init_dmma8(kl);
@@ -340,7 +342,9 @@ cudaError_t predict_aos_staged(const aderstp_plan* plan, const aderstp::BatchArg
   sp.out_stride = m;
   const size_t t9 = (size_t)n * n * n * m;  // one AoSoA tensor (doubles)
   const size_t per = t9 * (a.favg ? 5 : 2);  // q, qavg (+ favg[3])
-  long long chunk = std::max<long long>(1, std::min<long long>(a.n_elem, (8ll << 30) / (long long)(per * 8)));
+  // staging capped at kStageBytes per call (a few waves of CTAs at every order); the pool returns
+  // what exceeds its release threshold (the same figure) at the next synchronisation
+  long long chunk = std::max<long long>(1, std::min<long long>(a.n_elem, kStageBytes / (long long)(per * 8)));
   if (lp.aos_chunk > 0) chunk = std::min<long long>(chunk, lp.aos_chunk);  // tests: force several chunks
   double* buf = nullptr;
   cudaError_t err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&buf), sizeof(double) * per * chunk, plan->pool, st);
@@ -635,12 +639,18 @@ int run_loop(const aderstp_plan* p, const aderstp_mesh* mesh, int z0, int nz, do
           sp.fc[q][d][k] *= s;
         }
   double *par_s = nullptr, *qavg = nullptr;
+  unsigned int* status = nullptr;  // this call's own check word (slabs sharing a plan never mix)
   auto cleanup = [&]() {
     if (par_s) cudaFreeAsync(par_s, st);
     if (qavg) cudaFreeAsync(qavg, st);
+    if (status) cudaFreeAsync(status, st);
   };
-  cudaError_t err = cudaSuccess;
-  if (elastic) {
+  cudaError_t err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&status), sizeof(unsigned int), p->pool, st);
+  if (err == cudaSuccess) err = cudaMemsetAsync(status, 0, sizeof(unsigned int), st);
+  sp.d_status = status;
+  aderstp::LaunchPlan cp = p->lp;  // the corrector reports into the same word
+  cp.d_status = status;
+  if (err == cudaSuccess && elastic) {
     err = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&par_s), sizeof(double) * 3 * (E > 0 ? E : 1), p->pool, st);
     if (err == cudaSuccess) err = aderstp::launch_scale_par(par, p->lp.par_kind, s, E, par_s, st);
     sp.par_kind = ADERSTP_PAR_LAMBDA_MU_RHO;
@@ -659,6 +669,10 @@ int run_loop(const aderstp_plan* p, const aderstp_mesh* mesh, int z0, int nz, do
   double t = 0.0;
   int64_t done = 0;
   int rc = ADERSTP_OK;
+  // rank-sync flag bits: 1 non-finite, 2 material, 4 a CUDA error on some rank.  Every rank makes
+  // the same two sync calls per step whatever happened locally, so a failing rank never leaves
+  // the others waiting in a collective: all of them leave the loop at the same step.
+  constexpr int kRankError = 4;
   while (t < t_end - 1e-14 * std::max(1.0, t_end)) {
     const double dt = std::min(dt0, t_end - t);
     aderstp::BatchArgs ba{u, elastic ? par_s : par, fused ? nullptr : qavg, nullptr, face_q, face_f, E, dt, t};
@@ -667,29 +681,31 @@ int run_loop(const aderstp_plan* p, const aderstp_mesh* mesh, int z0, int nz, do
     // other slabs read this slab's faces: the rank sync needs them complete (one GPU: the
     // corrector below is stream-ordered after the predictor, no host round trip)
     if (err == cudaSuccess && sync) err = cudaStreamSynchronize(st);
-    if (err != cudaSuccess) {
-      rc = cuda_fail(err, "run_simulation predictor");
+    if (err != cudaSuccess) rc = cuda_fail(err, "run_simulation predictor");
+    const int pre = sync ? sync(ctx, err != cudaSuccess ? kRankError : 0) : 0;  // every slab's faces are complete
+    if (err != cudaSuccess) break;
+    if (pre & kRankError) {
+      rc = fail(ADERSTP_ERR_CUDA, "run_simulation: another rank failed");
       break;
     }
-    if (sync) sync(ctx, 0);  // every slab's faces are complete
     aderstp::CorrArgs ca{u, par, fused ? nullptr : qavg, face_q, face_f, e, s, per_face_smax ? -1.0 : smax * s};
     ca.z0 = z0;
     ca.nz = nz;
     ca.lo = lo;
     ca.hi = hi;
-    err = E > 0 ? aderstp::launch_correct(p->lp, ca, st) : cudaSuccess;
+    err = E > 0 ? aderstp::launch_correct(cp, ca, st) : cudaSuccess;
     unsigned int flags = 0;
-    if (err == cudaSuccess) err = cudaMemcpyAsync(&flags, p->lp.d_status, sizeof flags, cudaMemcpyDeviceToHost, st);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(&flags, status, sizeof flags, cudaMemcpyDeviceToHost, st);
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
-    if (err != cudaSuccess) {
-      rc = cuda_fail(err, "run_simulation corrector");
+    if (err == cudaSuccess && flags) err = cudaMemsetAsync(status, 0, sizeof flags, st);
+    if (err != cudaSuccess) rc = cuda_fail(err, "run_simulation corrector");
+    const int local = err != cudaSuccess ? kRankError : (int)flags;
+    const int any = sync ? sync(ctx, local) : local;  // nobody reads the faces any more
+    if (err != cudaSuccess) break;
+    if (any & kRankError) {
+      rc = fail(ADERSTP_ERR_CUDA, "run_simulation: another rank failed");
       break;
     }
-    if (flags) {
-      cudaMemsetAsync(p->lp.d_status, 0, sizeof flags, st);
-      cudaStreamSynchronize(st);
-    }
-    const int any = sync ? sync(ctx, flags ? (int)flags : 0) : (int)flags;  // nobody reads the faces any more
     if (any) {
       rc = fail((any & 2) ? ADERSTP_ERR_MATERIAL : ADERSTP_ERR_NONFINITE,
                 (any & 2) ? "elastic_pde: need rho > 0, mu >= 0, lambda + 2mu > 0"

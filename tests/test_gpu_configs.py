@@ -61,7 +61,8 @@ def _check_outputs(S, oracle, n, q_rows, par_rows, dt, out_rows, q_stride):
 def test_generator_all_distributions(stp, oracle, dist, n, e0, grid):
     """Device generator vs the oracle's host generator: the SplitMix64 draws and the material are
     bit-identical; the transcendental distributions (Box-Muller log/cos, sinusoids) agree to the
-    last ulps (CUDA's and glibc's log/sin/cos may round differently)."""
+    last ulps (CUDA's and glibc's log/sin/cos may round differently).  The parity tests never
+    depend on this: they copy the device-generated inputs to the oracle."""
     S = stp
     E = 6
     qd, pd = S.generate(dist, SEED, n, e0, E, grid=grid, layout=S.LAYOUT_AOSOA, q_stride=9)
@@ -71,8 +72,10 @@ def test_generator_all_distributions(stp, oracle, dist, n, e0, grid):
     if dist == 0:
         assert np.array_equal(qd, qh)
     else:
+        # Box-Muller: a few ulps; sinusoids: the phase argument (up to ~40 rad) carries the
+        # rounding of both sides' sin/range reduction, ~1e-15 absolute per unit of argument
         err = np.max(np.abs(qd - qh)) / np.max(np.abs(qh))
-        assert err <= 4e-15, err
+        assert err <= (4e-15 if dist == 1 else 2e-14), err
 
 
 def test_generator_distribution_properties(stp):
