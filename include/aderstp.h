@@ -57,7 +57,7 @@
 extern "C" {
 #endif
 
-#define ADERSTP_ABI_VERSION 1
+#define ADERSTP_ABI_VERSION 2
 
 /* status codes */
 #define ADERSTP_OK 0
@@ -78,7 +78,9 @@ extern "C" {
                                         flux Jacobians A_d and ncp matrices B_d (aderstp_config) */
 
 /* point source spec in pde_args (include/ader/pde.hpp:47-56):
- *   [0..2] position, [3] component, [4] amplitude, [5] center, [6] width */
+ *   [0..2] position, [3] component, [4] amplitude, [5] center, [6] width
+ * ELASTIC_SOURCE and SOURCE_ONLY always carry one; ADERSTP_PDE_LINEAR carries one when
+ * pde_args[7] != 0 (a user LinearPde with source_count() == 1, pde.hpp:37-39). */
 
 #define ADERSTP_PAR_LAMBDA_MU_RHO 0
 #define ADERSTP_PAR_RHO_CP_CS 1
@@ -86,7 +88,9 @@ extern "C" {
 #define ADERSTP_LAYOUT_AOSOA 0
 #define ADERSTP_LAYOUT_AOS 1
 
-#define ADERSTP_MAX_QUANTITIES 16
+/* quantities per node: any m <= 64 (systems beyond the term-table kernels -- m > 16 or more than
+ * four nonzeros in a row of A_d + B_d -- run on the general kernel, stp_general.cu) */
+#define ADERSTP_MAX_QUANTITIES 64
 
 typedef struct aderstp_config {
   int order;       /* n = nodes per dimension (reference cfg.order); 2..10 compiled      */
@@ -154,18 +158,21 @@ typedef struct aderstp_mesh {
   double domain_len;
 } aderstp_mesh;
 
-/* corrector_step (src/solver.cpp:257-311; correct_cell :184-253): u += V(qavg) + the Rusanov
- * surface fluctuations lifted through the inverse mass, from this step's predictor outputs of every
- * element (qavg in the plan's output layout, face_q / face_f).  The predictor outputs must come
- * from the PDE scaled by 1/h (ScaledPde, src/solver.cpp:111-156), as aderstp_run_simulation does.
- * max_wavespeed: the PDE's unscaled max_wavespeed(); for ADERSTP_PDE_ELASTIC a negative value means
- * "per face, the larger cp of its two elements" (per-element material has no reference
- * counterpart; with one material it equals the reference).  Point-source kinds are unsupported.
- * Device buffers, asynchronous; a non-finite update is reported by aderstp_plan_status as
- * ADERSTP_ERR_NONFINITE (the reference throws "corrector_step: non-finite update"). */
+/* corrector_step(mesh, outs, pde, ops, dt, t) (src/solver.cpp:257-311; correct_cell :184-253):
+ * u += V(qavg) + the point source's projection x its time integral over [t, t + dt] (:206-216,
+ * integrals :266-278) + the Rusanov surface fluctuations lifted through the inverse mass, from
+ * this step's predictor outputs of every element (qavg in the plan's output layout, face_q /
+ * face_f).  The predictor outputs must come from the PDE scaled by 1/h (ScaledPde,
+ * src/solver.cpp:111-156), as aderstp_run_simulation does.  max_wavespeed: the PDE's unscaled
+ * max_wavespeed(); for ADERSTP_PDE_ELASTIC a negative value means "per face, the larger cp of its
+ * two elements" (per-element material has no reference counterpart; with one material it equals
+ * the reference).  dt and t only enter through the point source.  Device buffers, asynchronous; a
+ * non-finite update is reported by aderstp_plan_status as ADERSTP_ERR_NONFINITE (the reference
+ * throws "corrector_step: non-finite update"). */
 int aderstp_correct_batch(const aderstp_plan* plan, const aderstp_mesh* mesh, double* u,
                           const double* par, const double* qavg, const double* face_q,
-                          const double* face_f, double max_wavespeed, void* stream);
+                          const double* face_f, double max_wavespeed, double dt, double t,
+                          void* stream);
 
 /* run_simulation (src/solver.cpp:313-359): steps of dt = min(stable_dt, t_end - t) until t_end,
  * each = aderstp_predict_batch on the 1/h-scaled PDE + aderstp_correct_batch, with
@@ -198,7 +205,7 @@ typedef struct aderstp_halo {
 int aderstp_correct_slab(const aderstp_plan* plan, const aderstp_mesh* mesh, const aderstp_slab* slab,
                          double* u, const double* par, const double* qavg, const double* face_q,
                          const double* face_f, const aderstp_halo* lo, const aderstp_halo* hi,
-                         double max_wavespeed, void* stream);
+                         double max_wavespeed, double dt, double t, void* stream);
 
 /* Host synchronisation between the ranks, called twice per step: after the predictor (the faces
  * of every slab are complete) and after the corrector (nobody reads them any more).  It receives

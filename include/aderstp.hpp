@@ -42,7 +42,19 @@ inline void check(int rc) {
 struct LinearMatrices {
   int m = 0;
   std::array<std::vector<double>, 3> a, b;
+  // one Gaussian point source (PointSourceSpec, proj/include/ader/pde.hpp:47-56): position[3],
+  // component, amplitude, center, width -- a user LinearPde with source_count() == 1 whose
+  // source_derivative() is the reference's Gaussian; set with add_point_source()
+  bool has_source = false;
+  std::array<double, 7> source{};
+  double max_wavespeed = 0.0;  // the user's max_wavespeed(), for stable_dt / the corrector
 };
+
+inline void add_point_source(LinearMatrices& lm, const std::array<double, 3>& position, int component,
+                             double amplitude, double center, double width) {
+  lm.has_source = true;
+  lm.source = {position[0], position[1], position[2], static_cast<double>(component), amplitude, center, width};
+}
 
 // Works with any type exposing the reference's LinearPde hooks: quantities(),
 // flux(const double*, int, double*) and ncp(const double*, int, double*).
@@ -64,6 +76,7 @@ LinearMatrices probe_linear_pde(const Pde& pde) {
       e[r] = 0.0;
     }
   }
+  lm.max_wavespeed = pde.max_wavespeed();
   return lm;
 }
 
@@ -100,6 +113,10 @@ class Predictor {
       c.linear[d] = lm.a[d].data();
       c.linear[3 + d] = lm.b[d].data();
     }
+    if (lm.has_source) {
+      for (int i = 0; i < 7; ++i) c.pde_args[i] = lm.source[i];
+      c.pde_args[7] = 1.0;
+    }
     check(aderstp_plan_create(&c, &plan_));
   }
   Predictor(const Predictor&) = delete;
@@ -118,11 +135,12 @@ class Predictor {
   }
   void status(void* stream = nullptr) { check(aderstp_plan_status(plan_, stream)); }
 
-  // ader::corrector_step (proj/src/solver.cpp:257-311) on a periodic e^3 mesh, device buffers.
+  // ader::corrector_step(mesh, outs, pde, ops, dt, t) (proj/src/solver.cpp:257-311) on a periodic
+  // e^3 mesh, device buffers.
   void correct_device(const aderstp_mesh& mesh, double* u, const double* par, const double* qavg,
-                      const double* face_q, const double* face_f, double max_wavespeed,
+                      const double* face_q, const double* face_f, double max_wavespeed, double dt, double t,
                       void* stream = nullptr) const {
-    check(aderstp_correct_batch(plan_, &mesh, u, par, qavg, face_q, face_f, max_wavespeed, stream));
+    check(aderstp_correct_batch(plan_, &mesh, u, par, qavg, face_q, face_f, max_wavespeed, dt, t, stream));
   }
   // ader::run_simulation (proj/src/solver.cpp:313-359); returns the reference's RunResult fields.
   struct RunResult {

@@ -28,7 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REF_DIR = os.path.join(HERE, "_ref")
 REFERENCE_SRC = "/root/reference/proj"
 
-PDE_ELASTIC, PDE_ADVECTION, PDE_NCP_ADVECTION, PDE_DEMO, PDE_ELASTIC_SOURCE, PDE_SOURCE_ONLY = range(6)
+PDE_ELASTIC, PDE_ADVECTION, PDE_NCP_ADVECTION, PDE_DEMO, PDE_ELASTIC_SOURCE, PDE_SOURCE_ONLY, PDE_MATRIX = range(7)
 VARIANTS = {"generic": 0, "log": 1, "splitck": 2, "aosoa": 3}
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -179,6 +179,7 @@ class Reference:
         lib.ref_stp_batch.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp,
                                       _dp, ctypes.c_int, ctypes.c_double, ctypes.c_double, _dp, _dp,
                                       _dp, _dp, ctypes.c_int, _dp]
+        lib.ref_set_matrix_pde.argtypes = [ctypes.c_int, _dp, _dp, _dp, ctypes.c_double]
         lib.ref_stp_batch_matrix.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_long, _dp, _dp, _dp,
                                              ctypes.c_double, _dp, _dp, _dp, _dp, ctypes.c_int, _dp]
         lib.ref_last_error.restype = ctypes.c_char_p
@@ -235,6 +236,16 @@ class Reference:
             raise ValueError(self.lib.ref_last_error().decode())
         return Outputs(qavg, favg, fq, ff, secs.value)
 
+
+    def set_matrix_pde(self, A, B=None, source=None, max_wavespeed=1.0):
+        """Make pde kind PDE_MATRIX (6) a user LinearPde with flux A_d, ncp B_d, optional point
+        source (7 doubles: position, component, amplitude, center, width; the reference's own
+        Gaussian) and the given max_wavespeed(), for stp / corrector_step / run_simulation."""
+        a = np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.float64) for x in A]))
+        b = None if B is None else np.ascontiguousarray(np.stack([np.asarray(x, dtype=np.float64) for x in B]))
+        src = None if source is None else np.ascontiguousarray(source, dtype=np.float64)[:7].copy()
+        if self.lib.ref_set_matrix_pde(a.shape[1], _ptr(a), _ptr(b), _ptr(src), float(max_wavespeed)) != 0:
+            raise ValueError(self.lib.ref_last_error().decode())
 
     def stp_matrix(self, n, m, q, dt, A, B=None, variant="splitck", threads=None) -> Outputs:
         """The reference predict() + extrapolate_faces for a user LinearPde given by its

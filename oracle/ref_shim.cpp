@@ -40,6 +40,7 @@ enum : int {
   kDemo = 3,           // paper demo, m = 6
   kElasticSource = 4,  // par[e] = (lambda, mu, rho); args = point source spec (7 doubles)
   kSourceOnly = 5,     // args = point source spec
+  kMatrix = 6,         // a user LinearPde given by matrices (ref_set_matrix_pde), see MatrixPde
 };
 
 ader::PointSourceSpec source_from(const double* a) {
@@ -52,29 +53,28 @@ ader::PointSourceSpec source_from(const double* a) {
   return s;
 }
 
-std::unique_ptr<ader::LinearPde> make_pde(int kind, int m, const double* par, const double* args) {
-  switch (kind) {
-    case kElastic: return ader::elastic_pde(par[0], par[1], par[2]);
-    case kAdvection: return ader::advection_pde({args[0], args[1], args[2]}, m);
-    case kNcpAdvection: return ader::ncp_advection_pde({args[0], args[1], args[2]}, m);
-    case kDemo: return ader::paper_demo_pde();
-    case kElasticSource: return ader::elastic_pde(par[0], par[1], par[2], source_from(args));
-    case kSourceOnly: return ader::source_only_pde(m, source_from(args));
-  }
-  throw std::invalid_argument("ref_shim: unknown pde kind");
-}
-
-bool per_element_par(int kind) { return kind == kElastic || kind == kElasticSource; }
-
-// A user LinearPde defined by its coefficient matrices (see ref_stp_batch_matrix).
+// A user LinearPde defined by its coefficient matrices (see ref_set_matrix_pde): flux and ncp
+// are the matrix products, max_wavespeed the given value, and an optional Gaussian point source
+// whose time derivatives and position come from the reference's own source_only_pde
+// (proj/src/pde.cpp:286-308), so the source path is the unmodified reference's.
 class MatrixPde final : public ader::LinearPde {
 public:
-  MatrixPde(int m, const double* A, const double* B)
-      : ader::LinearPde(m, 0), a_(A, A + 3 * m * m), b_(B ? std::vector<double>(B, B + 3 * m * m)
-                                                          : std::vector<double>(3 * m * m, 0.0)) {}
+  MatrixPde(int m, const double* A, const double* B, const double* src = nullptr, double smax = 1.0)
+      : ader::LinearPde(m, src ? 1 : 0), a_(A, A + 3 * m * m), b_(B ? std::vector<double>(B, B + 3 * m * m)
+                                                                    : std::vector<double>(3 * m * m, 0.0)),
+        smax_(smax) {
+    if (src) src_ = ader::source_only_pde(m, source_from(src));
+  }
   void flux(const double* q, int dim, double* f) const override { apply(a_, q, dim, f); }
   void ncp(const double* grad, int dim, double* out) const override { apply(b_, grad, dim, out); }
-  double max_wavespeed() const override { return 1.0; }
+  void source_derivative(int order, double t, int src, double* out) const override {
+    if (src_) src_->source_derivative(order, t, src, out);
+    else ader::LinearPde::source_derivative(order, t, src, out);
+  }
+  std::array<double, 3> source_position(int src) const override {
+    return src_ ? src_->source_position(src) : ader::LinearPde::source_position(src);
+  }
+  double max_wavespeed() const override { return smax_; }
 
 private:
   void apply(const std::vector<double>& mat, const double* x, int dim, double* y) const {
@@ -86,7 +86,35 @@ private:
     }
   }
   std::vector<double> a_, b_;
+  double smax_;
+  std::unique_ptr<ader::LinearPde> src_;
 };
+
+// the matrix PDE that pde kind kMatrix builds (set by ref_set_matrix_pde)
+struct MatrixSpec {
+  int m = 0;
+  std::vector<double> a, b, src;
+  double smax = 1.0;
+} g_matrix;
+
+std::unique_ptr<ader::LinearPde> make_pde(int kind, int m, const double* par, const double* args) {
+  switch (kind) {
+    case kElastic: return ader::elastic_pde(par[0], par[1], par[2]);
+    case kAdvection: return ader::advection_pde({args[0], args[1], args[2]}, m);
+    case kNcpAdvection: return ader::ncp_advection_pde({args[0], args[1], args[2]}, m);
+    case kDemo: return ader::paper_demo_pde();
+    case kElasticSource: return ader::elastic_pde(par[0], par[1], par[2], source_from(args));
+    case kSourceOnly: return ader::source_only_pde(m, source_from(args));
+    case kMatrix:
+      if (g_matrix.m != m) throw std::invalid_argument("ref_shim: matrix pde not set for this m");
+      return std::make_unique<MatrixPde>(m, g_matrix.a.data(), g_matrix.b.data(),
+                                         g_matrix.src.empty() ? nullptr : g_matrix.src.data(), g_matrix.smax);
+  }
+  throw std::invalid_argument("ref_shim: unknown pde kind");
+}
+
+bool per_element_par(int kind) { return kind == kElastic || kind == kElasticSource; }
+
 
 int stp_batch(int variant, int n, int m, long n_elem, const double* q, const double* par,
               const double* args, int pde_kind, std::shared_ptr<ader::LinearPde> given, double dt,
@@ -179,21 +207,33 @@ int ref_stp_batch(int variant, int n, int m, long n_elem, const double* q, const
                    face_q, face_f, n_threads, seconds);
 }
 
-// The same batch for an arbitrary constant-coefficient system given as matrices: A[d] (m x m,
-// row-major, F_d(q) = A_d q) and B[d] (ncp, B_d grad; may be null), wrapped in MatrixPde -- a
-// user LinearPde subclass (proj/include/ader/pde.hpp:21-46) of the kind the reference's own
-// tests probe (proj/tests/test_pde.cpp:14-24).
-int ref_stp_batch_matrix(int variant, int n, int m, long n_elem, const double* q, const double* A,
-                         const double* B, double dt, double* qavg, double* favg, double* face_q,
-                         double* face_f, int n_threads, double* seconds) {
+// The matrix PDE of pde kind 6 (kMatrix) for every entry point of this shim: A[d] (m x m,
+// row-major, F_d(q) = A_d q), B[d] (ncp, B_d grad; may be null), an optional point source
+// (7 doubles as in pde_args; null = none) and the max_wavespeed() the solver sees.  A user
+// LinearPde subclass (proj/include/ader/pde.hpp:21-46) of the kind the reference's own tests
+// probe (proj/tests/test_pde.cpp:14-24).
+int ref_set_matrix_pde(int m, const double* A, const double* B, const double* src, double max_wavespeed) {
   try {
-    auto pde = std::make_shared<MatrixPde>(m, A, B);
-    return stp_batch(variant, n, m, n_elem, q, nullptr, nullptr, -1, pde, dt, 0.0, qavg, favg,
-                     face_q, face_f, n_threads, seconds);
+    g_matrix.m = m;
+    g_matrix.a.assign(A, A + 3 * m * m);
+    if (B) g_matrix.b.assign(B, B + 3 * m * m);
+    else g_matrix.b.assign(3 * m * m, 0.0);
+    if (src) g_matrix.src.assign(src, src + 7);
+    else g_matrix.src.clear();
+    g_matrix.smax = max_wavespeed;
+    return 0;
   } catch (const std::exception& ex) {
     g_err = ex.what();
     return -1;
   }
+}
+
+int ref_stp_batch_matrix(int variant, int n, int m, long n_elem, const double* q, const double* A,
+                         const double* B, double dt, double* qavg, double* favg, double* face_q,
+                         double* face_f, int n_threads, double* seconds) {
+  if (ref_set_matrix_pde(m, A, B, nullptr, 1.0) != 0) return -1;
+  return stp_batch(variant, n, m, n_elem, q, nullptr, nullptr, kMatrix, nullptr, dt, 0.0, qavg, favg,
+                   face_q, face_f, n_threads, seconds);
 }
 
 // Basis operators of the reference (proj/src/basis.cpp:110-122).

@@ -9,8 +9,9 @@ namespace aderstp {
 
 constexpr int kMinOrder = 2;
 constexpr int kMaxOrder = 10;
-constexpr int kMaxM = 16;      // ADERSTP_MAX_QUANTITIES
+constexpr int kMaxM = 16;      // quantities of the term-table kernels (stp_kernel, corrector tables)
 constexpr int kMaxTerms = 4;   // nonzeros per (row s, dim d) of a table PDE
+constexpr long long kGenScratchBytes = 512ll << 20;  // general kernel's global scratch per launch
 
 // Host-side basis, derived from scratch (basis.cpp).  d[k*n + l] = phi_l'(x_k).
 struct HostBasis {
@@ -37,6 +38,18 @@ struct LaunchPlan {
   double src_pos[3] = {0, 0, 0};
   double src_amp = 0, src_center = 0, src_width = 1;
   double src_proj[3][kMaxOrder];
+  double src_scale = 1.0;            // ScaledPde source scale 1/h^3 in the time loop (solver.cpp:147-150)
+  // general kernel (stp_general.cu): device CSR rows of C_d = A_d + B_d and of A_d, per (s, d)
+  struct GeneralTables {
+    const int* t_ptr = nullptr;
+    const int* t_col = nullptr;
+    const double* t_val = nullptr;
+    const int* f_ptr = nullptr;
+    const int* f_col = nullptr;
+    const double* f_val = nullptr;
+    double scale = 1.0;              // ScaledPde gradient scale 1/h in the time loop
+    cudaMemPool_t pool = nullptr;    // the plan's pool (global scratch for large m N^3)
+  } gen;
   unsigned int* d_status = nullptr;  // device word: bit0 non-finite q, bit1 bad material
   int force_generic = 0;             // env ADERSTP_FORCE_GENERIC=1: skip specialised kernels
   int no_dmma8 = 0;                  // env ADERSTP_NO_DMMA8=1: nDof 8 on the line-pass kernel
@@ -86,12 +99,21 @@ struct CorrArgs {
   double smax;           // scaled max wave speed, < 0: elastic per-face max(cp) / h
   int z0 = 0, nz = 0;    // this slab: layers [z0, z0 + nz); nz = 0 means the whole mesh
   HaloRef lo, hi;        // the slabs below / above (used for z-neighbours outside [z0, z0 + nz))
+  // point source (correct_cell, solver.cpp:206-216): u[comp] += proj[node] * sint
+  int src_comp = -1;
+  double src_sint = 0.0;
+  const double* src_proj = nullptr;  // n^3 doubles, point_source_projection (basis.cpp:124-142)
 };
 cudaError_t launch_correct(const LaunchPlan& p, const CorrArgs& a, cudaStream_t stream);
 cudaError_t launch_scale_par(const double* in, int par_kind, double s, long long n, double* out,
                              cudaStream_t stream);
 cudaError_t launch_max_cp(const double* par, int par_kind, long long n, unsigned long long* out,
                           cudaStream_t stream);
+
+// stp_general.cu: any m, dense / sparse matrices, point source, every order and layout
+bool general_selected(const LaunchPlan& p);
+cudaError_t launch_general(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
+void source_amplitudes(const LaunchPlan& p, double t, int n, double* amp);  // S^(o)(t) x src_scale
 
 // stp_kernels.cu
 cudaError_t launch_stp(const LaunchPlan& plan, const BatchArgs& args, cudaStream_t stream);

@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <vector>
 #include <new>
 #include <string>
 
@@ -37,7 +38,8 @@ constexpr long long kStageBytes = 512ll << 20;
 // table PDEs with m <= 8 at nDof 8 (stp_dmma8_table)
 bool aos_staged(const aderstp::LaunchPlan& lp) {
   const bool tuned = lp.kind == ADERSTP_PDE_ELASTIC || (lp.kind != ADERSTP_PDE_ELASTIC_SOURCE && lp.n == 8 && lp.m <= 9);
-  return tuned && lp.src_comp < 0 && lp.layout == ADERSTP_LAYOUT_AOS && !lp.force_generic;
+  return tuned && lp.src_comp < 0 && lp.layout == ADERSTP_LAYOUT_AOS && !lp.force_generic &&
+         lp.gen.t_ptr == nullptr;  // the general kernel reads and writes the AoS rows itself
 }
 
 cudaMemPoolProps& pool_props_of(int device) {
@@ -61,6 +63,10 @@ struct aderstp_plan {
   // stream-ordered scratch (AoS staging, time-loop buffers): a plan-owned pool that keeps up to
   // kStageBytes between calls, so repeated calls do not re-map it
   cudaMemPool_t pool = nullptr;
+  // general kernel tables (CSR rows of C_d and A_d; one cudaMalloc) and the corrector's point
+  // source projection (n^3 doubles)
+  void* gen_buf = nullptr;
+  double* src_proj = nullptr;
 };
 
 namespace {
@@ -107,6 +113,93 @@ int build_terms(LaunchPlan& lp, const double* A[3], const double* B[3]) {
   return ADERSTP_OK;
 }
 
+// The general kernel's tables: CSR rows (s, d) of C_d = A_d + B_d (the CK step) and of A_d
+// (favg, face_f), zeros dropped, in one device allocation owned by the plan.
+cudaError_t upload_general(aderstp_plan* p, const std::vector<double>& A, const std::vector<double>& B) {
+  const int m = p->lp.m;
+  std::vector<int> tp(3 * m + 1, 0), fp(3 * m + 1, 0), tc, fc;
+  std::vector<double> tv, fv;
+  for (int s = 0; s < m; ++s)
+    for (int d = 0; d < 3; ++d) {
+      for (int j = 0; j < m; ++j) {
+        const double a = A[(size_t)d * m * m + s * m + j], c = a + B[(size_t)d * m * m + s * m + j];
+        if (c != 0.0) {
+          tc.push_back(j);
+          tv.push_back(c);
+        }
+        if (a != 0.0) {
+          fc.push_back(j);
+          fv.push_back(a);
+        }
+      }
+      tp[3 * s + d + 1] = (int)tc.size();
+      fp[3 * s + d + 1] = (int)fc.size();
+    }
+  // layout: [t_val][f_val][t_ptr][f_ptr][t_col][f_col] (doubles first: 8-byte alignment)
+  const size_t bytes = sizeof(double) * (tv.size() + fv.size()) + sizeof(int) * (tp.size() + fp.size() + tc.size() + fc.size());
+  std::vector<char> host(bytes > 0 ? bytes : 8);
+  char* h = host.data();
+  size_t off = 0;
+  auto put = [&](const void* src, size_t n) {
+    if (n) std::memcpy(h + off, src, n);
+    const size_t at = off;
+    off += n;
+    return at;
+  };
+  const size_t o_tv = put(tv.data(), sizeof(double) * tv.size());
+  const size_t o_fv = put(fv.data(), sizeof(double) * fv.size());
+  const size_t o_tp = put(tp.data(), sizeof(int) * tp.size());
+  const size_t o_fp = put(fp.data(), sizeof(int) * fp.size());
+  const size_t o_tc = put(tc.data(), sizeof(int) * tc.size());
+  const size_t o_fc = put(fc.data(), sizeof(int) * fc.size());
+  cudaError_t e = cudaMalloc(&p->gen_buf, host.size());
+  if (e == cudaSuccess) e = cudaMemcpy(p->gen_buf, h, host.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) return e;
+  char* dv = static_cast<char*>(p->gen_buf);
+  aderstp::LaunchPlan::GeneralTables& g = p->lp.gen;
+  g.t_val = reinterpret_cast<const double*>(dv + o_tv);
+  g.f_val = reinterpret_cast<const double*>(dv + o_fv);
+  g.t_ptr = reinterpret_cast<const int*>(dv + o_tp);
+  g.f_ptr = reinterpret_cast<const int*>(dv + o_fp);
+  g.t_col = reinterpret_cast<const int*>(dv + o_tc);
+  g.f_col = reinterpret_cast<const int*>(dv + o_fc);
+  g.scale = 1.0;
+  return cudaSuccess;
+}
+
+// point_source_projection (proj/src/basis.cpp:124-142) with the reference's operation order:
+// phi_x phi_y phi_z / (w_x w_y w_z) at node (k3, k2, k1), for the corrector's source term
+cudaError_t upload_source_projection(aderstp_plan* p) {
+  const aderstp::LaunchPlan& lp = p->lp;
+  const int n = lp.n;
+  double phi[3][aderstp::kMaxOrder];
+  for (int d = 0; d < 3; ++d) aderstp::lagrange_values(n, lp.basis.nodes, lp.src_pos[d], phi[d]);
+  std::vector<double> proj((size_t)n * n * n);
+  for (int k3 = 0; k3 < n; ++k3)
+    for (int k2 = 0; k2 < n; ++k2)
+      for (int k1 = 0; k1 < n; ++k1) {
+        const double num = phi[0][k1] * phi[1][k2] * phi[2][k3];
+        const double mass = lp.basis.weights[k1] * lp.basis.weights[k2] * lp.basis.weights[k3];
+        proj[(k3 * n + k2) * n + k1] = num / mass;
+      }
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&p->src_proj), sizeof(double) * proj.size());
+  if (e == cudaSuccess) e = cudaMemcpy(p->src_proj, proj.data(), sizeof(double) * proj.size(), cudaMemcpyHostToDevice);
+  return e;
+}
+
+// time integral of the source amplitude over [t, t + dt], truncated like the predictor
+// (corrector_step, proj/src/solver.cpp:266-278), on the source-scaled PDE
+double source_integral(const aderstp::LaunchPlan& lp, double dt, double t) {
+  double amp[aderstp::kMaxOrder];
+  aderstp::source_amplitudes(lp, t, lp.n, amp);
+  double sint = 0.0, coeff = dt;
+  for (int o = 0; o < lp.n; ++o) {
+    sint += coeff * amp[o];
+    coeff *= dt / (o + 2);
+  }
+  return sint;
+}
+
 }  // namespace
 
 extern "C" {
@@ -147,7 +240,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     return fail(ADERSTP_ERR_UNSUPPORTED, "plan_create: order " + std::to_string(n) +
                                              " has no compiled kernel (2..10)");
   if (m < 1 || m > ADERSTP_MAX_QUANTITIES)
-    return fail(ADERSTP_ERR_UNSUPPORTED, "plan_create: quantity count out of range (1..16)");
+    return fail(ADERSTP_ERR_UNSUPPORTED, "plan_create: quantity count out of range (1.." +
+                                             std::to_string(ADERSTP_MAX_QUANTITIES) + ")");
   if (cfg->layout != ADERSTP_LAYOUT_AOSOA && cfg->layout != ADERSTP_LAYOUT_AOS)
     return fail(ADERSTP_ERR_INVALID_ARG, "plan_create: unknown layout");
   const int qs = cfg->q_stride ? cfg->q_stride : m;
@@ -199,10 +293,13 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
 
   // PDE terms (proj/src/pde.cpp): advection :61-85, ncp-advection :87-117, demo :119-146
   int rc = ADERSTP_OK;
+  bool general = false;
+  std::vector<double> Av, Bv;  // dense A_d, B_d (3 x m x m) of the non-elastic kinds
   if (!elastic) {
-    double A[3][aderstp::kMaxM * aderstp::kMaxM], B[3][aderstp::kMaxM * aderstp::kMaxM];
-    std::memset(A, 0, sizeof A);
-    std::memset(B, 0, sizeof B);
+    Av.assign(3 * (size_t)m * m, 0.0);
+    Bv.assign(3 * (size_t)m * m, 0.0);
+    double* A[3] = {Av.data(), Av.data() + m * m, Av.data() + 2 * m * m};
+    double* B[3] = {Bv.data(), Bv.data() + m * m, Bv.data() + 2 * m * m};
     const double* pa[3] = {A[0], A[1], A[2]};
     const double* pb[3] = {B[0], B[1], B[2]};
     const double* v = cfg->pde_args;
@@ -228,20 +325,46 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
       }
     } else if (kind == ADERSTP_PDE_LINEAR) {
       for (int d = 0; d < 3; ++d) {
-        pa[d] = cfg->linear[d];
-        pb[d] = cfg->linear[3 + d];
+        if (cfg->linear[d]) std::memcpy(A[d], cfg->linear[d], sizeof(double) * m * m);
+        if (cfg->linear[3 + d]) std::memcpy(B[d], cfg->linear[3 + d], sizeof(double) * m * m);
       }
     }
-    rc = build_terms(lp, pa, pb);
-    if (rc != ADERSTP_OK) {
-      delete p;
-      return rc;
+    for (double v : Av)
+      if (!std::isfinite(v)) {
+        delete p;
+        return fail(ADERSTP_ERR_INVALID_ARG, "linear pde: non-finite coefficient");
+      }
+    for (double v : Bv)
+      if (!std::isfinite(v)) {
+        delete p;
+        return fail(ADERSTP_ERR_INVALID_ARG, "linear pde: non-finite coefficient");
+      }
+    // the term-table kernels take m <= 16 and <= 4 nonzeros per (row, dim); everything else
+    // (and ADERSTP_GENERAL=1) runs on the general kernel
+    const char* ge = std::getenv("ADERSTP_GENERAL");
+    general = (ge && ge[0] == '1') || m > aderstp::kMaxM;
+    if (!general) {
+      rc = build_terms(lp, pa, pb);
+      if (rc == ADERSTP_ERR_UNSUPPORTED) general = true;
+      else if (rc != ADERSTP_OK) {
+        delete p;
+        return rc;
+      }
+    }
+    if (general) {
+      std::memset(lp.tr, 0, sizeof lp.tr);
+      std::memset(lp.fr, 0, sizeof lp.fr);
+      for (int q = 0; q < aderstp::kMaxM; ++q)
+        for (int d = 0; d < 3; ++d)
+          for (int k = 0; k < aderstp::kMaxTerms; ++k) lp.tc[q][d][k] = lp.fc[q][d][k] = 0.0;
+      lp.n_terms = 1;
     }
   } else {
     lp.n_terms = 1;
   }
   // point source (pde.hpp:47-56; weak Dirac projection predictor_common.cpp:261-283)
-  if (kind == ADERSTP_PDE_ELASTIC_SOURCE || kind == ADERSTP_PDE_SOURCE_ONLY) {
+  if (kind == ADERSTP_PDE_ELASTIC_SOURCE || kind == ADERSTP_PDE_SOURCE_ONLY ||
+      (kind == ADERSTP_PDE_LINEAR && cfg->pde_args[7] != 0.0)) {
     const double* a = cfg->pde_args;
     const int comp = (int)a[3];
     if (comp < 0 || comp >= m || (kind == ADERSTP_PDE_ELASTIC_SOURCE && (comp < 6 || comp > 8))) {
@@ -271,6 +394,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   cudaError_t e = cudaGetDevice(&p->device);
   if (e == cudaSuccess) e = cudaMalloc(&lp.d_status, sizeof(unsigned int));
   if (e == cudaSuccess) e = cudaMemset(lp.d_status, 0, sizeof(unsigned int));
+  if (e == cudaSuccess && general) e = upload_general(p, Av, Bv);
+  if (e == cudaSuccess && lp.src_comp >= 0) e = upload_source_projection(p);
   // device constants of the tuned kernels this plan can dispatch to -- for the reference AoS
   // layout those of its AoSoA staging (predict_aos_staged)
   aderstp::LaunchPlan kl = lp;
@@ -287,8 +412,9 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   if (e == cudaSuccess && kl.n == 8) e = aderstp::init_dmma8(kl);
   if (e == cudaSuccess && aderstp::pass_applicable(kl)) e = aderstp::init_pass(kl);
   if (e == cudaSuccess && aderstp::dmmap_applicable(kl)) e = aderstp::init_dmmap(kl);
+  if (e == cudaSuccess) lp.gen.pool = p->pool;
   if (e != cudaSuccess) {
-    delete p;
+    aderstp_plan_destroy(p);
     return cuda_fail(e, "plan_create");
   }
   *out = p;
@@ -302,6 +428,8 @@ void aderstp_plan_destroy(aderstp_plan* p) {
     if (p->streams[i]) cudaStreamDestroy(p->streams[i]);
   }
   if (p->lp.d_status) cudaFree(p->lp.d_status);
+  if (p->gen_buf) cudaFree(p->gen_buf);
+  if (p->src_proj) cudaFree(p->src_proj);
   if (p->pool) cudaMemPoolDestroy(p->pool);
   delete p;
 }
@@ -566,18 +694,62 @@ int validate_mesh(const aderstp_plan* p, const aderstp_mesh* mesh, const double*
   if (!(mesh->domain_len > 0.0)) return fail(ADERSTP_ERR_INVALID_ARG, "Mesh: domain length must be positive");
   if ((double)mesh->elements_per_dim * mesh->elements_per_dim * mesh->elements_per_dim > 2147483647.0)
     return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": mesh too large");
-  if (p->lp.src_comp >= 0)
-    return fail(ADERSTP_ERR_UNSUPPORTED, std::string(who) + ": point sources are not supported by the GPU corrector");
   if (p->lp.kind == ADERSTP_PDE_ELASTIC && !par)
     return fail(ADERSTP_ERR_INVALID_ARG, std::string(who) + ": elastic kinds need per-element parameters");
   return ADERSTP_OK;
+}
+
+// One corrector step on the elements of `a` (a slab, or the whole mesh when a.nz == 0), with
+// lp's status word: the volume term u += V(qavg) (the general kernel for general systems, the
+// tensor-core nDof 8 kernel in its volume mode for the elastic system, else inside the corrector
+// kernel), the point source u[comp] += proj * sint (solver.cpp:206-216), the surface terms.
+cudaError_t corrector_launch(const aderstp_plan* p, const aderstp::LaunchPlan& lp, aderstp::CorrArgs a,
+                             double dt, double t, cudaStream_t st) {
+  const long long E = (long long)a.e * a.e * (a.nz > 0 ? a.nz : a.e);
+  if (lp.src_comp >= 0) {  // ScaledPde(1/h, 1/h^3): the source scale of an element of size h
+    aderstp::LaunchPlan sl = lp;
+    sl.src_scale = a.inv_h * a.inv_h * a.inv_h;
+    a.src_comp = lp.src_comp;
+    a.src_sint = source_integral(sl, dt, t);
+    a.src_proj = p->src_proj;
+  }
+  if (E == 0) return cudaSuccess;
+  cudaError_t e = cudaSuccess;
+  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
+  if (a.qavg && aderstp::general_selected(lp)) {
+    aderstp::BatchArgs vb{a.u, nullptr, nullptr, nullptr, nullptr, nullptr, E, 1.0, 0.0};
+    vb.u_next = a.u;
+    vb.vol_r = a.qavg;
+    aderstp::LaunchPlan gl = lp;
+    gl.gen.scale = a.inv_h;  // ScaledPde: flux and ncp x 1/h
+    e = aderstp::launch_general(gl, vb, st);
+    a.qavg = nullptr;  // the volume term is applied
+  } else if (a.qavg && aderstp::dmma8_applicable(lp) && !lp.force_generic && !lp.no_dmma8 && al16(a.u) &&
+             al16(a.qavg)) {
+    // elastic nDof 8: the volume term on the tensor cores -- stp_dmma8's last Horner step with the
+    // iterate started from qavg on the 1/h-scaled material, u <- u + V(qavg) in place
+    aderstp::BatchArgs vb{a.u, nullptr, nullptr, nullptr, nullptr, nullptr, E, 1.0, 0.0};
+    vb.u_next = a.u;
+    vb.vol_r = a.qavg;
+    double* par_s = nullptr;
+    e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&par_s), sizeof(double) * 3 * E, p->pool, st);
+    if (e == cudaSuccess) e = aderstp::launch_scale_par(a.par, lp.par_kind, a.inv_h, E, par_s, st);
+    aderstp::LaunchPlan sp = lp;
+    sp.par_kind = ADERSTP_PAR_LAMBDA_MU_RHO;
+    vb.par = par_s;
+    if (e == cudaSuccess) e = aderstp::launch_dmma8(sp, vb, st);
+    if (par_s) cudaFreeAsync(par_s, st);
+    a.qavg = nullptr;
+  }
+  if (e == cudaSuccess) e = aderstp::launch_correct(lp, a, st);
+  return e;
 }
 
 }  // namespace
 
 int aderstp_correct_batch(const aderstp_plan* p, const aderstp_mesh* mesh, double* u, const double* par,
                           const double* qavg, const double* face_q, const double* face_f,
-                          double max_wavespeed, void* stream) {
+                          double max_wavespeed, double dt, double t, void* stream) {
   int rc = validate_mesh(p, mesh, u, par, "corrector_step");
   if (rc != ADERSTP_OK) return rc;
   if (!qavg || !face_q || !face_f)
@@ -587,31 +759,7 @@ int aderstp_correct_batch(const aderstp_plan* p, const aderstp_mesh* mesh, doubl
   const double inv_h = mesh->elements_per_dim / mesh->domain_len;
   aderstp::CorrArgs a{u, par, qavg, face_q, face_f, mesh->elements_per_dim, inv_h,
                       max_wavespeed >= 0.0 ? max_wavespeed * inv_h : -1.0};
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const long long E = (long long)mesh->elements_per_dim * mesh->elements_per_dim * mesh->elements_per_dim;
-  // elastic nDof 8: the volume term on the tensor cores -- stp_dmma8's last Horner step with the
-  // iterate started from qavg on the 1/h-scaled material, u <- u + V(qavg) in place -- then the
-  // surface-only corrector
-  aderstp::BatchArgs vb{u, nullptr, nullptr, nullptr, nullptr, nullptr, E, 1.0, 0.0};
-  vb.u_next = u;
-  vb.vol_r = qavg;
-  auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
-  if (E > 0 && aderstp::dmma8_applicable(p->lp) && !p->lp.force_generic && !p->lp.no_dmma8 && al16(u) &&
-      al16(qavg)) {
-    double* par_s = nullptr;
-    cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void**>(&par_s), sizeof(double) * 3 * E, p->pool, st);
-    if (e == cudaSuccess) e = aderstp::launch_scale_par(par, p->lp.par_kind, inv_h, E, par_s, st);
-    aderstp::LaunchPlan sp = p->lp;
-    sp.par_kind = ADERSTP_PAR_LAMBDA_MU_RHO;
-    vb.par = par_s;
-    if (e == cudaSuccess) e = aderstp::launch_dmma8(sp, vb, st);
-    if (par_s) cudaFreeAsync(par_s, st);
-    a.qavg = nullptr;  // the volume term is applied
-    if (e == cudaSuccess) e = aderstp::launch_correct(p->lp, a, st);
-    if (e != cudaSuccess) return cuda_fail(e, "correct_batch launch");
-    return ADERSTP_OK;
-  }
-  cudaError_t e = aderstp::launch_correct(p->lp, a, st);
+  cudaError_t e = corrector_launch(p, p->lp, a, dt, t, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "correct_batch launch");
   return ADERSTP_OK;
 }
@@ -630,7 +778,9 @@ int run_loop(const aderstp_plan* p, const aderstp_mesh* mesh, int z0, int nz, do
   const long long E = (long long)e * e * nz;
   const int n = p->lp.n;
   const double h = mesh->domain_len / e, s = 1.0 / h;
-  aderstp::LaunchPlan sp = p->lp;  // the predictor on ScaledPde(1/h)
+  aderstp::LaunchPlan sp = p->lp;  // the predictor on ScaledPde(1/h, 1/h^3)
+  sp.gen.scale = s;
+  sp.src_scale = s * s * s;
   if (!elastic)
     for (int q = 0; q < aderstp::kMaxM; ++q)
       for (int d = 0; d < 3; ++d)
@@ -693,7 +843,7 @@ int run_loop(const aderstp_plan* p, const aderstp_mesh* mesh, int z0, int nz, do
     ca.nz = nz;
     ca.lo = lo;
     ca.hi = hi;
-    err = E > 0 ? aderstp::launch_correct(cp, ca, st) : cudaSuccess;
+    err = corrector_launch(p, cp, ca, dt, t, st);
     unsigned int flags = 0;
     if (err == cudaSuccess) err = cudaMemcpyAsync(&flags, status, sizeof flags, cudaMemcpyDeviceToHost, st);
     if (err == cudaSuccess) err = cudaStreamSynchronize(st);
@@ -751,7 +901,8 @@ int validate_slab(const aderstp_mesh* mesh, const aderstp_slab* slab, const ader
 
 int aderstp_correct_slab(const aderstp_plan* p, const aderstp_mesh* mesh, const aderstp_slab* slab, double* u,
                          const double* par, const double* qavg, const double* face_q, const double* face_f,
-                         const aderstp_halo* lo, const aderstp_halo* hi, double max_wavespeed, void* stream) {
+                         const aderstp_halo* lo, const aderstp_halo* hi, double max_wavespeed, double dt,
+                         double t, void* stream) {
   int rc = validate_mesh(p, mesh, u, par, "corrector_step");
   if (rc == ADERSTP_OK) rc = validate_slab(mesh, slab, lo, hi, p->lp.kind == ADERSTP_PDE_ELASTIC, "corrector_step");
   if (rc != ADERSTP_OK) return rc;
@@ -766,7 +917,7 @@ int aderstp_correct_slab(const aderstp_plan* p, const aderstp_mesh* mesh, const 
   a.nz = slab->nz;
   a.lo = halo_of(lo);
   a.hi = halo_of(hi);
-  cudaError_t e = aderstp::launch_correct(p->lp, a, static_cast<cudaStream_t>(stream));
+  cudaError_t e = corrector_launch(p, p->lp, a, dt, t, static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "correct_slab launch");
   return ADERSTP_OK;
 }

@@ -15,7 +15,8 @@
 // owner and one neighbour), and every state entry is updated by one coalesced read-modify-write in
 // the state's own layout.  Per-element elastic material (the reference has one material per mesh)
 // is supported; smax is then max(cp) of the two elements of a face unless the caller passes one.
-// Point sources are not supported on this path (the caller is told ADERSTP_ERR_UNSUPPORTED).
+// A point source adds its projection times the time integral of its amplitude to its component
+// (solver.cpp:206-216), between the volume and the surface terms like the reference.
 #include <cstdint>
 
 #include "../../include/aderstp.h"
@@ -234,6 +235,8 @@ __global__ void __launch_bounds__(kCorrThreads) correct_kernel(CorrParams kp, Co
       }
     }
     double val = ue[j] + vol;
+    // point source: projection x time integral of the amplitude (solver.cpp:206-216)
+    if (s == ca.src_comp) val += ca.src_proj[(k3 * N + k2) * N + k1] * ca.src_sint;
     // surface (solver.cpp:228-249): in-face (a, b) in (z, y, x) order without dimension d
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -416,6 +419,10 @@ __global__ void __launch_bounds__(surf_threads<N, VOL>()) surface_kernel(CorrPar
       }
 #pragma unroll
       for (int k = 0; k < V; ++k) VecT<V>::at(v, k) += vol[k];
+    }
+    if (s == ca.src_comp) {  // point source (solver.cpp:206-216), after the volume term
+#pragma unroll
+      for (int k = 0; k < V; ++k) VecT<V>::at(v, k) += ca.src_proj[k32 * N + k1 + k] * ca.src_sint;
     }
     // x faces: the in-face node (k3, k2) is shared by the k1 run, the lifting differs; y faces
     // (k3, k1) and z faces (k2, k1): per-node fluctuations, shared lifting

@@ -72,7 +72,15 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr, unsigned long long 
 }
 
 
+#ifdef DMMAP_ROLES_OLD
 __constant__ int kRoleP[NWP] = {6, 7, 8, 4, -1, -2, 3, 5};
+#else
+// warps w and w + 4 share an SM sub-partition (and its fp64 / tensor pipe): per CK step at N = 6
+// (16 cycles per DMMA, 2 per warp DFMA on a sub-partition) u, v, w cost 528, sxy 384, sxz and
+// syz 336, the normal-stress halves 264 each; pairing (u, n0) (v, n1) (w, sxz) (sxy, syz) puts
+// at most 864 on one sub-partition (the alternative pairing with sxy beside w: 912)
+__constant__ int kRoleP[NWP] = {6, 7, 8, 3, -1, -2, 4, 5};
+#endif
 __constant__ int kInP[NVP][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8, 0, 6},
                                  {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
 __constant__ int kCoefP[NVP][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},

@@ -403,22 +403,8 @@ void fill_params(const LaunchPlan& p, const BatchArgs& a, KParams<N>& kp) {
   for (int d = 0; d < 3; ++d)
     for (int j = 0; j < N; ++j) kp.src_proj[d][j] = p.src_proj[d][j];
   // S^(o-1)(t0) for o = 1..N-1: Gaussian derivatives via the Hermite recurrence
-  // (proj/src/pde.cpp:48-59), evaluated at this launch's t_start
-  for (int o = 0; o < N; ++o) {
-    double amp = 0.0;
-    if (p.src_comp >= 0) {
-      const double u = (a.t_start - p.src_center) / p.src_width;
-      double hm = 0.0, h = 1.0, scale = 1.0;
-      for (int k = 0; k < o; ++k) {
-        const double hn = u * h - k * hm;
-        hm = h;
-        h = hn;
-      }
-      for (int k = 0; k < o; ++k) scale *= -1.0 / p.src_width;
-      amp = p.src_amp * scale * h * std::exp(-0.5 * u * u);
-    }
-    kp.src_amp[o] = amp;
-  }
+  // (proj/src/pde.cpp:48-59), evaluated at this launch's t_start, times the source scale
+  source_amplitudes(p, a.t_start, N, kp.src_amp);
   kp.m = p.m;
   kp.q_stride = p.q_stride;
   kp.out_stride = p.out_stride;
@@ -507,6 +493,7 @@ bool fused_supported(const LaunchPlan& p, const BatchArgs& a) {
 cudaError_t launch_stp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   const bool aligned = al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) && al16(a.face_f);
+  if (general_selected(p)) return launch_general(p, a, stream);
   if (use_dmma8(p, a)) return launch_dmma8(p, a, stream);
   if (dmma8_table_applicable(p, a)) return launch_dmma8_table(p, a, stream);
   if (a.u_next && use_dmmap(p, a)) return launch_dmmap(p, a, stream);

@@ -100,11 +100,13 @@ def _load():
                                          _vp, ctypes.c_int, ctypes.c_int, _vp, _vp]
     L.aderstp_generate.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, _i64, _i64, ctypes.c_int,
                                    ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]
-    L.aderstp_correct_batch.argtypes = [_vp, ctypes.POINTER(_Mesh), _vp, _vp, _vp, _vp, _vp, ctypes.c_double, _vp]
+    L.aderstp_correct_batch.argtypes = [_vp, ctypes.POINTER(_Mesh), _vp, _vp, _vp, _vp, _vp, ctypes.c_double,
+                                        ctypes.c_double, ctypes.c_double, _vp]
     L.aderstp_run_simulation.argtypes = [_vp, ctypes.POINTER(_Mesh), _vp, _vp, ctypes.c_double, ctypes.c_double,
                                          ctypes.c_double, ctypes.POINTER(_i64), _dp, _vp]
     L.aderstp_correct_slab.argtypes = [_vp, ctypes.POINTER(_Mesh), ctypes.POINTER(_Slab), _vp, _vp, _vp, _vp, _vp,
-                                       ctypes.POINTER(_Halo), ctypes.POINTER(_Halo), ctypes.c_double, _vp]
+                                       ctypes.POINTER(_Halo), ctypes.POINTER(_Halo), ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_double, _vp]
     L.aderstp_run_simulation_slab.argtypes = [_vp, ctypes.POINTER(_Mesh), ctypes.POINTER(_Slab), _vp, _vp, _vp, _vp,
                                               ctypes.POINTER(_Halo), ctypes.POINTER(_Halo), ctypes.c_double,
                                               ctypes.c_double, ctypes.c_double, _SyncFn, _vp,
@@ -194,8 +196,28 @@ class LinearPde:
     quantities: int
     args: list = field(default_factory=list)
     linear: list | None = None  # [A_x, A_y, A_z, B_x, B_y, B_z] (m x m) for PDE_LINEAR
+    wavespeed: float | None = None  # PDE_LINEAR: the user's max_wavespeed() (pde.hpp:41)
+
+    @property
+    def has_source(self) -> bool:
+        return self.kind in (PDE_ELASTIC_SOURCE, PDE_SOURCE_ONLY) or (
+            self.kind == PDE_LINEAR and len(self.args) >= 8 and self.args[7] != 0.0)
 
     def max_wavespeed(self) -> float:
+        if self.kind == PDE_LINEAR:
+            if self.wavespeed is not None:
+                return float(self.wavespeed)
+            # the characteristic speeds of q_t = sum_d (A_d + B_d) d_d q: the largest |eigenvalue|
+            # over the three directions
+            m = self.quantities
+            best = 0.0
+            for d in range(3):
+                c = np.zeros((m, m))
+                for mat in (self.linear[d], self.linear[3 + d]):
+                    if mat is not None:
+                        c = c + np.asarray(mat, dtype=np.float64)
+                best = max(best, float(np.max(np.abs(np.linalg.eigvals(c)))) if m else 0.0)
+            return best
         if self.kind in (PDE_ADVECTION, PDE_NCP_ADVECTION):
             return max(abs(v) for v in self.args[:3])
         if self.kind == PDE_DEMO:
@@ -227,8 +249,8 @@ def elastic_pde(lam=None, mu=None, rho=None, source: PointSourceSpec | None = No
         if not 6 <= source.component <= 8:
             raise StpError(ADERSTP_ERR_INVALID_ARG,
                            "elastic_pde: source must act on a velocity component (6..8)")
-        return ElasticPde(PDE_ELASTIC_SOURCE, 9, source.args(), None, lam, mu, rho)
-    return ElasticPde(PDE_ELASTIC, 9, [], None, lam, mu, rho)
+        return ElasticPde(PDE_ELASTIC_SOURCE, 9, source.args(), lam=lam, mu=mu, rho=rho)
+    return ElasticPde(PDE_ELASTIC, 9, [], lam=lam, mu=mu, rho=rho)
 
 
 def advection_pde(velocity, m: int) -> LinearPde:
@@ -247,13 +269,22 @@ def source_only_pde(m: int, source: PointSourceSpec) -> LinearPde:
     return LinearPde(PDE_SOURCE_ONLY, m, source.args())
 
 
-def linear_pde(flux_jacobians, ncp_matrices=None) -> LinearPde:
-    """Any constant-coefficient system given by A_d (F_d(q) = A_d q) and B_d.  This is the
-    probed form of an arbitrary reference LinearPde (tests/test_pde.cpp:14-24 probes it the
-    same way: F_d(e_r) is column r of A_d)."""
+def linear_pde(flux_jacobians, ncp_matrices=None, source: PointSourceSpec | None = None,
+               max_wavespeed: float | None = None) -> LinearPde:
+    """Any constant-coefficient system given by A_d (F_d(q) = A_d q) and B_d, any m up to 64,
+    dense or sparse, optionally with one Gaussian point source.  This is the probed form of an
+    arbitrary reference LinearPde (tests/test_pde.cpp:14-24 probes it the same way: F_d(e_r) is
+    column r of A_d); max_wavespeed is the user's max_wavespeed() (default: the largest
+    characteristic speed, max_d max |eig(A_d + B_d)|)."""
     A = [np.ascontiguousarray(a, dtype=np.float64) for a in flux_jacobians]
     B = [None] * 3 if ncp_matrices is None else [np.ascontiguousarray(b, dtype=np.float64) for b in ncp_matrices]
-    return LinearPde(PDE_LINEAR, A[0].shape[0], [], A + B)
+    m = A[0].shape[0]
+    args = []
+    if source is not None:
+        if not 0 <= source.component < m:
+            raise StpError(ADERSTP_ERR_INVALID_ARG, "point source: component out of range")
+        args = source.args() + [1.0]  # pde_args[7] != 0: the LinearPde carries this source
+    return LinearPde(PDE_LINEAR, m, args, A + B, max_wavespeed)
 
 
 # ----------------------------------------------------------------------------- outputs ------
@@ -367,10 +398,11 @@ class Plan:
 
     # ---- GPU corrector and time loop (proj/src/solver.cpp) ---------------------------------
     def correct(self, u, elements_per_dim: int, out: PredictorOutput, par=None, domain_len: float = 1.0,
-                max_wavespeed: float | None = None, stream=None):
-        """corrector_step (solver.cpp:257-311) in place on the device mesh state u [e^3, q_size]
-        from this step's predictor outputs (computed on the 1/h-scaled PDE).  max_wavespeed: the
-        PDE's unscaled max_wavespeed(); None = the PDE's own (elastic: per face from the material)."""
+                max_wavespeed: float | None = None, stream=None, dt: float | None = None, t: float = 0.0):
+        """corrector_step(mesh, outs, pde, ops, dt, t) (solver.cpp:257-311) in place on the device
+        mesh state u [e^3, q_size] from this step's predictor outputs (computed on the 1/h-scaled
+        PDE).  max_wavespeed: the PDE's unscaled max_wavespeed(); None = the PDE's own (elastic:
+        per face from the material).  dt, t: the step (they enter through a point source only)."""
         import torch
         E = elements_per_dim ** 3
         if not (isinstance(u, torch.Tensor) and u.is_cuda and u.dtype == torch.float64 and u.is_contiguous()
@@ -380,9 +412,17 @@ class Plan:
             par = self._uniform_par(E, u)
         smax = self._smax(max_wavespeed)
         mesh = _Mesh(elements_per_dim, domain_len)
-        ptr = lambda t: None if t is None else ctypes.c_void_p(t.data_ptr())  # noqa: E731
+        ptr = lambda x: None if x is None else ctypes.c_void_p(x.data_ptr())  # noqa: E731
         _check(lib.aderstp_correct_batch(self._h, ctypes.byref(mesh), ptr(u), ptr(par), ptr(out.qavg),
-                                         ptr(out.face_q), ptr(out.face_f), smax, _stream_handle(stream)))
+                                         ptr(out.face_q), ptr(out.face_f), smax, self._step_dt(dt), float(t),
+                                         _stream_handle(stream)))
+
+    def _step_dt(self, dt):
+        if dt is None:
+            if self.pde.has_source:
+                raise StpError(ADERSTP_ERR_INVALID_ARG, "corrector_step: a point-source PDE needs the step's dt")
+            return 0.0
+        return float(dt)
 
     def _smax(self, max_wavespeed):
         if max_wavespeed is not None:
@@ -422,7 +462,8 @@ class Plan:
         return _Halo(ptr(h[0]), ptr(h[1]), ptr(h[2]), int(h[3]))
 
     def correct_slab(self, u, elements_per_dim: int, slab, out: PredictorOutput, lo=None, hi=None, par=None,
-                     domain_len: float = 1.0, max_wavespeed: float | None = None, stream=None):
+                     domain_len: float = 1.0, max_wavespeed: float | None = None, stream=None,
+                     dt: float | None = None, t: float = 0.0):
         """corrector_step on the layers [z0, z0 + nz) (slab = (z0, nz)); z-neighbours outside the
         slab come from the halos lo / hi = (face_q, face_f, par, z_base) of the adjacent slabs."""
         mesh, sl = _Mesh(elements_per_dim, domain_len), _Slab(*slab)
@@ -431,7 +472,8 @@ class Plan:
         _check(lib.aderstp_correct_slab(self._h, ctypes.byref(mesh), ctypes.byref(sl), ptr(u), ptr(par),
                                         ptr(out.qavg), ptr(out.face_q), ptr(out.face_f),
                                         ctypes.byref(hl) if hl else None, ctypes.byref(hh) if hh else None,
-                                        self._smax(max_wavespeed), _stream_handle(stream)))
+                                        self._smax(max_wavespeed), self._step_dt(dt), float(t),
+                                        _stream_handle(stream)))
 
     def run_simulation_slab(self, u, elements_per_dim: int, slab, face_q, face_f, t_end: float,
                             max_wavespeed: float, lo=None, hi=None, par=None, cfl: float = 0.35,

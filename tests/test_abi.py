@@ -43,7 +43,7 @@ def test_library_is_sm100a(S):
 
 
 def test_abi_version(S):
-    assert S.lib.aderstp_abi_version() == 1
+    assert S.lib.aderstp_abi_version() == 2
 
 
 def test_basis_matches_oracle_and_reference_golden(S, oracle):
@@ -105,7 +105,7 @@ def test_corrector_entry_points_validate_arguments(S):
     """aderstp_correct_batch / aderstp_run_simulation reject bad arguments before any device work."""
     L = S.lib
     mesh = S.stp._Mesh(2, 1.0)
-    rc = L.aderstp_correct_batch(None, ctypes.byref(mesh), None, None, None, None, None, 1.0, None)
+    rc = L.aderstp_correct_batch(None, ctypes.byref(mesh), None, None, None, None, None, 1.0, 0.0, 0.0, None)
     assert rc == S.ADERSTP_ERR_INVALID_ARG
     steps, t_final = ctypes.c_int64(7), ctypes.c_double(7.0)
     rc = L.aderstp_run_simulation(None, ctypes.byref(mesh), None, None, 0.35, 1.0, 1.0,

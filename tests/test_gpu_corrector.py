@@ -245,12 +245,18 @@ def test_instability_is_reported(S, oracle):
     assert not ok
 
 
-def test_corrector_rejects_point_sources(S):
+def test_source_only_run_simulation_accumulates_the_source_integral(S, oracle, reference):
+    """A source-only PDE (no flux): run_simulation is pure accumulation of the projected source
+    integrals (correct_cell, solver.cpp:206-216), matching ader::run_simulation."""
     src = S.PointSourceSpec((0.5, 0.5, 0.5), 0, 1.0, 0.1, 0.05)
-    plan = S.Plan(4, S.source_only_pde(2, src), layout=S.LAYOUT_AOSOA)
-    u = torch.zeros(8, plan.q_size, dtype=torch.float64, device="cuda")
-    with pytest.raises(S.StpError):
-        plan.run_simulation(u, 2, 0.1, max_wavespeed=0.0)
+    n, m, e = 4, 2, 2
+    plan = S.Plan(n, S.source_only_pde(m, src), layout=S.LAYOUT_AOSOA)
+    u = torch.zeros(e ** 3, plan.q_size, dtype=torch.float64, device="cuda")
+    ok, steps, t = plan.run_simulation(u, e, 0.1)  # max_wavespeed() = 0: one step of dt = t_end
+    ref_u, ok2, steps2, _ = reference.run_simulation(n, m, e, 1.0, np.zeros((e ** 3, n ** 3 * m)), 0.35, 0.1,
+                                                     pde_kind=O.PDE_SOURCE_ONLY, args=src.args())
+    assert ok and ok2 and steps == steps2 > 0
+    assert O.per_element_rel_diff(ref_u, from_dev(oracle, n, m, u)) <= 1e-11
 
 
 # ---- the slab decomposition of the multi-GPU time loop (one slab per thread on one GPU) --------
