@@ -362,6 +362,38 @@ def measure_table_pde(S, steps, warmup):
             "elements_per_s": E / (ms * 1e-3), "ms_per_step": ms, "kernel": "stp_dmma8_table"}
 
 
+def measure_general_pde(S, steps, warmup, m=21, n=8, E=16384):
+    """The general user-LinearPde kernel (stp_general.cu): a dense m = 21 system (the paper's
+    application size, every A_d and B_d entry nonzero) at nDof 8, device-resident."""
+    import numpy as np
+    import torch
+    rng = np.random.default_rng(SEED)
+    A = [rng.uniform(-1, 1, (m, m)) / m ** 0.5 for _ in range(3)]
+    B = [rng.uniform(-0.5, 0.5, (m, m)) / m ** 0.5 for _ in range(3)]
+    pde = S.linear_pde(A, B)
+    g = torch.Generator(device="cuda").manual_seed(SEED)
+    q = torch.rand(E, n ** 3 * m, dtype=torch.float64, device="cuda", generator=g) * 2.0 - 1.0
+    plan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=m, out_stride=m)
+    out = plan.alloc_output(E)
+    dt = 0.5 / (3.0 * pde.max_wavespeed() * (2 * n - 1))
+    for _ in range(warmup):
+        plan.predict(q, dt, out=out)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(steps):
+        plan.predict(q, dt, out=out)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    plan.status()
+    ms = ev0.elapsed_time(ev1) / steps
+    del q, out
+    return {"workload": f"dense LinearPde (m = {m}, every A_d / B_d entry nonzero), nDof {n}, {E} elements, "
+                        "Q~U[-1,1] (general kernel)",
+            "elements_per_s": E / (ms * 1e-3), "ms_per_step": ms, "kernel": "stp_general_kernel"}
+
+
 def measure_timestep(S, n, e, steps, warmup):
     """One full time step of the GPU solver on an e^3 periodic mesh: the
     predictor on the 1/h-scaled PDE without favg (the corrector never reads it, solver.cpp:184-253)
@@ -762,6 +794,7 @@ def main():
         others["timestep_n8"] = measure_timestep(S, 8, 50, max(5, args.steps // 4), 3)
         others["c3_reference_layout"] = measure_reference_layout(S, CONFIGS["c3"], max(5, args.steps // 4), 3)
         others["table_pde_advection_m8_n8"] = measure_table_pde(S, max(5, args.steps // 4), 3)
+        others["general_pde_dense_m21_n8"] = measure_general_pde(S, max(3, args.steps // 8), 3)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:

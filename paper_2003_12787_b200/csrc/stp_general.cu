@@ -62,12 +62,14 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
   const long long e = blockIdx.x;
   const int tid = threadIdx.x;
   double* Ds = smg;                         // D, N x N
-  double* W = smg + N2 + (N2 & 1);          // plane workspace: 3 m N^2 (CK), 6 m N^2 (faces)
+  // plane workspace: 3 m N^2 (CK step); for N < 6 also the face staging (6 m N^2), for N >= 6 the
+  // faces are staged in the dead iterate buffer instead (m N^3 >= 6 m N^2)
+  double* W = smg + N2 + (N2 & 1);
   double* P;                                // p_(o-1)
   if (kp.scratch) {
     P = kp.scratch + e * (2ll * m * N3);
   } else {
-    P = W + 6 * m * N2;
+    P = W + (N >= 6 ? 3 : 6) * m * N2;
   }
   double* R = P + (long long)m * N3;        // p_o; the final Qbar in the epilogue
   unsigned int flags = 0;
@@ -153,6 +155,7 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
     return;
   }
   const double* Q = P;  // Qbar [s][k3][k2][k1]
+  double* F = N >= 6 ? R : W;  // face_q staging
 
   // ---- favg_d = A_d Qbar (the reference's F_d(Qbar), stp_splitck.cpp:72-78) -----------------
   if (a.favg) {
@@ -194,7 +197,7 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
         const int node = d == 0 ? (ia * N + ib) * N + j : d == 1 ? (ia * N + j) * N + ib : (j * N + ia) * N + ib;
         v = fma(ph[j], qs[node], v);
       }
-      W[i] = v;
+      F[i] = v;
       if (a.face_q) a.face_q[e * 6ll * FACE + i] = v;
     }
     __syncthreads();
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
         const int f = i / FACE, r = i - f * FACE, ab = r / m, s = r - ab * m, d = f >> 1;
         double v = 0.0;
         const int b = kp.f_ptr[3 * s + d], end = kp.f_ptr[3 * s + d + 1];
-        for (int k = b; k < end; ++k) v = fma(kp.f_val[k], W[f * FACE + ab * m + kp.f_col[k]], v);
+        for (int k = b; k < end; ++k) v = fma(kp.f_val[k], F[f * FACE + ab * m + kp.f_col[k]], v);
         a.face_f[e * 6ll * FACE + i] = v * kp.scale;  // the flux of the (scaled) PDE
       }
   }
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
 template <int N>
 size_t general_smem(int m, bool scratch) {
   const size_t n2 = N * N, n3 = n2 * N;
-  return sizeof(double) * (n2 + (n2 & 1) + 6 * (size_t)m * n2 + (scratch ? 0 : 2 * (size_t)m * n3));
+  return sizeof(double) * (n2 + (n2 & 1) + (N >= 6 ? 3 : 6) * (size_t)m * n2 + (scratch ? 0 : 2 * (size_t)m * n3));
 }
 
 template <int N>

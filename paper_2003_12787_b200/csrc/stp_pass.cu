@@ -641,6 +641,54 @@ __device__ __forceinline__ void bip_line_z(const double* src, double* const* dst
   }
 }
 
+// Pass z of phase S.  For the normal stresses (slot 0) the x and y passes left the raw derivatives
+// a = Dx u in the sxx slot and b = Dy v in the syy slot; with c = Dz w of this z-line
+//   sxx = (lambda+2mu) a + lambda (b + c),  syy = (lambda+2mu) b + lambda (a + c),
+//   szz = (lambda+2mu) c + lambda (a + b),  plus the Horner term c_o q (TMEM targets k0..k0+2):
+// one write per target instead of three read-modify-writes (the sxx/syy/szz passes of the
+// per-direction scheme), and the x / y passes of slot 0 store one line instead of three.
+// Slots 1, 2 (shear) as bip_line_z.  Warp-collective TMEM loads (ntw = the warp's maximum).
+template <int N>
+__device__ __forceinline__ void bip_line_z_s(const double* src, double* const* dst, const double* cf, int nt, int ntw,
+                                             bool normal, double* sxx, double L, double lam, uint32_t ta, int k0,
+                                             double co) {
+  using G = GeoB<N>;
+  double out[N], a[N], b[N];
+  if (nt > 0) {
+    double p[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) p[l] = src[l * G::PL];
+    eo_apply<N>(p, out);  // slot 0: c = Dz w
+  }
+  if (normal) {
+#pragma unroll
+    for (int l = 0; l < N; ++l) {
+      a[l] = sxx[l * G::PL];
+      b[l] = sxx[G::VS + l * G::PL];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k >= ntw) break;
+    double q[N];
+    tm_load_q<N>(ta, k0 + k, q);
+    if (normal) {
+      double* d = sxx + k * G::VS;
+#pragma unroll
+      for (int l = 0; l < N; ++l) {
+        const double own = k == 0 ? a[l] : k == 1 ? b[l] : out[l];
+        const double rest = k == 0 ? b[l] + out[l] : k == 1 ? a[l] + out[l] : a[l] + b[l];
+        d[l * G::PL] = fma(co, q[l], fma(L, own, lam * rest));
+      }
+    } else if (k < nt) {
+      double* d = dst[k];
+      const double c = cf[k];
+#pragma unroll
+      for (int l = 0; l < N; ++l) d[l * G::PL] = fma(co, q[l], fma(c, out[l], d[l * G::PL]));
+    }
+  }
+}
+
 // AOS: the reference's ElementTensor / PredictorOutput node rows [k3][k2][k1][s < 16] in and out
 // (proj/src/layout.cpp:9-21): q is staged node-wise from the rows, qavg / favg leave as whole
 // 128-byte node rows (4 nodes per warp instruction, padding slots as zeros).
@@ -649,6 +697,14 @@ __global__ void __launch_bounds__(GeoB<N>::THREADS, GeoB<N>::MINB)
 stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   static_assert(!(FUSED && AOS), "the time loop runs on AoSoA");
   using G = GeoB<N>;
+  // phase S with raw a = Dx u, b = Dy v combined in the z pass (bip_line_z_s): measured +3.5 % at
+  // nDof 9 (5.33 -> 5.52 M elem/s); at nDof 10 the combining pass spills at the 96-register
+  // bound of two 320-thread CTAs per SM (-14 %), so nDof 10 keeps the per-direction scheme
+#ifdef BIP_NO_RAWAB
+  constexpr bool kRawAB = false;
+#else
+  constexpr bool kRawAB = N == 9;
+#endif
   extern __shared__ __align__(16) double smb[];
   __shared__ uint32_t tmem_base_s;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -962,9 +1018,15 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
       int srcf, nt;
       if (slot == 0) {
         srcf = vb;
-        nt = 3;
+        if constexpr (!kRawAB) {
+          nt = 3;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[0][k]);
+          for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[0][k]);
+        } else {
+          nt = 1;  // raw a = Dx u into the sxx slot (bip_line_z_s combines)
+          cf[0] = 1.0;
+          cf[1] = cf[2] = 0.0;
+        }
       } else {
         srcf = vb + (kBipS12[0][sl > 0 ? sl - 1 : 0][0] - 6);
         nt = 1;
@@ -989,9 +1051,15 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
       int srcf, nt;
       if (slot == 0) {
         srcf = vb + 1;
-        nt = 3;
+        if constexpr (!kRawAB) {
+          nt = 3;
 #pragma unroll
-        for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[1][k]);
+          for (int k = 0; k < 3; ++k) cf[k] = pick4(c4, kBipS0[1][k]);
+        } else {
+          nt = 1;  // raw b = Dy v into the syy slot
+          cf[0] = 1.0;
+          cf[1] = cf[2] = 0.0;
+        }
       } else {
         srcf = vb + (kBipS12[1][sl > 0 ? sl - 1 : 0][0] - 6);
         nt = 1;
@@ -1000,15 +1068,20 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
       }
       const int st = bip_start<N, 1>(la, lb);
       if (slot == 0) {
-        dst[0] = E + st;
-        dst[1] = E + G::VS + st;
-        dst[2] = E + 2 * G::VS + st;
+        if constexpr (!kRawAB) {
+          dst[0] = E + st;
+          dst[1] = E + G::VS + st;
+          dst[2] = E + 2 * G::VS + st;
+        } else {
+          dst[0] = E + G::VS + st;
+          dst[1] = dst[2] = nullptr;
+        }
       } else {
         dst[0] = E + kBipS12[1][sl > 0 ? sl - 1 : 0][1] * G::VS + st;
         dst[1] = dst[2] = nullptr;
       }
-      // syz (slot 2) gets its first contribution here
-      if (active) bip_line<N, 1>(E + srcf * G::VS + st, dst, cf, nt, slot == 2);
+      // syz (slot 2) gets its first contribution here (and raw b in slot 0)
+      if (active) bip_line<N, 1>(E + srcf * G::VS + st, dst, cf, nt, kRawAB ? slot != 1 : slot == 2);
     }
     __syncthreads();
     {
@@ -1030,7 +1103,13 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
         dst[1] = E + 3 * G::VS + zst;
         dst[2] = nullptr;
       }
-      bip_line_z<N>(E + srcf * G::VS + zst, dst, cf, ntS, ntS_w, ta, 1, co);
+      if constexpr (!kRawAB) {
+        bip_line_z<N>(E + srcf * G::VS + zst, dst, cf, ntS, ntS_w, ta, 1, co);
+      } else {
+        // slot 0 (normal stresses) combines the raw a, b with c = Dz w; slots 1, 2 as before --
+        // each warp runs the TMEM loads of the larger of its slots' target counts
+        bip_line_z_s<N>(E + srcf * G::VS + zst, dst, cf, ntS, ntS_w, slot == 0, E + zst, c4[0], c4[1], ta, 1, co);
+      }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
