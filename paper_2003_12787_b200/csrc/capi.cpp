@@ -35,7 +35,7 @@ constexpr int kHostStreams = 3;
 constexpr long long kStageBytes = 512ll << 20;
 
 // the reference layout through device transposes to a tuned AoSoA kernel: the elastic PDE, and
-// table PDEs with m <= 8 at nDof 8 (stp_dmma8_table)
+// table PDEs with m <= 9 at nDof 8 (stp_dmma8_table)
 bool aos_staged(const aderstp::LaunchPlan& lp) {
   const bool tuned = lp.kind == ADERSTP_PDE_ELASTIC || (lp.kind != ADERSTP_PDE_ELASTIC_SOURCE && lp.n == 8 && lp.m <= 9);
   return tuned && lp.src_comp < 0 && lp.layout == ADERSTP_LAYOUT_AOS && !lp.force_generic &&

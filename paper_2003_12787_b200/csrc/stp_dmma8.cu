@@ -587,8 +587,9 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
   TM3(6);
 }
 
-// ---- table PDEs (any constant-coefficient LinearPde given as term tables, m <= 8) -----------
-// The user-PDE path on the tensor cores: warp s owns output quantity s (m <= 8 warps), and a CK step
+// ---- table PDEs (any constant-coefficient LinearPde given as term tables, m <= 9) -----------
+// The user-PDE path on the tensor cores: warp s owns output quantity s (s < 8; a ninth quantity is
+// split over the warps by k3 plane, compiled only into the HAS9 instance), and a CK step
 // is  t_s = c_o q_s + sum_d sum_k tc[s][d][k] D_d r_{tr[s][d][k]}  (build_terms folds the ncp
 // matrices in: D_d (A_d + B_d) p, proj/src/stp_splitck.cpp:53-61 for constant coefficients) --
 // every term one more pair of DMMAs (x, y) or register DFMAs (z) into the same accumulators, the
@@ -606,6 +607,9 @@ struct ParamsG {
   int m, n_terms, q_stride, check;
 };
 
+// HAS9: m == 9 (the ninth quantity's accumulators and branches); m <= 8 compiles without them and
+// keeps its registers (80, no ninth-quantity spill traffic)
+template <bool HAS9>
 __global__ void __maxnreg__(80) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, unsigned int* status) {
   constexpr int THREADS8 = NWARP * 32;
   extern __shared__ __align__(16) double smg[];
@@ -655,7 +659,7 @@ __global__ void __maxnreg__(80) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, 
         if (cz != 0.0) dfma_z<8>(tt, P + kp.tr[s][2][k] * PV, 0, col, cz);
       }
     }
-    if (m == GM) {  // quantity 8: warp w takes plane k3 = w
+    if (HAS9) {  // quantity 8: warp w takes plane k3 = w
       const double co = kp.cf[o];
       const double2 v = lds2(Q + 8 * PV + warp * 64 + col);
       t8[0][0] = co * v.x;
@@ -673,7 +677,7 @@ __global__ void __maxnreg__(80) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, 
 #pragma unroll
       for (int k = 0; k < 8; ++k) sts2(P + s * PV + k * 64 + col, tt[k][0], tt[k][1]);
     }
-    if (m == GM) sts2(P + 8 * PV + warp * 64 + col, t8[0][0], t8[0][1]);
+    if (HAS9) sts2(P + 8 * PV + warp * 64 + col, t8[0][0], t8[0][1]);
     __syncthreads();  // new r (qavg after the last step) complete
   }
   // ---- epilogue: qavg and favg of quantity s, x/y/z faces --------------------------------------
@@ -742,7 +746,7 @@ __global__ void __maxnreg__(80) stp_dmma8_table_kernel(ParamsG kp, BatchArgs a, 
       }
     }
   }
-  if (m == GM) {  // quantity 8, plane k3 = warp: qavg, favg, x / y faces; warp 0 also the z faces
+  if (HAS9) {  // quantity 8, plane k3 = warp: qavg, favg, x / y faces; warp 0 also the z faces
     const int k3 = warp;
     double* qout = a.qavg + e * (long long)(PV * m) + 8 * 8 + 2 * t;
     st_cs2(qout + (k3 * 8 + g) * m * 8, t8[0][0], t8[0][1]);
@@ -848,7 +852,7 @@ bool dmma8_aos_applicable(const LaunchPlan& p, const BatchArgs& a) {
          !a.u_next && al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) && al16(a.face_f);
 }
 
-// table PDEs at nDof 8 on the tensor cores: m <= 8, compact AoSoA outputs, no point source
+// table PDEs at nDof 8 on the tensor cores: m <= 9, compact AoSoA outputs, no point source
 bool dmma8_table_applicable(const LaunchPlan& p, const BatchArgs& a) {
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
   return p.n == 8 && p.kind != ADERSTP_PDE_ELASTIC && p.kind != ADERSTP_PDE_ELASTIC_SOURCE && p.src_comp < 0 &&
@@ -886,14 +890,14 @@ cudaError_t launch_dmma8_table(const LaunchPlan& p, const BatchArgs& a, cudaStre
   kp.q_stride = p.q_stride;
   kp.check = p.check;
   const int smem = 2 * p.m * PV * 8;
-  cudaError_t err = cudaFuncSetAttribute(stp_dmma8_table_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  auto kern = p.m == GM ? stp_dmma8_table_kernel<true> : stp_dmma8_table_kernel<false>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (err == cudaSuccess)
-    err = cudaFuncSetAttribute(stp_dmma8_table_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
-                               cudaSharedmemCarveoutMaxShared);
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (err != cudaSuccess) return err;
   if (a.n_elem == 0) return cudaSuccess;
   if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
-  stp_dmma8_table_kernel<<<(unsigned)a.n_elem, NWARP * 32, smem, stream>>>(kp, a, p.d_status);
+  kern<<<(unsigned)a.n_elem, NWARP * 32, smem, stream>>>(kp, a, p.d_status);
   return cudaGetLastError();
 }
 
