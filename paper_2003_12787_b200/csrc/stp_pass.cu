@@ -653,53 +653,6 @@ __device__ __forceinline__ void bip_line_z_s(const double* src, double* const* d
                                              bool normal, double* sxx, double L, double lam, uint32_t ta, int k0,
                                              double co) {
   using G = GeoB<N>;
-  if constexpr (N == 10) {  // halves of the line: a, b and q five at a time (96-register budget)
-    double out[N];
-    if (nt > 0) {
-      double p[N];
-#pragma unroll
-      for (int l = 0; l < N; ++l) p[l] = src[l * G::PL];
-      eo_apply<N>(p, out);
-    }
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      double a[5], b[5];
-      if (normal) {
-#pragma unroll
-        for (int l = 0; l < 5; ++l) {
-          a[l] = sxx[(5 * h + l) * G::PL];
-          b[l] = sxx[G::VS + (5 * h + l) * G::PL];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        if (k >= ntw) break;
-        uint32_t r[10];
-        tm_ld8(ta + 2 * N * (k0 + k) + 10 * h, r);
-        tm_ld2(ta + 2 * N * (k0 + k) + 10 * h + 8, r + 8);
-        tm_wait_ld();
-        if (normal) {
-          double* d = sxx + k * G::VS;
-#pragma unroll
-          for (int l = 0; l < 5; ++l) {
-            const double c = out[5 * h + l];
-            const double own = k == 0 ? a[l] : k == 1 ? b[l] : c;
-            const double rest = k == 0 ? b[l] + c : k == 1 ? a[l] + c : a[l] + b[l];
-            d[(5 * h + l) * G::PL] = fma(co, tm_double(r, l), fma(L, own, lam * rest));
-          }
-        } else if (k < nt) {
-          double* d = dst[k];
-          const double c = cf[k];
-#pragma unroll
-          for (int l = 0; l < 5; ++l) {
-            const int j = 5 * h + l;
-            d[j * G::PL] = fma(co, tm_double(r, l), fma(c, out[j], d[j * G::PL]));
-          }
-        }
-      }
-    }
-    return;
-  }
   double out[N], a[N], b[N];
   if (nt > 0) {
     double p[N];
@@ -746,14 +699,12 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
   using G = GeoB<N>;
   // phase S with raw a = Dx u, b = Dy v combined in the z pass (bip_line_z_s): measured +3.5 % at
   // nDof 9 (5.33 -> 5.52 M elem/s); at nDof 10 the combining pass spills at the 96-register
-  // bound of two 320-thread CTAs per SM (-14 %), so nDof 10 keeps the per-direction scheme
+  // bound of two 320-thread CTAs per SM (-14 %; -8 % with the pass split into half lines), so
+  // nDof 10 keeps the per-direction scheme
 #ifdef BIP_NO_RAWAB
   constexpr bool kRawAB = false;
 #else
-#ifndef BIP_RAW10
-#define BIP_RAW10 1
-#endif
-  constexpr bool kRawAB = N == 9 || (N == 10 && BIP_RAW10);
+  constexpr bool kRawAB = N == 9;
 #endif
   extern __shared__ __align__(16) double smb[];
   __shared__ uint32_t tmem_base_s;
