@@ -39,8 +39,9 @@ struct GenParams {
   int m, q_stride, out_stride, layout, check;
   double scale;                      // ScaledPde gradient scale (1 outside the time loop)
   const int* t_ptr;                  // C_d rows: entries [t_ptr[3s+d], t_ptr[3s+d+1])
-  const int* t_col;
+  const int* t_col;                  // workspace offset (d m + j) N^2 of the entry's D_d p_j
   const double* t_val;
+  int t_nnz, csr_smem;               // csr_smem: stage the C rows in shared memory
   const int* f_ptr;                  // A_d rows (favg, face_f)
   const int* f_col;
   const double* f_val;
@@ -74,6 +75,24 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
   double* R = P + (long long)m * N3;        // p_o; the final Qbar in the epilogue
   unsigned int flags = 0;
   for (int i = tid; i < N2; i += kGenThreads) Ds[i] = kp.d[i];
+  // the CK step's coefficient rows, staged once per element next to the buffers when they fit
+  // (warp-uniform broadcast reads instead of dependent L1 round trips)
+  const double* tv = kp.t_val;
+  const int* to = kp.t_col;
+  const int* tp = kp.t_ptr;
+  if (kp.csr_smem) {
+    double* sv = (kp.scratch ? W + (N >= 6 ? 3 : 6) * m * N2 : R + (long long)m * N3);
+    int* so = reinterpret_cast<int*>(sv + kp.t_nnz);
+    int* sp = so + kp.t_nnz;
+    for (int i = tid; i < kp.t_nnz; i += kGenThreads) {
+      sv[i] = kp.t_val[i];
+      so[i] = kp.t_col[i];
+    }
+    for (int i = tid; i <= 3 * m; i += kGenThreads) sp[i] = kp.t_ptr[i];
+    tv = sv;
+    to = so;
+    tp = sp;
+  }
 
   // ---- stage p_0 = q (canonical [s][k3][k2][k1]) and Qbar = dt q into the output --------
   const double* qe = a.q + e * (long long)N3 * kp.q_stride;
@@ -122,13 +141,16 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
       for (int i = tid; i < m * N2; i += kGenThreads) {
         const int s = i / N2, node = i - s * N2;
         const int k2 = node / N, k1 = node - k2 * N;
-        double t = 0.0;
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const int b = kp.t_ptr[3 * s + d], end = kp.t_ptr[3 * s + d + 1];
-          for (int k = b; k < end; ++k) t = fma(kp.t_val[k], W[(d * m + kp.t_col[k]) * N2 + node], t);
+        // the row of s over all three directions is contiguous: [tp[3s], tp[3s + 3])
+        double t0 = 0.0, t1 = 0.0;
+        const int end = tp[3 * s + 3];
+        int k = tp[3 * s];
+        for (; k + 1 < end; k += 2) {
+          t0 = fma(tv[k], W[to[k] + node], t0);
+          t1 = fma(tv[k + 1], W[to[k + 1] + node], t1);
         }
-        t *= kp.scale;
+        if (k < end) t0 = fma(tv[k], W[to[k] + node], t0);
+        double t = (t0 + t1) * kp.scale;
         const int node3 = k3 * N2 + node;
         if (kp.vol_mode) {  // corrector: u += V(qavg)
           double* u = a.u_next + e * (long long)N3 * kp.q_stride + lidx<N>(kp.layout, kp.q_stride, s, k3, k2, k1);
@@ -247,6 +269,7 @@ cudaError_t launch_general_n(const LaunchPlan& p, const BatchArgs& a, cudaStream
   kp.t_ptr = p.gen.t_ptr;
   kp.t_col = p.gen.t_col;
   kp.t_val = p.gen.t_val;
+  kp.t_nnz = p.gen.t_nnz;
   kp.f_ptr = p.gen.f_ptr;
   kp.f_col = p.gen.f_col;
   kp.f_val = p.gen.f_val;
@@ -258,8 +281,11 @@ cudaError_t launch_general_n(const LaunchPlan& p, const BatchArgs& a, cudaStream
   if (err == cudaSuccess) err = cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (err != cudaSuccess) return err;
   const bool scratch = general_smem<N>(p.m, false) > (size_t)max_smem;
-  const size_t smem = general_smem<N>(p.m, scratch);
+  size_t smem = general_smem<N>(p.m, scratch);
   if (smem > (size_t)max_smem) return cudaErrorInvalidConfiguration;
+  const size_t csr = sizeof(double) * p.gen.t_nnz + sizeof(int) * (p.gen.t_nnz + 3 * p.m + 1);
+  kp.csr_smem = smem + csr <= (size_t)max_smem;
+  if (kp.csr_smem) smem += csr;
   err = cudaFuncSetAttribute(stp_general_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   if (!scratch) {
