@@ -131,6 +131,11 @@ int aderstp_predict_batch_host(aderstp_plan* plan, int64_t n_elem, const double*
                                double* favg, double* face_q, double* face_f);
 int aderstp_plan_reserve_host_path(aderstp_plan* plan, int64_t chunk_elems);
 
+/* The plan keeps the device scratch its calls allocated (AoS staging <= 512 MiB per call, the
+ * time loop's face buffers) in a stream-ordered pool until it is destroyed; this returns that
+ * memory to the device now (synchronises the device). */
+int aderstp_plan_trim(aderstp_plan* plan);
+
 /* Synchronises `stream` and returns (and clears) the input-check status of the plan's
  * previous launches: ADERSTP_OK, ADERSTP_ERR_NONFINITE or ADERSTP_ERR_MATERIAL. */
 int aderstp_plan_status(aderstp_plan* plan, void* stream);

@@ -31,7 +31,7 @@ int cuda_fail(cudaError_t e, const char* what) {
 }
 
 constexpr int kHostStreams = 3;
-// per-call device scratch of the AoS staged path, and the plan pool's release threshold
+// per-call device scratch of the AoS staged path
 constexpr long long kStageBytes = 512ll << 20;
 
 // the reference layout through device transposes to a tuned AoSoA kernel: the elastic PDE, and
@@ -60,8 +60,8 @@ struct aderstp_plan {
   int64_t chunk = 0;
   double* buf[kHostStreams] = {nullptr, nullptr, nullptr};
   cudaStream_t streams[kHostStreams] = {nullptr, nullptr, nullptr};
-  // stream-ordered scratch (AoS staging, time-loop buffers): a plan-owned pool that keeps up to
-  // kStageBytes between calls, so repeated calls do not re-map it
+  // stream-ordered scratch (AoS staging, time-loop buffers): a plan-owned pool that keeps its
+  // memory between calls (no re-mapping per call) until aderstp_plan_trim / destroy
   cudaMemPool_t pool = nullptr;
   // general kernel tables (CSR rows of C_d and A_d; one cudaMalloc) and the corrector's point
   // source projection (n^3 doubles)
@@ -408,7 +408,9 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   // plan-owned stream-ordered pool (AoS staging, time-loop faces): keeps its memory between
   // calls, returned when the plan is destroyed
   if (e == cudaSuccess) e = cudaMemPoolCreate(&p->pool, &pool_props_of(p->device));
-  const uint64_t keep = (uint64_t)kStageBytes;
+  // keep what the plan's calls allocated (a time loop re-maps GBs of face buffers otherwise);
+  // the AoS staging is capped at kStageBytes per call, and aderstp_plan_trim returns the rest
+  const uint64_t keep = UINT64_MAX;
   if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, (void*)&keep);
   // D of nDof 8 in the constant bank: the elastic and the table-PDE tensor-core kernels
   if (e == cudaSuccess && kl.n == 8) e = aderstp::init_dmma8(kl);
@@ -472,8 +474,7 @@ cudaError_t predict_aos_staged(const aderstp_plan* plan, const aderstp::BatchArg
   sp.out_stride = m;
   const size_t t9 = (size_t)n * n * n * m;  // one AoSoA tensor (doubles)
   const size_t per = t9 * (a.favg ? 5 : 2);  // q, qavg (+ favg[3])
-  // staging capped at kStageBytes per call (a few waves of CTAs at every order); the pool returns
-  // what exceeds its release threshold (the same figure) at the next synchronisation
+  // staging capped at kStageBytes per call (a few waves of CTAs at every order)
   long long chunk = std::max<long long>(1, std::min<long long>(a.n_elem, kStageBytes / (long long)(per * 8)));
   if (lp.aos_chunk > 0) chunk = std::min<long long>(chunk, lp.aos_chunk);  // tests: force several chunks
   double* buf = nullptr;
@@ -524,6 +525,14 @@ int aderstp_predict_batch(const aderstp_plan* p, int64_t n_elem, const double* q
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaError_t e = predict_device(p, a, st);
   if (e != cudaSuccess) return cuda_fail(e, "predict_batch launch");
+  return ADERSTP_OK;
+}
+
+int aderstp_plan_trim(aderstp_plan* p) {
+  if (!p) return fail(ADERSTP_ERR_INVALID_ARG, "plan_trim: null plan");
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e == cudaSuccess && p->pool) e = cudaMemPoolTrimTo(p->pool, 0);
+  if (e != cudaSuccess) return cuda_fail(e, "plan_trim");
   return ADERSTP_OK;
 }
 

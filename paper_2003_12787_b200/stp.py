@@ -96,6 +96,7 @@ def _load():
                                              _dp, _dp, _dp, _dp]
     L.aderstp_plan_reserve_host_path.argtypes = [_vp, _i64]
     L.aderstp_plan_status.argtypes = [_vp, _vp]
+    L.aderstp_plan_trim.argtypes = [_vp]
     L.aderstp_convert_layout.argtypes = [ctypes.c_int, ctypes.c_int, _i64, ctypes.c_int, ctypes.c_int,
                                          _vp, ctypes.c_int, ctypes.c_int, _vp, _vp]
     L.aderstp_generate.argtypes = [ctypes.c_int, ctypes.c_uint64, ctypes.c_int, _i64, _i64, ctypes.c_int,
@@ -494,6 +495,10 @@ class Plan:
         if rc not in (ADERSTP_OK, ADERSTP_ERR_NONFINITE):
             _check(rc)
         return rc == ADERSTP_OK, steps.value, t_final.value
+
+    def trim(self):
+        """Return the plan's pooled device scratch (AoS staging, time-loop buffers) to the device."""
+        _check(lib.aderstp_plan_trim(self._h))
 
     def status(self, stream=None):
         """Synchronise and raise on flagged inputs (validate_stp's non-finite / material checks)."""

@@ -347,3 +347,17 @@ def test_long_run_matches_reference(S, oracle, reference):
     assert ok and our_steps == steps
     worst = O.per_element_rel_diff(ref_u, from_dev(oracle, n, m, u))
     assert worst <= 1e-10, worst
+
+
+def test_plan_trim_returns_pooled_scratch(S, oracle):
+    """The time loop's face buffers stay pooled between calls (no re-mapping per call) until
+    Plan.trim(); the loop runs the same before and after a trim."""
+    n, e = 4, 3
+    q, par = S.generate(0, 3, n, 0, e ** 3, layout=S.LAYOUT_AOSOA, q_stride=9)
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
+    u1, u2 = (q * 1e-3).clone(), (q * 1e-3).clone()
+    assert plan.run_simulation(u1, e, 2e-3, par=par)[0]
+    plan.trim()
+    assert plan.run_simulation(u2, e, 2e-3, par=par)[0]
+    plan.trim()
+    assert torch.equal(u1, u2)
