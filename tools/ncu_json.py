@@ -1,7 +1,8 @@
 """Build profiles/ncu_summary.json from a round's ncu --set full captures.
-Usage: python tools/ncu_json.py gpurun_out/prof_rNN [round-tag]
-Each full_<cfg>.ncu-rep is one launch of the config's STP kernel on `elements` elements
-(tools/profile_round.sh); the per-element DRAM traffic feeds bench.py's roofline.traffic."""
+Usage: python tools/ncu_json.py DIR [round-tag] [prefix]
+Each <prefix><cfg>.ncu-rep (default prefix full_) is one launch of the config's STP kernel; the
+elements of the launch are its grid size (one CTA per element: every tuned kernel) unless the
+config is in ELEMS.  The per-element DRAM traffic feeds bench.py's roofline.traffic."""
 import csv
 import io
 import json
@@ -9,7 +10,7 @@ import os
 import subprocess
 import sys
 
-ELEMS = {"c2": 32768, "c3": 16384, "c4": 8192, "n9": 8192}
+ELEMS = {"c2": None, "c3": None, "c4": None, "n9": None}
 KEYS = {
     "duration_ms": "gpu__time_duration.sum",
     "fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
@@ -35,13 +36,15 @@ def to_bytes(v, u):
     return float(v.replace(",", "")) * scale
 
 
-def main(d, tag):
+def main(d, tag, prefix="full_"):
     out = {}
     for cfg, elems in ELEMS.items():
-        rep = os.path.join(d, f"full_{cfg}.ncu-rep")
+        rep = os.path.join(d, f"{prefix}{cfg}.ncu-rep")
         if not os.path.exists(rep):
             continue
         v, u = raw(rep)
+        if elems is None:
+            elems = int(float(v["launch__grid_size"].replace(",", "")))
         traffic = to_bytes(v["dram__bytes_read.sum"], u["dram__bytes_read.sum"]) + \
             to_bytes(v["dram__bytes_write.sum"], u["dram__bytes_write.sum"])
         ent = {"kernel": v.get("Kernel Name", v.get("Function Name", "")), "elements_per_launch": elems,
@@ -52,8 +55,8 @@ def main(d, tag):
                     ent[k] = float(v[m].replace(",", ""))
                 except ValueError:
                     ent[k] = v[m]
-        ent["note"] = (f"round {tag}: ncu --set full --clock-control none, one launch after 2 warm-ups "
-                       "(cold caches, serialised); tools/profile_stp.py")
+        ent["note"] = (f"round {tag}: ncu --set full --clock-control none, one launch of the bench.py "
+                       "config after 3 warm-ups (cold caches, serialised); tools/gpu_ncu_full.sh")
         out[cfg] = ent
     with open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
                            "ncu_summary.json"), "w") as f:
@@ -62,4 +65,4 @@ def main(d, tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "r01")
+    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "r01", sys.argv[3] if len(sys.argv) > 3 else "full_")
