@@ -42,7 +42,7 @@ struct LaunchPlan {
   // general kernel (stp_general.cu): device CSR rows of C_d = A_d + B_d and of A_d, per (s, d)
   struct GeneralTables {
     const int* t_ptr = nullptr;
-    const int* t_col = nullptr;      // (d m + j) n^2: offset of D_d p_j in the plane workspace
+    const int* t_col = nullptr;
     int t_nnz = 0;
     const double* t_val = nullptr;
     const int* f_ptr = nullptr;

@@ -113,9 +113,8 @@ int build_terms(LaunchPlan& lp, const double* A[3], const double* B[3]) {
   return ADERSTP_OK;
 }
 
-// The general kernel's tables: CSR rows (s, d) of C_d = A_d + B_d (the CK step; column stored as
-// the plane-workspace offset of D_d p_j) and of A_d (favg, face_f; plain columns), zeros
-// dropped, in one device allocation owned by the plan.
+// The general kernel's tables: CSR rows (s, d) of C_d = A_d + B_d (the CK step) and of A_d
+// (favg, face_f), zeros dropped, in one device allocation owned by the plan.
 cudaError_t upload_general(aderstp_plan* p, const std::vector<double>& A, const std::vector<double>& B) {
   const int m = p->lp.m;
   std::vector<int> tp(3 * m + 1, 0), fp(3 * m + 1, 0), tc, fc;
@@ -124,8 +123,8 @@ cudaError_t upload_general(aderstp_plan* p, const std::vector<double>& A, const 
     for (int d = 0; d < 3; ++d) {
       for (int j = 0; j < m; ++j) {
         const double a = A[(size_t)d * m * m + s * m + j], c = a + B[(size_t)d * m * m + s * m + j];
-        if (c != 0.0) {  // the general kernel's plane workspace offset of D_d p_j: (d m + j) n^2
-          tc.push_back((d * m + j) * p->lp.n * p->lp.n);
+        if (c != 0.0) {
+          tc.push_back(j);
           tv.push_back(c);
         }
         if (a != 0.0) {

@@ -7,16 +7,18 @@
 //   p_0 = q,  Qbar = dt q,  p_o = sum_d D_d F_d(p_(o-1)) + B_d (D_d p_(o-1)) + P S^(o-1)(t0),
 //   Qbar += c_o p_o (c_o = c_(o-1) dt / (o+1)),  favg_d = F_d(Qbar),  faces of Qbar / favg.
 // For constant coefficients D_d F_d(p) + B_d D_d p = C_d (D_d p) with C_d = A_d + B_d, so a CK
-// step is "derivatives first, then one pointwise matrix": per k3 plane of the element,
-//   phase 1: W[d][j] = D_d p_j on the plane, for every quantity j and direction d (3 m N^2
-//            line dot products of length N, from the iterate in shared memory),
-//   phase 2: t_s = sum_d sum_(j in row s of C_d) C_d[s][j] W[d][j] (+ the point source), which
-//            is p_o of the plane; Qbar += c_o t_s is kept in the caller's qavg buffer (the
+// step is "derivatives first, then one pointwise matrix":
+//   phase z: D_z p_j for every quantity j, one z-line per task (N loads, N outputs), into the
+//            buffer that will hold p_o (the z workspace of a plane is dead once its p_o is known);
+//   then per k3 plane -- phase xy: D_x p_j and D_y p_j of the plane, one line per task;
+//            phase 2: t_s = sum_d sum_(j in row s of C_d) C_d[s][j] (D_d p_j) (+ the point
+//            source) = p_o of the plane, staged and copied over the plane's z workspace while the
+//            next plane's lines run; Qbar += c_o t_s is kept in the caller's qavg buffer (the
 //            thread that owns an entry owns it in every step: no race, L2-resident).
 // The matrices live in device memory as per-(s, d) row lists (CSR), read warp-uniformly.  The
 // iterate pair (p_(o-1), p_o) and the plane workspace sit in shared memory when they fit
-// (2 m N^3 + 6 m N^2 doubles); larger systems (e.g. m = 21 at nDof 10) use a per-element slice of
-// a plan-owned global scratch instead -- correct for every size, just not as fast.
+// (2 m N^3 + 3 m N^2 doubles, 6 m N^2 for N < 6); larger systems (e.g. m = 21 at nDof 10) use a
+// per-element slice of a plan-owned global scratch instead -- correct for every size, slower.
 #include <cmath>
 #include <cstdint>
 
@@ -39,7 +41,7 @@ struct GenParams {
   int m, q_stride, out_stride, layout, check;
   double scale;                      // ScaledPde gradient scale (1 outside the time loop)
   const int* t_ptr;                  // C_d rows: entries [t_ptr[3s+d], t_ptr[3s+d+1])
-  const int* t_col;                  // workspace offset (d m + j) N^2 of the entry's D_d p_j
+  const int* t_col;                  // source quantity j of the entry
   const double* t_val;
   int t_nnz, csr_smem;               // csr_smem: stage the C rows in shared memory
   const int* f_ptr;                  // A_d rows (favg, face_f)
@@ -110,48 +112,81 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
   __syncthreads();
 
   const int steps = kp.vol_mode ? 1 : N - 1;
+  double* Wx = W;                    // D_x p_j on the current plane   [j][k2][k1]
+  double* Wy = W + m * N2;           // D_y p_j on the current plane
+  double* Wt = W + 2 * m * N2;       // p_o of the current plane, staged until its copy into R
 #pragma unroll 1
   for (int o = 1; o <= steps; ++o) {
-#pragma unroll 1
-    for (int k3 = 0; k3 < N; ++k3) {
-      // phase 1: W[d][j][k2][k1] = (D_d p_j) at the plane's nodes
-      for (int i = tid; i < 3 * m * N2; i += kGenThreads) {
-        const int dj = i / N2, node = i - dj * N2;
-        const int d = dj / m, j = dj - d * m;
-        const int k2 = node / N, k1 = node - k2 * N;
-        const double* pj = P + (long long)j * N3;
+    // phase z (all planes at once): R[j][k3][k2][k1] = (D_z p_j), one z-line per task -- N
+    // loads and N outputs (R doubles as the z workspace until each plane's p_o replaces it)
+    for (int i = tid; i < m * N2; i += kGenThreads) {
+      const int j = i / N2, node = i - j * N2;
+      const double* col = P + (long long)j * N3 + node;
+      double c[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) c[l] = col[l * N2];
+      double* out = R + (long long)j * N3 + node;
+#pragma unroll
+      for (int k = 0; k < N; ++k) {
         double acc = 0.0;
-        if (d == 0) {
-          const double* row = pj + k3 * N2 + k2 * N;
 #pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(Ds[k1 * N + l], row[l], acc);
-        } else if (d == 1) {
-          const double* col = pj + k3 * N2 + k1;
-#pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(Ds[k2 * N + l], col[l * N], acc);
-        } else {
-          const double* col = pj + k2 * N + k1;
-#pragma unroll
-          for (int l = 0; l < N; ++l) acc = fma(Ds[k3 * N + l], col[l * N2], acc);
-        }
-        W[i] = acc;
+        for (int l = 0; l < N; ++l) acc = fma(Ds[k * N + l], c[l], acc);
+        out[k * N2] = acc;
       }
+    }
+#pragma unroll 1
+    for (int k3 = 0; k3 <= N; ++k3) {
+      // phase xy of plane k3 (x lines (j, k2), y lines (j, k1): N loads, N outputs each), and
+      // the copy of plane k3-1's p_o from Wt into R (its z workspace is no longer read)
+      if (k3 < N)
+        for (int i = tid; i < 2 * m * N; i += kGenThreads) {
+          const int dj = i / N, r = i - dj * N;
+          const int d = dj / m, j = dj - d * m;
+          const double* pj = P + (long long)j * N3 + k3 * N2;
+          double c[N];
+          if (d == 0) {
+#pragma unroll
+            for (int l = 0; l < N; ++l) c[l] = pj[r * N + l];
+          } else {
+#pragma unroll
+            for (int l = 0; l < N; ++l) c[l] = pj[l * N + r];
+          }
+          double* out = (d == 0 ? Wx + j * N2 + r * N : Wy + j * N2 + r);
+          const int ostride = d == 0 ? 1 : N;
+#pragma unroll
+          for (int k = 0; k < N; ++k) {
+            double acc = 0.0;
+#pragma unroll
+            for (int l = 0; l < N; ++l) acc = fma(Ds[k * N + l], c[l], acc);
+            out[k * ostride] = acc;
+          }
+        }
+      if (k3 > 0 && !kp.vol_mode)
+        for (int i = tid; i < m * N2; i += kGenThreads) {
+          const int j = i / N2, node = i - j * N2;
+          R[(long long)j * N3 + (k3 - 1) * N2 + node] = Wt[i];
+        }
       __syncthreads();
-      // phase 2: t_s = sum_d C_d[s][.] W[d][.] (+ source); p_o -> R, Qbar += c_o p_o
+      if (k3 == N) break;
+      // phase 2: t_s = sum_d C_d[s][.] (D_d p)[.] (+ source); Qbar += c_o p_o; p_o -> Wt
+      const double* Wz = R + k3 * N2;
       for (int i = tid; i < m * N2; i += kGenThreads) {
         const int s = i / N2, node = i - s * N2;
         const int k2 = node / N, k1 = node - k2 * N;
-        // the row of s over all three directions is contiguous: [tp[3s], tp[3s + 3])
         double t0 = 0.0, t1 = 0.0;
-        const int end = tp[3 * s + 3];
-        int k = tp[3 * s];
-        for (; k + 1 < end; k += 2) {
-          t0 = fma(tv[k], W[to[k] + node], t0);
-          t1 = fma(tv[k + 1], W[to[k + 1] + node], t1);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          const double* base = d == 0 ? Wx + node : d == 1 ? Wy + node : Wz + node;
+          const int js = d == 2 ? N3 : N2;
+          const int end = tp[3 * s + d + 1];
+          int k = tp[3 * s + d];
+          for (; k + 1 < end; k += 2) {
+            t0 = fma(tv[k], base[to[k] * js], t0);
+            t1 = fma(tv[k + 1], base[to[k + 1] * js], t1);
+          }
+          if (k < end) t0 = fma(tv[k], base[to[k] * js], t0);
         }
-        if (k < end) t0 = fma(tv[k], W[to[k] + node], t0);
         double t = (t0 + t1) * kp.scale;
-        const int node3 = k3 * N2 + node;
         if (kp.vol_mode) {  // corrector: u += V(qavg)
           double* u = a.u_next + e * (long long)N3 * kp.q_stride + lidx<N>(kp.layout, kp.q_stride, s, k3, k2, k1);
           const double nv = *u + t;
@@ -164,7 +199,7 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
         double* acc = qa + lidx<N>(kp.layout, kp.out_stride, s, k3, k2, k1);
         const double nq = fma(kp.cf[o], t, *acc);
         *acc = nq;
-        R[(long long)s * N3 + node3] = o == N - 1 ? nq : t;  // the last step leaves Qbar in R
+        Wt[i] = o == N - 1 ? nq : t;  // the last step leaves Qbar
       }
       __syncthreads();
     }
