@@ -44,6 +44,7 @@ struct LaunchPlan {
     const int* t_ptr = nullptr;
     const int* t_col = nullptr;
     int t_nnz = 0;
+    const double* t_dense = nullptr;  // C_d dense [d][j][s < m rounded up to 8] (general kernel)
     const double* t_val = nullptr;
     const int* f_ptr = nullptr;
     const int* f_col = nullptr;

@@ -135,8 +135,16 @@ cudaError_t upload_general(aderstp_plan* p, const std::vector<double>& A, const 
       tp[3 * s + d + 1] = (int)tc.size();
       fp[3 * s + d + 1] = (int)fc.size();
     }
-  // layout: [t_val][f_val][t_ptr][f_ptr][t_col][f_col] (doubles first: 8-byte alignment)
-  const size_t bytes = sizeof(double) * (tv.size() + fv.size()) + sizeof(int) * (tp.size() + fp.size() + tc.size() + fc.size());
+  // dense C_d [d][j][s < mp] (mp = m rounded up to 8: whole target blocks of the dense phase 2)
+  const int mp = (m + 7) / 8 * 8;
+  std::vector<double> cd(3 * (size_t)m * mp, 0.0);
+  for (int d = 0; d < 3; ++d)
+    for (int s = 0; s < m; ++s)
+      for (int j = 0; j < m; ++j)
+        cd[((size_t)d * m + j) * mp + s] = A[(size_t)d * m * m + s * m + j] + B[(size_t)d * m * m + s * m + j];
+  // layout: [cd][t_val][f_val][t_ptr][f_ptr][t_col][f_col] (doubles first: 16-byte alignment)
+  const size_t bytes = sizeof(double) * (cd.size() + tv.size() + fv.size()) +
+                       sizeof(int) * (tp.size() + fp.size() + tc.size() + fc.size());
   std::vector<char> host(bytes > 0 ? bytes : 8);
   char* h = host.data();
   size_t off = 0;
@@ -146,6 +154,7 @@ cudaError_t upload_general(aderstp_plan* p, const std::vector<double>& A, const 
     off += n;
     return at;
   };
+  const size_t o_cd = put(cd.data(), sizeof(double) * cd.size());
   const size_t o_tv = put(tv.data(), sizeof(double) * tv.size());
   const size_t o_fv = put(fv.data(), sizeof(double) * fv.size());
   const size_t o_tp = put(tp.data(), sizeof(int) * tp.size());
@@ -157,6 +166,7 @@ cudaError_t upload_general(aderstp_plan* p, const std::vector<double>& A, const 
   if (e != cudaSuccess) return e;
   char* dv = static_cast<char*>(p->gen_buf);
   aderstp::LaunchPlan::GeneralTables& g = p->lp.gen;
+  g.t_dense = reinterpret_cast<const double*>(dv + o_cd);
   g.t_val = reinterpret_cast<const double*>(dv + o_tv);
   g.f_val = reinterpret_cast<const double*>(dv + o_fv);
   g.t_ptr = reinterpret_cast<const int*>(dv + o_tp);

@@ -30,6 +30,7 @@ namespace aderstp {
 namespace {
 
 constexpr int kGenThreads = 256;
+constexpr int kSB = 8;  // targets per task of the dense phase 2 (the padded dense rows cover them)
 
 struct GenParams {
   double d[kMaxOrder * kMaxOrder];   // d[k*N + l]
@@ -44,6 +45,8 @@ struct GenParams {
   const int* t_col;                  // source quantity j of the entry
   const double* t_val;
   int t_nnz, csr_smem;               // csr_smem: stage the C rows in shared memory
+  const double* t_dense;             // dense C: [d][j][s < m_pad] (null: rows only)
+  int dense, m_pad;                  // dense: phase 2 by target blocks from the dense C in smem
   const int* f_ptr;                  // A_d rows (favg, face_f)
   const int* f_col;
   const double* f_val;
@@ -82,7 +85,12 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
   const double* tv = kp.t_val;
   const int* to = kp.t_col;
   const int* tp = kp.t_ptr;
-  if (kp.csr_smem) {
+  double* Cd = nullptr;  // dense C staged in shared memory (dense mode)
+  if (kp.dense) {
+    Cd = (kp.scratch ? W + (N >= 6 ? 3 : 6) * m * N2 : R + (long long)m * N3);
+    Cd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(Cd) + 15) & ~uintptr_t(15));  // LDS.128
+    for (int i = tid; i < 3 * m * kp.m_pad; i += kGenThreads) Cd[i] = kp.t_dense[i];
+  } else if (kp.csr_smem) {
     double* sv = (kp.scratch ? W + (N >= 6 ? 3 : 6) * m * N2 : R + (long long)m * N3);
     int* so = reinterpret_cast<int*>(sv + kp.t_nnz);
     int* sp = so + kp.t_nnz;
@@ -170,6 +178,54 @@ __global__ void __launch_bounds__(kGenThreads) stp_general_kernel(GenParams kp, 
       if (k3 == N) break;
       // phase 2: t_s = sum_d C_d[s][.] (D_d p)[.] (+ source); Qbar += c_o p_o; p_o -> Wt
       const double* Wz = R + k3 * N2;
+      if (kp.dense) {  // dense C: a task = (node, block of kSB targets), each D_d p_j loaded once
+        const int nb = (m + kSB - 1) / kSB;
+        for (int i = tid; i < nb * N2; i += kGenThreads) {
+          const int sb = i / N2, node = i - sb * N2;
+          const int k2 = node / N, k1 = node - k2 * N, s0 = sb * kSB;
+          double acc[kSB];
+#pragma unroll
+          for (int q = 0; q < kSB; ++q) acc[q] = 0.0;
+#pragma unroll 1
+          for (int d = 0; d < 3; ++d) {
+            const double* base = d == 0 ? Wx + node : d == 1 ? Wy + node : Wz + node;
+            const int js = d == 2 ? N3 : N2;
+            const double* cr = Cd + (long long)d * m * kp.m_pad + s0;
+#pragma unroll 2
+            for (int j = 0; j < m; ++j) {
+              const double w = base[j * js];
+              const double* c = cr + j * kp.m_pad;
+#pragma unroll
+              for (int q = 0; q < kSB; q += 2) {
+                const double2 cc = *reinterpret_cast<const double2*>(c + q);
+                acc[q] = fma(cc.x, w, acc[q]);
+                acc[q + 1] = fma(cc.y, w, acc[q + 1]);
+              }
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < kSB; ++q) {
+            const int s = s0 + q;
+            if (s >= m) break;
+            double t = acc[q] * kp.scale;
+            if (kp.vol_mode) {
+              double* u = a.u_next + e * (long long)N3 * kp.q_stride + lidx<N>(kp.layout, kp.q_stride, s, k3, k2, k1);
+              const double nv = *u + t;
+              if (!isfinite(nv)) flags |= 1u;
+              *u = nv;
+              continue;
+            }
+            if (s == kp.src_comp)
+              t = fma(kp.src_proj[2][k3] * (kp.src_proj[1][k2] * kp.src_proj[0][k1]), kp.src_amp[o - 1], t);
+            double* ac = qa + lidx<N>(kp.layout, kp.out_stride, s, k3, k2, k1);
+            const double nq = fma(kp.cf[o], t, *ac);
+            *ac = nq;
+            Wt[s * N2 + node] = o == N - 1 ? nq : t;
+          }
+        }
+        __syncthreads();
+        continue;
+      }
       for (int i = tid; i < m * N2; i += kGenThreads) {
         const int s = i / N2, node = i - s * N2;
         const int k2 = node / N, k1 = node - k2 * N;
@@ -319,8 +375,14 @@ cudaError_t launch_general_n(const LaunchPlan& p, const BatchArgs& a, cudaStream
   size_t smem = general_smem<N>(p.m, scratch);
   if (smem > (size_t)max_smem) return cudaErrorInvalidConfiguration;
   const size_t csr = sizeof(double) * p.gen.t_nnz + sizeof(int) * (p.gen.t_nnz + 3 * p.m + 1);
-  kp.csr_smem = smem + csr <= (size_t)max_smem;
-  if (kp.csr_smem) smem += csr;
+  // dense C (rows padded to whole target blocks) when the matrices are mostly nonzero
+  kp.m_pad = (p.m + kSB - 1) / kSB * kSB;
+  kp.t_dense = p.gen.t_dense;
+  const size_t dense = sizeof(double) * (3 * p.m * kp.m_pad + 2);  // + alignment slack
+  kp.dense = p.gen.t_dense != nullptr && 2 * p.gen.t_nnz >= 3 * p.m * p.m && smem + dense <= (size_t)max_smem;
+  kp.csr_smem = !kp.dense && smem + csr <= (size_t)max_smem;
+  if (kp.dense) smem += dense;
+  else if (kp.csr_smem) smem += csr;
   err = cudaFuncSetAttribute(stp_general_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   if (!scratch) {
