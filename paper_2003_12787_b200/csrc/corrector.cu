@@ -280,7 +280,9 @@ struct VecT<2> {
 template <int N, bool VOL>
 constexpr int surf_threads() { return VOL && N >= 9 ? 512 : kSurfThreads; }  // 1 CTA/SM at N >= 9
 
-template <int N, int QS, bool VOL>
+// SRC: a point source (compiled only into the instances that need it: the branch alone costs the
+// common instance 8 registers and a spill)
+template <int N, int QS, bool VOL, bool SRC>
 __global__ void __launch_bounds__(surf_threads<N, VOL>()) surface_kernel(CorrParams kp, CorrArgs ca, unsigned int* status) {
   constexpr int NT = surf_threads<N, VOL>();
   constexpr int V = N % 2 == 0 ? 2 : 1;
@@ -420,7 +422,7 @@ __global__ void __launch_bounds__(surf_threads<N, VOL>()) surface_kernel(CorrPar
 #pragma unroll
       for (int k = 0; k < V; ++k) VecT<V>::at(v, k) += vol[k];
     }
-    if (s == ca.src_comp) {  // point source (solver.cpp:206-216), after the volume term
+    if (SRC && s == ca.src_comp) {  // point source (solver.cpp:206-216), after the volume term
 #pragma unroll
       for (int k = 0; k < V; ++k) VecT<V>::at(v, k) += ca.src_proj[k32 * N + k1 + k] * ca.src_sint;
     }
@@ -505,8 +507,11 @@ cudaError_t launch_correct_n(const LaunchPlan& p, const CorrArgs& a, cudaStream_
   if (elastic && p.layout == ADERSTP_LAYOUT_AOSOA && p.m == NVC && (!vol || p.out_stride == NVC)) {
     // tuned elastic path (any q stride; qavg in the compact AoSoA output layout)
     const size_t ssm = sizeof(double) * (6 * N * N * NVC + (vol ? NVC * (N * N * N + 8) : 0));
-    auto sk = vol ? surface_kernel<N, 0, true> : surface_kernel<N, 0, false>;
-    if (p.q_stride == NVC) sk = vol ? surface_kernel<N, NVC, true> : surface_kernel<N, NVC, false>;
+    auto sk = vol ? surface_kernel<N, 0, true, false> : surface_kernel<N, 0, false, false>;
+    if (p.q_stride == NVC) sk = vol ? surface_kernel<N, NVC, true, false> : surface_kernel<N, NVC, false, false>;
+    if (a.src_comp >= 0)  // elastic point source: the volume term is never fused (generic predictor)
+      sk = p.q_stride == NVC ? surface_kernel<N, NVC, true, true> : surface_kernel<N, 0, true, true>;
+    if (a.src_comp >= 0 && !vol) return cudaErrorInvalidValue;
     cudaError_t err = cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ssm);
     if (err != cudaSuccess) return err;
     const long long cells = (long long)a.e * a.e * (a.nz > 0 ? a.nz : a.e);
