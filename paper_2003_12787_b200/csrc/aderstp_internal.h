@@ -131,6 +131,10 @@ bool kernel_available(int n);
 bool dmma8_applicable(const LaunchPlan& p);
 bool dmma8_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
 bool dmma8_table_applicable(const LaunchPlan& p, const BatchArgs& a);
+// stp_dmma_table.cu: table PDEs at nDof 4..7 on zero-padded DMMA tiles
+bool dmmat_applicable(const LaunchPlan& p, const BatchArgs& a);
+cudaError_t init_dmmat(const LaunchPlan& p);
+cudaError_t launch_dmmat(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 cudaError_t launch_dmma8_table(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 bool bip_aos_applicable(const LaunchPlan& p, const BatchArgs& a);
 bool dmmap_aos_applicable(const LaunchPlan& p, const BatchArgs& a);

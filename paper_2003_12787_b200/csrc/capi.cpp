@@ -425,6 +425,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   if (e == cudaSuccess && kl.n == 8) e = aderstp::init_dmma8(kl);
   if (e == cudaSuccess && aderstp::pass_applicable(kl)) e = aderstp::init_pass(kl);
   if (e == cudaSuccess && aderstp::dmmap_applicable(kl)) e = aderstp::init_dmmap(kl);
+  if (e == cudaSuccess && kl.kind != ADERSTP_PDE_ELASTIC && kl.n >= 5 && kl.n <= 7) e = aderstp::init_dmmat(kl);
   if (e == cudaSuccess) lp.gen.pool = p->pool;
   if (e != cudaSuccess) {
     aderstp_plan_destroy(p);

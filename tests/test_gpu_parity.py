@@ -416,15 +416,16 @@ def test_reference_layout_checks_and_edges(stp, oracle, n):
         assert O.per_element_rel_diff(b.cpu().numpy().reshape(E, -1), a.cpu().numpy().reshape(E, -1)) <= TOL
 
 
+@pytest.mark.parametrize("n", [4, 5, 6, 7, 8])
 @pytest.mark.parametrize("case", ["advection_m3", "ncp_advection_m2", "demo_m6", "probed_m5", "probed_m8", "probed_m9"])
-def test_table_pdes_on_tensor_cores_nDof8(stp, oracle, monkeypatch, case):
-    """Table PDEs (the user-LinearPde path) at nDof 8 run on stp_dmma8_table; the reference's
-    PDEs against the oracle, random probed systems (flux + ncp matrices) against the unmodified
-    reference's predict() on a MatrixPde with the same matrices; all against the generic table
-    kernel on the same inputs."""
+def test_table_pdes_on_tensor_cores(stp, oracle, monkeypatch, case, n):
+    """Table PDEs (the user-LinearPde path) run on the tensor cores: stp_dmma8_table at nDof 8,
+    stp_dmmat (zero-padded tiles) at nDof 4..7; the reference's PDEs against the oracle, random
+    probed systems (flux + ncp matrices) against the unmodified reference's predict() on a
+    MatrixPde with the same matrices; all against the generic table kernel on the same inputs."""
     S = stp
-    n, E = 8, 7
-    rng = np.random.default_rng(_zlib.crc32(case.encode()))
+    E = 7
+    rng = np.random.default_rng(_zlib.crc32(case.encode()) + n)
     if case == "advection_m3":
         m, pde, kind, args = 3, S.advection_pde((1.0, 0.5, 0.25), 3), O.PDE_ADVECTION, [1.0, 0.5, 0.25]
     elif case == "ncp_advection_m2":
