@@ -46,7 +46,9 @@ constexpr int THREADSP = NWP * 32;
 
 template <int N>
 struct GeoP {
-  static constexpr int PV = N * 64;                  // one quantity: N planes of 8 x 8
+  // one quantity: N planes of 8 x 8, plus 6 doubles so that PV / 2 = 3 mod 8: the epilogue's
+  // output-ordered 16-byte reads (k1 pair fastest, then the quantity) hit 8 distinct bank groups
+  static constexpr int PV = N * 64 + 6;
   static constexpr int FACE = N * N * NVP;           // one face array
   static constexpr int SMEM = 2 * NVP * PV * 8;      // p + qavg accumulator
   static constexpr int KS = N > 4 ? 2 : 1;           // k-steps of 4
@@ -85,6 +87,13 @@ __constant__ int kInP[NVP][3] = {{6, 7, 8}, {6, 7, 8}, {6, 7, 8}, {7, 6, 0}, {8,
                                  {0, 8, 7}, {0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
 __constant__ int kCoefP[NVP][3] = {{0, 1, 1}, {1, 0, 1}, {1, 1, 0}, {2, 2, 4}, {2, 4, 2},
                                    {4, 2, 2}, {3, 3, 3}, {3, 3, 3}, {3, 3, 3}};
+
+// e_in(s, d) (coef: e_coef) of the 9 output quantities packed 4 bits each, quantity s at bit 4 s
+constexpr unsigned long long pack_flux(int d, bool coef) {
+  unsigned long long v = 0;
+  for (int s = 0; s < NVP; ++s) v |= (unsigned long long)(coef ? e_coef(s, d) : e_in(s, d)) << (4 * s);
+  return v;
+}
 
 __device__ __forceinline__ double ldcp(const double* p) {
   double v;
@@ -491,47 +500,52 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   }
   TM2(3);
   if (faces) {
-    // x and y faces of plane k3 (DMMA against phi), every quantity of the plane per warp
-#pragma unroll 1
-    for (int k3 = warp; k3 < N; k3 += NWP) {
+    // Face extrapolations as line tasks over all 8 warps (FMAs; a DMMA against phi would use 2
+    // of its 8 output columns): task (direction, line, quantity) reads its line of the padded
+    // qavg planes (16-byte pairs where the line runs along k1) and writes both sides; the
+    // quantity is the fastest task index, so 8 consecutive lanes read 8 distinct bank groups
+    // (PV / 2 = 3 mod 8) and store consecutive face entries.
+    {
+      constexpr int KP = (N + 1) / 2;            // k1 pairs (the last one half padding for odd N)
+      constexpr int TX = N * N * NVP, TY = N * KP * NVP;
+      for (int i = tid; i < TX + 2 * TY; i += THREADSP) {
+        if (i < TX) {  // x: row (k3, k2) of quantity s
+          const int s = i % NVP, r = i / NVP, k2 = r % N, k3 = r / N;
+          const double* row = P + s * PV + k3 * 64 + k2 * 8;
+          double f0 = 0.0, f1 = 0.0;
 #pragma unroll
-      for (int s = 0; s < NVP; ++s) {
-        const double* qs = P + s * PV + k3 * 64;
-        double x0 = 0.0, x1 = 0.0, y0 = 0.0, y1 = 0.0;
-        dmmap(x0, x1, qs[physp(g, t)], bphi0);
-        if (G::KS > 1) dmmap(x0, x1, qs[physp(g, 4 + t)], bphi1);
-        dmmap(y0, y1, bphi0, qs[physp(t, g)]);
-        if (G::KS > 1) dmmap(y0, y1, bphi1, qs[physp(4 + t, g)]);
-        if (t == 0 && g < N) {
-          FQ[0 * FACE + (k3 * N + g) * NVP + s] = x0;
-          FQ[1 * FACE + (k3 * N + g) * NVP + s] = x1;
-        }
-        if (g < 2) {
-          if (k1a) FQ[(2 + g) * FACE + (k3 * N + 2 * t) * NVP + s] = y0;
-          if (k1b) FQ[(2 + g) * FACE + (k3 * N + 2 * t + 1) * NVP + s] = y1;
-        }
-      }
-    }
-#pragma unroll 1
-    for (int s = warp; s < NVP; s += NWP) {
-      const double* qs = P + s * PV;
-      if (rowok) {
-        double z0[2] = {0.0, 0.0}, z1[2] = {0.0, 0.0};
+          for (int k = 0; k < KP; ++k) {
+            const double2 v = lds2p(row + ((2 * k) ^ ((k2 & 2) << 1)));
+            f0 = fma(kp.phi[0][2 * k], v.x, f0);
+            f1 = fma(kp.phi[1][2 * k], v.x, f1);
+            if (2 * k + 1 < N) {
+              f0 = fma(kp.phi[0][2 * k + 1], v.y, f0);
+              f1 = fma(kp.phi[1][2 * k + 1], v.y, f1);
+            }
+          }
+          FQ[0 * FACE + (k3 * N + k2) * NVP + s] = f0;
+          FQ[1 * FACE + (k3 * N + k2) * NVP + s] = f1;
+        } else {  // y: column pair (k3, k1 = 2 kp, 2 kp + 1) over k2; z: (k2, k1 pair) over k3
+          const bool ydir = i < TX + TY;
+          const int j = i - (ydir ? TX : TX + TY);
+          const int s = j % NVP, r = j / NVP, kq = r % KP, a0 = r / KP;
+          double f0[2] = {0.0, 0.0}, f1[2] = {0.0, 0.0};
 #pragma unroll
-        for (int k3 = 0; k3 < N; ++k3) {
-          const double2 v = lds2p(qs + k3 * 64 + col);
-          z0[0] = fma(kp.phi[0][k3], v.x, z0[0]);
-          z0[1] = fma(kp.phi[0][k3], v.y, z0[1]);
-          z1[0] = fma(kp.phi[1][k3], v.x, z1[0]);
-          z1[1] = fma(kp.phi[1][k3], v.y, z1[1]);
-        }
-        if (k1a) {
-          FQ[4 * FACE + (g * N + 2 * t) * NVP + s] = z0[0];
-          FQ[5 * FACE + (g * N + 2 * t) * NVP + s] = z1[0];
-        }
-        if (k1b) {
-          FQ[4 * FACE + (g * N + 2 * t + 1) * NVP + s] = z0[1];
-          FQ[5 * FACE + (g * N + 2 * t + 1) * NVP + s] = z1[1];
+          for (int k = 0; k < N; ++k) {
+            const double2 v = ydir ? lds2p(P + s * PV + a0 * 64 + physp(k, 2 * kq)) : lds2p(P + s * PV + k * 64 + physp(a0, 2 * kq));
+            f0[0] = fma(kp.phi[0][k], v.x, f0[0]);
+            f0[1] = fma(kp.phi[0][k], v.y, f0[1]);
+            f1[0] = fma(kp.phi[1][k], v.x, f1[0]);
+            f1[1] = fma(kp.phi[1][k], v.y, f1[1]);
+          }
+          const int fb = ydir ? 2 : 4;
+          const int o = (a0 * N + 2 * kq) * NVP + s;
+          FQ[fb * FACE + o] = f0[0];
+          FQ[(fb + 1) * FACE + o] = f1[0];
+          if (2 * kq + 1 < N) {
+            FQ[fb * FACE + o + NVP] = f0[1];
+            FQ[(fb + 1) * FACE + o + NVP] = f1[1];
+          }
         }
       }
     }
