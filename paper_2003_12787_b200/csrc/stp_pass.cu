@@ -97,6 +97,25 @@ __device__ __forceinline__ void ceo_row(int i, double (&r)[6]) {
   }
 }
 
+// e_in / e_coef of output quantity s (runtime index) in direction D, from 4-bit packed tables
+template <int D>
+__device__ __forceinline__ int e_in_rt(int s) {
+  constexpr unsigned long long v = [] {
+    unsigned long long r = 0;
+    for (int q = 0; q < NVE; ++q) r |= (unsigned long long)e_in(q, D) << (4 * q);
+    return r;
+  }();
+  return (int)((v >> (4 * s)) & 15);
+}
+template <int D>
+__device__ __forceinline__ int e_coef_rt(int s) {
+  constexpr unsigned long long v = [] {
+    unsigned long long r = 0;
+    for (int q = 0; q < NVE; ++q) r |= (unsigned long long)e_coef(q, D) << (4 * q);
+    return r;
+  }();
+  return (int)((v >> (4 * s)) & 15);
+}
 __device__ __forceinline__ double pick4(const double c[4], int i) {
   return i == 0 ? c[0] : i == 1 ? c[1] : i == 2 ? c[2] : c[3];
 }
@@ -925,53 +944,48 @@ stp_bip_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     }
   }
   };
+  // Faces: a warp takes three face nodes (d, a, b) at a time, one 9-lane group per node and one
+  // lane per quantity s (lanes 27..31 idle): lane (node, s) contracts the normal line of quantity
+  // s (both sides) and face_f[s] = F_d(face_q)_s = coef(s, d) face_q[in(s, d)] comes from lane
+  // in(s, d) of its group by shuffles, so every face entry is computed once and a warp stores 27
+  // consecutive doubles per array (coalesced, [f][a][b][s]).
   auto emit_faces = [&]() {
   if (a.face_q || a.face_f) {
     constexpr int FV = N * N * NVE;
-    for (int i = tid; i < 3 * N * N; i += G::THREADS) {
-      const int d = i / (N * N);
-      const int ab = i - d * N * N;
+    constexpr int T = 3 * N * N;  // face nodes (d, a, b)
+    const int lane = tid & 31, grp = lane / NVE, s = lane - grp * NVE;
+    const bool live = lane < 3 * NVE;
+    for (int it = warp; 3 * it < T; it += G::NW) {
+      const int node = 3 * it + (live ? grp : 0);
+      const bool ok = live && node < T;
+      const int nd = ok ? node : 0;
+      const int d = nd / (N * N), ab = nd - d * N * N;
       const int aa = ab / N, bb = ab - aa * N;
       const int start = d == 0 ? aa * G::PL + bb * G::RS : d == 1 ? aa * G::PL + bb : aa * G::RS + bb;
       const int stride = d == 0 ? 1 : d == 1 ? G::RS : G::PL;
-      double f0[NVE], f1[NVE];
+      const double* q0 = E + fld(live ? s : 0) * G::VS + start;
+      double x0 = 0.0, x1 = 0.0;
 #pragma unroll
-      for (int s = 0; s < NVE; ++s) {
-        const double* q0 = E + fld(s) * G::VS + start;
-        double x0 = 0.0, x1 = 0.0;
-#pragma unroll
-        for (int j = 0; j < N; ++j) {
-          const double x = q0[j * stride];
-          x0 = fma(kp.phi[0][j], x, x0);
-          x1 = fma(kp.phi[1][j], x, x1);
-        }
-        f0[s] = x0;
-        f1[s] = x1;
+      for (int j = 0; j < N; ++j) {
+        const double x = q0[j * stride];
+        x0 = fma(kp.phi[0][j], x, x0);
+        x1 = fma(kp.phi[1][j], x, x1);
       }
-      const long long fb = e * 6LL * FV + (2 * d) * FV + ab * NVE;
-      if (a.face_q) {
-#pragma unroll
-        for (int s = 0; s < NVE; ++s) {
-          __stcs(a.face_q + fb + s, f0[s]);
-          __stcs(a.face_q + fb + FV + s, f1[s]);
-        }
+      const long long fb = e * 6LL * FV + (2 * d) * FV + ab * NVE + s;
+      if (ok && a.face_q) {
+        __stcs(a.face_q + fb, x0);
+        __stcs(a.face_q + fb + FV, x1);
       }
       if (a.face_f) {
-#pragma unroll
-        for (int s = 0; s < NVE; ++s) {
-          double g0, g1;
-          if (d == 0) {
-            g0 = e_coef(s, 0) == 4 ? 0.0 : c4[e_coef(s, 0)] * f0[e_in(s, 0)];
-            g1 = e_coef(s, 0) == 4 ? 0.0 : c4[e_coef(s, 0)] * f1[e_in(s, 0)];
-          } else if (d == 1) {
-            g0 = e_coef(s, 1) == 4 ? 0.0 : c4[e_coef(s, 1)] * f0[e_in(s, 1)];
-            g1 = e_coef(s, 1) == 4 ? 0.0 : c4[e_coef(s, 1)] * f1[e_in(s, 1)];
-          } else {
-            g0 = e_coef(s, 2) == 4 ? 0.0 : c4[e_coef(s, 2)] * f0[e_in(s, 2)];
-            g1 = e_coef(s, 2) == 4 ? 0.0 : c4[e_coef(s, 2)] * f1[e_in(s, 2)];
-          }
-          __stcs(a.face_f + fb + s, g0);
-          __stcs(a.face_f + fb + FV + s, g1);
+        const int so = live ? s : 0;
+        const int ci = d == 0 ? e_coef_rt<0>(so) : d == 1 ? e_coef_rt<1>(so) : e_coef_rt<2>(so);
+        const int src = d == 0 ? e_in_rt<0>(so) : d == 1 ? e_in_rt<1>(so) : e_in_rt<2>(so);
+        const int sl2 = (live ? grp : 0) * NVE + src;
+        const double y0 = __shfl_sync(0xffffffffu, x0, sl2), y1 = __shfl_sync(0xffffffffu, x1, sl2);
+        if (ok) {
+          const double c = ci == 4 ? 0.0 : pick4(c4, ci);
+          __stcs(a.face_f + fb, c * y0);
+          __stcs(a.face_f + fb + FV, c * y1);
         }
       }
     }
