@@ -57,7 +57,13 @@ constexpr int NWARP = 8;  // default CTA: 8 warps, 3 CTAs/SM
 constexpr int PV = N8 * N8 * N8;    // doubles per quantity plane
 constexpr int FACE = N8 * N8 * NV;  // doubles per face array (576)
 // r and q, 73,728 B: 3 CTAs/SM, two barriers per CK step.
-constexpr int kSmem8 = 2 * NV * PV * 8;
+#ifndef D8_FPAD
+#define D8_FPAD 8
+#endif
+constexpr int kSmem8 = 2 * NV * (PV + 8) * 8;
+// staged face arrays [6][64][9], FACES doubles apart (FACE + 8: the y-face stores of lanes g = 0, 1
+// fall on different banks); they leave as one bulk copy per face
+constexpr int FACES = FACE + D8_FPAD;
 
 struct Params8 {
   double d[64];      // d[k*8+l] = phi_l'(x_k)
@@ -287,7 +293,7 @@ __device__ __forceinline__ void ck_normal(double* P, const double* Q, const doub
 // then 514 doubles apart, so that the 5 slot pairs of a node stored by neighbouring lanes fall on
 // different banks (a uniform shift per plane: the fragment and column accesses stay conflict free).
 template <bool AOS>
-constexpr int plane_stride() { return AOS ? PV + 2 : PV; }
+constexpr int plane_stride() { return AOS ? PV + 2 : PV + 8; }
 
 template <bool FUSED, bool AOS = false, bool VOLM = false>
 __global__ void __maxnreg__(80)
@@ -469,12 +475,12 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
       for (int k = 0; k < 4; ++k) {
         const int k3 = K0 + k;
         if (t == 0) {  // lane (g, 0) holds C[k2 = g][side 0, 1]
-          FQ[0 * FACE + (k3 * 8 + g) * NV + s] = xf[k][0];
-          FQ[1 * FACE + (k3 * 8 + g) * NV + s] = xf[k][1];
+          FQ[0 * FACES + (k3 * 8 + g) * NV + s] = xf[k][0];
+          FQ[1 * FACES + (k3 * 8 + g) * NV + s] = xf[k][1];
         }
         if (g < 2) {  // lane (side = g, t) holds C[side][k1 = 2t, 2t+1]
-          FQ[(2 + g) * FACE + (k3 * 8 + 2 * t) * NV + s] = yf[k][0];
-          FQ[(2 + g) * FACE + (k3 * 8 + 2 * t + 1) * NV + s] = yf[k][1];
+          FQ[(2 + g) * FACES + (k3 * 8 + 2 * t) * NV + s] = yf[k][0];
+          FQ[(2 + g) * FACES + (k3 * 8 + 2 * t + 1) * NV + s] = yf[k][1];
         }
       }
       if (h == 0) {  // z normal (faces 4, 5): (a, b) = (k2, k1), full column
@@ -489,8 +495,8 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
         }
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-          FQ[4 * FACE + (g * 8 + 2 * t + j) * NV + s] = z0[j];
-          FQ[5 * FACE + (g * 8 + 2 * t + j) * NV + s] = z1[j];
+          FQ[4 * FACES + (g * 8 + 2 * t + j) * NV + s] = z0[j];
+          FQ[5 * FACES + (g * 8 + 2 * t + j) * NV + s] = z1[j];
         }
       }
     }
@@ -533,10 +539,10 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     // (TMA bulk store, SASS UBLKCP) and its copy overlaps the face_f pass below.
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
-    if (tid == 0 && a.face_q) {
+    if (tid < 6 && a.face_q) {  // one bulk copy per face (the staged faces are FACES apart)
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
-                       a.face_q + e * (long long)(6 * FACE)),
-                   "r"((unsigned)__cvta_generic_to_shared(FQ)), "r"((unsigned)(6 * FACE * 8))
+                       a.face_q + e * (long long)(6 * FACE) + tid * FACE),
+                   "r"((unsigned)__cvta_generic_to_shared(FQ + tid * FACES)), "r"((unsigned)(FACE * 8))
                    : "memory");
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     }
@@ -548,8 +554,8 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
 #pragma unroll 1
       for (int i = tid; i < 6 * 64; i += THREADS8) {
         const int f = i >> 6, d = f >> 1;
-        const double* src = FQ + f * FACE + (i & 63) * NV;
-        double* dst = FF + f * FACE + (i & 63) * NV;
+        const double* src = FQ + f * FACES + (i & 63) * NV;
+        double* dst = FF + f * FACES + (i & 63) * NV;
         double w[NV];
 #pragma unroll
         for (int s = 0; s < NV; ++s) w[s] = src[s];
@@ -572,12 +578,11 @@ stp_dmma8_kernel(Params8 kp, BatchArgs a, unsigned int* status) {
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     __syncthreads();
     TM3(5);
-    if (tid == 0) {
-      const unsigned bytes = 6 * FACE * 8;
+    if (tid < 6) {
       if (a.face_f)
         asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(
-                         a.face_f + e * (long long)(6 * FACE)),
-                     "r"((unsigned)__cvta_generic_to_shared(FF)), "r"(bytes)
+                         a.face_f + e * (long long)(6 * FACE) + tid * FACE),
+                     "r"((unsigned)__cvta_generic_to_shared(FF + tid * FACES)), "r"((unsigned)(FACE * 8))
                      : "memory");
       asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
