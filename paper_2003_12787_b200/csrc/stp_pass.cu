@@ -503,7 +503,10 @@ struct GeoB {
   // (nDof 9 with three CTAs per SM -- 12 x 737 doubles -- measured 4 % slower: the kernel is
   // bound by the shared-memory pipe, not by latency)
   static constexpr int PL = N == 10 ? 106 : 89;
-  static constexpr int VS = N == 10 ? 1060 : 801;
+  // nDof 10: 1070 = 14 mod 16 (round 2; was 1060 = 4 mod 16) spreads the 9 quantities of a face node
+  // over 8 bank groups in the face groups' line loads (the CK passes touch one slot per warp and are
+  // unaffected): C4 +0.7 %
+  static constexpr int VS = N == 10 ? 1070 : 801;
   static constexpr bool X128 = N % 2 == 0;
   static constexpr int EB = 12 * VS;  // field slots: 0-5 stresses, 6-8 / 9-11 velocities
   static constexpr int LINES = N * N;
