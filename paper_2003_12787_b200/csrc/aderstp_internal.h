@@ -146,6 +146,9 @@ cudaError_t init_dmmap(const LaunchPlan& p);
 cudaError_t launch_dmmap(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 // stp_pass.cu: line-pass elastic kernel for every order (even/odd split D, uniform operands)
 bool pass_applicable(const LaunchPlan& p);
+// table PDEs (term tables) at nDof 9, 10 on line passes (stp_tlp); init_pass uploads its even/odd D
+bool tlp_applicable(const LaunchPlan& p, const BatchArgs& a);
+cudaError_t launch_tlp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 cudaError_t init_pass(const LaunchPlan& p);
 cudaError_t launch_pass(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 bool bip_selected(const LaunchPlan& p, const BatchArgs& a);  // launch_pass takes the bipartite kernel

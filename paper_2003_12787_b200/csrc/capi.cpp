@@ -423,7 +423,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   if (e == cudaSuccess) e = cudaMemPoolSetAttribute(p->pool, cudaMemPoolAttrReleaseThreshold, (void*)&keep);
   // D of nDof 8 in the constant bank: the elastic and the table-PDE tensor-core kernels
   if (e == cudaSuccess && kl.n == 8) e = aderstp::init_dmma8(kl);
-  if (e == cudaSuccess && aderstp::pass_applicable(kl)) e = aderstp::init_pass(kl);
+  if (e == cudaSuccess && (aderstp::pass_applicable(kl) || (kl.kind != ADERSTP_PDE_ELASTIC && kl.n >= 9)))
+    e = aderstp::init_pass(kl);  // the even/odd D of the line-pass kernels (stp_pass, stp_bip, stp_tlp)
   if (e == cudaSuccess && aderstp::dmmap_applicable(kl)) e = aderstp::init_dmmap(kl);
   if (e == cudaSuccess && kl.kind != ADERSTP_PDE_ELASTIC && kl.n >= 5 && kl.n <= 7) e = aderstp::init_dmmat(kl);
   if (e == cudaSuccess) lp.gen.pool = p->pool;

@@ -497,6 +497,7 @@ cudaError_t launch_stp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t str
   if (use_dmma8(p, a)) return launch_dmma8(p, a, stream);
   if (dmma8_table_applicable(p, a)) return launch_dmma8_table(p, a, stream);
   if (dmmat_applicable(p, a)) return launch_dmmat(p, a, stream);
+  if (tlp_applicable(p, a)) return launch_tlp(p, a, stream);
   if (a.u_next && use_dmmap(p, a)) return launch_dmmap(p, a, stream);
   if (a.u_next && use_bip(p, a)) return launch_pass(p, a, stream);
   if (a.u_next) return cudaErrorInvalidValue;  // the fused mode exists only where fused_supported()

@@ -1170,7 +1170,314 @@ cudaError_t launch_bip_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   return cudaGetLastError();
 }
 
+
+// =============================================================================================
+// Table PDEs at nDof 9, 10 (the user-LinearPde path; stp_tlp): any constant-coefficient system
+// with m <= 9 quantities given as term tables (build_terms: C_d = A_d + B_d, at most 4 nonzeros
+// per row), as line passes on the bipartite kernel's machinery (even/odd D from the constant
+// bank, the GeoB padding).  A CK step in Horner form, r <- c_o q + sum_d sum_k tc[s][d][k] D_d
+// r_(tr[s][d][k]) (proj/src/stp_splitck.cpp:46-70 with D_d F_d(p) + B_d D_d p = C_d D_d p for
+// constant coefficients), runs as three passes x, y, z over the lines of every target quantity:
+// thread (s, line) owns one line of target s, contracts the lines of its sources and writes
+// (pass x) or accumulates (y, z) the next iterate T; pass z adds c_o q from tensor memory
+// (thread-private columns: the thread keeps exactly its z-line of q).  The iterate pair (P, T)
+// is 2 m field slots of shared memory.  Outputs as in proj/src/predictor_common.cpp:311-341.
+template <int N>
+struct TlpParams {
+  double phi[2][N];
+  double cf[N];  // cf[o] = dt^(o+1)/(o+1)! (stp_splitck.cpp:45,64)
+  int m, q_stride, out_stride, check, n_terms;
+  signed char tr[kMaxM][3][kMaxTerms];
+  signed char fr[kMaxM][3][kMaxTerms];
+  double tc[kMaxM][3][kMaxTerms];
+  double fc[kMaxM][3][kMaxTerms];
+};
+constexpr int kTlpM = 9;  // quantities per element of this kernel
+
+template <int N, int MQ = kTlpM>  // MQ: quantities the instance is sized for (threads = MQ N^2)
+struct GeoT {
+  using B = GeoB<N>;
+  static constexpr int LINES = N * N;
+  static constexpr int THREADS = ((MQ * LINES + 31) / 32) * 32;
+  static constexpr int NW = THREADS / 32;
+  static constexpr int QC = 2 * N;  // TMEM columns per thread (its q z-line)
+  static constexpr int TCOLS = ((NW + 3) / 4) * QC <= 128 ? 128 : 256;
+};
+
+// acc += c D line, for one line (start, stride) of a field slot: eo_apply with the update folded in
+// (out[] never materialised: 2N registers fewer, the same operations and rounding as
+// acc = fma(c, out, acc) after eo_apply)
+template <int N>
+__device__ __forceinline__ void tlp_contract_acc(const double* src, int stride, double c, double (&acc)[N]) {
+  constexpr int H = N / 2;
+  constexpr int LA = H + (N % 2);
+  const int base = N * 80;
+  double e[H + 1], o[H];
+#pragma unroll
+  for (int l = 0; l < H; ++l) {
+    const double a0 = src[l * stride], a1 = src[(N - 1 - l) * stride];
+    e[l] = a0 + a1;
+    o[l] = a0 - a1;
+  }
+  if (N % 2) e[H] = src[H * stride];
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    double ra[6], rb[6];
+    ceo_row<LA>(base + k * 6, ra);
+    ceo_row<H>(base + 30 + k * 6, rb);
+    double al = 0.0, be = 0.0;
+#pragma unroll
+    for (int l = 0; l < LA; ++l) al = fma(ra[l], e[l], al);
+#pragma unroll
+    for (int l = 0; l < H; ++l) be = fma(rb[l], o[l], be);
+    acc[k] = fma(c, al + be, acc[k]);
+    acc[N - 1 - k] = fma(c, be - al, acc[N - 1 - k]);
+  }
+  if (N % 2) {
+    double rm[6];
+    ceo_row<H + 1>(base + 60, rm);
+    double mid = 0.0;
+#pragma unroll
+    for (int l = 0; l < H; ++l) mid = fma(rm[l], o[l], mid);
+    acc[H] = fma(c, fma(rm[H], e[H], mid), acc[H]);
+  }
+}
+
+template <int N, int MQ>
+__global__ void __launch_bounds__(GeoT<N, MQ>::THREADS, 1)
+stp_tlp_kernel(TlpParams<N> kp, BatchArgs a, unsigned int* status) {
+  using B = GeoB<N>;
+  using G = GeoT<N, MQ>;
+  extern __shared__ __align__(16) double smt[];
+  __shared__ uint32_t tmem_base_s;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int m = kp.m;
+  const long long e = blockIdx.x;
+  constexpr int N3 = N * N * N;
+  const int s = tid / G::LINES, line = tid - s * G::LINES;
+  const bool active = s < m;
+  const int sa = active ? s : 0;
+  const int la = line / N, lb = line - la * N;
+  double* bufs[2] = {smt, smt + m * B::VS};
+  unsigned int flags = 0;
+
+  if (warp == 0) tm_alloc<G::TCOLS>(&tmem_base_s);
+  tm_fence_before();
+  __syncthreads();
+  tm_fence_after();
+  const uint32_t ta = tmem_base_s + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * G::QC);
+
+  // ---- stage: thread (s, k2 = la, k1 = lb) loads the z-line of q_s: c_(N-1) q -> P, q -> TMEM
+  {
+    double qz[N];
+    const int qs = kp.q_stride;
+    const double* src = a.q + e * (long long)(N3 * qs) + (la * qs + sa) * N + lb;
+#pragma unroll
+    for (int l = 0; l < N; ++l) qz[l] = active ? __ldcs(src + (long long)l * N * qs * N) : 0.0;
+    if (kp.check && active) {
+#pragma unroll
+      for (int l = 0; l < N; ++l)
+        if (!isfinite(qz[l])) flags |= 1u;
+    }
+    double* pz = bufs[0] + sa * B::VS + la * B::RS + lb;
+    const double c0 = kp.cf[N - 1];
+    if (active) {
+#pragma unroll
+      for (int l = 0; l < N; ++l) pz[l * B::PL] = c0 * qz[l];
+    }
+    tm_store_q<N>(ta, 0, qz);
+    tm_wait_st();
+  }
+  __syncthreads();
+
+  // ---- CK recursion, Horner form: step i reads bufs[i & 1], writes bufs[(i + 1) & 1] --------
+  const int nterm = kp.n_terms;
+  int i = 0;
+#pragma unroll 1
+  for (int o = N - 2; o >= 0; --o, ++i) {
+    const double* P = bufs[i & 1];
+    double* T = bufs[(i + 1) & 1];
+    // pass x: line (k3 = la, k2 = lb) of target s, written
+    if (active) {
+      double acc[N];
+#pragma unroll
+      for (int l = 0; l < N; ++l) acc[l] = 0.0;
+      const int st = la * B::PL + lb * B::RS;
+#pragma unroll 1
+      for (int k = 0; k < nterm; ++k) {
+        const double c = kp.tc[s][0][k];
+        if (c == 0.0) continue;
+        tlp_contract_acc<N>(P + kp.tr[s][0][k] * B::VS + st, 1, c, acc);
+      }
+#pragma unroll
+      for (int l = 0; l < N; ++l) T[s * B::VS + st + l] = acc[l];
+    }
+    __syncthreads();
+    // pass y: line (k3 = la, k1 = lb), accumulated
+    if (active) {
+      const int st = la * B::PL + lb;
+      double acc[N];
+      double* tl = T + s * B::VS + st;
+#pragma unroll
+      for (int l = 0; l < N; ++l) acc[l] = tl[l * B::RS];
+#pragma unroll 1
+      for (int k = 0; k < nterm; ++k) {
+        const double c = kp.tc[s][1][k];
+        if (c == 0.0) continue;
+        tlp_contract_acc<N>(P + kp.tr[s][1][k] * B::VS + st, B::RS, c, acc);
+      }
+#pragma unroll
+      for (int l = 0; l < N; ++l) tl[l * B::RS] = acc[l];
+    }
+    __syncthreads();
+    // pass z: line (k2 = la, k1 = lb), accumulated, plus the Horner term c_o q (TMEM, all lanes)
+    {
+      const int st = la * B::RS + lb;
+      double acc[N];
+      double* tl = T + sa * B::VS + st;
+      if (active) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) acc[l] = tl[l * B::PL];
+#pragma unroll 1
+        for (int k = 0; k < nterm; ++k) {
+          const double c = kp.tc[s][2][k];
+          if (c == 0.0) continue;
+          tlp_contract_acc<N>(P + kp.tr[s][2][k] * B::VS + st, B::PL, c, acc);
+        }
+      }
+      double q[N];
+      tm_load_q<N>(ta, 0, q);
+      const double co = kp.cf[o];
+      if (active) {
+#pragma unroll
+        for (int l = 0; l < N; ++l) tl[l * B::PL] = fma(co, q[l], acc[l]);
+      }
+    }
+    __syncthreads();
+  }
+  tm_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tm_fence_after();
+    tm_dealloc<G::TCOLS>(tmem_base_s);
+  }
+
+  // ---- epilogue: qavg = the last iterate; favg_d = A_d qavg; faces (predictor_common.cpp:311-341)
+  const double* Q = bufs[i & 1];
+  const int os = kp.out_stride;
+  auto qv = [&](int q, int k3, int k2, int k1) { return Q[q * B::VS + k3 * B::PL + k2 * B::RS + k1]; };
+  if (a.qavg) {
+    double* out = a.qavg + e * (long long)(N3 * os);
+    for (int j = tid; j < N3 * os; j += G::THREADS) {
+      const int k1 = j % N, r = j / N, so = r % os, k32 = r / os;
+      __stcs(out + j, so < m ? qv(so, k32 / N, k32 % N, k1) : 0.0);
+    }
+  }
+  if (a.favg) {
+    double* out = a.favg + e * (long long)(3 * N3 * os);
+    for (int j = tid; j < 3 * N3 * os; j += G::THREADS) {
+      const int d = j / (N3 * os), jj = j - d * N3 * os;
+      const int k1 = jj % N, r = jj / N, so = r % os, k32 = r / os;
+      double v = 0.0;
+      if (so < m)
+        for (int k = 0; k < nterm; ++k) {
+          const double c = kp.fc[so][d][k];
+          if (c != 0.0) v = fma(c, qv(kp.fr[so][d][k], k32 / N, k32 % N, k1), v);
+        }
+      __stcs(out + j, v);
+    }
+  }
+  if (a.face_q || a.face_f) {
+    const int FV = N * N * m;
+    for (int j = tid; j < 6 * FV; j += G::THREADS) {
+      const int f = j / FV, rem = j - f * FV, so = rem % m, ab = rem / m;
+      const int d = f >> 1, side = f & 1, aa = ab / N, bb = ab - aa * N;
+      const int st = d == 0 ? aa * B::PL + bb * B::RS : d == 1 ? aa * B::PL + bb : aa * B::RS + bb;
+      const int stride = d == 0 ? 1 : d == 1 ? B::RS : B::PL;
+      auto extrap = [&](int q) {
+        const double* l0 = Q + q * B::VS + st;
+        double x = 0.0;
+#pragma unroll
+        for (int l = 0; l < N; ++l) x = fma(kp.phi[side][l], l0[l * stride], x);
+        return x;
+      };
+      if (a.face_q) __stcs(a.face_q + e * 6ll * FV + j, extrap(so));
+      if (a.face_f) {
+        double v = 0.0;
+        for (int k = 0; k < nterm; ++k) {
+          const double c = kp.fc[so][d][k];
+          if (c != 0.0) v = fma(c, extrap(kp.fr[so][d][k]), v);
+        }
+        __stcs(a.face_f + e * 6ll * FV + j, v);
+      }
+    }
+  }
+  if (kp.check && flags) atomicOr(status, flags);
+}
+
+template <int N, int MQ>
+cudaError_t launch_tlp_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
+  using B = GeoB<N>;
+  using G = GeoT<N, MQ>;
+  TlpParams<N> kp;
+  for (int j = 0; j < N; ++j) {
+    kp.phi[0][j] = p.basis.face_left[j];
+    kp.phi[1][j] = p.basis.face_right[j];
+  }
+  double c = a.dt;  // the reference's operation sequence (stp_splitck.cpp:45,64)
+  kp.cf[0] = c;
+  for (int o = 1; o < N; ++o) {
+    c *= a.dt / (o + 1);
+    kp.cf[o] = c;
+  }
+  kp.m = p.m;
+  kp.q_stride = p.q_stride;
+  kp.out_stride = p.out_stride;
+  kp.check = p.check;
+  kp.n_terms = p.n_terms;
+  for (int q = 0; q < kMaxM; ++q)
+    for (int d = 0; d < 3; ++d)
+      for (int k = 0; k < kMaxTerms; ++k) {
+        kp.tr[q][d][k] = p.tr[q][d][k];
+        kp.fr[q][d][k] = p.fr[q][d][k];
+        kp.tc[q][d][k] = p.tc[q][d][k];
+        kp.fc[q][d][k] = p.fc[q][d][k];
+      }
+  const int smem = 2 * p.m * B::VS * 8;
+  auto kern = stp_tlp_kernel<N, MQ>;
+  cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * MQ * B::VS * 8);
+  if (err == cudaSuccess)
+    err = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+  if (err != cudaSuccess) return err;
+  if (a.n_elem == 0) return cudaSuccess;
+  if (a.n_elem > 0x7fffffffLL) return cudaErrorInvalidValue;
+  kern<<<(unsigned)a.n_elem, G::THREADS, smem, stream>>>(kp, a, p.d_status);
+  return cudaGetLastError();
+}
 }  // namespace
+
+// table PDEs at nDof 9, 10 (stp_tlp): term tables, no point source, compact or padded AoSoA
+bool tlp_applicable(const LaunchPlan& p, const BatchArgs& a) {
+  return (p.n == 9 || p.n == 10) && p.kind != ADERSTP_PDE_ELASTIC && p.kind != ADERSTP_PDE_ELASTIC_SOURCE &&
+         p.src_comp < 0 && p.gen.t_ptr == nullptr && p.m >= 1 && p.m <= kTlpM &&
+         p.layout == ADERSTP_LAYOUT_AOSOA && p.out_stride >= p.m && p.q_stride >= p.m && p.q_stride <= 64 &&
+         p.n_terms <= kMaxTerms && !p.force_generic && !a.u_next;
+}
+
+// m <= 6 / m <= 8 / m = 9 instances: fewer threads leave more registers per thread (nDof 10:
+// 608 / 800 / 928 threads)
+cudaError_t launch_tlp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
+  const int mq = p.m <= 6 ? 6 : p.m <= 8 ? 8 : 9;
+  switch (p.n * 16 + mq) {
+    case 9 * 16 + 6: return launch_tlp_n<9, 6>(p, a, stream);
+    case 9 * 16 + 8: return launch_tlp_n<9, 8>(p, a, stream);
+    case 9 * 16 + 9: return launch_tlp_n<9, 9>(p, a, stream);
+    case 10 * 16 + 6: return launch_tlp_n<10, 6>(p, a, stream);
+    case 10 * 16 + 8: return launch_tlp_n<10, 8>(p, a, stream);
+    case 10 * 16 + 9: return launch_tlp_n<10, 9>(p, a, stream);
+  }
+  return cudaErrorInvalidValue;
+}
 
 bool pass_applicable(const LaunchPlan& p) {
   return p.n >= 2 && p.n <= 10 && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&

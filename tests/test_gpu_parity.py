@@ -416,11 +416,12 @@ def test_reference_layout_checks_and_edges(stp, oracle, n):
         assert O.per_element_rel_diff(b.cpu().numpy().reshape(E, -1), a.cpu().numpy().reshape(E, -1)) <= TOL
 
 
-@pytest.mark.parametrize("n", [4, 5, 6, 7, 8])
+@pytest.mark.parametrize("n", [4, 5, 6, 7, 8, 9, 10])
 @pytest.mark.parametrize("case", ["advection_m3", "ncp_advection_m2", "demo_m6", "probed_m5", "probed_m8", "probed_m9"])
 def test_table_pdes_on_tensor_cores(stp, oracle, monkeypatch, case, n):
-    """Table PDEs (the user-LinearPde path) run on the tensor cores: stp_dmma8_table at nDof 8,
-    stp_dmmat (zero-padded tiles) at nDof 4..7; the reference's PDEs against the oracle, random
+    """Table PDEs (the user-LinearPde path) on their tuned kernels: stp_dmma8_table at nDof 8,
+    stp_dmmat (zero-padded tiles) at nDof 5..7, the line-pass table kernel stp_tlp at nDof 9, 10
+    (nDof 4: the generic kernel); the reference's PDEs against the oracle, random
     probed systems (flux + ncp matrices) against the unmodified reference's predict() on a
     MatrixPde with the same matrices; all against the generic table kernel on the same inputs."""
     S = stp
