@@ -466,12 +466,14 @@ def test_table_pdes_on_tensor_cores(stp, oracle, monkeypatch, case, n):
         assert O.per_element_rel_diff(y.cpu().numpy().reshape(E, -1), x.cpu().numpy().reshape(E, -1)) <= TOL
 
 
+@pytest.mark.parametrize("n", [8, 9, 10])
 @pytest.mark.parametrize("case", ["advection_m3", "demo_m6"])
-def test_table_pdes_reference_layout_nDof8(stp, oracle, case):
+def test_table_pdes_reference_layout_nDof8(stp, oracle, case, n):
     """The reference layout (AoS, m_pad = 8 for m <= 8, layout.cpp:9-21) of a table PDE at nDof 8
-    goes through the device transposes to stp_dmma8_table; it agrees with the oracle."""
+    goes through the device transposes to stp_dmma8_table (nDof 9, 10: stp_tlp, the padded AoSoA
+    staging with out_stride 8); it agrees with the oracle and the padding slots stay zero."""
     S = stp
-    n, E = 8, 5
+    E = 5
     m, pde, kind, args = ((3, S.advection_pde((1.0, 0.5, 0.25), 3), O.PDE_ADVECTION, [1.0, 0.5, 0.25])
                           if case == "advection_m3" else (6, S.paper_demo_pde(), O.PDE_DEMO, []))
     rng = np.random.default_rng(_zlib.crc32(case.encode()) + 1)
