@@ -1258,7 +1258,9 @@ stp_tlp_kernel(TlpParams<N> kp, BatchArgs a, unsigned int* status) {
   const bool active = s < m;
   const int sa = active ? s : 0;
   const int la = line / N, lb = line - la * N;
-  double* bufs[2] = {smt, smt + m * B::VS};
+  // the iterate pair: step i reads smt + (i & 1) * mvs and writes the other half (computed, not
+  // indexed: a runtime-indexed pointer array turns every access into a generic load)
+  const int mvs = m * B::VS;
   unsigned int flags = 0;
 
   if (warp == 0) tm_alloc<G::TCOLS>(&tmem_base_s);
@@ -1279,7 +1281,7 @@ stp_tlp_kernel(TlpParams<N> kp, BatchArgs a, unsigned int* status) {
       for (int l = 0; l < N; ++l)
         if (!isfinite(qz[l])) flags |= 1u;
     }
-    double* pz = bufs[0] + sa * B::VS + la * B::RS + lb;
+    double* pz = smt + sa * B::VS + la * B::RS + lb;
     const double c0 = kp.cf[N - 1];
     if (active) {
 #pragma unroll
@@ -1290,13 +1292,13 @@ stp_tlp_kernel(TlpParams<N> kp, BatchArgs a, unsigned int* status) {
   }
   __syncthreads();
 
-  // ---- CK recursion, Horner form: step i reads bufs[i & 1], writes bufs[(i + 1) & 1] --------
+  // ---- CK recursion, Horner form: step i reads half i & 1 of the pair, writes the other -------
   const int nterm = kp.n_terms;
   int i = 0;
 #pragma unroll 1
   for (int o = N - 2; o >= 0; --o, ++i) {
-    const double* P = bufs[i & 1];
-    double* T = bufs[(i + 1) & 1];
+    const double* P = smt + (i & 1) * mvs;
+    double* T = smt + ((i + 1) & 1) * mvs;
     // pass x: line (k3 = la, k2 = lb) of target s, written
     if (active) {
       double acc[N];
@@ -1363,21 +1365,26 @@ stp_tlp_kernel(TlpParams<N> kp, BatchArgs a, unsigned int* status) {
   }
 
   // ---- epilogue: qavg = the last iterate; favg_d = A_d qavg; faces (predictor_common.cpp:311-341)
-  const double* Q = bufs[i & 1];
+  const double* Q = smt + (i & 1) * mvs;
   const int os = kp.out_stride;
+  // x / os and x / m by a float reciprocal: (x + 0.5) / d is at least 0.5 / d <= 1/128 away from
+  // an integer, x < 2^15 and the float product is within 2^-23 relative: it truncates to the
+  // exact quotient
+  const float inv_os = 1.0f / (float)os, inv_m = 1.0f / (float)m;
+  auto qdiv = [](int x, float inv) { return (int)(((float)x + 0.5f) * inv); };
   auto qv = [&](int q, int k3, int k2, int k1) { return Q[q * B::VS + k3 * B::PL + k2 * B::RS + k1]; };
   if (a.qavg) {
     double* out = a.qavg + e * (long long)(N3 * os);
     for (int j = tid; j < N3 * os; j += G::THREADS) {
-      const int k1 = j % N, r = j / N, so = r % os, k32 = r / os;
+      const int r = j / N, k1 = j - r * N, k32 = qdiv(r, inv_os), so = r - k32 * os;
       __stcs(out + j, so < m ? qv(so, k32 / N, k32 % N, k1) : 0.0);
     }
   }
   if (a.favg) {
     double* out = a.favg + e * (long long)(3 * N3 * os);
     for (int j = tid; j < 3 * N3 * os; j += G::THREADS) {
-      const int d = j / (N3 * os), jj = j - d * N3 * os;
-      const int k1 = jj % N, r = jj / N, so = r % os, k32 = r / os;
+      const int r0 = j / N, k1 = j - r0 * N, dk = qdiv(r0, inv_os), so = r0 - dk * os;
+      const int d = dk / (N * N), k32 = dk - d * N * N;
       double v = 0.0;
       if (so < m)
         for (int k = 0; k < nterm; ++k) {
@@ -1390,7 +1397,7 @@ stp_tlp_kernel(TlpParams<N> kp, BatchArgs a, unsigned int* status) {
   if (a.face_q || a.face_f) {
     const int FV = N * N * m;
     for (int j = tid; j < 6 * FV; j += G::THREADS) {
-      const int f = j / FV, rem = j - f * FV, so = rem % m, ab = rem / m;
+      const int fab = qdiv(j, inv_m), so = j - fab * m, f = fab / (N * N), ab = fab - f * N * N;
       const int d = f >> 1, side = f & 1, aa = ab / N, bb = ab - aa * N;
       const int st = d == 0 ? aa * B::PL + bb * B::RS : d == 1 ? aa * B::PL + bb : aa * B::RS + bb;
       const int stride = d == 0 ? 1 : d == 1 ? B::RS : B::PL;
