@@ -63,7 +63,10 @@ __device__ __forceinline__ long long lidx(int layout, int stride, int s, int k3,
                                         : (((long long)k3 * N + k2) * N + k1) * stride + s;
 }
 
-template <int N>
+// GS: the iterate pair in the plan's global scratch (large m N^3) instead of shared memory -- a
+// compile-time choice, so that the shared-memory instance addresses it with LDS / STS (a pointer
+// that may point to either space makes every access a generic LD / ST)
+template <int N, bool GS>
 __global__ void __launch_bounds__(gen_threads<N>()) stp_general_kernel(GenParams kp, BatchArgs a, unsigned int* status) {
   constexpr int kGenThreads = gen_threads<N>();
   extern __shared__ __align__(16) double smg[];
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(gen_threads<N>()) stp_general_kernel(GenParams
   // faces are staged in the dead iterate buffer instead (m N^3 >= 6 m N^2)
   double* W = smg + N2 + (N2 & 1);
   double* P;                                // p_(o-1)
-  if (kp.scratch) {
+  if constexpr (GS) {
     P = kp.scratch + e * (2ll * m * N3);
   } else {
     P = W + (N >= 6 ? 3 : 6) * m * N2;
@@ -86,16 +89,17 @@ __global__ void __launch_bounds__(gen_threads<N>()) stp_general_kernel(GenParams
   for (int i = tid; i < N2; i += kGenThreads) Ds[i] = kp.d[i];
   // the CK step's coefficient rows, staged once per element next to the buffers when they fit
   // (warp-uniform broadcast reads instead of dependent L1 round trips)
-  const double* tv = kp.t_val;
-  const int* to = kp.t_col;
-  const int* tp = kp.t_ptr;
+  double* csr_v = nullptr;  // the CSR rows staged in shared memory (csr_smem)
+  int* csr_c = nullptr;
+  int* csr_p = nullptr;
   double* Cd = nullptr;  // dense C staged in shared memory (dense mode)
   if (kp.dense) {
-    Cd = (kp.scratch ? W + (N >= 6 ? 3 : 6) * m * N2 : R + (long long)m * N3);
-    Cd = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(Cd) + 15) & ~uintptr_t(15));  // LDS.128
+    Cd = (GS ? W + (N >= 6 ? 3 : 6) * m * N2 : R + (long long)m * N3);
+    Cd += (reinterpret_cast<uintptr_t>(Cd) & 15) ? 1 : 0;  // 16-byte aligned for LDS.128 (pointer arithmetic
+                                                           // keeps the shared address space)
     for (int i = tid; i < 3 * m * kp.m_pad; i += kGenThreads) Cd[i] = kp.t_dense[i];
   } else if (kp.csr_smem) {
-    double* sv = (kp.scratch ? W + (N >= 6 ? 3 : 6) * m * N2 : R + (long long)m * N3);
+    double* sv = (GS ? W + (N >= 6 ? 3 : 6) * m * N2 : R + (long long)m * N3);
     int* so = reinterpret_cast<int*>(sv + kp.t_nnz);
     int* sp = so + kp.t_nnz;
     for (int i = tid; i < kp.t_nnz; i += kGenThreads) {
@@ -103,9 +107,9 @@ __global__ void __launch_bounds__(gen_threads<N>()) stp_general_kernel(GenParams
       so[i] = kp.t_col[i];
     }
     for (int i = tid; i <= 3 * m; i += kGenThreads) sp[i] = kp.t_ptr[i];
-    tv = sv;
-    to = so;
-    tp = sp;
+    csr_v = sv;
+    csr_c = so;
+    csr_p = sp;
   }
 
   // ---- stage p_0 = q (canonical [s][k3][k2][k1]) and Qbar = dt q into the output --------
@@ -234,18 +238,26 @@ __global__ void __launch_bounds__(gen_threads<N>()) stp_general_kernel(GenParams
         const int s = i / N2, node = i - s * N2;
         const int k2 = node / N, k1 = node - k2 * N;
         double t0 = 0.0, t1 = 0.0;
+        // the CSR rows from shared memory (staged) or from the global tables: two code paths, so
+        // that each addresses its own space (LDS / LDG instead of generic loads)
+        auto rows = [&](const double* rv, const int* rc, const int* rp) {
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          const double* base = d == 0 ? Wx + node : d == 1 ? Wy + node : Wz + node;
-          const int js = d == 2 ? N3 : N2;
-          const int end = tp[3 * s + d + 1];
-          int k = tp[3 * s + d];
-          for (; k + 1 < end; k += 2) {
-            t0 = fma(tv[k], base[to[k] * js], t0);
-            t1 = fma(tv[k + 1], base[to[k + 1] * js], t1);
+          for (int d = 0; d < 3; ++d) {
+            const double* base = d == 0 ? Wx + node : d == 1 ? Wy + node : Wz + node;
+            const int js = d == 2 ? N3 : N2;
+            const int end = rp[3 * s + d + 1];
+            int k = rp[3 * s + d];
+            for (; k + 1 < end; k += 2) {
+              t0 = fma(rv[k], base[rc[k] * js], t0);
+              t1 = fma(rv[k + 1], base[rc[k + 1] * js], t1);
+            }
+            if (k < end) t0 = fma(rv[k], base[rc[k] * js], t0);
           }
-          if (k < end) t0 = fma(tv[k], base[to[k] * js], t0);
-        }
+        };
+        if (kp.csr_smem)
+          rows(csr_v, csr_c, csr_p);
+        else
+          rows(kp.t_val, kp.t_col, kp.t_ptr);
         double t = (t0 + t1) * kp.scale;
         if (kp.vol_mode) {  // corrector: u += V(qavg)
           double* u = a.u_next + e * (long long)N3 * kp.q_stride + lidx<N>(kp.layout, kp.q_stride, s, k3, k2, k1);
@@ -390,11 +402,12 @@ cudaError_t launch_general_n(const LaunchPlan& p, const BatchArgs& a, cudaStream
   kp.csr_smem = !kp.dense && smem + csr <= (size_t)max_smem;
   if (kp.dense) smem += dense;
   else if (kp.csr_smem) smem += csr;
-  err = cudaFuncSetAttribute(stp_general_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  err = cudaFuncSetAttribute(scratch ? stp_general_kernel<N, true> : stp_general_kernel<N, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (err != cudaSuccess) return err;
   if (!scratch) {
     kp.scratch = nullptr;
-    stp_general_kernel<N><<<(unsigned)a.n_elem, gen_threads<N>(), smem, stream>>>(kp, a, p.d_status);
+    stp_general_kernel<N, false><<<(unsigned)a.n_elem, gen_threads<N>(), smem, stream>>>(kp, a, p.d_status);
     return cudaGetLastError();
   }
   // iterate pair in global scratch from the plan's pool, in chunks of <= kGenScratchBytes
@@ -420,7 +433,7 @@ cudaError_t launch_general_n(const LaunchPlan& p, const BatchArgs& a, cudaStream
     if (a.u_next) b.u_next = a.u_next + e0 * qin;
     if (a.vol_r) b.vol_r = a.vol_r + e0 * qout;
     b.n_elem = c;
-    stp_general_kernel<N><<<(unsigned)c, gen_threads<N>(), smem, stream>>>(kp, b, p.d_status);
+    stp_general_kernel<N, true><<<(unsigned)c, gen_threads<N>(), smem, stream>>>(kp, b, p.d_status);
     err = cudaGetLastError();
   }
   cudaFreeAsync(buf, stream);
