@@ -334,11 +334,12 @@ def measure_reference_layout(S, cfg, steps, warmup):
             "path": "stp_dmma8<AOS>: planes staged from the node rows, qavg/favg written as node rows"}
 
 
-def measure_table_pde(S, steps, warmup):
-    """The user-LinearPde path on the tensor cores: the reference's advection system with m = 8
-    quantities (proj/src/pde.cpp:61-85) at nDof 8, 65,536 elements, device-resident."""
+def measure_table_pde(S, steps, warmup, n=8, E=65536):
+    """The user-LinearPde path: the reference's advection system with m = 8 quantities
+    (proj/src/pde.cpp:61-85), device-resident -- at nDof 8 on the tensor cores (stp_dmma8_table),
+    at nDof 9 / 10 on the line-pass table kernel (stp_tlp)."""
     import torch
-    n, m, E = 8, 8, 65536
+    m = 8
     pde = S.advection_pde((1.0, 0.5, 0.25), m)
     g = torch.Generator(device="cuda").manual_seed(SEED)
     q = torch.rand(E, n ** 3 * m, dtype=torch.float64, device="cuda", generator=g) * 2.0 - 1.0
@@ -358,8 +359,9 @@ def measure_table_pde(S, steps, warmup):
     plan.status()
     ms = ev0.elapsed_time(ev1) / steps
     del q, out
-    return {"workload": "advection PDE, m = 8 quantities, nDof 8, 65,536 elements, Q~U[-1,1] (user LinearPde path)",
-            "elements_per_s": E / (ms * 1e-3), "ms_per_step": ms, "kernel": "stp_dmma8_table"}
+    return {"workload": f"advection PDE, m = 8 quantities, nDof {n}, {E:,} elements, Q~U[-1,1] (user LinearPde path)",
+            "elements_per_s": E / (ms * 1e-3), "ms_per_step": ms,
+            "kernel": "stp_dmma8_table" if n == 8 else "stp_tlp" if n >= 9 else "stp_dmmat / stp_kernel"}
 
 
 def measure_general_pde(S, steps, warmup, m=21, n=8, E=16384):
@@ -794,6 +796,7 @@ def main():
         others["timestep_n8"] = measure_timestep(S, 8, 50, max(5, args.steps // 4), 3)
         others["c3_reference_layout"] = measure_reference_layout(S, CONFIGS["c3"], max(5, args.steps // 4), 3)
         others["table_pde_advection_m8_n8"] = measure_table_pde(S, max(5, args.steps // 4), 3)
+        others["table_pde_advection_m8_n10"] = measure_table_pde(S, max(5, args.steps // 4), 3, n=10, E=16384)
         others["general_pde_dense_m21_n8"] = measure_general_pde(S, max(3, args.steps // 8), 3)
 
     cpu = None
