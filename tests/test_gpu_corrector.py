@@ -132,7 +132,8 @@ def test_corrector_elastic_per_face_wavespeed(S, oracle):
 # ---- the time loop ---------------------------------------------------------------------------
 @pytest.mark.parametrize("case,n,e", [("elastic", 4, 2), ("elastic", 5, 2), ("elastic", 6, 2), ("elastic", 7, 2),
                                       ("elastic", 8, 2), ("elastic", 9, 2), ("elastic", 10, 2), ("elastic", 8, 3),
-                                      ("advection", 5, 3), ("demo", 3, 2)])
+                                      ("advection", 5, 3), ("demo", 3, 2), ("advection", 9, 2), ("demo", 10, 2),
+                                      ("ncp_advection", 10, 2)])
 def test_run_simulation_matches_reference(S, oracle, reference, case, n, e):
     pde, kind, m, args, par = pde_cases(S)[case]
     init = lambda x, y, z, t, s: np.sin(2 * np.pi * x + s) + 0.3 * np.cos(2 * np.pi * (y - z) + 0.2 * s)  # noqa: E731
