@@ -1395,27 +1395,47 @@ stp_tlp_kernel(TlpParams<N> kp, BatchArgs a, unsigned int* status) {
     }
   }
   if (a.face_q || a.face_f) {
+    // faces by m-lane groups (32 / m face nodes per warp, one lane per quantity): lane (node, s)
+    // contracts the normal line of quantity s for both sides; face_f[s] = sum_k fc[s][d][k]
+    // face_q[fr[s][d][k]] comes from the group's lanes by shuffles; a warp stores consecutive
+    // entries of [f][a][b][s]
     const int FV = N * N * m;
-    for (int j = tid; j < 6 * FV; j += G::THREADS) {
-      const int fab = qdiv(j, inv_m), so = j - fab * m, f = fab / (N * N), ab = fab - f * N * N;
-      const int d = f >> 1, side = f & 1, aa = ab / N, bb = ab - aa * N;
+    const int gpw = 32 / m;  // groups per warp
+    const int lane = tid & 31, grp = lane / m, sq = lane - grp * m;
+    const bool live = grp < gpw;
+    for (int it = warp; it * gpw < 3 * N * N; it += G::NW) {
+      const int node = it * gpw + (live ? grp : 0);
+      const bool ok = live && node < 3 * N * N;
+      const int nd = ok ? node : 0, d = nd / (N * N), ab = nd - d * N * N;
+      const int aa = ab / N, bb = ab - aa * N;
       const int st = d == 0 ? aa * B::PL + bb * B::RS : d == 1 ? aa * B::PL + bb : aa * B::RS + bb;
       const int stride = d == 0 ? 1 : d == 1 ? B::RS : B::PL;
-      auto extrap = [&](int q) {
-        const double* l0 = Q + q * B::VS + st;
-        double x = 0.0;
+      const double* l0 = Q + (live ? sq : 0) * B::VS + st;
+      double x0 = 0.0, x1 = 0.0;
 #pragma unroll
-        for (int l = 0; l < N; ++l) x = fma(kp.phi[side][l], l0[l * stride], x);
-        return x;
-      };
-      if (a.face_q) __stcs(a.face_q + e * 6ll * FV + j, extrap(so));
+      for (int l = 0; l < N; ++l) {
+        const double v = l0[l * stride];
+        x0 = fma(kp.phi[0][l], v, x0);
+        x1 = fma(kp.phi[1][l], v, x1);
+      }
+      const long long fb = e * 6ll * FV + (2 * d) * FV + ab * m + sq;
+      if (ok && a.face_q) {
+        __stcs(a.face_q + fb, x0);
+        __stcs(a.face_q + fb + FV, x1);
+      }
       if (a.face_f) {
-        double v = 0.0;
-        for (int k = 0; k < nterm; ++k) {
-          const double c = kp.fc[so][d][k];
-          if (c != 0.0) v = fma(c, extrap(kp.fr[so][d][k]), v);
+        double g0 = 0.0, g1 = 0.0;
+        for (int k = 0; k < nterm; ++k) {  // warp-uniform trip count: every lane shuffles
+          const double c = ok ? kp.fc[sq][d][k] : 0.0;
+          const int src = (live ? grp : 0) * m + (ok ? kp.fr[sq][d][k] : 0);
+          const double y0 = __shfl_sync(0xffffffffu, x0, src), y1 = __shfl_sync(0xffffffffu, x1, src);
+          g0 = fma(c, y0, g0);
+          g1 = fma(c, y1, g1);
         }
-        __stcs(a.face_f + e * 6ll * FV + j, v);
+        if (ok) {
+          __stcs(a.face_f + fb, g0);
+          __stcs(a.face_f + fb + FV, g1);
+        }
       }
     }
   }
