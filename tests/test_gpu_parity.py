@@ -487,3 +487,49 @@ def test_table_pdes_reference_layout_nDof8(stp, oracle, case, n):
     worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOS, 8, m=m)
     assert max(worst.values()) <= TOL, worst
     assert not np.any(out.qavg.cpu().numpy().reshape(E, n ** 3, 8)[:, :, m:])
+
+
+@pytest.mark.parametrize("n", [9, 10])
+def test_table_pde_line_pass_edges(stp, oracle, monkeypatch, n):
+    """stp_tlp (table PDEs at nDof 9, 10) on padded AoSoA strides (q_stride, out_stride > m: the
+    output padding slots are written as zeros), a single-quantity system (32 face groups per warp),
+    an empty batch and a non-finite input, against the generic table kernel and the oracle."""
+    S = stp
+    E = 3
+    rng = np.random.default_rng(11 + n)
+    for m, pde, kind, args, qs, os_ in ((3, S.advection_pde((1.0, 0.5, 0.25), 3), O.PDE_ADVECTION, [1.0, 0.5, 0.25], 5, 4),
+                                        (1, S.advection_pde((0.3, -0.7, 0.2), 1), O.PDE_ADVECTION, [0.3, -0.7, 0.2], 1, 1)):
+        qn = rng.uniform(-1, 1, (E, n ** 3 * m))
+        q = torch.from_numpy(oracle.to_aosoa(n, m, qs, qn)).cuda()
+        plan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=qs, out_stride=os_)
+        out = plan.predict(q, 2e-3)
+        plan.status()
+        ref = oracle.stp(n, m, qn, 2e-3, pde_kind=kind, args=args)
+        worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, os_, m=m)
+        assert max(worst.values()) <= TOL, (m, worst)
+        if os_ > m:  # padding slots of qavg / favg are exact zeros
+            qa = out.qavg.cpu().numpy().reshape(E, n, n, os_, n)
+            fa = out.favg.cpu().numpy().reshape(E, 3, n, n, os_, n)
+            assert not np.any(qa[:, :, :, m:, :]) and not np.any(fa[:, :, :, :, m:, :])
+        monkeypatch.setenv("ADERSTP_FORCE_GENERIC", "1")
+        gplan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=qs, out_stride=os_)
+        gen = gplan.predict(q, 2e-3)
+        gplan.status()
+        monkeypatch.delenv("ADERSTP_FORCE_GENERIC")
+        for x, y in ((out.qavg, gen.qavg), (out.favg, gen.favg), (out.face_q, gen.face_q), (out.face_f, gen.face_f)):
+            assert O.per_element_rel_diff(y.cpu().numpy().reshape(E, -1), x.cpu().numpy().reshape(E, -1)) <= TOL
+        empty = plan.predict(q[:0], 2e-3)
+        plan.status()
+        assert empty.qavg.shape[0] == 0
+        cplan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=qs, out_stride=os_, check_inputs=True)
+        pad = q.clone()  # a NaN in a padding slot (s >= m) is never read: no flag
+        if qs > m:
+            pad[E - 1, ((n * n - 1) * qs + m) * n] = float("nan")
+        cplan.predict(pad, 2e-3)
+        cplan.status()
+        bad = q.clone()  # quantity 0 of the last node of the last element
+        bad[E - 1, ((n * n - 1) * qs) * n + n - 1] = float("nan")
+        cplan.predict(bad, 2e-3)
+        with pytest.raises(S.StpError) as err:
+            cplan.status()
+        assert err.value.code == S.ADERSTP_ERR_NONFINITE
