@@ -143,3 +143,77 @@ def test_time_loop_guard_bands(stp, n):
     assert ok and steps >= 1
     assert _canaries_intact(buf, E * n ** 3 * 9) and _canaries_intact(pbuf, E * 3)
     assert bool(torch.isfinite(u).all())
+
+
+def _dense_pde(S, m, seed):
+    rng = np.random.default_rng(seed)
+    A = [rng.uniform(-1, 1, (m, m)) / m for _ in range(3)]
+    B = [rng.uniform(-0.5, 0.5, (m, m)) / m for _ in range(3)]
+    return S.linear_pde(A, B), A, B
+
+
+USER_FAMILIES = [  # (name, nDof, pde, m, q stride, out stride): the user-LinearPde kernels
+    ("tlp9_adv", 9, "advection", 8, 10, 8),
+    ("tlp10_demo", 10, "demo", 6, 6, 7),
+    ("dmmat6_adv", 6, "advection", 3, 3, 3),
+    ("dmma8_table_demo", 8, "demo", 6, 6, 6),
+    ("general6_dense12", 6, "dense", 12, 12, 12),
+    ("generic4_adv", 4, "advection", 3, 4, 4),
+]
+
+
+@pytest.mark.parametrize("name,n,kind,m,qs,os_", USER_FAMILIES, ids=[f[0] for f in USER_FAMILIES])
+def test_user_pde_kernels_guard_bands_and_poisoned_neighbours(stp, oracle, name, n, kind, m, qs, os_):
+    """The user-LinearPde kernels (line-pass table kernel, DMMA table kernels, general, generic):
+    guard bands around every output, NaN neighbours and NaN padding slots in the input, results
+    against the oracle / the reference, bit-identical on another offset under a graph replay."""
+    S = stp
+    E, off = 5, 2
+    if kind == "advection":
+        pde, ref_kw = S.advection_pde((1.0, 0.5, 0.25), m), dict(pde_kind=O.PDE_ADVECTION, args=[1.0, 0.5, 0.25])
+    elif kind == "demo":
+        pde, ref_kw = S.paper_demo_pde(), dict(pde_kind=O.PDE_DEMO, args=[])
+    else:
+        pde, A, B = _dense_pde(S, m, 3)
+        ref_kw = None
+    rng = np.random.default_rng(len(name) + n)
+    qn = rng.uniform(-1, 1, (E, n ** 3 * m))
+    big = torch.full((E + 2 * off, n ** 3 * qs), float("nan"), dtype=torch.float64, device="cuda")
+    big[off:off + E] = torch.from_numpy(oracle.to_aosoa(n, m, qs, qn)).cuda()
+    big.view(E + 2 * off, n, n, qs, n)[:, :, :, m:, :] = float("nan")  # padding slots stay NaN
+    q = big[off:off + E]
+    plan = S.Plan(n, pde, layout=S.LAYOUT_AOSOA, q_stride=qs, out_stride=os_, check_inputs=True)
+    shapes = [(E, n ** 3 * os_), (E, 3, n ** 3 * os_), (E, 6, n * n * m), (E, 6, n * n * m)]
+    views, bufs = zip(*[_guarded(s) for s in shapes])
+    out = S.PredictorOutput(*views)
+    dt = 2e-3
+    plan.predict(q, dt, out=out)
+    plan.status()  # raises if a NaN neighbour or padding slot was read as data
+    torch.cuda.synchronize()
+    for s, b in zip(shapes, bufs):
+        assert _canaries_intact(b, int(np.prod(s))), (name, s)
+    if ref_kw is not None:
+        ref = oracle.stp(n, m, qn, dt, **ref_kw)
+    else:
+        if not O.reference_available():
+            pytest.skip("oracle/_ref not built")
+        ref = O.Reference().stp_matrix(n, m, qn, dt, A, B)
+    got = oracle.from_aosoa(n, m, os_, out.qavg.cpu().numpy())
+    assert O.per_element_rel_diff(ref.qavg, got) <= 1e-12
+    assert O.per_element_rel_diff(ref.face_f.reshape(E, -1), out.face_f.cpu().numpy().reshape(E, -1)) <= 1e-12
+    if os_ > m:
+        assert not np.any(out.qavg.cpu().numpy().reshape(E, n, n, os_, n)[:, :, :, m:, :])
+    q2 = torch.full_like(big, float("nan"))
+    q2[2 * off - 1:2 * off - 1 + E] = q
+    o2 = plan.alloc_output(E)
+    plan.predict(q2[2 * off - 1:2 * off - 1 + E], dt, out=o2)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        plan.predict(q2[2 * off - 1:2 * off - 1 + E], dt, out=o2)
+    for _ in range(3):
+        g.replay()
+        torch.cuda.synchronize()
+        for a, b in ((o2.qavg, out.qavg), (o2.favg, out.favg), (o2.face_q, out.face_q), (o2.face_f, out.face_f)):
+            assert torch.equal(a, b), name
+    plan.status()
