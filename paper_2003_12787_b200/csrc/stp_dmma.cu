@@ -32,6 +32,9 @@ int aderstp_dbg_clock2_copy(long long* host, int count) {
 #endif
 }
 
+#ifndef DMMAP_ODD_OUT
+#define DMMAP_ODD_OUT 1
+#endif
 #ifndef DMMAP_MAXN
 #define DMMAP_MAXN 7
 #endif
@@ -286,8 +289,21 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
     }
     __syncthreads();
   }
+  // nDof 7, AoSoA: rows of N doubles are not 16-byte pairs, and lane-wise 8-byte loads of the
+  // C-fragment positions scatter; the element's q is staged into the Q planes with coalesced
+  // loads (consecutive threads = consecutive doubles of [k3][k2][s][k1], slots s >= 9 skipped)
+  constexpr bool STAGEQ = AOS || N == 7;  // measured: nDof 7 +2.9 %, nDof 5 -1.2 %
+  if constexpr (!AOS && N == 7) {
+    const int qs = kp.q_stride;
+    const int rowl = qs * N;  // one (k3, k2) row group: qs quantities x N nodes
+    for (int i = tid; i < N * N * rowl; i += THREADSP) {
+      const int k32 = i / rowl, rem = i - k32 * rowl, sq = rem / N, k1 = rem - sq * N;
+      if (sq < NVP) Q[sq * PV + (k32 / N) * 64 + physp(k32 % N, k1)] = __ldcs(qe + i);
+    }
+    __syncthreads();
+  }
   auto ldq = [&](int sq, int k3, double& v0, double& v1) {
-    if constexpr (AOS) {  // from the staged planes (C-fragment positions, padding lanes: 0)
+    if constexpr (STAGEQ) {  // from the staged planes (C-fragment positions, padding lanes: 0)
       const double* src = Q + sq * PV + k3 * 64 + col;
       v0 = ok0 ? src[0] : 0.0;
       v1 = ok1 ? src[1] : 0.0;
@@ -473,6 +489,31 @@ __global__ void __maxnreg__(N <= 6 ? 64 : 80) stp_dmmap_kernel(ParamsP kp, Batch
   } else {
     double* qout = FUSED ? nullptr : a.qavg + e * (long long)(N * N * N * NVP);
     double* fout = a.favg ? a.favg + e * (long long)(3 * N * N * N * NVP) : nullptr;
+#if DMMAP_ODD_OUT
+    if constexpr (N == 7) {
+      // nDof 7: rows of 7 doubles give only scattered 8-byte stores in the plane-per-warp scheme;
+      // every output array is written in its own order by all warps instead (consecutive lanes
+      // store consecutive doubles), each value read from the planes (favg: flux source x coef).
+      // Measured: nDof 7 +8.7 %, nDof 5 -10 % (kept plane-per-warp)
+      constexpr int N3 = N * N * N, UNITS = NVP * N3;
+      constexpr unsigned long long IN[3] = {pack_flux(0, false), pack_flux(1, false), pack_flux(2, false)};
+      constexpr unsigned long long CO[3] = {pack_flux(0, true), pack_flux(1, true), pack_flux(2, true)};
+#pragma unroll 1
+      for (int u = tid; u < UNITS; u += THREADSP) {
+        const int k1 = u % N, r1 = u / N, so = r1 % NVP, r2 = r1 / NVP, k2 = r2 % N, k3 = r2 / N;
+        const double* pl = P + k3 * 64 + physp(k2, k1);
+        if (qout) __stcs(qout + u, pl[so * PV]);
+        if (fout) {
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const int src = (int)((IN[d] >> (4 * so)) & 15), ci = (int)((CO[d] >> (4 * so)) & 15);
+            const double c = ci == 0 ? c4[0] : ci == 1 ? c4[1] : ci == 2 ? c4[2] : ci == 3 ? c4[3] : 0.0;
+            __stcs(fout + d * UNITS + u, c * pl[src * PV]);
+          }
+        }
+      }
+    } else
+#endif
 #pragma unroll 1
     for (int k3 = warp; k3 < N; k3 += NWP) {
       double2 v[NVP];
