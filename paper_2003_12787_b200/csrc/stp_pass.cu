@@ -58,6 +58,9 @@ __constant__ PassSlot kPass[3][6] = {
     {{7, 3, {0, 1, 2}, {1, 0, 1}}, {6, 1, {3}, {2}}, {8, 1, {5}, {2}}, {3, 1, {6}, {3}}, {1, 1, {7}, {3}}, {5, 1, {8}, {3}}},
     {{8, 3, {0, 1, 2}, {1, 1, 0}}, {6, 1, {4}, {2}}, {7, 1, {5}, {2}}, {4, 1, {6}, {3}}, {5, 1, {7}, {3}}, {2, 1, {8}, {3}}}};
 
+#ifndef PASS_GROUP_FACES
+#define PASS_GROUP_FACES 1
+#endif
 template <int N, int SL = 6>
 struct Geo {
   static constexpr int RS = (N % 2 == 0) ? N + 1 : N;  // odd row stride: conflict-free lines
@@ -376,6 +379,74 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
           __stcs(fo + d * (NVE * N3) + s * N, e_coef(s, d) == 4 ? 0.0 : cc[e_coef(s, d)] * v[e_in(s, d)]);
     }
   }
+#if PASS_GROUP_FACES
+  if constexpr (N <= 3) {
+  if (a.face_q || a.face_f) {
+    // nDof 2, 3: faces by 9-lane groups as in stp_bip (a warp takes three face nodes, lane =
+    // quantity; face_f = F_d(face_q) from the group's lanes by shuffles; 27 consecutive doubles
+    // per warp store)
+    constexpr int FV = N * N * NVE;
+    constexpr int T = G::EPB * 3 * N * N;
+    const int lane = tid & 31, grp = lane / NVE, s = lane - grp * NVE;
+    const bool live = lane < 3 * NVE;
+    for (int it = tid >> 5; 3 * it < T; it += G::THREADS / 32) {
+      const int node = 3 * it + (live ? grp : 0);
+      const int nd = node < T ? node : 0;
+      const int ee = nd / (3 * N * N);
+      const bool ok = live && node < T && e0 + ee < a.n_elem;
+      const int r = nd - ee * 3 * N * N;
+      const int d = r / (N * N), ab = r - d * N * N;
+      const int aa = ab / N, bb = ab - aa * N;
+      const int start = d == 0 ? aa * G::PL + bb * G::RS : d == 1 ? aa * G::PL + bb : aa * G::RS + bb;
+      const int stride = d == 0 ? 1 : d == 1 ? G::RS : G::PL;
+      const double* q0 = buf(ee, 0) + start + (live ? s : 0) * G::VS;
+      double x0 = 0.0, x1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double x = q0[j * stride];
+        x0 = fma(kp.phi[0][j], x, x0);
+        x1 = fma(kp.phi[1][j], x, x1);
+      }
+      const long long fb = (e0 + ee) * 6LL * FV + (2 * d) * FV + ab * NVE + s;
+      if (ok && a.face_q) {
+        __stcs(a.face_q + fb, x0);
+        __stcs(a.face_q + fb + FV, x1);
+      }
+      if (a.face_f) {
+        const int so = live ? s : 0;
+        const int ci = d == 0 ? e_coef_rt<0>(so) : d == 1 ? e_coef_rt<1>(so) : e_coef_rt<2>(so);
+        const int src = d == 0 ? e_in_rt<0>(so) : d == 1 ? e_in_rt<1>(so) : e_in_rt<2>(so);
+        const int sl2 = (live ? grp : 0) * NVE + src;
+        const double y0 = __shfl_sync(0xffffffffu, x0, sl2), y1 = __shfl_sync(0xffffffffu, x1, sl2);
+        if (ok) {
+          double c = 0.0;
+          if (ci != 4) {
+            const double* pr = a.par + 3 * (e0 + ee);
+            double cc[4];
+            if (kp.par_kind == ADERSTP_PAR_RHO_CP_CS) {
+              const double mu = __dmul_rn(__dmul_rn(pr[0], pr[2]), pr[2]);
+              const double lam = __dsub_rn(__dmul_rn(__dmul_rn(pr[0], pr[1]), pr[1]), __dmul_rn(2.0, mu));
+              cc[0] = lam + 2.0 * mu;
+              cc[1] = lam;
+              cc[2] = mu;
+              cc[3] = 1.0 / pr[0];
+            } else {
+              cc[0] = pr[0] + 2.0 * pr[1];
+              cc[1] = pr[0];
+              cc[2] = pr[1];
+              cc[3] = 1.0 / pr[2];
+            }
+            c = pick4(cc, ci);
+          }
+          __stcs(a.face_f + fb, c * y0);
+          __stcs(a.face_f + fb + FV, c * y1);
+        }
+      }
+    }
+  }
+  } else
+#endif
+  {
   if (a.face_q || a.face_f) {
     // one task per (normal d, in-face node a, b): all 9 quantities of the normal line, both
     // sides; face_f = F_d(face_q) on the spot.  Output [f][a][b][s]: 9 contiguous doubles per
@@ -447,6 +518,7 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
         }
       }
     }
+  }
   }
   if (kp.check && flags) atomicOr(status, flags);
 #ifdef ADERSTP_EXPT_TIMING
