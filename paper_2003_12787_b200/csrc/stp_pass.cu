@@ -61,6 +61,11 @@ __constant__ PassSlot kPass[3][6] = {
 #ifndef PASS_GROUP_FACES
 #define PASS_GROUP_FACES 1
 #endif
+// 9-lane group faces up to nDof 7 (measured: nDof 2 / 3 +63 / +23 % (the default path there), the
+// fallback at nDof 4-7 +2..+13 %; nDof 8 -9 %)
+#ifndef PASS_GROUP_FACES_MAXN
+#define PASS_GROUP_FACES_MAXN 7
+#endif
 template <int N, int SL = 6>
 struct Geo {
   static constexpr int RS = (N % 2 == 0) ? N + 1 : N;  // odd row stride: conflict-free lines
@@ -380,9 +385,9 @@ stp_pass_kernel(PassParams<N> kp, BatchArgs a, unsigned int* status) {
     }
   }
 #if PASS_GROUP_FACES
-  if constexpr (N <= 3) {
+  if constexpr (N <= PASS_GROUP_FACES_MAXN) {
   if (a.face_q || a.face_f) {
-    // nDof 2, 3: faces by 9-lane groups as in stp_bip (a warp takes three face nodes, lane =
+    // nDof <= 7: faces by 9-lane groups as in stp_bip (a warp takes three face nodes, lane =
     // quantity; face_f = F_d(face_q) from the group's lanes by shuffles; 27 consecutive doubles
     // per warp store)
     constexpr int FV = N * N * NVE;
