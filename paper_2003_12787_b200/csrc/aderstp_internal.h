@@ -45,6 +45,7 @@ struct LaunchPlan {
     const int* t_col = nullptr;
     int t_nnz = 0;
     const double* t_dense = nullptr;  // C_d dense [d][j][s < m rounded up to 8] (general kernel)
+    const double* f_dense = nullptr;  // A_d dense, same layout (stp_gdense favg / face_f)
     const double* t_val = nullptr;
     const int* f_ptr = nullptr;
     const int* f_col = nullptr;
@@ -60,6 +61,7 @@ struct LaunchPlan {
   int pass_slots = 0;                // env ADERSTP_PASS_SLOTS: 6 = line-pass kernel, 12 = bipartite, 0 auto
   int aos_staged = 0;                // env ADERSTP_AOS_STAGED=1: reference layout through the transposes
   int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel
+  int no_gdense = 0;                 // env ADERSTP_NO_GDENSE=1: dense systems at nDof 8 on stp_general
 };
 
 struct BatchArgs {
@@ -116,6 +118,9 @@ cudaError_t launch_max_cp(const double* par, int par_kind, long long n, unsigned
 bool general_selected(const LaunchPlan& p);
 cudaError_t launch_general(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 void source_amplitudes(const LaunchPlan& p, double t, int n, double* amp);  // S^(o)(t) x src_scale
+// stp_gdense.cu: the general systems at nDof 8 (m <= 21, no point source) on the tensor cores
+bool gdense_applicable(const LaunchPlan& p, const BatchArgs& a);
+cudaError_t launch_gdense(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 
 // stp_kernels.cu
 cudaError_t launch_stp(const LaunchPlan& plan, const BatchArgs& args, cudaStream_t stream);

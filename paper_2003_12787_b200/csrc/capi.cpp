@@ -136,12 +136,15 @@ cudaError_t upload_general(aderstp_plan* p, const std::vector<double>& A, const 
       fp[3 * s + d + 1] = (int)fc.size();
     }
   // dense C_d [d][j][s < mp] (mp = m rounded up to 8: whole target blocks of the dense phase 2)
+  // and dense A_d in the same layout (stp_gdense's favg / face_f GEMMs)
   const int mp = (m + 7) / 8 * 8;
-  std::vector<double> cd(3 * (size_t)m * mp, 0.0);
+  std::vector<double> cd(6 * (size_t)m * mp, 0.0);
   for (int d = 0; d < 3; ++d)
     for (int s = 0; s < m; ++s)
-      for (int j = 0; j < m; ++j)
+      for (int j = 0; j < m; ++j) {
         cd[((size_t)d * m + j) * mp + s] = A[(size_t)d * m * m + s * m + j] + B[(size_t)d * m * m + s * m + j];
+        cd[((size_t)(3 + d) * m + j) * mp + s] = A[(size_t)d * m * m + s * m + j];
+      }
   // layout: [cd][t_val][f_val][t_ptr][f_ptr][t_col][f_col] (doubles first: 16-byte alignment)
   const size_t bytes = sizeof(double) * (cd.size() + tv.size() + fv.size()) +
                        sizeof(int) * (tp.size() + fp.size() + tc.size() + fc.size());
@@ -167,6 +170,7 @@ cudaError_t upload_general(aderstp_plan* p, const std::vector<double>& A, const 
   char* dv = static_cast<char*>(p->gen_buf);
   aderstp::LaunchPlan::GeneralTables& g = p->lp.gen;
   g.t_dense = reinterpret_cast<const double*>(dv + o_cd);
+  g.f_dense = g.t_dense + 3 * (size_t)m * mp;
   g.t_val = reinterpret_cast<const double*>(dv + o_tv);
   g.f_val = reinterpret_cast<const double*>(dv + o_fv);
   g.t_ptr = reinterpret_cast<const int*>(dv + o_tp);
@@ -295,6 +299,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     lp.aos_staged = (as && as[0] == '1') ? 1 : 0;
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");
     lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
+    const char* ng = std::getenv("ADERSTP_NO_GDENSE");
+    lp.no_gdense = (ng && ng[0] == '1') ? 1 : 0;
     const char* ac = std::getenv("ADERSTP_AOS_CHUNK");
     lp.aos_chunk = ac ? std::atoi(ac) : 0;
     const char* ps = std::getenv("ADERSTP_PASS_SLOTS");

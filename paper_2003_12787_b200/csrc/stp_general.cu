@@ -465,6 +465,7 @@ void source_amplitudes(const LaunchPlan& p, double t, int n, double* amp) {
 bool general_selected(const LaunchPlan& p) { return p.kind != ADERSTP_PDE_ELASTIC && p.gen.t_ptr != nullptr; }
 
 cudaError_t launch_general(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
+  if (gdense_applicable(p, a)) return launch_gdense(p, a, stream);
   switch (p.n) {
     case 2: return launch_general_n<2>(p, a, stream);
     case 3: return launch_general_n<3>(p, a, stream);

@@ -2,8 +2,8 @@
 time loop, against the unmodified reference.
 
 * predictor: dense flux + ncp systems (m = 12 at nDof 6 and 8, m = 21 -- the paper's application
-  size, proj PAPER.md:676 -- at nDof 4, 8 and 10, the last on the global-scratch path), both
-  layouts, against predict() + extrapolate_faces of a reference LinearPde subclass with the same
+  size, proj PAPER.md:676 -- at nDof 4, 8 and 10, the last on the global-scratch path; at nDof 8
+  m = 4 .. 21 on the tensor-core kernel stp_gdense, every k-step count 1..6), both layouts, against predict() + extrapolate_faces of a reference LinearPde subclass with the same
   matrices (oracle/ref_shim.cpp MatrixPde); the reference's own PDEs forced onto the general
   kernel (ADERSTP_GENERAL=1) against the oracle; built-in kinds beyond the table kernels
   (advection with m = 20); a LinearPde with a point source;
@@ -70,7 +70,9 @@ def run_gpu(S, oracle, n, m, pde, qn, dt, layout, stride, t_start=0.0):
 
 
 @pytest.mark.parametrize("m,n,layout", [(12, 6, "aosoa"), (12, 8, "aosoa"), (12, 8, "aos"), (21, 4, "aosoa"),
-                                        (21, 8, "aos"), (21, 10, "aosoa"), (5, 3, "aosoa")])
+                                        (21, 8, "aos"), (21, 8, "aosoa"), (21, 10, "aosoa"), (5, 3, "aosoa"),
+                                        (7, 8, "aosoa"), (9, 8, "aos"), (16, 8, "aosoa"), (17, 8, "aosoa"),
+                                        (20, 8, "aos")])
 def test_dense_system_matches_reference(S, oracle, reference, m, n, layout):
     A, B = dense_system(m, 1000 * m + n)
     E = 3 if n >= 10 else 5
@@ -84,6 +86,28 @@ def test_dense_system_matches_reference(S, oracle, reference, m, n, layout):
     ref = reference.stp(n, m, qn, dt, pde_kind=O.PDE_MATRIX, threads=4)
     worst = compare(S, oracle, n, m, out, ref, lay, stride)
     assert max(worst.values()) <= TOL, worst
+
+
+@pytest.mark.parametrize("m,layout", [(21, "aosoa"), (13, "aos"), (6, "aosoa")])
+def test_dense_tensor_core_kernel_matches_general_kernel(S, oracle, monkeypatch, m, layout):
+    """nDof 8 dense systems run on stp_gdense (DMMA GEMMs); ADERSTP_NO_GDENSE=1 keeps them on the
+    scalar general kernel.  Both against each other on 37 elements (several CTA waves' worth of
+    element offsets), plus the padding slots of the AoS rows."""
+    n = 8
+    A, B = dense_system(m, 4242 + m)
+    E = 37
+    rng = np.random.default_rng(m)
+    qn = rng.standard_normal((E, n ** 3 * m))
+    lay = S.LAYOUT_AOS if layout == "aos" else S.LAYOUT_AOSOA
+    stride = (m + 7) // 8 * 8 if layout == "aos" else m
+    dt = 0.3 / (3 * 2.0 * (2 * n - 1))
+    outs = []
+    for flag in ("0", "1"):
+        monkeypatch.setenv("ADERSTP_NO_GDENSE", flag)
+        outs.append(run_gpu(S, oracle, n, m, S.linear_pde(A, B), qn, dt, lay, stride))
+    for name in ("qavg", "favg", "face_q", "face_f"):
+        a, b = (getattr(o, name).cpu().numpy().reshape(E, -1) for o in outs)
+        assert O.per_element_rel_diff(b, a) <= TOL, name
 
 
 @pytest.mark.parametrize("case", ["advection", "ncp_advection", "demo", "source_only", "elastic_matrix"])
@@ -213,7 +237,8 @@ def test_corrector_step_with_sources_and_general_systems(S, oracle, reference, c
 
 
 @pytest.mark.parametrize("case,n,e", [("elastic_source", 4, 2), ("elastic_source", 6, 2), ("elastic_source", 8, 3),
-                                      ("matrix_dense", 4, 2), ("matrix_source", 3, 2), ("matrix_m21", 3, 2)])
+                                      ("matrix_dense", 4, 2), ("matrix_source", 3, 2), ("matrix_m21", 3, 2),
+                                      ("matrix_m21", 8, 2)])
 def test_run_simulation_with_sources_and_general_systems(S, oracle, reference, case, n, e):
     """Several full time steps (predictor on the scaled PDE + corrector) against
     ader::run_simulation."""
