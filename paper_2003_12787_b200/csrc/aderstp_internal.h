@@ -62,6 +62,7 @@ struct LaunchPlan {
   int aos_staged = 0;                // env ADERSTP_AOS_STAGED=1: reference layout through the transposes
   int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel
   int no_gdense = 0;                 // env ADERSTP_NO_GDENSE=1: dense systems at nDof 8 on stp_general
+  int wpe = 0;                       // warp-per-element kernel at nDof 4, 6 (env ADERSTP_WPE=0|1)
 };
 
 struct BatchArgs {
@@ -149,6 +150,10 @@ cudaError_t init_dmma8(const LaunchPlan& p);  // once per device, at plan creati
 bool dmmap_applicable(const LaunchPlan& p);
 cudaError_t init_dmmap(const LaunchPlan& p);
 cudaError_t launch_dmmap(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
+// stp_wpe.cu: nDof 4, 6 with one warp per element (DFMA tile tasks, no CTA barrier)
+bool wpe_applicable(const LaunchPlan& p, const BatchArgs& a);
+cudaError_t init_wpe(const LaunchPlan& p);
+cudaError_t launch_wpe(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream);
 // stp_pass.cu: line-pass elastic kernel for every order (even/odd split D, uniform operands)
 bool pass_applicable(const LaunchPlan& p);
 // table PDEs (term tables) at nDof 9, 10 on line passes (stp_tlp); init_pass uploads its even/odd D

@@ -299,6 +299,8 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     lp.aos_staged = (as && as[0] == '1') ? 1 : 0;
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");
     lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
+    const char* wp = std::getenv("ADERSTP_WPE");
+    lp.wpe = wp ? (wp[0] == '1' ? 1 : 0) : 0;
     const char* ng = std::getenv("ADERSTP_NO_GDENSE");
     lp.no_gdense = (ng && ng[0] == '1') ? 1 : 0;
     const char* ac = std::getenv("ADERSTP_AOS_CHUNK");
@@ -432,6 +434,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
   if (e == cudaSuccess && (aderstp::pass_applicable(kl) || (kl.kind != ADERSTP_PDE_ELASTIC && kl.n >= 9)))
     e = aderstp::init_pass(kl);  // the even/odd D of the line-pass kernels (stp_pass, stp_bip, stp_tlp)
   if (e == cudaSuccess && aderstp::dmmap_applicable(kl)) e = aderstp::init_dmmap(kl);
+  if (e == cudaSuccess && kl.wpe && kl.kind == ADERSTP_PDE_ELASTIC) e = aderstp::init_wpe(kl);
   if (e == cudaSuccess && kl.kind != ADERSTP_PDE_ELASTIC && kl.n >= 5 && kl.n <= 7) e = aderstp::init_dmmat(kl);
   if (e == cudaSuccess) lp.gen.pool = p->pool;
   if (e != cudaSuccess) {

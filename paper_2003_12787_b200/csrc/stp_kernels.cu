@@ -501,6 +501,7 @@ cudaError_t launch_stp(const LaunchPlan& p, const BatchArgs& a, cudaStream_t str
   if (a.u_next && use_dmmap(p, a)) return launch_dmmap(p, a, stream);
   if (a.u_next && use_bip(p, a)) return launch_pass(p, a, stream);
   if (a.u_next) return cudaErrorInvalidValue;  // the fused mode exists only where fused_supported()
+  if (wpe_applicable(p, a)) return launch_wpe(p, a, stream);
   if (!p.force_generic && !p.no_dmmap && aligned && dmmap_applicable(p)) return launch_dmmap(p, a, stream);
   if (!p.force_generic && pass_applicable(p)) return launch_pass(p, a, stream);
   if (p.kind == ADERSTP_PDE_ELASTIC) return dispatch<true>(p, a, stream);

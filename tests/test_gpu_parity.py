@@ -107,6 +107,29 @@ def test_kernel_variants_agree(stp, oracle, monkeypatch, n):
         assert max(worst.values()) <= TOL, (env, worst)
 
 
+@pytest.mark.parametrize("n,E,qs", [(6, 19, 9), (6, 1037, 9), (6, 50, 12), (4, 19, 9), (4, 2100, 9), (4, 50, 12)])
+def test_warp_per_element_kernel(stp, oracle, monkeypatch, n, E, qs):
+    """The opt-in warp-per-element kernel (ADERSTP_WPE=1, csrc/stp_wpe.cu: nDof 4 / 6, persistent
+    warps, several elements per warp, ragged last wave, padded input stride) against the oracle."""
+    S = stp
+    monkeypatch.setenv("ADERSTP_WPE", "1")
+    q, par = S.generate(0, 11 + n, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=qs)
+    par_h = par.cpu().numpy()
+    dt = O.cfl_dt(n, par_h[:, 1].max())
+    ref = oracle.stp(n, 9, oracle.from_aosoa(n, 9, qs, q.cpu().numpy()), dt, par=oracle.material_lmr(par_h))
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, q_stride=qs, par_kind=S.PAR_RHO_CP_CS)
+    out = plan.predict(q, dt, par=par)
+    plan.status()
+    worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, 9)
+    assert max(worst.values()) <= TOL, worst
+    # non-finite input and bad material are flagged like in the default kernels
+    q2 = q.clone()
+    q2.view(-1)[7] = float("nan")
+    plan.predict(q2, dt, par=par)
+    with pytest.raises(Exception):
+        plan.status()
+
+
 # ---------------------------------------------------------------------------------------------
 # Against the reference's own outputs (tests/golden, produced by the unmodified reference)
 # ---------------------------------------------------------------------------------------------
