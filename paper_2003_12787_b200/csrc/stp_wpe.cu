@@ -45,7 +45,8 @@ struct GeoW {
   static constexpr int S3 = N == 6 ? 37 : 17;
   static constexpr int FS = N == 6 ? 223 : 69;
   static constexpr int FACE = N2 * NVW;                       // one face array
-  static constexpr int BUF = ((NVW * FS > 6 * FACE ? NVW * FS : 6 * FACE) + 1) & ~1;  // doubles, even
+  static constexpr int BUF = ((NVW * FS > 6 * FACE ? NVW * FS : 6 * FACE) + 2) & ~1;  // doubles, even, >= fields + 1
+  static constexpr int DUMMY = NVW * FS;                      // a slot no field uses (write-only sink)
   static constexpr int WARP_DOUBLES = 2 * BUF;
   static constexpr int QC = 2 * N2;                           // TMEM columns of one q tile
   static constexpr int TCW = 3 * QC;                          // TMEM columns per warp
@@ -55,7 +56,8 @@ struct GeoW {
 struct TaskW {
   int srcA, saA, sbA;  // term A: source tile origin and strides (doubles) along a, b
   int srcB, saB, sbB;  // term B
-  int dst1, dst2, dst3, part;
+  int dst1, dst2, dst3, part;  // idle lanes and unused outputs point at the buffer's dummy slot
+  int s2a, s2b;        // strides of dst2 / dst3 (0 where they are the dummy slot)
   int mode, coef;
 };
 
@@ -95,6 +97,10 @@ constexpr unsigned long long pack_flux_w(int d, bool coef) {
 }
 
 // One phase of a CK step for the calling lane's task: R (source iterate), W (destination).
+// Branch-free: every lane runs every load, FMA and store; idle lanes and unused outputs have zero
+// strides and the buffer's dummy slot as destination.  out1 = co q1 + c1 (a + b + p) + c2 a; the
+// normal-stress lanes (phase B) also write out2 = co q2 + c1 S + c2 b and out3 = co q3 + c1 S +
+// c2 p; the raw-derivative lanes (phase A: co = c1 = 0, c2 = 1) write a to dst1 and b to dst2.
 template <int N, bool PHASEB>
 __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const double* __restrict__ R,
                                           double* __restrict__ W, uint32_t tq, double co, double c1, double c2) {
@@ -113,11 +119,12 @@ __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const doub
     for (int ib = 0; ib < N; ++ib) {
       double v[N];
 #pragma unroll
-      for (int l = 0; l < N; ++l) v[l] = p[l * t.saA + ib * t.sbA];
+      for (int l = 0; l < N; ++l) v[l] = p[l * t.saA];
 #pragma unroll
       for (int l = 0; l < N; ++l)
 #pragma unroll
         for (int ia = 0; ia < N; ++ia) accA[ia][ib] = fma(kp.d[ia * N + l], v[l], accA[ia][ib]);
+      p += t.sbA;
     }
   }
   {  // term B: derivative along b, one line (fixed ia) at a time
@@ -126,15 +133,18 @@ __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const doub
     for (int ia = 0; ia < N; ++ia) {
       double v[N];
 #pragma unroll
-      for (int l = 0; l < N; ++l) v[l] = p[ia * t.saB + l * t.sbB];
+      for (int l = 0; l < N; ++l) v[l] = p[l * t.sbB];
 #pragma unroll
       for (int l = 0; l < N; ++l)
 #pragma unroll
         for (int ib = 0; ib < N; ++ib) accB[ia][ib] = fma(kp.d[ib * N + l], v[l], accB[ia][ib]);
+      p += t.saB;
     }
   }
-  const int mode = t.mode;
-  const bool haspart = PHASEB && t.part >= 0;
+  double* w1 = W + t.dst1;
+  double* w2 = W + t.dst2;
+  double* w3 = W + t.dst3;
+  const double* wp = W + t.part;
 #pragma unroll
   for (int ia = 0; ia < N; ++ia) {
     uint32_t r1[2 * N], r2[2 * N], r3[2 * N];
@@ -146,22 +156,22 @@ __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const doub
     tm_wait_ld();
 #pragma unroll
     for (int ib = 0; ib < N; ++ib) {
-      const int off = ia * t.saA + ib * t.sbA;
       const double a = accA[ia][ib], b = accB[ia][ib];
-      const double p = haspart ? W[t.part + off] : 0.0;
-      const double S = a + b + p;
-      const double q1 = mode == MODE_PAIR ? 0.0 : tm_double(r1, ib);
-      const double o1 = fma(co, q1, fma(c1, S, c2 * a));
-      if (mode != MODE_IDLE) W[t.dst1 + off] = o1;
       if (PHASEB) {
-        if (mode == MODE_NORMAL) {
-          W[t.dst2 + off] = fma(co, tm_double(r2, ib), fma(c1, S, c2 * b));
-          W[t.dst3 + off] = fma(co, tm_double(r3, ib), fma(c1, S, c2 * p));
-        }
+        const double p = wp[ib * t.sbA];
+        const double S = a + b + p, cS = c1 * S;
+        w1[ib * t.sbA] = fma(co, tm_double(r1, ib), fma(c2, a, cS));
+        w2[ib * t.s2b] = fma(co, tm_double(r2, ib), fma(c2, b, cS));
+        w3[ib * t.s2b] = fma(co, tm_double(r3, ib), fma(c2, p, cS));
       } else {
-        if (mode == MODE_PAIR) W[t.dst2 + ia * t.saB + ib * t.sbB] = b;
+        w1[ib * t.sbA] = fma(co, tm_double(r1, ib), fma(c2, a, c1 * (a + b)));
+        w2[ib * t.s2b] = b;
       }
     }
+    w1 += t.saA;
+    w2 += t.s2a;
+    w3 += t.s2a;
+    wp += t.saA;
   }
 }
 
@@ -286,7 +296,7 @@ __global__ void __launch_bounds__(WPC * 32, 1) stp_wpe_kernel(ParamsW kp, BatchA
         const TaskW tA = task_s[0][lane];
         const double cc = tA.coef == 0 ? c4[0] : tA.coef == 1 ? c4[1] : tA.coef == 2 ? c4[2] : c4[3];
         const bool pair = tA.mode == MODE_PAIR;
-        run_phase<N, false>(kp, tA, R, W, tq, co, pair ? 0.0 : cc * sc, pair ? 1.0 : 0.0);
+        run_phase<N, false>(kp, tA, R, W, tq, pair ? 0.0 : co, pair ? 0.0 : cc * sc, pair ? 1.0 : 0.0);
       }
       __syncwarp();
       {
@@ -300,25 +310,31 @@ __global__ void __launch_bounds__(WPC * 32, 1) stp_wpe_kernel(ParamsW kp, BatchA
     const double* Y = ((N - 1) & 1) ? B1 : B0;  // qavg: the last iterate (B1: N - 1 is odd)
     double* X = ((N - 1) & 1) ? B0 : B1;        // free: the face staging buffer
     const bool faces = a.face_q || a.face_f;
-    // ---- faces: line tasks (direction, in-face node, quantity) -> X [6][N][N][9] ----------------
+    // ---- faces: line tasks (in-face node, quantity) per direction -> X [6][N][N][9]; the line
+    // strides are compile-time constants per direction (immediate offsets) -----------------------
     if (faces) {
       constexpr int TD = N2 * NVW;
-#pragma unroll 1
-      for (int i = lane; i < 3 * TD; i += 32) {
-        const int d = i / TD, r = i - d * TD, ab = r / NVW, s = r - ab * NVW, a0 = ab / N, b0 = ab - a0 * N;
-        // x: (a0, b0) = (k3, k2); y: (k3, k1); z: (k2, k1)
-        const int base = s * FS + (d == 0 ? a0 * S3 + b0 * S2 : d == 1 ? a0 * S3 + b0 : a0 * S2 + b0);
-        const int st = d == 0 ? 1 : d == 1 ? S2 : S3;
-        double f0 = 0.0, f1 = 0.0;
+      auto face_dir = [&](auto dd) {
+        constexpr int D = decltype(dd)::value;
+        constexpr int SA = D == 2 ? S2 : S3, SB = D == 0 ? S2 : 1, SL = D == 0 ? 1 : D == 1 ? S2 : S3;
+#pragma unroll 2
+        for (int i = lane; i < TD; i += 32) {
+          const int ab = i / NVW, s = i - ab * NVW, a0 = ab / N, b0 = ab - a0 * N;
+          const double* line = Y + s * FS + a0 * SA + b0 * SB;
+          double f0 = 0.0, f1 = 0.0;
 #pragma unroll
-        for (int k = 0; k < N; ++k) {
-          const double v = Y[base + k * st];
-          f0 = fma(kp.phi[0][k], v, f0);
-          f1 = fma(kp.phi[1][k], v, f1);
+          for (int k = 0; k < N; ++k) {
+            const double v = line[k * SL];
+            f0 = fma(kp.phi[0][k], v, f0);
+            f1 = fma(kp.phi[1][k], v, f1);
+          }
+          X[(2 * D) * FACE + i] = f0;
+          X[(2 * D + 1) * FACE + i] = f1;
         }
-        X[(2 * d) * FACE + r] = f0;
-        X[(2 * d + 1) * FACE + r] = f1;
-      }
+      };
+      face_dir(std::integral_constant<int, 0>{});
+      face_dir(std::integral_constant<int, 1>{});
+      face_dir(std::integral_constant<int, 2>{});
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
       if (lane == 0 && a.face_q) {
@@ -329,28 +345,41 @@ __global__ void __launch_bounds__(WPC * 32, 1) stp_wpe_kernel(ParamsW kp, BatchA
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       }
     }
-    // ---- qavg / favg in output order: consecutive lanes store consecutive 16-byte pairs --------
+    // ---- qavg / favg in output order: lane = (quantity s, k1 pair) of a (k3, k2) row group, so a
+    // warp store covers the row group's 9 N contiguous doubles; per-lane flux sources and
+    // coefficients are loop constants and every shared / global offset is an immediate ----------
     {
-      constexpr int NP = N3 * NVW / 2;
+      constexpr int PR = NVW * N / 2;  // 16-byte pairs per row group
       constexpr unsigned long long IN[3] = {pack_flux_w(0, false), pack_flux_w(1, false), pack_flux_w(2, false)};
       constexpr unsigned long long CO[3] = {pack_flux_w(0, true), pack_flux_w(1, true), pack_flux_w(2, true)};
-      double2* qo = reinterpret_cast<double2*>(a.qavg + e * (long long)(N3 * NVW));
-      double2* fo = a.favg ? reinterpret_cast<double2*>(a.favg + e * (long long)(3 * N3 * NVW)) : nullptr;
-#pragma unroll 2
-      for (int p = lane; p < NP; p += 32) {
-        const int kp1 = p % (N / 2), r1 = p / (N / 2), s = r1 % NVW, k32 = r1 / NVW;
-        const int node = (k32 / N) * S3 + (k32 % N) * S2 + 2 * kp1;
-        const double* src = Y + node;
-        __stcs(qo + p, make_double2(src[s * FS], src[s * FS + 1]));
-        if (fo) {
+      if (lane < PR) {
+        const int s = lane / (N / 2), kp1 = lane - s * (N / 2);
+        const double* sq = Y + s * FS + 2 * kp1;
+        const double* sf[3];
+        double cf3[3];
 #pragma unroll
-          for (int d = 0; d < 3; ++d) {
-            const int si = (int)((IN[d] >> (4 * s)) & 15), ci = (int)((CO[d] >> (4 * s)) & 15);
-            const double c = ci == 0 ? c4[0] : ci == 1 ? c4[1] : ci == 2 ? c4[2] : ci == 3 ? c4[3] : 0.0;
-            const double x = ci == 4 ? 0.0 : c * src[si * FS], y = ci == 4 ? 0.0 : c * src[si * FS + 1];
-            __stcs(fo + d * NP + p, make_double2(x, y));
-          }
+        for (int d = 0; d < 3; ++d) {
+          const int si = (int)((IN[d] >> (4 * s)) & 15), ci = (int)((CO[d] >> (4 * s)) & 15);
+          sf[d] = Y + si * FS + 2 * kp1;
+          cf3[d] = ci == 0 ? c4[0] : ci == 1 ? c4[1] : ci == 2 ? c4[2] : ci == 3 ? c4[3] : 0.0;
         }
+        double2* qo = reinterpret_cast<double2*>(a.qavg + e * (long long)(N3 * NVW)) + lane;
+        double2* fo = a.favg ? reinterpret_cast<double2*>(a.favg + e * (long long)(3 * N3 * NVW)) + lane : nullptr;
+#pragma unroll
+        for (int k3 = 0; k3 < N; ++k3)
+#pragma unroll
+          for (int k2 = 0; k2 < N; ++k2) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int node = k3 * S3 + k2 * S2, rg = k3 * N + k2;
+            __stcs(qo + rg * PR, make_double2(sq[node], sq[node + 1]));
+            if (fo) {
+#pragma unroll
+              for (int d = 0; d < 3; ++d)
+                __stcs(fo + d * (N3 * NVW / 2) + rg * PR,
+                       make_double2(cf3[d] * sf[d][node], cf3[d] * sf[d][node + 1]));
+            }
+          }
       }
     }
     // ---- face_f = F_d(face_q) in place, once the face_q copy has read the staging buffer ---------
@@ -409,9 +438,9 @@ void build_tasks(TaskW (&tab)[2][32]) {
   enum { SXX, SYY, SZZ, SXY, SXZ, SYZ, U, V, Wq };
   for (int ph = 0; ph < 2; ++ph)
     for (int l = 0; l < 32; ++l) {
-      TaskW t{};
+      TaskW t{};  // idle: zero strides, every access at offset 0 / the dummy slot
       t.mode = MODE_IDLE;
-      t.part = -1;
+      t.dst1 = t.dst2 = t.dst3 = t.part = G::DUMMY;
       tab[ph][l] = t;
     }
   // tile (a, b) at fixed third direction c = k; sources fA (derivative along a), fB (along b)
@@ -422,8 +451,9 @@ void build_tasks(TaskW (&tab)[2][32]) {
     t.srcA = fA * FS + k * st[dc];
     t.srcB = fB * FS + k * st[dc];
     t.dst1 = dst * FS + k * st[dc];
-    t.dst2 = t.dst3 = 0;
-    t.part = part < 0 ? -1 : part * FS + k * st[dc];
+    t.dst2 = t.dst3 = G::DUMMY;
+    t.s2a = t.s2b = 0;
+    t.part = part < 0 ? G::DUMMY : part * FS + k * st[dc];
     t.mode = MODE_SUM;
     t.coef = coef;
     return t;
@@ -439,7 +469,7 @@ void build_tasks(TaskW (&tab)[2][32]) {
     const int u1 = i / N, u2 = 2 + i / N, k = i % N;  // tiles at fixed k2 = k
     TaskW t{};
     t.mode = MODE_PAIR;
-    t.part = -1;
+    t.part = t.dst3 = G::DUMMY;
     t.coef = 0;
     t.saA = st[2];  // term A: a = z, b = x
     t.sbA = st[0];
@@ -449,6 +479,8 @@ void build_tasks(TaskW (&tab)[2][32]) {
     t.sbB = st[2];
     t.srcB = psrc[u2] * FS + k * st[1];
     t.dst2 = pdst[u2] * FS + k * st[1];
+    t.s2a = t.saB;
+    t.s2b = t.sbB;
     tab[0][lane++] = t;
   }
   // phase B: velocities (coef 3 = 1/rho) on x,y tiles + the stored z term; normal stresses
@@ -461,6 +493,8 @@ void build_tasks(TaskW (&tab)[2][32]) {
     t.mode = MODE_NORMAL;
     t.dst2 = SYY * FS + k * st[2];
     t.dst3 = SZZ * FS + k * st[2];
+    t.s2a = t.saA;
+    t.s2b = t.sbA;
     tab[1][lane++] = t;
   }
 }

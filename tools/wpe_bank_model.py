@@ -1,92 +1,99 @@
 #!/usr/bin/env python3
-"""Bank model of the warp-per-element kernel (stp_wpe): shared-memory wavefronts of the CK-step
-loads/stores for a layout [k3][k2][s][k1] with strides (1, 6, S2, S3) and a lane -> task map.
-64-bit accesses: a warp instruction is served per half-warp; wavefronts = max distinct addresses
-per 8-byte bank (16 banks)."""
-import itertools, sys
-N = 6
-def wf(addrs):  # addrs: list of (lane, addr) active
+"""Bank model of the warp-per-element kernel (csrc/stp_wpe.cu): shared-memory wavefronts of one
+CK step (both phases: term loads, partial loads, stores) for the compute layout
+[field][k3][k2][k1] with strides (FS, S3, S2, 1) and a lane -> task table that mirrors
+build_tasks().  64-bit accesses are served per half-warp; wavefronts of an instruction = sum over
+the two half-warps of the largest number of distinct addresses on one 8-byte bank (16 banks).
+Usage: python tools/wpe_bank_model.py [N]      (searches S2, S3, FS; prints the best layouts)"""
+import sys
+
+SXX, SYY, SZZ, SXY, SXZ, SYZ, U, V, W = range(9)
+
+
+def wf(addrs):
+    """addrs[lane] for 32 lanes -> wavefronts"""
     tot = 0
     for h in (0, 1):
         banks = {}
-        for lane, a in addrs:
-            if lane // 16 == h:
-                banks.setdefault(a % 16, set()).add(a)
-        if banks:
-            tot += max(len(v) for v in banks.values())
+        for a in addrs[16 * h:16 * h + 16]:
+            banks.setdefault(a % 16, set()).add(a)
+        tot += max(len(v) for v in banks.values())
     return tot
 
-def strides(S2, S3):
-    return {'x': 1, 'y': S2, 'z': S3}
 
-def model(S2, S3, tasksA, tasksB, verbose=False):
-    st = strides(S2, S3)
-    total = 0
-    ideal = 0
-    for tasks in (tasksA, tasksB):
-        # each task: list of terms (field, d, o, fixed_dir, fixed_idx); loads per (j, l)
-        for term in (0, 1):
-            for j in range(N):
-                for l in range(N):
-                    addrs = []
-                    for lane, t in enumerate(tasks):
-                        if t is None or t[term] is None: continue
-                        f, d, o, fd, fi = t[term]
-                        addrs.append((lane, 6 * f + l * st[d] + j * st[o] + fi * st[fd]))
-                    if addrs:
-                        total += wf(addrs); ideal += (len(addrs) + 15) // 16
-        # stores of the result (dst field, tile dirs) : index (i, j) over the tile of term 0 dst
-        for i in range(N):
-            for j in range(N):
-                for which in (2, 3):
-                    addrs = []
-                    for lane, t in enumerate(tasks):
-                        if t is None or len(t) <= which or t[which] is None: continue
-                        f, d, o, fd, fi = t[which]
-                        addrs.append((lane, 6 * f + i * st[d] + j * st[o] + fi * st[fd]))
-                    if addrs:
-                        total += wf(addrs); ideal += (len(addrs) + 15) // 16
-    return total, ideal
+def build(N, S2, S3, FS, orderA=None, orderB=None):
+    st = (1, S2, S3)
+    DUMMY = 9 * FS
+    idle = dict(srcA=0, saA=0, sbA=0, srcB=0, saB=0, sbB=0, dst1=DUMMY, dst2=DUMMY, dst3=DUMMY, part=DUMMY, s2a=0, s2b=0)
 
-SXX, SYY, SZZ, SXY, SXZ, SYZ, U, V, W = range(9)
-def build(part_orient='x', orderA=None):
-    # phase A: shear tasks and partial pairs.  task = (termA, termB, dst1, dst2)
-    A = []
-    for k in range(N): A.append(((V, 'x', 'y', 'z', k), (U, 'y', 'x', 'z', k), (SXY, 'x', 'y', 'z', k), None))
-    for k in range(N): A.append(((W, 'x', 'z', 'y', k), (U, 'z', 'x', 'y', k), (SXZ, 'x', 'z', 'y', k), None))
-    for k in range(N): A.append(((W, 'y', 'z', 'x', k), (V, 'z', 'y', 'x', k), (SYZ, 'y', 'z', 'x', k), None))
-    # partial units: z-derivative of src -> dst slot, tile (z, o) at fixed third dir
-    units = []
-    for src, dst in ((SXZ, U), (SYZ, V), (SZZ, W), (W, SZZ)):
-        for k in range(N):
-            o, fd = ('x', 'y') if part_orient == 'x' else ('y', 'x')
-            units.append(((src, 'z', o, fd, k), (dst, 'z', o, fd, k)))
-    return A, units
+    def tile(da, db, dc, k, fA, fB, dst, part):
+        t = dict(idle)
+        t.update(saA=st[da], saB=st[da], sbA=st[db], sbB=st[db], srcA=fA * FS + k * st[dc], srcB=fB * FS + k * st[dc],
+                 dst1=dst * FS + k * st[dc], part=DUMMY if part < 0 else part * FS + k * st[dc])
+        return t
+    A, B = [], []
+    for k in range(N): A.append(tile(0, 1, 2, k, V, U, SXY, -1))
+    for k in range(N): A.append(tile(0, 2, 1, k, W, U, SXZ, -1))
+    for k in range(N): A.append(tile(1, 2, 0, k, W, V, SYZ, -1))
+    psrc, pdst = (SXZ, SYZ, SZZ, W), (U, V, W, SZZ)
+    for i in range(2 * N):
+        u1, u2, k = i // N, 2 + i // N, i % N
+        t = dict(idle)
+        t.update(saA=st[2], sbA=st[0], srcA=psrc[u1] * FS + k * st[1], dst1=pdst[u1] * FS + k * st[1],
+                 saB=st[0], sbB=st[2], srcB=psrc[u2] * FS + k * st[1], dst2=pdst[u2] * FS + k * st[1], s2a=st[0], s2b=st[2])
+        A.append(t)
+    for k in range(N): B.append(tile(0, 1, 2, k, SXX, SXY, U, U))
+    for k in range(N): B.append(tile(0, 1, 2, k, SXY, SYY, V, V))
+    for k in range(N): B.append(tile(0, 1, 2, k, SXZ, SYZ, W, W))
+    for k in range(N):
+        t = tile(0, 1, 2, k, U, V, SXX, SZZ)
+        t.update(dst2=SYY * FS + k * st[2], dst3=SZZ * FS + k * st[2], s2a=st[0], s2b=st[1])
+        B.append(t)
 
-def phaseB():
-    B = []
-    for k in range(N): B.append(((SXX, 'x', 'y', 'z', k), (SXY, 'y', 'x', 'z', k), (U, 'x', 'y', 'z', k), None))
-    for k in range(N): B.append(((SXY, 'x', 'y', 'z', k), (SYY, 'y', 'x', 'z', k), (V, 'x', 'y', 'z', k), None))
-    for k in range(N): B.append(((SXZ, 'x', 'y', 'z', k), (SYZ, 'y', 'x', 'z', k), (W, 'x', 'y', 'z', k), None))
-    for k in range(N): B.append(((U, 'x', 'y', 'z', k), (V, 'y', 'x', 'z', k), (SXX, 'x', 'y', 'z', k), (SYY, 'x', 'y', 'z', k)))
-    return B
+    def place(tasks, order):
+        lanes = [dict(idle) for _ in range(32)]
+        for i, t in enumerate(tasks):
+            lanes[order[i] if order else i] = t
+        return lanes
+    return place(A, orderA), place(B, orderB)
+
+
+def step_wavefronts(N, lanesA, lanesB):
+    tot = 0
+    for ph, lanes in ((0, lanesA), (1, lanesB)):
+        for ib in range(N):
+            for l in range(N):
+                tot += wf([t['srcA'] + l * t['saA'] + ib * t['sbA'] for t in lanes])
+        for ia in range(N):
+            for l in range(N):
+                tot += wf([t['srcB'] + ia * t['saB'] + l * t['sbB'] for t in lanes])
+        for ia in range(N):
+            for ib in range(N):
+                if ph == 1:
+                    tot += wf([t['part'] + ia * t['saA'] + ib * t['sbA'] for t in lanes])
+                tot += wf([t['dst1'] + ia * t['saA'] + ib * t['sbA'] for t in lanes])
+                tot += wf([t['dst2'] + ia * t['s2a'] + ib * t['s2b'] for t in lanes])
+                if ph == 1:
+                    tot += wf([t['dst3'] + ia * t['s2a'] + ib * t['s2b'] for t in lanes])
+    return tot
+
+
+def ideal(N):
+    # instructions x 2 half-warps (every phase has lanes in both halves)
+    return 2 * (2 * 2 * N * N + N * N * (2 + 4))
+
 
 if __name__ == '__main__':
-    best = []
-    for po in ('x', 'y'):
-        A, units = build(po)
-        # pairings of the 24 partial units onto 12 lanes: (unit i, unit i+12) or (2i, 2i+1)
-        for pairing in ('half', 'adjacent', 'stride6'):
-            if pairing == 'half': pairs = [(units[i], units[i + 12]) for i in range(12)]
-            elif pairing == 'adjacent': pairs = [(units[2 * i], units[2 * i + 1]) for i in range(12)]
-            else: pairs = [(units[(i % 6) + 12 * (i // 6)], units[(i % 6) + 12 * (i // 6) + 6]) for i in range(12)]
-            tA = list(A) + [(p[0][0], p[1][0], p[0][1], p[1][1]) for p in pairs]
-            tB = phaseB()
-            for S2 in range(54, 72, 2):
-                for p3 in range(0, 34, 2):
-                    S3 = 6 * S2 + p3
-                    t, i = model(S2, S3, tA, tB)
-                    best.append((t, i, po, pairing, S2, S3))
-    best.sort()
-    for b in best[:15]: print(b)
-    print('compact', [b for b in best if b[4] == 54 and b[5] == 324])
+    N = int(sys.argv[1]) if len(sys.argv) > 1 else 6
+    res = []
+    for S2 in range(N, N + 4):
+        for S3 in range(N * S2, N * S2 + 12):
+            for FS in range(N * S3, N * S3 + 18):
+                a, b = build(N, S2, S3, FS)
+                res.append((step_wavefronts(N, a, b), S2, S3, FS))
+    res.sort()
+    print('ideal', ideal(N))
+    for r in res[:12]: print(r)
+    cur = (N, 37 if N == 6 else 17, 223 if N == 6 else 69)
+    a, b = build(N, *cur)
+    print('current', cur, step_wavefronts(N, a, b))
