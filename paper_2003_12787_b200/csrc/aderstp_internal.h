@@ -12,6 +12,7 @@ constexpr int kMaxOrder = 10;
 constexpr int kMaxM = 16;      // quantities of the term-table kernels (stp_kernel, corrector tables)
 constexpr int kMaxTerms = 4;   // nonzeros per (row s, dim d) of a table PDE
 constexpr long long kGenScratchBytes = 512ll << 20;  // general kernel's global scratch per launch
+constexpr long long kWpeMinElems = 16384;  // stp_wpe beats stp_dmmap at nDof 4 from ~9,000 elements on
 
 // Host-side basis, derived from scratch (basis.cpp).  d[k*n + l] = phi_l'(x_k).
 struct HostBasis {
@@ -62,7 +63,8 @@ struct LaunchPlan {
   int aos_staged = 0;                // env ADERSTP_AOS_STAGED=1: reference layout through the transposes
   int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel
   int no_gdense = 0;                 // env ADERSTP_NO_GDENSE=1: dense systems at nDof 8 on stp_general
-  int wpe = 0;                       // warp-per-element kernel at nDof 4, 6 (env ADERSTP_WPE=0|1)
+  int wpe = 2;                       // warp-per-element kernel: 0 off, 1 forced at nDof 4 / 6, 2 automatic
+                                     // (nDof 4 from kWpeMinElems elements on); env ADERSTP_WPE=0|1
 };
 
 struct BatchArgs {

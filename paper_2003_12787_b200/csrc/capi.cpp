@@ -300,7 +300,7 @@ int aderstp_plan_create(const aderstp_config* cfg, aderstp_plan** out) {
     const char* nq = std::getenv("ADERSTP_NO_DMMAP");
     lp.no_dmmap = (nq && nq[0] == '1') ? 1 : 0;
     const char* wp = std::getenv("ADERSTP_WPE");
-    lp.wpe = wp ? (wp[0] == '1' ? 1 : 0) : 0;
+    lp.wpe = wp ? (wp[0] == '1' ? 1 : 0) : 2;  // 2: automatic (large nDof 4 batches)
     const char* ng = std::getenv("ADERSTP_NO_GDENSE");
     lp.no_gdense = (ng && ng[0] == '1') ? 1 : 0;
     const char* ac = std::getenv("ADERSTP_AOS_CHUNK");

@@ -1,8 +1,10 @@
-// Elastic STP for even nDof <= 6 (C2 / C5 nDof 6, C1 nDof 4): one WARP per element, no CTA barrier.
+// Elastic STP for even nDof <= 6: one WARP per element, no CTA barrier.  The default for nDof 4
+// batches of >= kWpeMinElems elements (96.5 vs 78.3 M elem/s for stp_dmmap); at nDof 6 opt-in
+// (ADERSTP_WPE=1: 21.0 vs 30.4 M).
 //
 // The padded-DMMA kernel (stp_dmma.cu) carries (8/N)^2 of the useful fragment traffic and fp64
 // work at nDof <= 6 and spends its largest stall on CTA barriers.  Here every warp owns an element
-// from load to store (persistent warps, 7 per SM, each with 2 x 9 fields of shared memory), and a
+// from load to store (persistent warps, 7 / 16 per SM at nDof 6 / 4, each with 2 x 9 fields of shared memory), and a
 // CK step r <- c_o q + L r (Horner form, see stp_dmma8.cu; proj/src/stp_splitck.cpp:46-70) is two
 // warp-synchronous phases of TILE tasks: a lane owns an N x N tile (a, b) of one target field at a
 // fixed third index, keeps its N^2 accumulators in registers and contracts
@@ -34,16 +36,20 @@ namespace aderstp {
 namespace {
 
 constexpr int NVW = 9;
-constexpr int WPC = 7;  // warps (= elements in flight) per CTA, one CTA per SM
 enum { MODE_IDLE = 0, MODE_SUM = 1, MODE_NORMAL = 2, MODE_PAIR = 3 };
 
 template <int N>
 struct GeoW {
   static constexpr int N2 = N * N, N3 = N * N * N;
+  // warps (= elements in flight) per CTA, one CTA per SM: as many as the shared memory holds
+  static constexpr int WPC = N == 6 ? 7 : 16;
   // compute layout [field][k3][k2][k1]: strides in doubles (bank model: tools/wpe_bank_model.py)
-  static constexpr int S2 = N;
-  static constexpr int S3 = N == 6 ? 37 : 17;
-  static constexpr int FS = N == 6 ? 223 : 69;
+  static constexpr int S2 = N == 6 ? 6 : 5;
+  static constexpr int S3 = N == 6 ? 37 : 21;
+  static constexpr int FS = N == 6 ? 223 : 94;
+  // idle lanes / absent outputs: predicated off (N = 4: whole half-warps fall idle, +8 %) or sent to
+  // the dummy slot with plain stores (N = 6: the predicated form measured -10 %)
+  static constexpr bool PRED = N == 4;
   static constexpr int FACE = N2 * NVW;                       // one face array
   static constexpr int BUF = ((NVW * FS > 6 * FACE ? NVW * FS : 6 * FACE) + 2) & ~1;  // doubles, even, >= fields + 1
   static constexpr int DUMMY = NVW * FS;                      // a slot no field uses (write-only sink)
@@ -96,6 +102,19 @@ constexpr unsigned long long pack_flux_w(int d, bool coef) {
   return v;
 }
 
+// predicated shared-memory store (one @p STS; a plain `if` makes ptxas branch around each store)
+template <bool PRED>
+__device__ __forceinline__ void sts_if(bool pred, double* p, double v) {
+  if (!PRED) {
+    *p = v;
+    return;
+  }
+  asm volatile(
+      "{\n .reg .pred q;\n .reg .u64 a;\n setp.ne.s32 q, %2, 0;\n cvta.to.shared.u64 a, %0;\n @q st.shared.f64 [a], %1;\n}\n" ::"l"(p),
+      "d"(v), "r"((int)pred)
+      : "memory");
+}
+
 // One phase of a CK step for the calling lane's task: R (source iterate), W (destination).
 // Branch-free: every lane runs every load, FMA and store; idle lanes and unused outputs have zero
 // strides and the buffer's dummy slot as destination.  out1 = co q1 + c1 (a + b + p) + c2 a; the
@@ -108,6 +127,10 @@ __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const doub
   // the strides are opaque per call: ptxas would otherwise hoist all 2 N^2 tile offsets out of the
   // CK loop and spill them
   asm volatile("" : "+r"(t.saA), "+r"(t.sbA), "+r"(t.saB), "+r"(t.sbB));
+  // idle lanes and absent outputs are predicated off (no wavefront for a half-warp without a
+  // live lane): the second / third outputs sit in one half-warp (build_tasks)
+  const bool act = !G::PRED || t.mode != MODE_IDLE;
+  const bool has2 = !G::PRED || (PHASEB ? t.mode == MODE_NORMAL : t.mode == MODE_PAIR);
   double accA[N][N], accB[N][N];
 #pragma unroll
   for (int i = 0; i < N; ++i)
@@ -119,7 +142,7 @@ __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const doub
     for (int ib = 0; ib < N; ++ib) {
       double v[N];
 #pragma unroll
-      for (int l = 0; l < N; ++l) v[l] = p[l * t.saA];
+      for (int l = 0; l < N; ++l) v[l] = act ? p[l * t.saA] : 0.0;
 #pragma unroll
       for (int l = 0; l < N; ++l)
 #pragma unroll
@@ -133,7 +156,7 @@ __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const doub
     for (int ia = 0; ia < N; ++ia) {
       double v[N];
 #pragma unroll
-      for (int l = 0; l < N; ++l) v[l] = p[l * t.sbB];
+      for (int l = 0; l < N; ++l) v[l] = act ? p[l * t.sbB] : 0.0;
 #pragma unroll
       for (int l = 0; l < N; ++l)
 #pragma unroll
@@ -158,14 +181,18 @@ __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const doub
     for (int ib = 0; ib < N; ++ib) {
       const double a = accA[ia][ib], b = accB[ia][ib];
       if (PHASEB) {
-        const double p = wp[ib * t.sbA];
+        const double p = act ? wp[ib * t.sbA] : 0.0;
         const double S = a + b + p, cS = c1 * S;
-        w1[ib * t.sbA] = fma(co, tm_double(r1, ib), fma(c2, a, cS));
-        w2[ib * t.s2b] = fma(co, tm_double(r2, ib), fma(c2, b, cS));
-        w3[ib * t.s2b] = fma(co, tm_double(r3, ib), fma(c2, p, cS));
+        const double o1 = fma(co, tm_double(r1, ib), fma(c2, a, cS));
+        const double o2 = fma(co, tm_double(r2, ib), fma(c2, b, cS));
+        const double o3 = fma(co, tm_double(r3, ib), fma(c2, p, cS));
+        sts_if<G::PRED>(act, w1 + ib * t.sbA, o1);
+        sts_if<G::PRED>(has2, w2 + ib * t.s2b, o2);
+        sts_if<G::PRED>(has2, w3 + ib * t.s2b, o3);
       } else {
-        w1[ib * t.sbA] = fma(co, tm_double(r1, ib), fma(c2, a, c1 * (a + b)));
-        w2[ib * t.s2b] = b;
+        const double o1 = fma(co, tm_double(r1, ib), fma(c2, a, c1 * (a + b)));
+        sts_if<G::PRED>(act, w1 + ib * t.sbA, o1);
+        sts_if<G::PRED>(has2, w2 + ib * t.s2b, b);
       }
     }
     w1 += t.saA;
@@ -194,9 +221,9 @@ __device__ __forceinline__ unsigned fill_tile(const double* q, int off, int sa, 
 }
 
 template <int N>
-__global__ void __launch_bounds__(WPC * 32, 1) stp_wpe_kernel(ParamsW kp, BatchArgs a, unsigned int* status) {
+__global__ void __launch_bounds__(GeoW<N>::WPC * 32, 1) stp_wpe_kernel(ParamsW kp, BatchArgs a, unsigned int* status) {
   using G = GeoW<N>;
-  constexpr int N2 = G::N2, N3 = G::N3, S2 = G::S2, S3 = G::S3, FS = G::FS, FACE = G::FACE;
+  constexpr int N2 = G::N2, N3 = G::N3, S2 = G::S2, S3 = G::S3, FS = G::FS, FACE = G::FACE, WPC = G::WPC;
   extern __shared__ __align__(16) double smw[];
   __shared__ uint32_t tmem_base_s;
   __shared__ TaskW task_s[2][32];
@@ -213,7 +240,8 @@ __global__ void __launch_bounds__(WPC * 32, 1) stp_wpe_kernel(ParamsW kp, BatchA
   const int qs = kp.q_stride;
   const long long estride = (long long)gridDim.x * WPC;
 
-  for (long long e = (long long)blockIdx.x * WPC + warp; e < a.n_elem; e += estride) {
+  // element = CTA + grid * (warp + WPC * round): a small batch spreads over the SMs first
+  for (long long e = blockIdx.x + (long long)gridDim.x * warp; e < a.n_elem; e += estride) {
     // ---- material -----------------------------------------------------------------------------
     double c4[4];
     {
@@ -278,9 +306,12 @@ __global__ void __launch_bounds__(WPC * 32, 1) stp_wpe_kernel(ParamsW kp, BatchA
       unsigned bad = 0;
       const TaskW tA = task_s[0][lane], tB = task_s[1][lane];
       const bool nB = tB.mode == MODE_NORMAL;
-      bad |= fill_tile<N>(B0, nB ? tB.dst2 : tA.dst1, nB ? tB.saA : tA.saA, nB ? tB.sbA : tA.sbA, tq, kp.check);
-      bad |= fill_tile<N>(B0, tB.dst1, tB.saA, tB.sbA, tq + G::QC, kp.check);
-      bad |= fill_tile<N>(B0, nB ? tB.dst3 : 0, tB.saA, tB.sbA, tq + 2 * G::QC, kp.check);
+      // lanes without a tile in a region copy field 0 (any finite-or-not value: never used, never checked)
+      const bool r0 = nB || tA.mode == MODE_SUM, r1 = tB.mode != MODE_IDLE;
+      bad |= fill_tile<N>(B0, nB ? tB.dst2 : r0 ? tA.dst1 : 0, nB ? tB.saA : tA.saA, nB ? tB.sbA : tA.sbA, tq,
+                          kp.check && r0);
+      bad |= fill_tile<N>(B0, r1 ? tB.dst1 : 0, tB.saA, tB.sbA, tq + G::QC, kp.check && r1);
+      bad |= fill_tile<N>(B0, nB ? tB.dst3 : 0, tB.saA, tB.sbA, tq + 2 * G::QC, kp.check && nB);
       tm_wait_st();
       if (bad) flags |= 1u;
     }
@@ -465,6 +496,7 @@ void build_tasks(TaskW (&tab)[2][32]) {
   for (int k = 0; k < N; ++k) tab[0][lane++] = tile(1, 2, 0, k, Wq, V, SYZ, 2, -1);
   // phase A: raw z derivatives, two per lane: d_z sxz -> u', d_z syz -> v' | d_z szz -> w', d_z w -> szz'
   const int psrc[4] = {SXZ, SYZ, SZZ, Wq}, pdst[4] = {U, V, Wq, SZZ};
+  if (lane < 16 && 16 + 2 * N <= 32) lane = 16;  // the raw-derivative lanes share one half-warp
   for (int i = 0; i < 2 * N; ++i) {
     const int u1 = i / N, u2 = 2 + i / N, k = i % N;  // tiles at fixed k2 = k
     TaskW t{};
@@ -528,9 +560,8 @@ cudaError_t launch_wpe_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
   if (a.n_elem == 0) return cudaSuccess;
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const long long need = (a.n_elem + WPC - 1) / WPC;
-  const unsigned grid = (unsigned)(need < sms ? need : sms);
-  kern<<<grid, WPC * 32, G::SMEM, stream>>>(kp, a, p.d_status);
+  const unsigned grid = (unsigned)(a.n_elem < sms ? a.n_elem : sms);
+  kern<<<grid, G::WPC * 32, G::SMEM, stream>>>(kp, a, p.d_status);
   return cudaGetLastError();
 }
 
@@ -538,7 +569,8 @@ cudaError_t launch_wpe_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
 
 bool wpe_applicable(const LaunchPlan& p, const BatchArgs& a) {
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
-  return p.wpe && (p.n == 4 || p.n == 6) && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
+  const bool sel = p.wpe == 1 ? (p.n == 4 || p.n == 6) : p.wpe == 2 && p.n == 4 && a.n_elem >= kWpeMinElems;
+  return sel && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
          p.layout == ADERSTP_LAYOUT_AOSOA && p.out_stride == 9 && p.q_stride >= 9 && p.q_stride <= 64 &&
          !p.force_generic && !a.u_next && a.qavg && al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) &&
          al16(a.face_f);

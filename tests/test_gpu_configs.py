@@ -118,6 +118,35 @@ def test_full_size_config_parity(stp, oracle, bench, name):
                     out.face_q[idx].cpu().numpy(), out.face_f[idx].cpu().numpy()), cfg["q_stride"])
 
 
+@pytest.mark.parametrize("E", [16384, 40000])
+def test_ndof4_large_batch_dispatch_parity(stp, oracle, monkeypatch, E):
+    """nDof 4 from 16,384 elements on runs on the warp-per-element kernel (csrc/stp_wpe.cu,
+    kWpeMinElems; persistent warps walking several elements each, a ragged last round at 40,000):
+    oracle parity on the first, last and 30 interior elements, and agreement with the padded-DMMA
+    kernel (ADERSTP_WPE=0) on every element."""
+    S = stp
+    n = 4
+    monkeypatch.delenv("ADERSTP_WPE", raising=False)
+    q, par = S.generate(0, SEED, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
+    dt = O.cfl_dt(n, 6.0)
+    plan = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
+    out = plan.predict(q, dt, par=par)
+    plan.status()
+    rng = np.random.default_rng(E)
+    idx = torch.tensor(sorted({0, E - 1, *rng.integers(1, E - 1, 30).tolist()}), device="cuda")
+    _check_outputs(S, oracle, n, q[idx].cpu().numpy(), par[idx].cpu().numpy(), dt,
+                   (out.qavg[idx].cpu().numpy(), out.favg[idx].cpu().numpy(),
+                    out.face_q[idx].cpu().numpy(), out.face_f[idx].cpu().numpy()), 9)
+    monkeypatch.setenv("ADERSTP_WPE", "0")
+    plan0 = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
+    out0 = plan0.predict(q, dt, par=par)
+    plan0.status()
+    for a, b in ((out.qavg, out0.qavg), (out.favg, out0.favg), (out.face_q, out0.face_q), (out.face_f, out0.face_f)):
+        a2, b2 = a.reshape(E, -1), b.reshape(E, -1)
+        scale = torch.maximum(b2.abs().amax(dim=1), torch.tensor(1e-300, device="cuda", dtype=torch.float64))
+        assert float(((a2 - b2).abs().amax(dim=1) / scale).max()) <= TOL
+
+
 @pytest.mark.parametrize("name", ["c5", "c5n6"])
 def test_c5_chunked_launch_loop_parity(stp, oracle, bench, name):
     """C5 through bench.py's own loop: the rank's shard of 1,048,576 elements resident in HBM,

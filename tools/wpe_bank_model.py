@@ -11,24 +11,26 @@ SXX, SYY, SZZ, SXY, SXZ, SYZ, U, V, W = range(9)
 
 
 def wf(addrs):
-    """addrs[lane] for 32 lanes -> wavefronts"""
+    """addrs[lane] for 32 lanes (None: predicated off) -> wavefronts"""
     tot = 0
     for h in (0, 1):
         banks = {}
         for a in addrs[16 * h:16 * h + 16]:
-            banks.setdefault(a % 16, set()).add(a)
-        tot += max(len(v) for v in banks.values())
+            if a is not None:
+                banks.setdefault(a % 16, set()).add(a)
+        if banks:
+            tot += max(len(v) for v in banks.values())
     return tot
 
 
 def build(N, S2, S3, FS, orderA=None, orderB=None):
     st = (1, S2, S3)
     DUMMY = 9 * FS
-    idle = dict(srcA=0, saA=0, sbA=0, srcB=0, saB=0, sbB=0, dst1=DUMMY, dst2=DUMMY, dst3=DUMMY, part=DUMMY, s2a=0, s2b=0)
+    idle = dict(srcA=0, saA=0, sbA=0, srcB=0, saB=0, sbB=0, dst1=DUMMY, dst2=DUMMY, dst3=DUMMY, part=DUMMY, s2a=0, s2b=0, act=False, has2=False)
 
     def tile(da, db, dc, k, fA, fB, dst, part):
         t = dict(idle)
-        t.update(saA=st[da], saB=st[da], sbA=st[db], sbB=st[db], srcA=fA * FS + k * st[dc], srcB=fB * FS + k * st[dc],
+        t.update(act=True, saA=st[da], saB=st[da], sbA=st[db], sbB=st[db], srcA=fA * FS + k * st[dc], srcB=fB * FS + k * st[dc],
                  dst1=dst * FS + k * st[dc], part=DUMMY if part < 0 else part * FS + k * st[dc])
         return t
     A, B = [], []
@@ -39,7 +41,7 @@ def build(N, S2, S3, FS, orderA=None, orderB=None):
     for i in range(2 * N):
         u1, u2, k = i // N, 2 + i // N, i % N
         t = dict(idle)
-        t.update(saA=st[2], sbA=st[0], srcA=psrc[u1] * FS + k * st[1], dst1=pdst[u1] * FS + k * st[1],
+        t.update(act=True, has2=True, saA=st[2], sbA=st[0], srcA=psrc[u1] * FS + k * st[1], dst1=pdst[u1] * FS + k * st[1],
                  saB=st[0], sbB=st[2], srcB=psrc[u2] * FS + k * st[1], dst2=pdst[u2] * FS + k * st[1], s2a=st[0], s2b=st[2])
         A.append(t)
     for k in range(N): B.append(tile(0, 1, 2, k, SXX, SXY, U, U))
@@ -47,15 +49,28 @@ def build(N, S2, S3, FS, orderA=None, orderB=None):
     for k in range(N): B.append(tile(0, 1, 2, k, SXZ, SYZ, W, W))
     for k in range(N):
         t = tile(0, 1, 2, k, U, V, SXX, SZZ)
-        t.update(dst2=SYY * FS + k * st[2], dst3=SZZ * FS + k * st[2], s2a=st[0], s2b=st[1])
+        t.update(has2=True, dst2=SYY * FS + k * st[2], dst3=SZZ * FS + k * st[2], s2a=st[0], s2b=st[1])
         B.append(t)
 
-    def place(tasks, order):
+    def place(tasks, order, pair_start=None):
         lanes = [dict(idle) for _ in range(32)]
         for i, t in enumerate(tasks):
-            lanes[order[i] if order else i] = t
+            lane = order[i] if order else i
+            if not order and pair_start is not None and i >= 3 * N:
+                lane = pair_start + i - 3 * N
+            lanes[lane] = t
         return lanes
-    return place(A, orderA), place(B, orderB)
+    ps = 16 if 3 * N < 16 and 16 + 2 * N <= 32 else None
+    return place(A, orderA, ps), place(B, orderB)
+
+
+PRED = True  # idle lanes / absent outputs predicated off (the N = 4 instance); False: dummy slot
+
+
+def sel(t, key, a):
+    if not PRED:
+        return a
+    return a if t[key] else None
 
 
 def step_wavefronts(N, lanesA, lanesB):
@@ -63,24 +78,27 @@ def step_wavefronts(N, lanesA, lanesB):
     for ph, lanes in ((0, lanesA), (1, lanesB)):
         for ib in range(N):
             for l in range(N):
-                tot += wf([t['srcA'] + l * t['saA'] + ib * t['sbA'] for t in lanes])
+                tot += wf([sel(t, 'act', t['srcA'] + l * t['saA'] + ib * t['sbA']) for t in lanes])
         for ia in range(N):
             for l in range(N):
-                tot += wf([t['srcB'] + ia * t['saB'] + l * t['sbB'] for t in lanes])
+                tot += wf([sel(t, 'act', t['srcB'] + ia * t['saB'] + l * t['sbB']) for t in lanes])
         for ia in range(N):
             for ib in range(N):
                 if ph == 1:
-                    tot += wf([t['part'] + ia * t['saA'] + ib * t['sbA'] for t in lanes])
-                tot += wf([t['dst1'] + ia * t['saA'] + ib * t['sbA'] for t in lanes])
-                tot += wf([t['dst2'] + ia * t['s2a'] + ib * t['s2b'] for t in lanes])
+                    tot += wf([sel(t, 'act', t['part'] + ia * t['saA'] + ib * t['sbA']) for t in lanes])
+                tot += wf([sel(t, 'act', t['dst1'] + ia * t['saA'] + ib * t['sbA']) for t in lanes])
+                tot += wf([sel(t, 'has2', t['dst2'] + ia * t['s2a'] + ib * t['s2b']) for t in lanes])
                 if ph == 1:
-                    tot += wf([t['dst3'] + ia * t['s2a'] + ib * t['s2b'] for t in lanes])
+                    tot += wf([sel(t, 'has2', t['dst3'] + ia * t['s2a'] + ib * t['s2b']) for t in lanes])
     return tot
 
 
 def ideal(N):
-    # instructions x 2 half-warps (every phase has lanes in both halves)
-    return 2 * (2 * 2 * N * N + N * N * (2 + 4))
+    # one wavefront per 16 live lanes (or part thereof) of every instruction
+    h = lambda n: (n + 15) // 16
+    a = 2 * N * N * h(5 * N) + N * N * (h(5 * N) + 1)
+    b = 2 * N * N * h(4 * N) + N * N * (2 * h(4 * N) + 2)
+    return a + b
 
 
 if __name__ == '__main__':

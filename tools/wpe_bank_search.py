@@ -6,34 +6,39 @@ import math
 import random
 import sys
 
-from wpe_bank_model import build, wf
+from wpe_bank_model import build, sel, wf
 
 
 def phase_cost(N, lanes, ph):
     tot = 0
     for ib in range(N):
         for l in range(N):
-            tot += wf([t['srcA'] + l * t['saA'] + ib * t['sbA'] for t in lanes])
+            tot += wf([sel(t, 'act', t['srcA'] + l * t['saA'] + ib * t['sbA']) for t in lanes])
     for ia in range(N):
         for l in range(N):
-            tot += wf([t['srcB'] + ia * t['saB'] + l * t['sbB'] for t in lanes])
+            tot += wf([sel(t, 'act', t['srcB'] + ia * t['saB'] + l * t['sbB']) for t in lanes])
     for ia in range(N):
         for ib in range(N):
             if ph == 1:
-                tot += wf([t['part'] + ia * t['saA'] + ib * t['sbA'] for t in lanes])
-            tot += wf([t['dst1'] + ia * t['saA'] + ib * t['sbA'] for t in lanes])
-            tot += wf([t['dst2'] + ia * t['s2a'] + ib * t['s2b'] for t in lanes])
+                tot += wf([sel(t, 'act', t['part'] + ia * t['saA'] + ib * t['sbA']) for t in lanes])
+            tot += wf([sel(t, 'act', t['dst1'] + ia * t['saA'] + ib * t['sbA']) for t in lanes])
+            tot += wf([sel(t, 'has2', t['dst2'] + ia * t['s2a'] + ib * t['s2b']) for t in lanes])
             if ph == 1:
-                tot += wf([t['dst3'] + ia * t['s2a'] + ib * t['s2b'] for t in lanes])
+                tot += wf([sel(t, 'has2', t['dst3'] + ia * t['s2a'] + ib * t['s2b']) for t in lanes])
     return tot
 
 
 def anneal(N, S2, S3, FS, ph, iters, seed):
     rnd = random.Random(seed)
     a, b = build(N, S2, S3, FS)
-    base = (a, b)[ph]
+    placed = (a, b)[ph]
+    base = [t for t in placed if t['act']] + [t for t in placed if not t['act']]
     ntask = 5 * N if ph == 0 else 4 * N
-    perm = list(range(32))  # perm[lane] = index into base (tasks then idle entries)
+    perm = [base.index(t) if t['act'] else -1 for t in placed]  # start from build()'s placement
+    free = [i for i in range(32) if i >= ntask]
+    for lane in range(32):
+        if perm[lane] < 0:
+            perm[lane] = free.pop()
     cur = phase_cost(N, [base[perm[i]] for i in range(32)], ph)
     best = (cur, list(perm))
     for it in range(iters):
