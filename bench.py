@@ -70,6 +70,10 @@ CONFIGS = {
                     "(nVar padded to 12), Q~U[-1,1], per-element random material"),
     "c4": dict(n=10, elems=65536, dist=1, q_stride=9,
                desc="C4: elastic STP order N=9 (nDof 10), 65,536 elements, Q~N(0,1)"),
+    # order N=3 (nDof 4) as a large batch: not a BASELINE config (C1 has 64 elements); the
+    # warp-per-element kernel stp_wpe takes nDof 4 batches of >= 16,384 elements
+    "n4": dict(n=4, elems=131072, dist=0, q_stride=9,
+               desc="elastic STP order N=3 (nDof 4), 131,072 elements, Q~U[-1,1] (kernel stp_wpe)"),
     # order N=8 (nDof 9): not a BASELINE config, measured because north_star's >=50% target covers
     # every order >= 7
     "n9": dict(n=9, elems=65536, dist=1, q_stride=9,
@@ -88,7 +92,7 @@ SEED = 20031278
 CFL, CP_BOUND = 0.5, 6.0
 # elements timed per step by the CPU reference (C1/C2 the full set, C3-C5 a
 # fixed 16,384-element subset -- elements 0..16,383 of the same seeded workload)
-REFERENCE_SAMPLE = {"c1": 64, "c2": 32768, "c3": 16384, "c4": 16384, "n9": 16384, "c5": 16384, "c5n6": 16384}
+REFERENCE_SAMPLE = {"c1": 64, "n4": 16384, "c2": 32768, "c3": 16384, "c4": 16384, "n9": 16384, "c5": 16384, "c5n6": 16384}
 REFERENCE_REPS = 3
 
 
@@ -784,7 +788,7 @@ def main():
 
     others = {}
     if not args.no_other_configs and world == 1:
-        for name in ("c1", "c2", "c4", "n9"):
+        for name in ("c1", "n4", "c2", "c4", "n9"):
             if name == args.config:
                 continue
             c = CONFIGS[name]
