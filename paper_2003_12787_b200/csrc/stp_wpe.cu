@@ -1,6 +1,6 @@
-// Elastic STP for even nDof <= 6: one WARP per element, no CTA barrier.  The default for nDof 4
-// batches of >= kWpeMinElems elements (96.5 vs 78.3 M elem/s for stp_dmmap); at nDof 6 opt-in
-// (ADERSTP_WPE=1: 21.0 vs 30.4 M).
+// Elastic STP for nDof 4..6: one WARP per element, no CTA barrier.  The default for nDof 4
+// batches of >= kWpeMinElems elements (96.5 vs 78.3 M elem/s for stp_dmmap); at nDof 5 / 6 opt-in
+// (ADERSTP_WPE=1: 36.5 vs 37.7 M and 21.0 vs 30.4 M).
 //
 // The padded-DMMA kernel (stp_dmma.cu) carries (8/N)^2 of the useful fragment traffic and fp64
 // work at nDof <= 6 and spends its largest stall on CTA barriers.  Here every warp owns an element
@@ -42,13 +42,13 @@ template <int N>
 struct GeoW {
   static constexpr int N2 = N * N, N3 = N * N * N;
   // warps (= elements in flight) per CTA, one CTA per SM: as many as the shared memory holds
-  static constexpr int WPC = N == 6 ? 7 : 16;
+  static constexpr int WPC = N == 6 ? 7 : N == 5 ? 10 : 16;
   // compute layout [field][k3][k2][k1]: strides in doubles (bank model: tools/wpe_bank_model.py)
   static constexpr int S2 = N == 6 ? 6 : 5;
-  static constexpr int S3 = N == 6 ? 37 : 21;
-  static constexpr int FS = N == 6 ? 223 : 94;
+  static constexpr int S3 = N == 6 ? 37 : N == 5 ? 25 : 21;
+  static constexpr int FS = N == 6 ? 223 : N == 5 ? 125 : 94;
   // idle lanes / absent outputs: predicated off (N = 4: whole half-warps fall idle, +8 %) or sent to
-  // the dummy slot with plain stores (N = 6: the predicated form measured -10 %)
+  // the dummy slot with plain stores (N = 5, 6: the predicated form measured -6 %, -10 %)
   static constexpr bool PRED = N == 4;
   static constexpr int FACE = N2 * NVW;                       // one face array
   static constexpr int BUF = ((NVW * FS > 6 * FACE ? NVW * FS : 6 * FACE) + 2) & ~1;  // doubles, even, >= fields + 1
@@ -74,25 +74,19 @@ struct ParamsW {
   int check, par_kind, q_stride, prefetch;
 };
 
-__constant__ TaskW kTaskW[2][2][32];  // [N == 6][phase][lane]
+__constant__ TaskW kTaskW[3][2][32];  // [N - 4][phase][lane]
 
 template <int N>
 __device__ __forceinline__ void tm_ld_row(uint32_t ta, uint32_t* r) {
-  if constexpr (N == 6) {
-    tm_ld8(ta, r);
-    tm_ld4(ta + 8, r + 8);
-  } else {
-    tm_ld8(ta, r);
-  }
+  tm_ld8(ta, r);
+  if constexpr (N == 6) tm_ld4(ta + 8, r + 8);
+  if constexpr (N == 5) tm_ld2(ta + 8, r + 8);
 }
 template <int N>
 __device__ __forceinline__ void tm_st_row(uint32_t ta, const uint32_t* r) {
-  if constexpr (N == 6) {
-    tm_st8(ta, r);
-    tm_st4(ta + 8, r + 8);
-  } else {
-    tm_st8(ta, r);
-  }
+  tm_st8(ta, r);
+  if constexpr (N == 6) tm_st4(ta + 8, r + 8);
+  if constexpr (N == 5) tm_st2(ta + 8, r + 8);
 }
 
 // e_in(s, d) / e_coef(s, d) of the 9 output quantities packed 4 bits each
@@ -228,7 +222,7 @@ __global__ void __launch_bounds__(GeoW<N>::WPC * 32, 1) stp_wpe_kernel(ParamsW k
   __shared__ uint32_t tmem_base_s;
   __shared__ TaskW task_s[2][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < 64) task_s[threadIdx.x >> 5][lane] = kTaskW[N == 6][threadIdx.x >> 5][lane];
+  if (threadIdx.x < 64) task_s[threadIdx.x >> 5][lane] = kTaskW[N - 4][threadIdx.x >> 5][lane];
   if (warp == 0) tm_alloc<512>(&tmem_base_s);
   tm_fence_before();
   __syncthreads();
@@ -266,10 +260,36 @@ __global__ void __launch_bounds__(GeoW<N>::WPC * 32, 1) stp_wpe_kernel(ParamsW k
     const double* qe = a.q + e * (long long)(N3 * qs);
     if (kp.prefetch && lane == 0 && e + estride < a.n_elem) {
       const unsigned long long pa = reinterpret_cast<unsigned long long>(a.q + (e + estride) * (long long)(N3 * qs));
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(pa), "r"((unsigned)(8u * N3 * qs)) : "memory");
+      const unsigned long long p0 = pa & ~15ull, p1 = (pa + 8ull * N3 * qs + 15ull) & ~15ull;  // 16-byte bounds
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p0), "r"((unsigned)(p1 - p0)) : "memory");
     }
     if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // B0 was the face staging
     __syncwarp();
+    if constexpr (N % 2 != 0) {  // rows of N doubles are 8-byte aligned only: scalar loads
+      if (qs == NVW) {
+        constexpr int ND = N3 * NVW, IT = (ND + 31) / 32;
+        double v[IT];
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {
+          const int p = lane + 32 * i;
+          v[i] = p < ND ? __ldcs(qe + p) : 0.0;
+        }
+#pragma unroll
+        for (int i = 0; i < IT; ++i) {
+          const int p = lane + 32 * i;
+          if (p < ND) {
+            const int k1 = p % N, r1 = p / N, s = r1 % NVW, k32 = r1 / NVW;
+            B0[s * FS + (k32 / N) * S3 + (k32 % N) * S2 + k1] = v[i];
+          }
+        }
+      } else {
+        const int rowd = qs * N;
+        for (int p = lane; p < N2 * rowd; p += 32) {
+          const int k32 = p / rowd, rem = p - k32 * rowd, s = rem / N, k1 = rem - s * N;
+          if (s < NVW) B0[s * FS + (k32 / N) * S3 + (k32 % N) * S2 + k1] = __ldcs(qe + p);
+        }
+      }
+    } else
     if (qs == NVW) {
       constexpr int NP = N3 * NVW / 2, IT = (NP + 31) / 32;
       double2 v[IT];
@@ -379,6 +399,42 @@ __global__ void __launch_bounds__(GeoW<N>::WPC * 32, 1) stp_wpe_kernel(ParamsW k
     // ---- qavg / favg in output order: lane = (quantity s, k1 pair) of a (k3, k2) row group, so a
     // warp store covers the row group's 9 N contiguous doubles; per-lane flux sources and
     // coefficients are loop constants and every shared / global offset is an immediate ----------
+    if constexpr (N % 2 != 0) {
+      // odd N: rows of N doubles are 8-byte aligned only; lane = (quantity s, k1) of a row group in
+      // passes of 32 lanes, 8-byte stores of consecutive doubles
+      constexpr int RD = NVW * N;  // doubles per row group
+      constexpr unsigned long long IN[3] = {pack_flux_w(0, false), pack_flux_w(1, false), pack_flux_w(2, false)};
+      constexpr unsigned long long CO[3] = {pack_flux_w(0, true), pack_flux_w(1, true), pack_flux_w(2, true)};
+      double* qo = a.qavg + e * (long long)(N3 * NVW);
+      double* fo = a.favg ? a.favg + e * (long long)(3 * N3 * NVW) : nullptr;
+#pragma unroll
+      for (int base = 0; base < RD; base += 32) {
+        const int idx = base + lane;
+        if (idx < RD) {
+          const int s = idx / N, k1 = idx - s * N;
+          const double* sq = Y + s * FS + k1;
+          const double* sf[3];
+          double cf3[3];
+#pragma unroll
+          for (int d = 0; d < 3; ++d) {
+            const int si = (int)((IN[d] >> (4 * s)) & 15), ci = (int)((CO[d] >> (4 * s)) & 15);
+            sf[d] = Y + si * FS + k1;
+            cf3[d] = ci == 0 ? c4[0] : ci == 1 ? c4[1] : ci == 2 ? c4[2] : ci == 3 ? c4[3] : 0.0;
+          }
+#pragma unroll
+          for (int k3 = 0; k3 < N; ++k3)
+#pragma unroll
+            for (int k2 = 0; k2 < N; ++k2) {
+              const int node = k3 * S3 + k2 * S2, o = (k3 * N + k2) * RD + idx;
+              __stcs(qo + o, sq[node]);
+              if (fo) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) __stcs(fo + d * (N3 * NVW) + o, cf3[d] * sf[d][node]);
+              }
+            }
+        }
+      }
+    } else
     {
       constexpr int PR = NVW * N / 2;  // 16-byte pairs per row group
       constexpr unsigned long long IN[3] = {pack_flux_w(0, false), pack_flux_w(1, false), pack_flux_w(2, false)};
@@ -520,6 +576,7 @@ void build_tasks(TaskW (&tab)[2][32]) {
   for (int k = 0; k < N; ++k) tab[1][lane++] = tile(0, 1, 2, k, SXX, SXY, U, 3, U);
   for (int k = 0; k < N; ++k) tab[1][lane++] = tile(0, 1, 2, k, SXY, SYY, V, 3, V);
   for (int k = 0; k < N; ++k) tab[1][lane++] = tile(0, 1, 2, k, SXZ, SYZ, Wq, 3, Wq);
+  if (lane < 16 && lane + N > 16) lane = 16;  // the normal-stress lanes share one half-warp
   for (int k = 0; k < N; ++k) {
     TaskW t = tile(0, 1, 2, k, U, V, SXX, 1, SZZ);
     t.mode = MODE_NORMAL;
@@ -569,7 +626,7 @@ cudaError_t launch_wpe_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
 
 bool wpe_applicable(const LaunchPlan& p, const BatchArgs& a) {
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
-  const bool sel = p.wpe == 1 ? (p.n == 4 || p.n == 6) : p.wpe == 2 && p.n == 4 && a.n_elem >= kWpeMinElems;
+  const bool sel = p.wpe == 1 ? (p.n >= 4 && p.n <= 6) : p.wpe == 2 && p.n == 4 && a.n_elem >= kWpeMinElems;
   return sel && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
          p.layout == ADERSTP_LAYOUT_AOSOA && p.out_stride == 9 && p.q_stride >= 9 && p.q_stride <= 64 &&
          !p.force_generic && !a.u_next && a.qavg && al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) &&
@@ -577,15 +634,17 @@ bool wpe_applicable(const LaunchPlan& p, const BatchArgs& a) {
 }
 
 cudaError_t init_wpe(const LaunchPlan& p) {
-  if (p.n != 4 && p.n != 6) return cudaSuccess;
+  if (p.n < 4 || p.n > 6) return cudaSuccess;
   TaskW tab[2][32];
   if (p.n == 6) build_tasks<6>(tab);
+  else if (p.n == 5) build_tasks<5>(tab);
   else build_tasks<4>(tab);
-  return cudaMemcpyToSymbol(kTaskW, tab, sizeof(tab), sizeof(tab) * (p.n == 6 ? 1 : 0));
+  return cudaMemcpyToSymbol(kTaskW, tab, sizeof(tab), sizeof(tab) * (p.n - 4));
 }
 
 cudaError_t launch_wpe(const LaunchPlan& p, const BatchArgs& a, cudaStream_t stream) {
   if (p.n == 6) return launch_wpe_n<6>(p, a, stream);
+  if (p.n == 5) return launch_wpe_n<5>(p, a, stream);
   if (p.n == 4) return launch_wpe_n<4>(p, a, stream);
   return cudaErrorInvalidValue;
 }

@@ -107,9 +107,10 @@ def test_kernel_variants_agree(stp, oracle, monkeypatch, n):
         assert max(worst.values()) <= TOL, (env, worst)
 
 
-@pytest.mark.parametrize("n,E,qs", [(6, 19, 9), (6, 1037, 9), (6, 50, 12), (4, 19, 9), (4, 2100, 9), (4, 50, 12)])
+@pytest.mark.parametrize("n,E,qs", [(6, 19, 9), (6, 1037, 9), (6, 50, 12), (5, 19, 9), (5, 1500, 9), (5, 50, 12),
+                                    (4, 19, 9), (4, 2100, 9), (4, 50, 12)])
 def test_warp_per_element_kernel(stp, oracle, monkeypatch, n, E, qs):
-    """The opt-in warp-per-element kernel (ADERSTP_WPE=1, csrc/stp_wpe.cu: nDof 4 / 6, persistent
+    """The opt-in warp-per-element kernel (ADERSTP_WPE=1, csrc/stp_wpe.cu: nDof 4 / 5 / 6, persistent
     warps, several elements per warp, ragged last wave, padded input stride) against the oracle."""
     S = stp
     monkeypatch.setenv("ADERSTP_WPE", "1")

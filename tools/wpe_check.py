@@ -54,13 +54,13 @@ def timeit(n, E, wpe, reps=20):
 
 
 if __name__ == "__main__":
-    for n in (6, 4):
+    for n in (6, 5, 4):
         for E, qs in ((1, 9), (50, 9), (1037, 9), (50, 12)):
             try:
                 e = run(n, E, True, qs)
                 print(f"wpe n={n} E={E} qs={qs} errs qavg/face_q/face_f/favg = " + " ".join(f"{x:.2e}" for x in e), flush=True)
             except Exception as ex:  # noqa: BLE001
                 print(f"wpe n={n} E={E} qs={qs} FAILED: {ex}", flush=True)
-    for n, E in ((6, 32768), (4, 131072)):
+    for n, E in ((6, 32768), (5, 65536), (4, 131072)):
         for wpe in (False, True):
             print(f"n={n} E={E} wpe={wpe}: {timeit(n, E, wpe) / 1e6:.2f} M elem/s", flush=True)
