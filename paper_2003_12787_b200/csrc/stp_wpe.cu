@@ -1,6 +1,6 @@
 // Elastic STP for nDof 4..6: one WARP per element, no CTA barrier.  The default for nDof 4
-// batches of >= kWpeMinElems elements (96.5 vs 78.3 M elem/s for stp_dmmap); at nDof 5 / 6 opt-in
-// (ADERSTP_WPE=1: 36.5 vs 37.7 M and 21.0 vs 30.4 M).
+// batches of >= kWpeMinElems elements (99.4 vs 78.3 M elem/s for stp_dmmap); at nDof 5 / 6 opt-in
+// (ADERSTP_WPE=1: 36.6 vs 37.7 M and 21.4 vs 30.4 M).
 //
 // The padded-DMMA kernel (stp_dmma.cu) carries (8/N)^2 of the useful fragment traffic and fp64
 // work at nDof <= 6 and spends its largest stall on CTA barriers.  Here every warp owns an element
@@ -47,8 +47,9 @@ struct GeoW {
   static constexpr int S2 = N == 6 ? 6 : 5;
   static constexpr int S3 = N == 6 ? 37 : N == 5 ? 25 : 21;
   static constexpr int FS = N == 6 ? 223 : N == 5 ? 125 : 94;
-  // idle lanes / absent outputs: predicated off (N = 4: whole half-warps fall idle, +8 %) or sent to
-  // the dummy slot with plain stores (N = 5, 6: the predicated form measured -6 %, -10 %)
+  // idle lanes / absent outputs: skipped by one branch per row and output set (N = 4: whole
+  // half-warps fall idle and cost no wavefront, +14 %) or sent to the dummy slot with plain stores
+  // (N = 5, 6: the branching form measured -5 %, -6 %; an inline-asm predicated store -6 %, -10 %)
   static constexpr bool PRED = N == 4;
   static constexpr int FACE = N2 * NVW;                       // one face array
   static constexpr int BUF = ((NVW * FS > 6 * FACE ? NVW * FS : 6 * FACE) + 2) & ~1;  // doubles, even, >= fields + 1
@@ -96,22 +97,9 @@ constexpr unsigned long long pack_flux_w(int d, bool coef) {
   return v;
 }
 
-// predicated shared-memory store (one @p STS; a plain `if` makes ptxas branch around each store)
-template <bool PRED>
-__device__ __forceinline__ void sts_if(bool pred, double* p, double v) {
-  if (!PRED) {
-    *p = v;
-    return;
-  }
-  asm volatile(
-      "{\n .reg .pred q;\n .reg .u64 a;\n setp.ne.s32 q, %2, 0;\n cvta.to.shared.u64 a, %0;\n @q st.shared.f64 [a], %1;\n}\n" ::"l"(p),
-      "d"(v), "r"((int)pred)
-      : "memory");
-}
-
 // One phase of a CK step for the calling lane's task: R (source iterate), W (destination).
-// Branch-free: every lane runs every load, FMA and store; idle lanes and unused outputs have zero
-// strides and the buffer's dummy slot as destination.  out1 = co q1 + c1 (a + b + p) + c2 a; the
+// Every lane runs every load and FMA; idle lanes and unused outputs have zero strides and the
+// buffer's dummy slot as destination (their stores are skipped in the PRED instance).  out1 = co q1 + c1 (a + b + p) + c2 a; the
 // normal-stress lanes (phase B) also write out2 = co q2 + c1 S + c2 b and out3 = co q3 + c1 S +
 // c2 p; the raw-derivative lanes (phase A: co = c1 = 0, c2 = 1) write a to dst1 and b to dst2.
 template <int N, bool PHASEB>
@@ -171,22 +159,33 @@ __device__ __forceinline__ void run_phase(const ParamsW& kp, TaskW t, const doub
       tm_ld_row<N>(tq + 2 * G::QC + 2 * N * ia, r3);
     }
     tm_wait_ld();
+    double o1[N], o2[N], o3[N];
 #pragma unroll
     for (int ib = 0; ib < N; ++ib) {
       const double a = accA[ia][ib], b = accB[ia][ib];
       if (PHASEB) {
         const double p = act ? wp[ib * t.sbA] : 0.0;
         const double S = a + b + p, cS = c1 * S;
-        const double o1 = fma(co, tm_double(r1, ib), fma(c2, a, cS));
-        const double o2 = fma(co, tm_double(r2, ib), fma(c2, b, cS));
-        const double o3 = fma(co, tm_double(r3, ib), fma(c2, p, cS));
-        sts_if<G::PRED>(act, w1 + ib * t.sbA, o1);
-        sts_if<G::PRED>(has2, w2 + ib * t.s2b, o2);
-        sts_if<G::PRED>(has2, w3 + ib * t.s2b, o3);
+        o1[ib] = fma(co, tm_double(r1, ib), fma(c2, a, cS));
+        o2[ib] = fma(co, tm_double(r2, ib), fma(c2, b, cS));
+        o3[ib] = fma(co, tm_double(r3, ib), fma(c2, p, cS));
       } else {
-        const double o1 = fma(co, tm_double(r1, ib), fma(c2, a, c1 * (a + b)));
-        sts_if<G::PRED>(act, w1 + ib * t.sbA, o1);
-        sts_if<G::PRED>(has2, w2 + ib * t.s2b, b);
+        o1[ib] = fma(co, tm_double(r1, ib), fma(c2, a, c1 * (a + b)));
+        o2[ib] = b;
+      }
+    }
+    // PRED: one branch per row and output set (a branch per store made ptxas emit BSSY / BSYNC
+    // around each; an inline-asm predicated store serialised the schedule): lanes without the
+    // output skip its stores, so a half-warp without a live lane costs no wavefront
+    if (act) {
+#pragma unroll
+      for (int ib = 0; ib < N; ++ib) w1[ib * t.sbA] = o1[ib];
+    }
+    if (has2) {
+#pragma unroll
+      for (int ib = 0; ib < N; ++ib) {
+        w2[ib * t.s2b] = o2[ib];
+        if (PHASEB) w3[ib * t.s2b] = o3[ib];
       }
     }
     w1 += t.saA;
