@@ -123,10 +123,20 @@ def test_warp_per_element_kernel(stp, oracle, monkeypatch, n, E, qs):
     plan.status()
     worst = _compare(S, oracle, n, out, ref, S.LAYOUT_AOSOA, 9)
     assert max(worst.values()) <= TOL, worst
+    # optional outputs: qavg alone, and qavg + favg without faces, match the full call bit for bit
+    o1 = plan.predict(q, dt, par=par, want_favg=False, want_faces=False)
+    o2 = plan.predict(q, dt, par=par, want_faces=False)
+    plan.status()
+    assert torch.equal(o1.qavg, out.qavg) and torch.equal(o2.qavg, out.qavg) and torch.equal(o2.favg, out.favg)
     # non-finite input and bad material are flagged like in the default kernels
     q2 = q.clone()
     q2.view(-1)[7] = float("nan")
     plan.predict(q2, dt, par=par)
+    with pytest.raises(Exception):
+        plan.status()
+    par2 = par.clone()
+    par2[E // 2, 0] = -1.0
+    plan.predict(q, dt, par=par2)
     with pytest.raises(Exception):
         plan.status()
 
