@@ -12,7 +12,8 @@ constexpr int kMaxOrder = 10;
 constexpr int kMaxM = 16;      // quantities of the term-table kernels (stp_kernel, corrector tables)
 constexpr int kMaxTerms = 4;   // nonzeros per (row s, dim d) of a table PDE
 constexpr long long kGenScratchBytes = 512ll << 20;  // general kernel's global scratch per launch
-constexpr long long kWpeMinElems = 16384;  // stp_wpe beats stp_dmmap at nDof 4 from ~9,000 elements on
+// stp_wpe beats stp_dmmap at nDof 4 from ~3,000 elements on, at nDof 5 from ~16,000
+constexpr long long kWpeMinElems4 = 8192, kWpeMinElems5 = 32768;
 
 // Host-side basis, derived from scratch (basis.cpp).  d[k*n + l] = phi_l'(x_k).
 struct HostBasis {
@@ -64,7 +65,7 @@ struct LaunchPlan {
   int no_dmmap = 0;                  // env ADERSTP_NO_DMMAP=1: nDof 4..7 on the line-pass kernel
   int no_gdense = 0;                 // env ADERSTP_NO_GDENSE=1: dense systems at nDof 8 on stp_general
   int wpe = 2;                       // warp-per-element kernel: 0 off, 1 forced at nDof 4 / 6, 2 automatic
-                                     // (nDof 4 from kWpeMinElems elements on); env ADERSTP_WPE=0|1
+                                     // (nDof 4 / 5 from kWpeMinElems4 / 5 elements on); env ADERSTP_WPE=0|1
 };
 
 struct BatchArgs {

@@ -1,6 +1,6 @@
-// Elastic STP for nDof 4..6: one WARP per element, no CTA barrier.  The default for nDof 4
-// batches of >= kWpeMinElems elements (99.4 vs 78.3 M elem/s for stp_dmmap); at nDof 5 / 6 opt-in
-// (ADERSTP_WPE=1: 36.6 vs 37.7 M and 21.4 vs 30.4 M).
+// Elastic STP for nDof 4..6: one WARP per element, no CTA barrier.  The default for large nDof 4
+// and nDof 5 batches (kWpeMinElems4 / 5: 104 vs 78 M and 40.9 vs 37.7 M elem/s for stp_dmmap); at
+// nDof 6 opt-in (ADERSTP_WPE=1: 21.4 vs 30.4 M).
 //
 // The padded-DMMA kernel (stp_dmma.cu) carries (8/N)^2 of the useful fragment traffic and fp64
 // work at nDof <= 6 and spends its largest stall on CTA barriers.  Here every warp owns an element
@@ -35,14 +35,27 @@ namespace aderstp {
 
 namespace {
 
+#ifndef WPE_WPC4
+#define WPE_WPC4 12
+#endif
+#ifndef WPE_WPC5
+#define WPE_WPC5 8
+#endif
+#ifndef WPE_PRED5
+#define WPE_PRED5 0
+#endif
 constexpr int NVW = 9;
 enum { MODE_IDLE = 0, MODE_SUM = 1, MODE_NORMAL = 2, MODE_PAIR = 3 };
 
 template <int N>
 struct GeoW {
   static constexpr int N2 = N * N, N3 = N * N * N;
-  // warps (= elements in flight) per CTA, one CTA per SM: as many as the shared memory holds
-  static constexpr int WPC = N == 6 ? 7 : N == 5 ? 10 : 16;
+  // warps (= elements in flight) per CTA, one CTA per SM.  nDof 6: as many as the shared memory
+  // holds.  nDof 4 / 5: a multiple of the 4 SM sub-partitions whose register budget leaves the
+  // tile accumulators unspilled -- measured nDof 4: 8 / 12 / 16 warps 95.6 / 104.1 / 99.4 M elem/s;
+  // nDof 5: 4 / 8 / 10 warps 33.1 / 40.7 / 36.6 M (10 warps = 3 + 3 + 2 + 2 per sub-partition at 168
+  // registers with spills)
+  static constexpr int WPC = N == 6 ? 7 : N == 5 ? WPE_WPC5 : WPE_WPC4;
   // compute layout [field][k3][k2][k1]: strides in doubles (bank model: tools/wpe_bank_model.py)
   static constexpr int S2 = N == 6 ? 6 : 5;
   static constexpr int S3 = N == 6 ? 37 : N == 5 ? 25 : 21;
@@ -50,7 +63,7 @@ struct GeoW {
   // idle lanes / absent outputs: skipped by one branch per row and output set (N = 4: whole
   // half-warps fall idle and cost no wavefront, +14 %) or sent to the dummy slot with plain stores
   // (N = 5, 6: the branching form measured -5 %, -6 %; an inline-asm predicated store -6 %, -10 %)
-  static constexpr bool PRED = N == 4;
+  static constexpr bool PRED = N == 4 || (N == 5 && WPE_PRED5);
   static constexpr int FACE = N2 * NVW;                       // one face array
   static constexpr int BUF = ((NVW * FS > 6 * FACE ? NVW * FS : 6 * FACE) + 2) & ~1;  // doubles, even, >= fields + 1
   static constexpr int DUMMY = NVW * FS;                      // a slot no field uses (write-only sink)
@@ -625,7 +638,7 @@ cudaError_t launch_wpe_n(const LaunchPlan& p, const BatchArgs& a, cudaStream_t s
 
 bool wpe_applicable(const LaunchPlan& p, const BatchArgs& a) {
   auto al16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15) == 0; };
-  const bool sel = p.wpe == 1 ? (p.n >= 4 && p.n <= 6) : p.wpe == 2 && p.n == 4 && a.n_elem >= kWpeMinElems;
+  const bool sel = p.wpe == 1 ? (p.n >= 4 && p.n <= 6) : p.wpe == 2 && ((p.n == 4 && a.n_elem >= kWpeMinElems4) || (p.n == 5 && a.n_elem >= kWpeMinElems5));
   return sel && p.kind == ADERSTP_PDE_ELASTIC && p.src_comp < 0 &&
          p.layout == ADERSTP_LAYOUT_AOSOA && p.out_stride == 9 && p.q_stride >= 9 && p.q_stride <= 64 &&
          !p.force_generic && !a.u_next && a.qavg && al16(a.q) && al16(a.qavg) && al16(a.favg) && al16(a.face_q) &&

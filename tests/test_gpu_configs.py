@@ -118,14 +118,13 @@ def test_full_size_config_parity(stp, oracle, bench, name):
                     out.face_q[idx].cpu().numpy(), out.face_f[idx].cpu().numpy()), cfg["q_stride"])
 
 
-@pytest.mark.parametrize("E", [16384, 40000])
-def test_ndof4_large_batch_dispatch_parity(stp, oracle, monkeypatch, E):
-    """nDof 4 from 16,384 elements on runs on the warp-per-element kernel (csrc/stp_wpe.cu,
-    kWpeMinElems; persistent warps walking several elements each, a ragged last round at 40,000):
-    oracle parity on the first, last and 30 interior elements, and agreement with the padded-DMMA
-    kernel (ADERSTP_WPE=0) on every element."""
+@pytest.mark.parametrize("n,E", [(4, 8192), (4, 40000), (5, 32768), (5, 40001)])
+def test_ndof4_large_batch_dispatch_parity(stp, oracle, monkeypatch, n, E):
+    """nDof 4 from 8,192 and nDof 5 from 32,768 elements on run on the warp-per-element kernel
+    (csrc/stp_wpe.cu, kWpeMinElems4 / 5; persistent warps walking several elements each, ragged
+    last rounds): oracle parity on the first, last and 30 interior elements, and agreement with the
+    padded-DMMA kernel (ADERSTP_WPE=0) on every element."""
     S = stp
-    n = 4
     monkeypatch.delenv("ADERSTP_WPE", raising=False)
     q, par = S.generate(0, SEED, n, 0, E, layout=S.LAYOUT_AOSOA, q_stride=9)
     dt = O.cfl_dt(n, 6.0)
