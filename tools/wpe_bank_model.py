@@ -112,6 +112,6 @@ if __name__ == '__main__':
     res.sort()
     print('ideal', ideal(N))
     for r in res[:12]: print(r)
-    cur = (N, 37 if N == 6 else 17, 223 if N == 6 else 69)
+    cur = {6: (6, 37, 223), 5: (5, 25, 125), 4: (5, 21, 94)}[N]  # GeoW<N> in csrc/stp_wpe.cu
     a, b = build(N, *cur)
     print('current', cur, step_wavefronts(N, a, b))
