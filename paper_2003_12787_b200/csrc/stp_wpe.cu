@@ -4,8 +4,8 @@
 //
 // The padded-DMMA kernel (stp_dmma.cu) carries (8/N)^2 of the useful fragment traffic and fp64
 // work at nDof <= 6 and spends its largest stall on CTA barriers.  Here every warp owns an element
-// from load to store (persistent warps, 7 / 16 per SM at nDof 6 / 4, each with 2 x 9 fields of shared memory), and a
-// CK step r <- c_o q + L r (Horner form, see stp_dmma8.cu; proj/src/stp_splitck.cpp:46-70) is two
+// from load to store (persistent warps, 7 / 8 / 12 per SM at nDof 6 / 5 / 4, each with 2 x 9
+// fields of shared memory), and a CK step r <- c_o q + L r (Horner form, see stp_dmma8.cu; proj/src/stp_splitck.cpp:46-70) is two
 // warp-synchronous phases of TILE tasks: a lane owns an N x N tile (a, b) of one target field at a
 // fixed third index, keeps its N^2 accumulators in registers and contracts
 //   term A: acc[ia][ib] += D[ia][l] srcA(l, ib)      (derivative along a)
@@ -22,8 +22,8 @@
 // The Horner term c_o q comes from tensor memory (thread-private columns, filled once per
 // element), the iterate ping-pongs between the warp's two buffers.  Epilogue: face extrapolations
 // as line tasks into the dead buffer, leaving as TMA bulk stores (face_f formed in place once the
-// face_q copy has been read); qavg / favg are written in output order (fully coalesced 16-byte
-// stores).  No CTA-wide barrier after the TMEM allocation.
+// face_q copy has been read); qavg / favg are written in output order (coalesced 16-byte stores,
+// 8-byte at the odd nDof 5).  No CTA-wide barrier after the TMEM allocation.
 #include <cstdint>
 #include <type_traits>
 
@@ -35,6 +35,7 @@ namespace aderstp {
 
 namespace {
 
+// A/B knobs (make variant EXTRA=-D...): warps per SM at nDof 4 / 5, branching stores at nDof 5
 #ifndef WPE_WPC4
 #define WPE_WPC4 12
 #endif
@@ -468,8 +469,6 @@ __global__ void __launch_bounds__(GeoW<N>::WPC * 32, 1) stp_wpe_kernel(ParamsW k
         for (int k3 = 0; k3 < N; ++k3)
 #pragma unroll
           for (int k2 = 0; k2 < N; ++k2) {
-            constexpr int dummy = 0;
-            (void)dummy;
             const int node = k3 * S3 + k2 * S2, rg = k3 * N + k2;
             __stcs(qo + rg * PR, make_double2(sq[node], sq[node + 1]));
             if (fo) {
