@@ -136,6 +136,10 @@ def test_ndof4_large_batch_dispatch_parity(stp, oracle, monkeypatch, n, E):
     _check_outputs(S, oracle, n, q[idx].cpu().numpy(), par[idx].cpu().numpy(), dt,
                    (out.qavg[idx].cpu().numpy(), out.favg[idx].cpu().numpy(),
                     out.face_q[idx].cpu().numpy(), out.face_f[idx].cpu().numpy()), 9)
+    again = plan.predict(q, dt, par=par)  # deterministic: a rerun is bit-identical (SURVEY 8(b) determinism)
+    plan.status()
+    assert all(torch.equal(x, y) for x, y in ((out.qavg, again.qavg), (out.favg, again.favg),
+                                              (out.face_q, again.face_q), (out.face_f, again.face_f)))
     monkeypatch.setenv("ADERSTP_WPE", "0")
     plan0 = S.Plan(n, S.elastic_pde(), layout=S.LAYOUT_AOSOA, par_kind=S.PAR_RHO_CP_CS)
     out0 = plan0.predict(q, dt, par=par)
